@@ -1,0 +1,116 @@
+/*
+ * oxygen_b200.h — C ABI of the B200 unified-KV hot path (liboxygen_b200.so).
+ *
+ * The reference (kvweaver, pure Python) has no FFI: its plugin boundary is the
+ * duck-typed backend protocol + KvManager.  This ABI sits
+ * UNDER that Python surface; paper_2603_14371_b200/_lib.py binds it with
+ * ctypes.  Each entry point names the reference interface it replaces.
+ *
+ * Conventions: every function returns int status (OXY_OK = 0); on failure
+ * oxy_last_error() returns a thread-local message.  Plain pointers and sizes
+ * only; "stream" is a cudaStream_t passed as void* (NULL = legacy stream).
+ * Host pointers are marked _h, device pointers _d.  Not thread-safe per
+ * object: one scheduler thread owns a pool/model.
+ */
+#ifndef OXYGEN_B200_H
+#define OXYGEN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OXY_OK 0
+#define OXY_EINVAL 1     /* bad argument (maps to ValueError)            */
+#define OXY_ENOBLOCKS 2  /* KV pool out of blocks (maps to MemoryError)  */
+#define OXY_ECUDA 3      /* CUDA runtime/driver failure (RuntimeError)   */
+#define OXY_ESTATE 4     /* allocator invariant violated (RuntimeError)  */
+
+const char *oxy_last_error(void);
+int oxy_abi_version(void);
+
+/* ------------------------------------------------------------------------
+ * Deterministic paged-KV block allocator (host side, no CUDA).
+ * Replaces the per-request numpy copies owned by kvweaver/kv_manager.py:35-105
+ * with shared refcounted blocks.  Semantics are pinned in oracle/paged_alloc.py
+ * (lowest free id first; refcount; per-block fill watermark; copy-on-write of
+ * a shared partially-filled tail).
+ * ---------------------------------------------------------------------- */
+typedef struct oxy_alloc oxy_alloc;
+
+int oxy_alloc_create(int32_t num_blocks, int32_t block_size, oxy_alloc **out);
+int oxy_alloc_destroy(oxy_alloc *a);
+/* fresh sequence of n_tokens positions (prefill, kvweaver/backend.py:309-314);
+ * writes ceil(n_tokens/B) block ids */
+int oxy_alloc_seq(oxy_alloc *a, int32_t n_tokens, int32_t *blocks_h);
+int oxy_alloc_incref(oxy_alloc *a, const int32_t *blocks_h, int32_t n);
+int oxy_alloc_decref(oxy_alloc *a, const int32_t *blocks_h, int32_t n);
+/* extend a handle (blocks, seq_len) by up to n_new positions (decode append,
+ * kvweaver/backend.py:389-411).  Writes ceil((seq_len+n_new)/B) ids to
+ * new_blocks_h and cow_h[3] = {src, dst, n_slots} (src = -1: no copy). */
+int oxy_alloc_reserve(oxy_alloc *a, const int32_t *blocks_h, int32_t seq_len, int32_t n_new,
+                      int32_t *new_blocks_h, int32_t *cow_h);
+/* after the decode: keep ceil((seq_len+n_actual)/B) blocks, free the rest,
+ * lower the tail watermark to what was written */
+int oxy_alloc_settle(oxy_alloc *a, const int32_t *blocks_h, int32_t seq_len,
+                     int32_t n_reserved, int32_t n_actual, int32_t *n_blocks_out);
+int oxy_alloc_num_free(const oxy_alloc *a, int32_t *out);
+/* full state for parity tests: refcount[nb], fill[nb], sorted free ids */
+int oxy_alloc_snapshot(const oxy_alloc *a, int32_t *refcount_h, int32_t *fill_h,
+                       int32_t *free_h, int32_t *n_free);
+/* slot(p) = blocks[p / B] * B + p % B for p in [start, start+count) */
+int oxy_build_slot_mapping(const int32_t *blocks_h, int32_t block_size, int32_t start,
+                           int32_t count, int32_t *slots_h);
+
+/* ------------------------------------------------------------------------
+ * F1: the reference toy transformer on the GPU (kvweaver/backend.py:235-420),
+ * fp32 verification mode (dtype 0) or fp64 (dtype 1).  KV pool per layer:
+ * K and V [num_blocks, block_size, d_model] in the model dtype.
+ * ---------------------------------------------------------------------- */
+typedef struct oxy_toy oxy_toy;
+
+typedef struct oxy_toy_config {
+  int32_t L, d_model, n_heads, vocab, eos_token, action_dim, H;
+  uint64_t seed;
+} oxy_toy_config;
+
+/* ToyBackend.__init__ (kvweaver/backend.py:238-267): weights drawn on device
+ * from the splitmix64 counter form, in the reference draw order. */
+int oxy_toy_create(const oxy_toy_config *cfg, int32_t dtype, int32_t num_blocks,
+                   int32_t block_size, void *stream, oxy_toy **out);
+int oxy_toy_destroy(oxy_toy *m);
+/* read (write=0) or overwrite (write=1) one weight tensor as float64:
+ * which 0 embed,1 wq,2 wk,3 wv,4 wo,5 w1,6 w2,7 unembed,8 action_head */
+int oxy_toy_weight(oxy_toy *m, int32_t which, int32_t layer, double *host, int64_t n,
+                   int32_t write, void *stream);
+/* prefill (kvweaver/backend.py:276-314): causal pass, K/V into the pool blocks */
+int oxy_toy_prefill(oxy_toy *m, const int32_t *tokens_h, int32_t T, const int32_t *blocks_h,
+                    void *stream);
+/* recompute_logits (kvweaver/backend.py:301-304): no-cache pass, last row */
+int oxy_toy_recompute_logits(oxy_toy *m, const int32_t *tokens_h, int32_t T,
+                             double *logits_h, void *stream);
+/* action_denoise (kvweaver/backend.py:316-332): reads the cache, S Euler steps */
+int oxy_toy_denoise(oxy_toy *m, const int32_t *blocks_h, int32_t seq_len, int32_t S,
+                    double *actions_h, void *stream);
+/* batched_language_decode (kvweaver/backend.py:334-420): up to k greedy steps
+ * for m rows; per-row stop on EOS / budget on device.  block_tables_h [m*max_blocks],
+ * cow_h [m*3] from oxy_alloc_reserve.  out_tokens_h [m*k], out_count_h [m]. */
+int oxy_toy_decode(oxy_toy *m, int32_t rows, int32_t k, const int32_t *block_tables_h,
+                   int32_t max_blocks, const int32_t *seq_lens_h, const int32_t *last_tokens_h,
+                   const int32_t *budgets_h, const int32_t *cow_h, int32_t *out_tokens_h,
+                   int32_t *out_count_h, void *stream);
+/* materialise one layer's K,V rows [seq_len, d_model] as float64 (KvLayer view) */
+int oxy_toy_read_kv(oxy_toy *m, const int32_t *blocks_h, int32_t seq_len, int32_t layer,
+                    double *keys_h, double *values_h, void *stream);
+
+/* inverse of oxy_toy_read_kv: write rows [0, seq_len) of one layer into the
+ * handle's blocks (adopting a host KvCache into the pool; fault injection) */
+int oxy_toy_write_kv(oxy_toy *m, const int32_t *blocks_h, int32_t seq_len, int32_t layer,
+                     const double *keys_h, const double *values_h, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OXYGEN_B200_H */

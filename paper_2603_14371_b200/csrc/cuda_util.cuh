@@ -1,0 +1,95 @@
+// CUDA helpers shared by the kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "common.h"
+
+#define OXY_CUDA(x)                                                                   \
+  do {                                                                                \
+    cudaError_t e_ = (x);                                                             \
+    if (e_ != cudaSuccess) oxy::fail(OXY_ECUDA, "%s failed: %s", #x, cudaGetErrorString(e_)); \
+  } while (0)
+
+#define OXY_LAUNCH_CHECK() OXY_CUDA(cudaGetLastError())
+
+namespace oxy {
+
+constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
+
+__host__ __device__ inline uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// draw i (0-based) of SplitMix64(seed).uniform(), bit-exact with the reference
+__host__ __device__ inline double splitmix_uniform(uint64_t seed, uint64_t i) {
+  return (double)(mix64(seed + (i + 1) * kGamma) >> 11) * 0x1.0p-53;
+}
+
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Grow-only device scratch buffer.
+struct DevBuf {
+  void *ptr = nullptr;
+  size_t bytes = 0;
+  void *get(size_t need) {
+    if (need > bytes) {
+      if (ptr) cudaFree(ptr);
+      size_t cap = need + need / 2 + 256;
+      OXY_CUDA(cudaMalloc(&ptr, cap));
+      bytes = cap;
+    }
+    return ptr;
+  }
+  template <typename T>
+  T *as(size_t n) { return static_cast<T *>(get(n * sizeof(T))); }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+  }
+};
+
+template <typename T>
+__device__ inline T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <typename T>
+__device__ inline T warp_max(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Deterministic block reductions (fixed shuffle tree, then warp 0).
+template <typename T>
+__device__ inline T block_sum(T v, T *red) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  T r = lane < nw ? red[lane] : T(0);
+  r = warp_sum(r);
+  return r;
+}
+
+template <typename T>
+__device__ inline T block_max(T v, T *red) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  v = warp_max(v);
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  T r = lane < nw ? red[lane] : red[0];
+  r = warp_max(r);
+  return r;
+}
+
+}  // namespace oxy

@@ -1,0 +1,149 @@
+"""Unified paged KV pool: block allocator binding and cache handles.
+
+One pool per backend holds every request's KV on HBM in fixed-size blocks
+(SURVEY.md Appendix D).  A cache is a *handle* ``(pool, block_ids, seq_len)``:
+the prefill writes blocks once, the action expert reads the same handle
+(cross-task sharing, ``kvweaver/scheduler.py:112-120``), and language decode
+extends it in place, copying a shared partially-filled tail block only when
+another handle already wrote past it.  Handles keep the reference's value
+semantics (``kvweaver/kv_manager.py:28-32``): an old handle still reads
+exactly its positions after any later decode.
+
+Block ids are assigned by the C++ allocator (``csrc/allocator.cpp``);
+``oracle/paged_alloc.py`` restates the same rules and the CPU tests replay
+random op sequences through both, comparing block tables, copy-on-write
+triples and the full allocator state after every op (bit-exact).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from .kv_manager import KvLayer
+
+__all__ = ["BlockAllocator", "PagedKvCache"]
+
+
+class BlockAllocator:
+    """Thin owner of an ``oxy_alloc``; all policy lives in C++."""
+
+    def __init__(self, num_blocks: int, block_size: int):
+        self.num_blocks = int(num_blocks)
+        self.block_size = int(block_size)
+        h = C.c_void_p()
+        _lib.call("oxy_alloc_create", C.c_int32(num_blocks), C.c_int32(block_size), C.byref(h))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                _lib.lib().oxy_alloc_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    def blocks_for(self, n: int) -> int:
+        return -(-n // self.block_size)
+
+    def alloc_seq(self, n_tokens: int) -> tuple[int, ...]:
+        out = np.empty(self.blocks_for(n_tokens), np.int32)
+        _lib.call("oxy_alloc_seq", self._h, C.c_int32(n_tokens), _lib.ptr_i32(out))
+        return tuple(out.tolist())
+
+    def incref(self, blocks) -> None:
+        b = _lib.as_i32(blocks)
+        _lib.call("oxy_alloc_incref", self._h, _lib.ptr_i32(b), C.c_int32(len(b)))
+
+    def decref(self, blocks) -> None:
+        b = _lib.as_i32(blocks)
+        _lib.call("oxy_alloc_decref", self._h, _lib.ptr_i32(b), C.c_int32(len(b)))
+
+    def reserve(self, blocks, seq_len: int, n_new: int):
+        b = _lib.as_i32(blocks)
+        out = np.empty(self.blocks_for(seq_len + n_new), np.int32)
+        cow = np.empty(3, np.int32)
+        _lib.call("oxy_alloc_reserve", self._h, _lib.ptr_i32(b), C.c_int32(seq_len),
+                  C.c_int32(n_new), _lib.ptr_i32(out), _lib.ptr_i32(cow))
+        return out, cow
+
+    def settle(self, blocks: np.ndarray, seq_len: int, n_reserved: int, n_actual: int):
+        nb = C.c_int32()
+        _lib.call("oxy_alloc_settle", self._h, _lib.ptr_i32(blocks), C.c_int32(seq_len),
+                  C.c_int32(n_reserved), C.c_int32(n_actual), C.byref(nb))
+        return tuple(blocks[:nb.value].tolist())
+
+    @property
+    def num_free(self) -> int:
+        n = C.c_int32()
+        _lib.call("oxy_alloc_num_free", self._h, C.byref(n))
+        return n.value
+
+    def snapshot(self):
+        ref = np.empty(self.num_blocks, np.int32)
+        fill = np.empty(self.num_blocks, np.int32)
+        free = np.empty(self.num_blocks, np.int32)
+        n = C.c_int32()
+        _lib.call("oxy_alloc_snapshot", self._h, _lib.ptr_i32(ref), _lib.ptr_i32(fill),
+                  _lib.ptr_i32(free), C.byref(n))
+        return ref, fill, free[:n.value].copy()
+
+    def slot_mapping(self, blocks, start: int, count: int) -> np.ndarray:
+        b = _lib.as_i32(blocks)
+        out = np.empty(count, np.int32)
+        _lib.call("oxy_build_slot_mapping", _lib.ptr_i32(b), C.c_int32(self.block_size),
+                  C.c_int32(start), C.c_int32(count), _lib.ptr_i32(out))
+        return out
+
+
+class PagedKvCache:
+    """Cache handle into a backend's pool.  Duck-types ``KvCache``:
+    ``seq_len``, ``backend_tag``, ``num_layers``, ``layers`` (materialised
+    lazily from HBM as read-only float64 ``KvLayer``s) and value equality.
+    Dropping the last reference returns the blocks to the pool."""
+
+    __slots__ = ("owner", "blocks", "seq_len", "backend_tag", "_layers", "__weakref__")
+
+    def __init__(self, owner, blocks: tuple, seq_len: int):
+        self.owner = owner
+        self.blocks = tuple(blocks)
+        self.seq_len = int(seq_len)
+        self.backend_tag = owner.backend_tag
+        self._layers = None
+
+    def __del__(self):
+        owner = getattr(self, "owner", None)
+        if owner is not None and self.blocks:
+            try:
+                owner.allocator.decref(self.blocks)
+            except Exception:
+                pass
+
+    @property
+    def num_layers(self) -> int:
+        return self.owner.num_layers
+
+    @property
+    def layers(self) -> tuple:
+        if self._layers is None:
+            self._layers = tuple(KvLayer(*self.owner.read_kv(self, l))
+                                 for l in range(self.num_layers))
+        return self._layers
+
+    def __eq__(self, other):
+        if not hasattr(other, "backend_tag") or not hasattr(other, "layers"):
+            return NotImplemented
+        if self.backend_tag != other.backend_tag or self.seq_len != other.seq_len:
+            return False
+        if isinstance(other, PagedKvCache) and other.owner is self.owner \
+                and other.blocks == self.blocks:
+            return True
+        return tuple(self.layers) == tuple(other.layers)
+
+    __hash__ = None
+
+    def __repr__(self):
+        return f"PagedKvCache(seq_len={self.seq_len}, blocks={self.blocks})"

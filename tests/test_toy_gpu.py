@@ -1,0 +1,241 @@
+"""F1 on the B200: the reference toy transformer through liboxygen_b200.so,
+checked against the reference's golden outputs (tests/golden/toy_kat.json,
+sim.json) and the numpy oracle (oracle/toy_ref.py), plus the reference's
+route-equality suites and fault injections (tests/test_verify.py:32-125 of
+the reference).
+
+Tolerances: greedy tokens identical; fp32 mode actions and KV
+within rtol 1e-5 (atol 1e-6), logits within 1e-4 abs; fp64 mode rtol 1e-10.
+"""
+
+import numpy as np
+import pytest
+
+from oracle.toy_ref import ToyRef
+from paper_2603_14371_b200 import (ActionChunk, BackendConfig, BatchedState, KvManager,
+                                   Observation, SimConfig, WorkloadSpec, run_simulation,
+                                   transcript_to_json)
+from paper_2603_14371_b200.rng import SplitMix64
+from paper_2603_14371_b200.verify import (suite_batching, suite_reference, suite_resumption,
+                                          suite_sharing)
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"f32": dict(rtol=1e-5, atol=1e-6), "f64": dict(rtol=1e-10, atol=1e-12)}
+
+
+def toy(dtype="f32", **cfg):
+    from paper_2603_14371_b200.toy_b200 import ToyBackend
+    return ToyBackend(BackendConfig(**cfg), dtype=dtype)
+
+
+def solo(b, obs, max_len, k, tokens=(), kv=None):
+    kv = kv if kv is not None else b.prefill(Observation(tuple(obs), 0))
+    return b.batched_language_decode(
+        BatchedState((kv,), (tuple(tokens),), (False,), (0,), (max_len,), (0,)), k)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_weights_drawn_on_device(dtype):
+    b = toy(dtype, vocab=50, d_model=16)
+    r = ToyRef(vocab=50, d_model=16)
+    if dtype == "f64":
+        np.testing.assert_array_equal(b._embed, r.embed)
+        np.testing.assert_array_equal(b._action_head, r.head)
+    else:
+        np.testing.assert_array_equal(b._unembed, r.unembed.astype(np.float32))
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+@pytest.mark.parametrize("name", ["A1", "A2", "A2b", "split", "A3", "A4"])
+def test_reference_kats(golden, name, dtype):
+    g = golden("toy_kat.json")[name]
+    b = toy(dtype, **g["config"])
+    kv = b.prefill(Observation(tuple(g["obs"]), 0))
+    out = solo(b, g["obs"], g["max_len"], g["k"], kv=kv)
+    assert list(out.token_buffers[0]) == g["tokens"]
+    assert out.flags[0] == g["flag"]
+    assert out.kv_batch[0].seq_len == len(g["obs"]) + len(g["tokens"])
+    if "action" in g:
+        np.testing.assert_allclose(b.action_denoise(kv, 10).actions, g["action"], **TOL[dtype])
+    if "final_kv" in g:
+        for layer, (gk, gv) in zip(out.kv_batch[0].layers, g["final_kv"]):
+            np.testing.assert_allclose(layer.keys, gk, **TOL[dtype])
+            np.testing.assert_allclose(layer.values, gv, **TOL[dtype])
+    if "first_logits" in g:
+        lg = b.recompute_logits(list(g["obs"]) + [0])
+        np.testing.assert_allclose(lg, g["first_logits"], atol=1e-4)
+    if "recompute_logits" in g:
+        np.testing.assert_allclose(b.recompute_logits(g["obs"] + [0]), g["recompute_logits"],
+                                   atol=1e-4)
+
+
+def test_paged_kv_equals_oracle_after_resumed_decodes():
+    # decode attention + KV append over paged blocks vs numpy on the same data
+    b = toy("f32", d_model=64, n_heads=4, vocab=97, seed=11)
+    r = ToyRef(d_model=64, n_heads=4, vocab=97, seed=11)
+    obs = (5, 17, 3, 88, 41, 9, 60, 2, 33, 71, 12, 4, 90, 26, 55, 8, 19)  # 17 > block 16
+    st = solo(b, obs, 30, 7)
+    st2 = b.batched_language_decode(
+        BatchedState(st.kv_batch, st.token_buffers, (False,), (0,), (30,), (0,)), 9)
+    toks, _, kvs = r.decode(r.prefill(obs), (), 30, 16)
+    assert st2.token_buffers[0] == toks
+    for layer, (k, v) in zip(st2.kv_batch[0].layers, kvs):
+        np.testing.assert_allclose(layer.keys, k, **TOL["f32"])
+        np.testing.assert_allclose(layer.values, v, **TOL["f32"])
+
+
+def test_tie_break_toward_lowest_id():
+    b = toy("f32")
+    b._unembed = np.zeros((32, 64))
+    out = solo(b, (1, 2), 8, 8)
+    assert out.token_buffers[0] == (0,) and out.flags[0] is True
+
+
+def test_any_step_count_lands_on_target():
+    b = toy("f32")
+    kv = b.prefill(Observation((2, 7, 1), 0))
+    c1, c5, c10 = (b.action_denoise(kv, s) for s in (1, 5, 10))
+    assert c1 == c5 == c10
+
+
+def test_validation_messages():
+    b = toy("f32")
+    with pytest.raises(ValueError, match="outside vocab"):
+        b.prefill(Observation((64,), 0))
+    kv = b.prefill(Observation((1,), 0))
+    with pytest.raises(ValueError, match="must be >= 1"):
+        b.action_denoise(kv, 0)
+    with pytest.raises(ValueError, match=">= 1, got 0"):
+        solo(b, (1,), 5, 0, kv=kv)
+    bad = BatchedState((kv,), ((2,),), (True,), (4,), (5,), (0,))
+    with pytest.raises(ValueError, match="request 4 is terminated"):
+        b.batched_language_decode(bad, 1)
+    other = toy("f32", seed=8)
+    with pytest.raises(ValueError, match="fed to"):
+        other.action_denoise(kv, 1)
+
+
+def test_batch_of_three_matches_solos_bit_exact():
+    b = toy("f32")
+    specs = [(1, 2, 3), (9, 8, 7, 6, 5), (41,)]
+    caches = [b.prefill(Observation(o, 0)) for o in specs]
+    big = BatchedState(tuple(caches), ((), (), ()), (False,) * 3, (0, 1, 2), (12,) * 3, (0,) * 3)
+    out = b.batched_language_decode(big, 12)
+    for i, o in enumerate(specs):
+        s = solo(b, o, 12, 12)
+        assert out.token_buffers[i] == s.token_buffers[0]
+        assert out.kv_batch[i] == s.kv_batch[0]   # batch-invariant kernels: exact
+
+
+def test_pool_blocks_return_when_handles_drop():
+    b = toy("f32")
+    free0 = b.allocator.num_free
+    kv = b.prefill(Observation(tuple(range(1, 40)), 0))
+    st = solo(b, (), 30, 10, kv=kv)
+    st2 = b.batched_language_decode(
+        BatchedState(st.kv_batch, st.token_buffers, (False,), (0,), (30,), (0,)), 5)
+    assert b.allocator.num_free < free0
+    del kv, st, st2
+    assert b.allocator.num_free == free0
+
+
+@pytest.mark.parametrize("suite, n", [(suite_batching, 25), (suite_reference, 20),
+                                      (suite_resumption, 30), (suite_sharing, 20)])
+def test_reference_suites_on_gpu_backend(suite, n):
+    rep = suite(n)
+    assert rep.ok, rep.failures[:3]
+
+
+def test_transcripts_match_reference(golden):
+    g = golden("sim.json")
+    import json
+    for variant in ("Unified", "SharedNoBatch", "IsolatedSequential"):
+        case = g[f"toy_{variant}"]
+        c = case["config"]
+        cfg = SimConfig(variant=variant, backend_kind="Toy",
+                        backend_config=BackendConfig(**c["backend_config"]),
+                        workload=WorkloadSpec(**c["workload"]), k=c["k"])
+        got = json.loads(transcript_to_json(run_simulation(cfg)))
+        want = json.loads(case["transcript"])
+        assert sorted(got) == sorted(want)
+        for rid in want:
+            assert got[rid]["tokens"] == want[rid]["tokens"], (variant, rid)
+            assert got[rid]["completion_frame"] == want[rid]["completion_frame"]
+            np.testing.assert_allclose(got[rid]["action"], want[rid]["action"], **TOL["f32"])
+
+
+def test_cross_variant_invariance_exact():
+    rng = SplitMix64(2026)
+    from paper_2603_14371_b200.toy_b200 import ToyBackend
+    for i in range(6):
+        bc = BackendConfig(vocab=16 + rng.below(49), seed=rng.below(1 << 32))
+        pattern = ("OnePerFrame", "Uniform", "Poisson", "MixedLength")[rng.below(4)]
+        wl = WorkloadSpec(pattern=pattern, default_N=2 + rng.below(9), obs_len=2 + rng.below(9),
+                          num_frames=4 + rng.below(8), seed=rng.below(1 << 32),
+                          lam=0.25 + rng.uniform(), r=rng.below(3), short_N=2 + rng.below(5),
+                          long_N=8 + rng.below(6), p_long=rng.uniform())
+        k = 1 + rng.below(6)
+        be = ToyBackend(bc)
+        base = run_simulation(SimConfig("Unified", "Toy", bc, workload=wl, k=k), be)
+        for variant in ("SharedNoBatch", "IsolatedSequential"):
+            other = run_simulation(SimConfig(variant, "Toy", bc, workload=wl, k=k), be)
+            assert sorted(other.transcript) == sorted(base.transcript)
+            for rid, e in base.transcript.items():
+                assert other.transcript[rid].tokens == e.tokens
+                assert other.transcript[rid].action == e.action   # exact
+
+
+# ---- fault injection: the suites must catch broken GPU backends ----------
+
+def _broken(kind):
+    from paper_2603_14371_b200.toy_b200 import ToyBackend
+
+    class BatchTamper(ToyBackend):
+        def batched_language_decode(self, batched, k):
+            out = super().batched_language_decode(batched, k)
+            if batched.size < 2 or len(out.token_buffers[0]) <= len(batched.token_buffers[0]):
+                return out
+            bufs = list(out.token_buffers)
+            bufs[0] = bufs[0][:-1] + ((bufs[0][-1] + 1) % self.config.vocab,)
+            return BatchedState(out.kv_batch, tuple(bufs), out.flags, out.request_ids,
+                                out.max_lens, out.created_frames)
+
+    class LostWrite(ToyBackend):
+        """Zeroes the last KV row each call wrote (a lost pool write): a single
+        call looks fine, resuming from the state does not."""
+        def batched_language_decode(self, batched, k):
+            out = super().batched_language_decode(batched, k)
+            for kv, old in zip(out.kv_batch, batched.kv_batch):
+                if kv.seq_len > old.seq_len:
+                    for l in range(self.num_layers):
+                        keys, vals = self.read_kv(kv, l)
+                        keys[-1] = 0.0
+                        vals[-1] = 0.0
+                        self.write_kv(kv, l, keys, vals)
+            return out
+
+    class DriftingDenoise(ToyBackend):
+        calls = 0
+
+        def action_denoise(self, kv, S):
+            chunk = super().action_denoise(kv, S)
+            DriftingDenoise.calls += 1
+            return ActionChunk(chunk.actions + 1e-3 * DriftingDenoise.calls)
+
+    return {"tamper": BatchTamper, "lost": LostWrite, "drift": DriftingDenoise}[kind]
+
+
+def test_batching_suite_catches_cross_request_leakage():
+    rep = suite_batching(15, backend_factory=_broken("tamper"))
+    assert not rep.ok and any("request" in f for f in rep.failures)
+
+
+def test_resumption_suite_catches_lost_cache_writes():
+    rep = suite_resumption(15, backend_factory=_broken("lost"))
+    assert not rep.ok
+
+
+def test_sharing_suite_catches_stateful_denoise():
+    rep = suite_sharing(6, backend_factory=_broken("drift"))
+    assert not rep.ok and any("action chunk" in f for f in rep.failures)
