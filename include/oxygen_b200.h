@@ -110,6 +110,21 @@ int oxy_toy_read_kv(oxy_toy *m, const int32_t *blocks_h, int32_t seq_len, int32_
 int oxy_toy_write_kv(oxy_toy *m, const int32_t *blocks_h, int32_t seq_len, int32_t layer,
                      const double *keys_h, const double *values_h, void *stream);
 
+/* ------------------------------------------------------------------------
+ * tcgen05 GEMM (the pi0.5 projections): Y[t, f] (op)= sum_k W[f, k] X[t, k],
+ * W [n_out, k] and X [t, k] bf16 row-major on device.  mode: 0 f32 store,
+ * 1 bf16 store, 2 f32 +=, 3 GeGLU (row pairs gate/up -> bf16 [t, n_out/2]),
+ * 4 GELU bf16, 5 bf16(acc + res_f32).  splits: 0 = auto (split-K needs
+ * ws_d of splits*t*n_out floats).  No reference counterpart (the reference's
+ * numpy matmuls, kvweaver/backend.py:290-297).
+ * ---------------------------------------------------------------------- */
+int oxy_gemm_bf16(const void *w_d, const void *x_d, int32_t n_out, int32_t k, int32_t t,
+                  int32_t mode, void *out_d, int32_t ldo, const float *bias_d,
+                  const float *res_d, int32_t ldr, int32_t splits, float *ws_d,
+                  int64_t ws_floats, void *stream);
+/* plan the launch: out6 = {bn, n_tiles, m_tiles, splits, stages, k_blocks} */
+int oxy_gemm_plan(int32_t n_out, int32_t k, int32_t t, int32_t splits, int32_t *out6);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,59 @@
+// tcgen05 GEMM for sm_100a: Y[t, f] (op)= sum_k W[f, k] * X[t, k].
+//
+// Weights are the UMMA A operand (M = 128 output features per tile) and the
+// activations the B operand (N = BN tokens per tile, 16..256, runtime), both
+// bf16 K-major, loaded by TMA with 128-byte swizzle into a multi-stage smem
+// ring; fp32 accumulators live in TMEM.  Putting the weights on M keeps the
+// same kernel efficient from 1-token decode (BN = 16) to 800-token prefill:
+// a weight tile is streamed from HBM once per token tile.  Split-K spreads
+// skinny (decode / denoise) GEMMs over all 148 SMs; partial sums are reduced
+// in a fixed order so results do not depend on timing.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace oxy {
+namespace gemm {
+
+enum Epi : int {
+  EPI_F32 = 0,        // out_f32[t, f] = acc (+ bias)
+  EPI_BF16 = 1,       // out_bf16[t, f] = acc (+ bias)
+  EPI_ADD_F32 = 2,    // out_f32[t, f] += acc (+ bias)          residual stream
+  EPI_GEGLU_BF16 = 3, // rows (2j, 2j+1) = (gate_j, up_j): out_bf16[t, j] = gelu_tanh(g) * u
+  EPI_GELU_BF16 = 4,  // out_bf16[t, f] = gelu_tanh(acc + bias)
+  EPI_ADD_BF16 = 5,   // out_bf16[t, f] = bf16(acc + bias + res_f32[t, f])  (no in-place)
+};
+
+struct EpiParams {
+  int mode;
+  void *out;
+  int ldo;              // row stride of out (elements)
+  const float *bias;    // [N] or null
+  const float *res;     // EPI_ADD_BF16 residual input [T, ldr]
+  int ldr;
+};
+
+constexpr int BM = 128;        // weight rows per tile (UMMA M)
+constexpr int BK = 64;         // K per stage: 64 bf16 = one 128-byte swizzle row
+constexpr int MAX_BN = 256;
+constexpr int MAX_STAGES = 8;
+constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
+constexpr int SMEM_BUDGET = 200 * 1024;
+
+struct Plan {
+  int bn, n_tiles, m_tiles, splits, stages, kb_total;
+};
+
+// Host: build a plan for (N_out, K, T) on `sms` SMs.
+Plan make_plan(int n_out, int k, int t, int sms, int force_splits = 0);
+
+// Host: launch.  ws must hold splits * T * N_out floats when splits > 1.
+void launch(const void *w, const void *x, int n_out, int k, int t, const EpiParams &epi,
+            const Plan &plan, float *ws, cudaStream_t st);
+
+}  // namespace gemm
+}  // namespace oxy
