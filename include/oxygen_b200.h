@@ -125,6 +125,64 @@ int oxy_gemm_bf16(const void *w_d, const void *x_d, int32_t n_out, int32_t k, in
 /* plan the launch: out6 = {bn, n_tiles, m_tiles, splits, stages, k_blocks} */
 int oxy_gemm_plan(int32_t n_out, int32_t k, int32_t t, int32_t splits, int32_t *out6);
 
+/* Paged decode attention (the language-decode hot kernel; replaces the padded
+ * dense re-materialisation of kvweaver/backend.py:365-384): rows x 8 query
+ * heads (q_d bf16 [rows, 2048]) over 1 KV head of dim 256 read through the
+ * block table from one layer's pool (bf16 [num_blocks, 64, 256] K and V),
+ * keys [0, pos[r]]; out_d bf16 [rows, 2048].  ws_d: rows*max_blocks*8*258
+ * floats.  Device pointers; scale 1/16. */
+int oxy_paged_decode_attention(const void *q_d, void *out_d, const void *kpool_d,
+                               const void *vpool_d, const int32_t *bt_d, int32_t bt_stride,
+                               const int32_t *pos_d, int32_t rows, int32_t max_blocks,
+                               float *ws_d, void *stream);
+
+/* kernels launched by this library so far (process-wide counter) */
+int64_t oxy_launch_count(void);
+
+/* ------------------------------------------------------------------------
+ * F2: pi0.5-shaped VLA (Gemma-2B prefix + Gemma-300M action expert + SigLIP),
+ * bf16 on tcgen05, one unified paged KV pool (block 64 x 256 per layer).
+ * The three calls replace the backend protocol of kvweaver/backend.py:309-420
+ * for this model family; pool blocks come from oxy_alloc_*.
+ * ---------------------------------------------------------------------- */
+typedef struct oxy_pi05 oxy_pi05;
+
+typedef struct oxy_pi05_config {
+  int32_t width, depth, mlp, vocab;
+  int32_t expert_width, expert_mlp;
+  int32_t vit_width, vit_depth, vit_mlp, vit_heads;
+  int32_t H, action_dim, eos_token;
+  uint64_t seed;
+} oxy_pi05_config;
+
+int oxy_pi05_create(const oxy_pi05_config *cfg, int32_t num_blocks, void *stream,
+                    oxy_pi05 **out);
+int oxy_pi05_destroy(oxy_pi05 *m);
+int oxy_pi05_num_tensors(oxy_pi05 *m, int32_t *n);
+int oxy_pi05_tensor_info(oxy_pi05 *m, int32_t i, char *name64, int64_t *shape2,
+                         int32_t *dtype, uint64_t *offset, float *bound, float *center);
+int oxy_pi05_tensor_read(oxy_pi05 *m, int32_t i, void *host, int64_t nbytes, void *stream);
+/* shared prefix prefill of n_obs observations (prefill, kvweaver/backend.py:309-314):
+ * prefix i = [n_img_h[i] camera images (uint8 [224,224,3] each, device, in order);
+ * n_txt_h[i] prompt tokens]; K/V of every layer written to blocks_h (concatenated
+ * per observation, ceil(P_i/64) ids each). */
+int oxy_pi05_prefill(oxy_pi05 *m, int32_t n_obs, const int32_t *n_img_h,
+                     const int32_t *n_txt_h, const int32_t *tokens_h, const uint8_t *images_d,
+                     const int32_t *blocks_h, void *stream);
+/* action expert (action_denoise, kvweaver/backend.py:316-332): S Euler steps for
+ * n streams reading each stream's prefix blocks; actions_d f32 [n, H, A]. */
+int oxy_pi05_denoise(oxy_pi05 *m, int32_t n, const int32_t *prefix_lens_h,
+                     const int32_t *blocks_h, int32_t S, float *actions_d, void *stream);
+/* continuous-batched greedy decode (batched_language_decode,
+ * kvweaver/backend.py:334-420); same contract as oxy_toy_decode; logits_h
+ * (optional) receives [k, rows, vocab] f32. */
+int oxy_pi05_decode(oxy_pi05 *m, int32_t rows, int32_t k, const int32_t *block_tables_h,
+                    int32_t max_blocks, const int32_t *seq_lens_h, const int32_t *last_tokens_h,
+                    const int32_t *budgets_h, const int32_t *cow_h, int32_t *out_tokens_h,
+                    int32_t *out_count_h, float *logits_h, void *stream);
+int oxy_pi05_read_kv(oxy_pi05 *m, const int32_t *blocks_h, int32_t seq_len, int32_t layer,
+                     float *keys_h, float *values_h, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -47,6 +47,7 @@ def lib():
                                f"(run __graft_entry__.build())")
         _lib = C.CDLL(LIB_PATH)
         _lib.oxy_last_error.restype = C.c_char_p
+        _lib.oxy_launch_count.restype = C.c_int64
     return _lib
 
 

@@ -23,6 +23,7 @@
 namespace oxy {
 
 static thread_local std::string g_err;
+unsigned long long g_launches = 0;
 
 void set_error(const char *fmt, ...) {
   char buf[1024];
@@ -76,6 +77,7 @@ extern "C" {
 
 const char *oxy_last_error(void) { return oxy::g_err.c_str(); }
 int oxy_abi_version(void) { return 1; }
+int64_t oxy_launch_count(void) { return (int64_t)__atomic_load_n(&oxy::g_launches, __ATOMIC_RELAXED); }
 
 int oxy_alloc_create(int32_t num_blocks, int32_t block_size, oxy_alloc **out) {
   OXY_API_BEGIN

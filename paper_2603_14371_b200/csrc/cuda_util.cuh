@@ -12,7 +12,16 @@
     if (e_ != cudaSuccess) oxy::fail(OXY_ECUDA, "%s failed: %s", #x, cudaGetErrorString(e_)); \
   } while (0)
 
-#define OXY_LAUNCH_CHECK() OXY_CUDA(cudaGetLastError())
+namespace oxy {
+// kernels launched by this library (read by bench.py as gpu_launches)
+extern unsigned long long g_launches;
+}
+
+#define OXY_LAUNCH_CHECK()                                  \
+  do {                                                      \
+    __atomic_fetch_add(&oxy::g_launches, 1ull, __ATOMIC_RELAXED); \
+    OXY_CUDA(cudaGetLastError());                           \
+  } while (0)
 
 namespace oxy {
 

@@ -131,6 +131,13 @@ __device__ __forceinline__ void epilogue_store(const EpiParams &e, int t, int f,
       static_cast<__nv_bfloat16 *>(e.out)[(size_t)t * e.ldo + f] =
           __float2bfloat16(acc + e.res[(size_t)t * e.ldr + f]);
       break;
+    case EPI_ADD_GATED_F32:
+      static_cast<float *>(e.out)[(size_t)t * e.ldo + f] += e.gate[f] * acc;
+      break;
+    case EPI_SWISH_BF16:
+      static_cast<__nv_bfloat16 *>(e.out)[(size_t)t * e.ldo + f] =
+          __float2bfloat16(acc / (1.f + __expf(-acc)));
+      break;
   }
 }
 
@@ -366,7 +373,7 @@ extern "C" int oxy_gemm_bf16(const void *w_d, const void *x_d, int32_t n_out, in
                              int64_t ws_floats, void *stream) {
   OXY_API_BEGIN
   OXY_REQUIRE(n_out > 0 && k > 0 && t >= 0, "bad GEMM shape");
-  OXY_REQUIRE(mode >= 0 && mode <= 5, "unknown epilogue mode %d", mode);
+  OXY_REQUIRE(mode >= 0 && mode <= 5, "unknown epilogue mode %d (0-5 via the C ABI)", mode);
   int dev = 0, sms = 148;
   OXY_CUDA(cudaGetDevice(&dev));
   OXY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -375,7 +382,7 @@ extern "C" int oxy_gemm_bf16(const void *w_d, const void *x_d, int32_t n_out, in
     OXY_REQUIRE(ws_d && ws_floats >= (int64_t)plan.splits * t * n_out,
                 "split-K workspace too small (%lld floats needed)",
                 (long long)plan.splits * t * n_out);
-  oxy::gemm::EpiParams e{mode, out_d, ldo, bias_d, res_d, ldr};
+  oxy::gemm::EpiParams e{mode, out_d, ldo, bias_d, res_d, ldr, nullptr};
   oxy::gemm::launch(w_d, x_d, n_out, k, t, e, plan, ws_d, oxy::as_stream(stream));
   OXY_API_END
 }

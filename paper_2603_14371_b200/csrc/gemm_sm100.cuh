@@ -26,6 +26,8 @@ enum Epi : int {
   EPI_GEGLU_BF16 = 3, // rows (2j, 2j+1) = (gate_j, up_j): out_bf16[t, j] = gelu_tanh(g) * u
   EPI_GELU_BF16 = 4,  // out_bf16[t, f] = gelu_tanh(acc + bias)
   EPI_ADD_BF16 = 5,   // out_bf16[t, f] = bf16(acc + bias + res_f32[t, f])  (no in-place)
+  EPI_ADD_GATED_F32 = 6,  // out_f32[t, f] += gate[f] * (acc + bias)     adaRMS gated residual
+  EPI_SWISH_BF16 = 7,     // out_bf16[t, f] = swish(acc + bias)
 };
 
 struct EpiParams {
@@ -35,6 +37,7 @@ struct EpiParams {
   const float *bias;    // [N] or null
   const float *res;     // EPI_ADD_BF16 residual input [T, ldr]
   int ldr;
+  const float *gate;    // EPI_ADD_GATED_F32 per-feature gate [N]
 };
 
 constexpr int BM = 128;        // weight rows per tile (UMMA M)

@@ -1,0 +1,770 @@
+// F2 kernels: norms, RoPE + paged KV append, flash attention over
+// [paged prefix || dense suffix], paged decode attention, greedy argmax.
+#include <cmath>
+
+#include "cuda_util.cuh"
+#include "pi05_kernels.cuh"
+
+namespace oxy {
+namespace pi05 {
+
+// ============================================================ elementwise
+
+__global__ void rmsnorm_kernel(const float *x, int ldx, bf16 *y, int ldy, const float *w,
+                               const float *ms, const float *mb, int D, float eps) {
+  __shared__ float red[32];
+  const float *xr = x + (size_t)blockIdx.x * ldx;
+  bf16 *yr = y + (size_t)blockIdx.x * ldy;
+  float ss = 0.f;
+  for (int j = threadIdx.x * 4; j < D; j += blockDim.x * 4) {
+    float4 v = *reinterpret_cast<const float4 *>(xr + j);
+    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  }
+  ss = block_sum(ss, red);
+  const float inv = rsqrtf(ss / (float)D + eps);
+  for (int j = threadIdx.x * 4; j < D; j += blockDim.x * 4) {
+    float4 v = *reinterpret_cast<const float4 *>(xr + j);
+    float o[4] = {v.x * inv, v.y * inv, v.z * inv, v.w * inv};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (w) o[e] *= 1.f + w[j + e];
+      else o[e] = o[e] * (1.f + ms[j + e]) + mb[j + e];
+    }
+    __nv_bfloat162 a = __floats2bfloat162_rn(o[0], o[1]), b = __floats2bfloat162_rn(o[2], o[3]);
+    *reinterpret_cast<__nv_bfloat162 *>(yr + j) = a;
+    *reinterpret_cast<__nv_bfloat162 *>(yr + j + 2) = b;
+  }
+}
+
+void rmsnorm(const float *x, int ldx, bf16 *y, int ldy, const float *w, const float *ms,
+             const float *mb, int rows, int D, float eps, cudaStream_t st) {
+  if (rows <= 0) return;
+  rmsnorm_kernel<<<rows, 256, 0, st>>>(x, ldx, y, ldy, w, ms, mb, D, eps);
+  OXY_LAUNCH_CHECK();
+}
+
+__global__ void layernorm_kernel(const float *x, int ldx, bf16 *y, int ldy, const float *w,
+                                 const float *b, int D, float eps) {
+  __shared__ float red[32];
+  const float *xr = x + (size_t)blockIdx.x * ldx;
+  bf16 *yr = y + (size_t)blockIdx.x * ldy;
+  float s = 0.f;
+  for (int j = threadIdx.x; j < D; j += blockDim.x) s += xr[j];
+  const float mean = block_sum(s, red) / (float)D;
+  float v = 0.f;
+  for (int j = threadIdx.x; j < D; j += blockDim.x) {
+    float d = xr[j] - mean;
+    v += d * d;
+  }
+  const float rstd = rsqrtf(block_sum(v, red) / (float)D + eps);
+  for (int j = threadIdx.x; j < D; j += blockDim.x)
+    yr[j] = __float2bfloat16((xr[j] - mean) * rstd * w[j] + b[j]);
+}
+
+void layernorm(const float *x, int ldx, bf16 *y, int ldy, const float *w, const float *b, int rows,
+               int D, float eps, cudaStream_t st) {
+  if (rows <= 0) return;
+  layernorm_kernel<<<rows, 256, 0, st>>>(x, ldx, y, ldy, w, b, D, eps);
+  OXY_LAUNCH_CHECK();
+}
+
+__global__ void embed_kernel(float *x, int ldx, const bf16 *table, const int *tok,
+                             const int *active, int D, float scale) {
+  const int r = blockIdx.x;
+  if (active && !active[r]) return;
+  const bf16 *row = table + (size_t)tok[r] * D;
+  for (int j = threadIdx.x; j < D; j += blockDim.x)
+    x[(size_t)r * ldx + j] = __bfloat162float(row[j]) * scale;
+}
+
+void embed_rows(float *x, int ldx, const bf16 *table, const int *tok, const int *active, int rows,
+                int D, float scale, cudaStream_t st) {
+  if (rows <= 0) return;
+  embed_kernel<<<rows, 256, 0, st>>>(x, ldx, table, tok, active, D, scale);
+  OXY_LAUNCH_CHECK();
+}
+
+// One CTA per token; thread i < 128 owns rotary pair (i, i+128) of every head.
+__global__ void rope_split_kernel(const float *qkv, int n_qh, const int *pos, const int *slot,
+                                  const int *active, bf16 *q_out, bf16 *kpool, bf16 *vpool,
+                                  bf16 *k_dense, bf16 *v_dense, float theta) {
+  const int t = blockIdx.x;
+  if (active && !active[t]) return;
+  const int ld = (n_qh + 2) * HEAD_DIM;
+  const float *row = qkv + (size_t)t * ld;
+  const int i = threadIdx.x;  // 0..127
+  const float inv = (float)pow((double)theta, -2.0 * (double)i / (double)HEAD_DIM);
+  float sn, cs;
+  sincosf((float)pos[t] * inv, &sn, &cs);
+  const int s = slot ? slot[t] : -1;
+  bf16 *kdst = s >= 0 ? kpool + (size_t)s * HEAD_DIM : (k_dense ? k_dense + (size_t)t * HEAD_DIM : nullptr);
+  bf16 *vdst = s >= 0 ? vpool + (size_t)s * HEAD_DIM : (v_dense ? v_dense + (size_t)t * HEAD_DIM : nullptr);
+  for (int h = 0; h <= n_qh; ++h) {
+    const float *src = row + h * HEAD_DIM;
+    const float x1 = src[i], x2 = src[i + 128];
+    const float o1 = x1 * cs - x2 * sn, o2 = x2 * cs + x1 * sn;
+    bf16 *dst = h < n_qh ? q_out + (size_t)t * n_qh * HEAD_DIM + h * HEAD_DIM : kdst;
+    if (dst) {
+      dst[i] = __float2bfloat16(o1);
+      dst[i + 128] = __float2bfloat16(o2);
+    }
+  }
+  if (vdst) {
+    const float *src = row + (n_qh + 1) * HEAD_DIM;
+    vdst[i] = __float2bfloat16(src[i]);
+    vdst[i + 128] = __float2bfloat16(src[i + 128]);
+  }
+}
+
+void rope_split(const float *qkv, int T, int n_qh, const int *pos, const int *slot,
+                const int *active, bf16 *q_out, bf16 *kpool, bf16 *vpool, bf16 *k_dense,
+                bf16 *v_dense, float theta, cudaStream_t st) {
+  if (T <= 0) return;
+  rope_split_kernel<<<T, 128, 0, st>>>(qkv, n_qh, pos, slot, active, q_out, kpool, vpool, k_dense,
+                                       v_dense, theta);
+  OXY_LAUNCH_CHECK();
+}
+
+__global__ void patchify_kernel(const uint8_t *img, bf16 *patches, int kpad) {
+  const int p = blockIdx.x;  // image * 256 + patch
+  const int im = p >> 8, py = (p & 255) >> 4, px = p & 15;
+  const uint8_t *base = img + (size_t)im * 224 * 224 * 3;
+  for (int e = threadIdx.x; e < kpad; e += blockDim.x) {
+    float v = 0.f;
+    if (e < 588) {
+      const int dy = e / 42, rem = e % 42, dx = rem / 3, c = rem % 3;
+      const int y = py * 14 + dy, x = px * 14 + dx;
+      v = (float)base[((size_t)y * 224 + x) * 3 + c] / 127.5f - 1.f;
+    }
+    patches[(size_t)p * kpad + e] = __float2bfloat16(v);
+  }
+}
+
+void patchify(const uint8_t *img, int n, bf16 *patches, int kpad, cudaStream_t st) {
+  if (n <= 0) return;
+  patchify_kernel<<<n * 256, 128, 0, st>>>(img, patches, kpad);
+  OXY_LAUNCH_CHECK();
+}
+
+__global__ void tile_rows_kernel(float *dst, int ld, const float *src, int ld_src, int period, int D) {
+  const int r = blockIdx.x;
+  const float *s = src + (size_t)(r % period) * ld_src;
+  for (int j = threadIdx.x; j < D; j += blockDim.x) dst[(size_t)r * ld + j] = s[j];
+}
+
+void tile_rows(float *dst, int ld, const float *src, int ld_src, int rows, int period, int D,
+               cudaStream_t st) {
+  if (rows <= 0) return;
+  tile_rows_kernel<<<rows, 256, 0, st>>>(dst, ld, src, ld_src, period, D);
+  OXY_LAUNCH_CHECK();
+}
+
+__global__ void f32_to_bf16_kernel(const float *x, bf16 *y, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = __float2bfloat16(x[i]);
+}
+
+void f32_to_bf16(const float *x, bf16 *y, int64_t n, cudaStream_t st) {
+  if (n <= 0) return;
+  f32_to_bf16_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, st>>>(x, y, n);
+  OXY_LAUNCH_CHECK();
+}
+
+__global__ void euler_kernel(float *a, const float *v, bf16 *ab, int64_t n, float dt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float x = a[i] + dt * v[i];
+    a[i] = x;
+    ab[i] = __float2bfloat16(x);
+  }
+}
+
+void euler_step(float *a, const float *v, bf16 *ab, int64_t n, float dt, cudaStream_t st) {
+  euler_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 1024), 256, 0, st>>>(a, v, ab, n, dt);
+  OXY_LAUNCH_CHECK();
+}
+
+// Box-Muller on consecutive splitmix64 uniforms: pair i uses draws 2i, 2i+1.
+__global__ void noise_kernel(float *out, int64_t n, uint64_t seed) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; 2 * i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double u1 = splitmix_uniform(seed, 2 * i), u2 = splitmix_uniform(seed, 2 * i + 1);
+    double r = sqrt(-2.0 * log(1.0 - u1)), th = 6.283185307179586 * u2;
+    out[2 * i] = (float)(r * cos(th));
+    if (2 * i + 1 < n) out[2 * i + 1] = (float)(r * sin(th));
+  }
+}
+
+void normal_noise(float *out, int64_t n, uint64_t seed, cudaStream_t st) {
+  noise_kernel<<<(unsigned)std::min<int64_t>((n / 2 + 256) / 256, 1024), 256, 0, st>>>(out, n, seed);
+  OXY_LAUNCH_CHECK();
+}
+
+__global__ void init_bf16_kernel(bf16 *out, int64_t n, uint64_t seed, uint64_t offset, float bound) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double u = splitmix_uniform(seed, offset + (uint64_t)i);
+    out[i] = __float2bfloat16((float)((2.0 * u - 1.0) * (double)bound));
+  }
+}
+
+void init_uniform_bf16(bf16 *out, int64_t n, uint64_t seed, uint64_t offset, float bound, cudaStream_t st) {
+  init_bf16_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 64), 256, 0, st>>>(out, n, seed, offset, bound);
+  OXY_LAUNCH_CHECK();
+}
+
+__global__ void init_f32_kernel(float *out, int64_t n, uint64_t seed, uint64_t offset, float bound, float center) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double u = splitmix_uniform(seed, offset + (uint64_t)i);
+    out[i] = (float)((double)center + (2.0 * u - 1.0) * (double)bound);
+  }
+}
+
+void init_uniform_f32(float *out, int64_t n, uint64_t seed, uint64_t offset, float bound, float center,
+                      cudaStream_t st) {
+  init_f32_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, st>>>(out, n, seed, offset, bound, center);
+  OXY_LAUNCH_CHECK();
+}
+
+__global__ void cow_kernel(bf16 *pool, const int *cow, size_t layer_stride, size_t kv_stride) {
+  const int r = blockIdx.x, l = blockIdx.y;
+  const int src = cow[r * 3], dst = cow[r * 3 + 1], n = cow[r * 3 + 2];
+  if (src < 0) return;
+  const size_t elems = (size_t)n * HEAD_DIM / 8;  // int4 chunks
+  for (int kv = 0; kv < 2; ++kv) {
+    const int4 *s = reinterpret_cast<const int4 *>(pool + l * layer_stride + kv * kv_stride +
+                                                   (size_t)src * KV_BLOCK * HEAD_DIM);
+    int4 *d = reinterpret_cast<int4 *>(pool + l * layer_stride + kv * kv_stride +
+                                       (size_t)dst * KV_BLOCK * HEAD_DIM);
+    for (size_t i = threadIdx.x; i < elems; i += blockDim.x) d[i] = s[i];
+  }
+}
+
+void cow_blocks(bf16 *pool, const int *cow, int rows, int L, size_t layer_stride, size_t kv_stride,
+                cudaStream_t st) {
+  if (rows <= 0) return;
+  cow_kernel<<<dim3(rows, L), 256, 0, st>>>(pool, cow, layer_stride, kv_stride);
+  OXY_LAUNCH_CHECK();
+}
+
+__global__ void next_slot_kernel(int *slot, const int *pos, const int *active, const int *bt,
+                                 int bt_stride, int rows) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  if (!active[r]) { slot[r] = -1; return; }
+  const int p = pos[r];
+  slot[r] = bt[(size_t)r * bt_stride + p / KV_BLOCK] * KV_BLOCK + p % KV_BLOCK;
+}
+
+void next_slots(int *slot, const int *pos, const int *active, const int *bt, int bt_stride, int rows,
+                cudaStream_t st) {
+  next_slot_kernel<<<(rows + 127) / 128, 128, 0, st>>>(slot, pos, active, bt, bt_stride, rows);
+  OXY_LAUNCH_CHECK();
+}
+
+// ============================================================ flash attention
+
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t &r0, uint32_t &r1, uint32_t &r2, uint32_t &r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t &r0, uint32_t &r1, uint32_t &r2, uint32_t &r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+__device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t *>(&v);
+}
+
+constexpr int FA_BQ = 64;  // query rows per CTA (4 warps x 16)
+constexpr int FA_BK = 64;  // keys per tile (= KV_BLOCK)
+
+template <int HD>
+struct FaCfg {
+  static constexpr int HDP = (HD + 15) / 16 * 16;  // padded to the MMA K step
+  static constexpr int LDS = HDP + 8;               // +16 B: conflict-free ldmatrix
+  static constexpr int CHUNKS = HD / 8;             // 16-byte chunks holding data
+  static constexpr int PCHUNKS = HDP / 8;
+  static constexpr int TILE = FA_BQ * LDS;          // elements per smem tile
+  static constexpr size_t SMEM = (size_t)5 * TILE * sizeof(bf16);
+};
+
+// Stage one 64-row tile (rows from `row_ptr(r)` or zero) into smem via cp.async.
+template <int HD>
+__device__ __forceinline__ void load_tile(bf16 *dst, const bf16 *base, int ld, int nrows_valid,
+                                          const int *map_block, int key0) {
+  using C = FaCfg<HD>;
+  for (int idx = threadIdx.x; idx < FA_BQ * C::PCHUNKS; idx += blockDim.x) {
+    const int r = idx / C::PCHUNKS, ch = idx % C::PCHUNKS;
+    bf16 *d = dst + r * C::LDS + ch * 8;
+    if (r < nrows_valid && ch < C::CHUNKS) {
+      const bf16 *src;
+      if (map_block) src = base + ((size_t)map_block[0] * KV_BLOCK + r) * HD + ch * 8;
+      else src = base + (size_t)(key0 + r) * ld + ch * 8;
+      cp_async16(smem_addr(d), src);
+    } else {
+      *reinterpret_cast<int4 *>(d) = make_int4(0, 0, 0, 0);
+    }
+  }
+}
+
+template <int HD>
+__global__ void __launch_bounds__(128)
+    flash_attn_kernel(const AttnGroup *groups, int max_q_tiles, const bf16 *kpool, const bf16 *vpool,
+                      float scale_log2, int splits, float *ws_o, float *ws_ml, int ws_rows) {
+  using C = FaCfg<HD>;
+  constexpr int NT = C::HDP / 8;  // output n-tiles per warp
+  extern __shared__ __align__(16) unsigned char fa_smem[];
+  bf16 *sQ = reinterpret_cast<bf16 *>(fa_smem);
+  bf16 *sK[2] = {sQ + C::TILE, sQ + 2 * C::TILE};
+  bf16 *sV[2] = {sQ + 3 * C::TILE, sQ + 4 * C::TILE};
+
+  const AttnGroup g = groups[blockIdx.x / max_q_tiles];
+  const int qt = blockIdx.x % max_q_tiles;
+  const int q0 = qt * FA_BQ;
+  if (q0 >= g.nq) return;
+  const int split = blockIdx.y;
+  const int ta = (g.nka + FA_BK - 1) / FA_BK, tb = (g.nkb + FA_BK - 1) / FA_BK;
+  const int tiles = ta + tb;
+  const int per = (tiles + splits - 1) / splits;
+  const int t_begin = split * per, t_end = min(tiles, t_begin + per);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  auto issue_tile = [&](int ti, int buf) {
+    if (ti < ta) {
+      const int nvalid = min(FA_BK, g.nka - ti * FA_BK);
+      load_tile<HD>(sK[buf], kpool, HD, nvalid, g.bt + ti, 0);
+      load_tile<HD>(sV[buf], vpool, HD, nvalid, g.bt + ti, 0);
+    } else {
+      const int j0 = (ti - ta) * FA_BK;
+      const int nvalid = min(FA_BK, g.nkb - j0);
+      load_tile<HD>(sK[buf], g.kb, g.ldkv, nvalid, nullptr, j0);
+      load_tile<HD>(sV[buf], g.vb, g.ldkv, nvalid, nullptr, j0);
+    }
+    cp_commit();
+  };
+
+  // Q tile
+  load_tile<HD>(sQ, g.q, g.ldq, min(FA_BQ, g.nq - q0), nullptr, q0);
+  cp_commit();
+  if (t_begin < t_end) issue_tile(t_begin, 0);
+
+  float o[NT][4];
+#pragma unroll
+  for (int i = 0; i < NT; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float m_r[2] = {-INFINITY, -INFINITY}, l_r[2] = {0.f, 0.f};
+  const uint32_t q_base = smem_addr(sQ + (warp * 16 + (lane & 15)) * C::LDS + (lane >> 4) * 8);
+
+  for (int ti = t_begin; ti < t_end; ++ti) {
+    const int buf = (ti - t_begin) & 1;
+    if (ti + 1 < t_end) {
+      issue_tile(ti + 1, buf ^ 1);
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
+    }
+    __syncthreads();
+    const int nvalid = ti < ta ? min(FA_BK, g.nka - ti * FA_BK) : min(FA_BK, g.nkb - (ti - ta) * FA_BK);
+
+    // S = Q K^T : 16 x 64 per warp
+    float s[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s[i][0] = s[i][1] = s[i][2] = s[i][3] = 0.f;
+    const bf16 *kt = sK[buf];
+#pragma unroll
+    for (int kk = 0; kk < C::HDP / 16; ++kk) {
+      uint32_t a0, a1, a2, a3;
+      ldsm_x4(q_base + kk * 32, a0, a1, a2, a3);
+#pragma unroll
+      for (int np = 0; np < 4; ++np) {
+        const int key = np * 16 + (lane & 7) + ((lane >> 4) << 3);
+        const int col = kk * 16 + ((lane >> 3) & 1) * 8;
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4(smem_addr(kt + key * C::LDS + col), b0, b1, b2, b3);
+        mma16816(s[2 * np], a0, a1, a2, a3, b0, b1);
+        mma16816(s[2 * np + 1], a0, a1, a2, a3, b2, b3);
+      }
+    }
+    // mask + online softmax (rows g and g+8 of this warp)
+    float mx[2] = {m_r[0], m_r[1]};
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int key = nt * 8 + (lane & 3) * 2 + (e & 1);
+        float v = s[nt][e] * scale_log2;
+        if (key >= nvalid) v = -INFINITY;
+        s[nt][e] = v;
+        mx[e >> 1] = fmaxf(mx[e >> 1], v);
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 1));
+      mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 2));
+    }
+    float corr[2], rs[2] = {0.f, 0.f};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) corr[h] = (mx[h] == -INFINITY) ? 1.f : exp2f(m_r[h] - mx[h]);
+    uint32_t pa[4][4];
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float mref = mx[e >> 1];
+        const float p = (mref == -INFINITY) ? 0.f : exp2f(s[nt][e] - mref);
+        s[nt][e] = p;
+        rs[e >> 1] += p;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      pa[j][0] = pack_bf16(s[2 * j][0], s[2 * j][1]);
+      pa[j][1] = pack_bf16(s[2 * j][2], s[2 * j][3]);
+      pa[j][2] = pack_bf16(s[2 * j + 1][0], s[2 * j + 1][1]);
+      pa[j][3] = pack_bf16(s[2 * j + 1][2], s[2 * j + 1][3]);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      rs[h] += __shfl_xor_sync(0xffffffffu, rs[h], 1);
+      rs[h] += __shfl_xor_sync(0xffffffffu, rs[h], 2);
+      l_r[h] = l_r[h] * corr[h] + rs[h];
+      m_r[h] = mx[h];
+    }
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      o[nt][0] *= corr[0];
+      o[nt][1] *= corr[0];
+      o[nt][2] *= corr[1];
+      o[nt][3] *= corr[1];
+    }
+    // O += P V
+    const bf16 *vt = sV[buf];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int np = 0; np < NT / 2; ++np) {
+        const int key = j * 16 + (lane & 15);
+        const int col = np * 16 + (lane >> 4) * 8;
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4_t(smem_addr(vt + key * C::LDS + col), b0, b1, b2, b3);
+        mma16816(o[2 * np], pa[j][0], pa[j][1], pa[j][2], pa[j][3], b0, b1);
+        mma16816(o[2 * np + 1], pa[j][0], pa[j][1], pa[j][2], pa[j][3], b2, b3);
+      }
+    }
+    __syncthreads();
+  }
+
+  // epilogue
+  const int rbase = q0 + warp * 16 + (lane >> 2);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int r = rbase + h * 8;
+    if (r >= g.nq) continue;
+    if (splits == 1) {
+      const float inv = l_r[h] > 0.f ? 1.f / l_r[h] : 0.f;
+      bf16 *orow = g.o + (size_t)r * g.ldo;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int c = nt * 8 + (lane & 3) * 2;
+        if (c < HD)
+          *reinterpret_cast<__nv_bfloat162 *>(orow + c) =
+              __floats2bfloat162_rn(o[nt][2 * h] * inv, o[nt][2 * h + 1] * inv);
+      }
+    } else {
+      const size_t wr = (size_t)split * ws_rows + g.wrow0 + r;
+      float *orow = ws_o + wr * C::HDP;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int c = nt * 8 + (lane & 3) * 2;
+        orow[c] = o[nt][2 * h];
+        orow[c + 1] = o[nt][2 * h + 1];
+      }
+      if ((lane & 3) == 0) {
+        ws_ml[wr * 2] = m_r[h];
+        ws_ml[wr * 2 + 1] = l_r[h];
+      }
+    }
+  }
+}
+
+// Combine split-KV partials in split order (log2 domain).
+template <int HD>
+__global__ void fa_merge_kernel(const AttnGroup *groups, int max_rows, int splits, const float *ws_o,
+                                const float *ws_ml, int ws_rows) {
+  using C = FaCfg<HD>;
+  const AttnGroup g = groups[blockIdx.y];
+  const int r = blockIdx.x;
+  if (r >= g.nq) return;
+  float M = -INFINITY;
+  for (int s = 0; s < splits; ++s) M = fmaxf(M, ws_ml[((size_t)s * ws_rows + g.wrow0 + r) * 2]);
+  float L = 0.f;
+  for (int s = 0; s < splits; ++s) {
+    const size_t wr = (size_t)s * ws_rows + g.wrow0 + r;
+    const float m = ws_ml[wr * 2];
+    if (m != -INFINITY) L += ws_ml[wr * 2 + 1] * exp2f(m - M);
+  }
+  for (int c = threadIdx.x; c < HD; c += blockDim.x) {
+    float acc = 0.f;
+    for (int s = 0; s < splits; ++s) {
+      const size_t wr = (size_t)s * ws_rows + g.wrow0 + r;
+      const float m = ws_ml[wr * 2];
+      if (m != -INFINITY) acc += ws_o[wr * C::HDP + c] * exp2f(m - M);
+    }
+    g.o[(size_t)r * g.ldo + c] = __float2bfloat16(L > 0.f ? acc / L : 0.f);
+  }
+}
+
+template <int HD>
+static void flash_launch(const AttnGroup *groups_d, int n_groups, int max_q_tiles, const bf16 *kpool,
+                         const bf16 *vpool, float scale, int splits, float *ws_o, float *ws_ml,
+                         int ws_rows, cudaStream_t st) {
+  using C = FaCfg<HD>;
+  static bool attr = false;
+  if (!attr) {
+    OXY_CUDA(cudaFuncSetAttribute(flash_attn_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)C::SMEM));
+    attr = true;
+  }
+  const float scale_log2 = scale * 1.4426950408889634f;
+  dim3 grid(n_groups * max_q_tiles, splits);
+  flash_attn_kernel<HD><<<grid, 128, C::SMEM, st>>>(groups_d, max_q_tiles, kpool, vpool, scale_log2,
+                                                    splits, ws_o, ws_ml, ws_rows);
+  OXY_LAUNCH_CHECK();
+  if (splits > 1) {
+    fa_merge_kernel<HD><<<dim3(max_q_tiles * FA_BQ, n_groups), 128, 0, st>>>(groups_d, max_q_tiles * FA_BQ,
+                                                                             splits, ws_o, ws_ml, ws_rows);
+    OXY_LAUNCH_CHECK();
+  }
+}
+
+void flash_attention(const AttnGroup *groups_d, int n_groups, int max_q_tiles, int head_dim,
+                     const bf16 *kpool, const bf16 *vpool, float scale, int splits, int max_key_tiles,
+                     float *ws_o, float *ws_ml, int ws_rows, cudaStream_t st) {
+  (void)max_key_tiles;
+  if (n_groups <= 0 || max_q_tiles <= 0) return;
+  if (head_dim == 256)
+    flash_launch<256>(groups_d, n_groups, max_q_tiles, kpool, vpool, scale, splits, ws_o, ws_ml, ws_rows, st);
+  else if (head_dim == 72)
+    flash_launch<72>(groups_d, n_groups, max_q_tiles, kpool, vpool, scale, splits, ws_o, ws_ml, ws_rows, st);
+  else
+    fail(OXY_EINVAL, "flash_attention: unsupported head_dim %d", head_dim);
+}
+
+// ============================================================ decode attention
+
+// CTA = (row, key block).  8 warps; warp w scores keys 8w..8w+7 of the block
+// for all 8 query heads (16-byte vector loads: lane holds 8 dims of a key),
+// then warp h runs the softmax of head h and all 256 threads do P.V with one
+// output dim each (coalesced 512-byte V rows).  Partials merged in order.
+constexpr int DA_THREADS = 256;
+constexpr int DA_PART = Q_HEADS * (HEAD_DIM + 2);
+
+__global__ void __launch_bounds__(DA_THREADS)
+    decode_attn_kernel(const bf16 *q, const bf16 *kpool, const bf16 *vpool, const int *bt, int bt_stride,
+                       const int *pos, const int *active, int max_blocks, float scale_log2, float *ws) {
+  __shared__ float qs[Q_HEADS][HEAD_DIM];
+  __shared__ float sc[Q_HEADS][KV_BLOCK];
+  __shared__ float mh[Q_HEADS], lh[Q_HEADS];
+  const int r = blockIdx.x, blk = blockIdx.y;
+  if (active && !active[r]) return;
+  const int n_keys = pos[r] + 1;
+  const int k0 = blk * KV_BLOCK;
+  float *part = ws + ((size_t)r * max_blocks + blk) * DA_PART;
+  if (k0 >= n_keys) return;
+  const int nvalid = min(KV_BLOCK, n_keys - k0);
+  const int b = bt[(size_t)r * bt_stride + blk];
+  const bf16 *kb = kpool + (size_t)b * KV_BLOCK * HEAD_DIM;
+  const bf16 *vb = vpool + (size_t)b * KV_BLOCK * HEAD_DIM;
+  for (int i = threadIdx.x; i < Q_HEADS * HEAD_DIM; i += DA_THREADS)
+    qs[i / HEAD_DIM][i % HEAD_DIM] = __bfloat162float(q[(size_t)r * Q_HEADS * HEAD_DIM + i]);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float qreg[Q_HEADS][8];
+#pragma unroll
+  for (int h = 0; h < Q_HEADS; ++h)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) qreg[h][e] = qs[h][lane * 8 + e];
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) {
+    const int j = warp * 8 + kk;
+    float acc[Q_HEADS];
+#pragma unroll
+    for (int h = 0; h < Q_HEADS; ++h) acc[h] = 0.f;
+    if (j < nvalid) {
+      const int4 raw = *reinterpret_cast<const int4 *>(kb + (size_t)j * HEAD_DIM + lane * 8);
+      const bf16 *kv = reinterpret_cast<const bf16 *>(&raw);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float kf = __bfloat162float(kv[e]);
+#pragma unroll
+        for (int h = 0; h < Q_HEADS; ++h) acc[h] = fmaf(qreg[h][e], kf, acc[h]);
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < Q_HEADS; ++h) {
+      const float v = warp_sum(acc[h]);
+      if (lane == 0) sc[h][j] = j < nvalid ? v * scale_log2 : -INFINITY;
+    }
+  }
+  __syncthreads();
+  {  // softmax of head `warp` over this block (2 keys per lane)
+    const int h = warp;
+    const float s0 = sc[h][lane], s1 = sc[h][lane + 32];
+    const float m = warp_max(fmaxf(s0, s1));
+    const float p0 = s0 == -INFINITY ? 0.f : exp2f(s0 - m), p1 = s1 == -INFINITY ? 0.f : exp2f(s1 - m);
+    sc[h][lane] = p0;
+    sc[h][lane + 32] = p1;
+    const float l = warp_sum(p0 + p1);
+    if (lane == 0) { mh[h] = m; lh[h] = l; }
+  }
+  __syncthreads();
+  const int d = threadIdx.x;  // one output dim per thread
+  float acc[Q_HEADS];
+#pragma unroll
+  for (int h = 0; h < Q_HEADS; ++h) acc[h] = 0.f;
+  for (int j = 0; j < nvalid; ++j) {
+    const float vf = __bfloat162float(vb[(size_t)j * HEAD_DIM + d]);
+#pragma unroll
+    for (int h = 0; h < Q_HEADS; ++h) acc[h] = fmaf(sc[h][j], vf, acc[h]);
+  }
+#pragma unroll
+  for (int h = 0; h < Q_HEADS; ++h) part[h * (HEAD_DIM + 2) + d] = acc[h];
+  if (d < Q_HEADS) {
+    part[d * (HEAD_DIM + 2) + HEAD_DIM] = mh[d];
+    part[d * (HEAD_DIM + 2) + HEAD_DIM + 1] = lh[d];
+  }
+}
+
+__global__ void decode_merge_kernel(const float *ws, bf16 *out, const int *pos, const int *active,
+                                    int max_blocks) {
+  const int r = blockIdx.x, h = blockIdx.y, d = threadIdx.x;
+  if (active && !active[r]) return;
+  const int nb = (pos[r] + 1 + KV_BLOCK - 1) / KV_BLOCK;
+  const float *base = ws + (size_t)r * max_blocks * DA_PART + h * (HEAD_DIM + 2);
+  float M = -INFINITY;
+  for (int b = 0; b < nb; ++b) M = fmaxf(M, base[(size_t)b * DA_PART + HEAD_DIM]);
+  float L = 0.f, acc = 0.f;
+  for (int b = 0; b < nb; ++b) {
+    const float *p = base + (size_t)b * DA_PART;
+    const float w = exp2f(p[HEAD_DIM] - M);
+    L += p[HEAD_DIM + 1] * w;
+    acc += p[d] * w;
+  }
+  out[(size_t)r * Q_HEADS * HEAD_DIM + h * HEAD_DIM + d] = __float2bfloat16(acc / L);
+}
+
+void decode_attention(const bf16 *q, bf16 *out, const bf16 *kpool, const bf16 *vpool, const int *bt,
+                      int bt_stride, const int *pos, const int *active, int rows, int max_blocks,
+                      float scale, float *ws, cudaStream_t st) {
+  if (rows <= 0) return;
+  const float sl2 = scale * 1.4426950408889634f;
+  decode_attn_kernel<<<dim3(rows, max_blocks), DA_THREADS, 0, st>>>(q, kpool, vpool, bt, bt_stride, pos,
+                                                                    active, max_blocks, sl2, ws);
+  OXY_LAUNCH_CHECK();
+  decode_merge_kernel<<<dim3(rows, Q_HEADS), HEAD_DIM, 0, st>>>(ws, out, pos, active, max_blocks);
+  OXY_LAUNCH_CHECK();
+}
+
+// ============================================================ argmax
+
+constexpr int AM_CHUNKS = 64;
+
+__device__ __forceinline__ void better(float &bv, int &bi, float v, int i) {
+  if (v > bv || (v == bv && i < bi)) { bv = v; bi = i; }
+}
+
+__global__ void argmax_partial_kernel(const float *logits, int V, const int *active, float *pv, int *pi) {
+  __shared__ float sv[32];
+  __shared__ int si[32];
+  const int r = blockIdx.x, c = blockIdx.y;
+  if (active && !active[r]) return;
+  const int per = (V + AM_CHUNKS - 1) / AM_CHUNKS;
+  const int j0 = c * per, j1 = min(V, j0 + per);
+  const float *lg = logits + (size_t)r * V;
+  float bv = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) better(bv, bi, lg[j], j);
+  for (int o = 16; o > 0; o >>= 1) {
+    float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    better(bv, bi, ov, oi);
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) { sv[w] = bv; si[w] = bi; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < (int)(blockDim.x >> 5); ++i) better(bv, bi, sv[i], si[i]);
+    pv[r * AM_CHUNKS + c] = bv;
+    pi[r * AM_CHUNKS + c] = bi;
+  }
+}
+
+__global__ void argmax_final_kernel(int rows, const float *pv, const int *pi, int step, int k, int eos,
+                                    int *active, int *tok, int *pos, int *count, const int *budget,
+                                    int *out_tokens, int *plain_out) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  if (active && !active[r]) return;
+  float bv = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int c = 0; c < AM_CHUNKS; ++c) better(bv, bi, pv[r * AM_CHUNKS + c], pi[r * AM_CHUNKS + c]);
+  if (bi == 0x7fffffff) bi = 0;
+  if (plain_out) { plain_out[r] = bi; return; }
+  out_tokens[(size_t)r * k + step] = bi;
+  tok[r] = bi;
+  pos[r] += 1;
+  const int c = ++count[r];
+  if (bi == eos || c == budget[r]) active[r] = 0;
+}
+
+void argmax_update(const float *logits, int rows, int V, int step, int k, int eos, int *active, int *tok,
+                   int *pos, int *count, const int *budget, int *out_tokens, float *pv, int *pi,
+                   cudaStream_t st) {
+  argmax_partial_kernel<<<dim3(rows, AM_CHUNKS), 256, 0, st>>>(logits, V, active, pv, pi);
+  OXY_LAUNCH_CHECK();
+  argmax_final_kernel<<<(rows + 63) / 64, 64, 0, st>>>(rows, pv, pi, step, k, eos, active, tok, pos, count,
+                                                       budget, out_tokens, nullptr);
+  OXY_LAUNCH_CHECK();
+}
+
+void argmax_rows(const float *logits, int rows, int V, int *out, float *pv, int *pi, cudaStream_t st) {
+  argmax_partial_kernel<<<dim3(rows, AM_CHUNKS), 256, 0, st>>>(logits, V, nullptr, pv, pi);
+  OXY_LAUNCH_CHECK();
+  argmax_final_kernel<<<(rows + 63) / 64, 64, 0, st>>>(rows, pv, pi, 0, 1, -1, nullptr, nullptr, nullptr,
+                                                       nullptr, nullptr, nullptr, out);
+  OXY_LAUNCH_CHECK();
+}
+
+}  // namespace pi05
+}  // namespace oxy
+
+extern "C" int oxy_paged_decode_attention(const void *q_d, void *out_d, const void *kpool_d,
+                                          const void *vpool_d, const int32_t *bt_d, int32_t bt_stride,
+                                          const int32_t *pos_d, int32_t rows, int32_t max_blocks,
+                                          float *ws_d, void *stream) {
+  OXY_API_BEGIN
+  OXY_REQUIRE(rows >= 1 && max_blocks >= 1 && bt_stride >= max_blocks, "bad decode-attention shape");
+  using oxy::pi05::bf16;
+  oxy::pi05::decode_attention(static_cast<const bf16 *>(q_d), static_cast<bf16 *>(out_d),
+                              static_cast<const bf16 *>(kpool_d), static_cast<const bf16 *>(vpool_d), bt_d,
+                              bt_stride, pos_d, nullptr, rows, max_blocks, 1.f / 16.f, ws_d,
+                              oxy::as_stream(stream));
+  OXY_API_END
+}

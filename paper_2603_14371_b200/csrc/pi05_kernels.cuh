@@ -1,0 +1,90 @@
+// F2 (pi0.5-shaped) kernels other than the GEMM.  See pi05_kernels.cu.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace oxy {
+namespace pi05 {
+
+using bf16 = __nv_bfloat16;
+
+constexpr int KV_BLOCK = 64;   // pool block size (positions) = one attention key tile
+constexpr int HEAD_DIM = 256;  // Gemma head dim (pool row)
+constexpr int Q_HEADS = 8;     // Gemma query heads per KV head (MQA)
+
+// ---- norms / elementwise --------------------------------------------------
+// y[r] = bf16( x[r] * rsqrt(mean(x[r]^2) + eps) * (1 + w) )            (w != null)
+//      = bf16( x[r] * rsqrt(...) * (1 + mod_scale) + mod_shift )       (adaRMS)
+void rmsnorm(const float *x, int ldx, bf16 *y, int ldy, const float *w, const float *mod_scale,
+             const float *mod_shift, int rows, int D, float eps, cudaStream_t st);
+// y[r] = bf16( (x - mean) * rstd * w + b )
+void layernorm(const float *x, int ldx, bf16 *y, int ldy, const float *w, const float *b, int rows,
+               int D, float eps, cudaStream_t st);
+// x[r] = float(table[tok[r]]) * scale (rows with active[r]==0 skipped if active)
+void embed_rows(float *x, int ldx, const bf16 *table, const int *tok, const int *active, int rows,
+                int D, float scale, cudaStream_t st);
+// RoPE on q (n_qh heads) and k from fp32 qkv [T, (n_qh+2)*256]; q -> q_out bf16 [T, n_qh*256];
+// k, v -> pool rows at slot[t] (layer base pointers) or dense rows (k_dense/v_dense, ld 256).
+void rope_split(const float *qkv, int T, int n_qh, const int *pos, const int *slot,
+                const int *active, bf16 *q_out, bf16 *kpool, bf16 *vpool, bf16 *k_dense,
+                bf16 *v_dense, float theta, cudaStream_t st);
+// images uint8 [n, 224, 224, 3] -> patches bf16 [n*256, kpad] (x/127.5 - 1, (dy,dx,c) order)
+void patchify(const uint8_t *img, int n, bf16 *patches, int kpad, cudaStream_t st);
+// dst[i*ld + j] = src[(i % period) * ld_src + j] (broadcast of per-image tables)
+void tile_rows(float *dst, int ld, const float *src, int ld_src, int rows, int period, int D,
+               cudaStream_t st);
+void f32_to_bf16(const float *x, bf16 *y, int64_t n, cudaStream_t st);
+// a += dt * v (fp32), and a_bf16 = bf16(a)
+void euler_step(float *a, const float *v, bf16 *a_bf, int64_t n, float dt, cudaStream_t st);
+// standard normal noise from splitmix64 (Box-Muller, counter form)
+void normal_noise(float *out, int64_t n, uint64_t seed, cudaStream_t st);
+// bf16 weights from splitmix64 counter: U(-bound, bound) in draw order starting at `offset`
+void init_uniform_bf16(bf16 *out, int64_t n, uint64_t seed, uint64_t offset, float bound,
+                       cudaStream_t st);
+void init_uniform_f32(float *out, int64_t n, uint64_t seed, uint64_t offset, float bound,
+                      float center, cudaStream_t st);
+// copy-on-write of shared tail blocks (cow[r] = {src, dst, n}) for all layers
+void cow_blocks(bf16 *pool, const int *cow, int rows, int L, size_t layer_stride,
+                size_t kv_stride, cudaStream_t st);
+// slot of each active row's next position
+void next_slots(int *slot, const int *pos, const int *active, const int *bt, int bt_stride,
+                int rows, cudaStream_t st);
+
+// ---- attention -------------------------------------------------------------
+struct AttnGroup {
+  const bf16 *q;   // query row r at q + r * ldq
+  bf16 *o;         // output row r at o + r * ldo
+  int ldq, ldo, nq;
+  const int *bt;   // segment A: paged keys [0, nka) through this block table
+  int nka;
+  const bf16 *kb, *vb;  // segment B: dense keys [0, nkb), row stride ldkv
+  int ldkv, nkb;
+  int wrow0;       // first workspace row of this group (split-KV)
+};
+
+// Bidirectional (prefix-LM / suffix / ViT) flash attention, mma.sync bf16.
+// head_dim 256 (paged allowed) or 72 (dense only).  splits > 1 uses ws.
+void flash_attention(const AttnGroup *groups_d, int n_groups, int max_q_tiles, int head_dim,
+                     const bf16 *kpool, const bf16 *vpool, float scale, int splits,
+                     int max_key_tiles, float *ws_o, float *ws_ml, int ws_rows, cudaStream_t st);
+
+// Paged decode attention: rows x 8 q-heads vs 1 KV head, keys [0, pos[r]].
+// q [rows, 8*256] bf16 -> out [rows, 8*256] bf16.  ws: rows*max_blocks*8*(256+2) floats.
+void decode_attention(const bf16 *q, bf16 *out, const bf16 *kpool, const bf16 *vpool,
+                      const int *bt, int bt_stride, const int *pos, const int *active, int rows,
+                      int max_blocks, float scale, float *ws, cudaStream_t st);
+
+// Greedy token + continuous-batching state update over logits [rows, V].
+// part: rows * 64 (val, idx) scratch.
+void argmax_update(const float *logits, int rows, int V, int step, int k, int eos, int *active,
+                   int *tok, int *pos, int *count, const int *budget, int *out_tokens,
+                   float *part_val, int *part_idx, cudaStream_t st);
+// plain argmax per row (prefill-free greedy checks)
+void argmax_rows(const float *logits, int rows, int V, int *out, float *part_val, int *part_idx,
+                 cudaStream_t st);
+
+}  // namespace pi05
+}  // namespace oxy

@@ -1,0 +1,719 @@
+// F2: pi0.5-shaped Mixture-of-Transformers VLA on the B200 (bf16, tcgen05).
+//
+// The reference models the action and language experts as one toy backbone
+// (kvweaver/backend.py:21-33); the paper's system is openpi pi0.5 (PAPER.md
+// 85-87).  This runtime implements the pi0.5 shape:
+//   * SigLIP So400m/14 vision tower, per camera, then a linear projection;
+//   * Gemma-2B prefix (RMSNorm(1+w), MQA 8q/1kv heads of 256, RoPE, GeGLU),
+//     prefix-LM bidirectional attention, K/V written ONCE into the unified
+//     paged pool through the block table (shared prefix prefill);
+//   * Gemma-300M action expert: flow-matching Euler from noise, adaRMS
+//     time conditioning with gated residuals, suffix queries attending to
+//     [paged prefix K/V of the same layer || suffix K/V] (cross-task sharing);
+//   * greedy language decode continuously batched over rows, K/V appended to
+//     the same pool, LM head + lowest-id argmax, per-row stop on device.
+// Weight values are the builder's choice (random init, stated in DESIGN.md):
+// splitmix64 counter draws, U(+-sqrt(3/fan_in)) for matrices.
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "cuda_util.cuh"
+#include "gemm_sm100.cuh"
+#include "pi05_kernels.cuh"
+
+
+namespace oxy {
+namespace pi05 {
+
+using gemm::EpiParams;
+
+struct Tensor {
+  std::string name;
+  int64_t rows, cols;
+  int dtype;  // 0 bf16, 1 f32
+  float bound, center;
+  uint64_t offset;
+  void *ptr;
+  int64_t numel() const { return rows * cols; }
+};
+
+struct LayerW {
+  float *ln1, *ln2;
+  bf16 *wqkv, *wo, *wgu, *wd;
+};
+struct ExpertW {
+  bf16 *wqkv, *wo, *wgu, *wd;
+};
+struct VitW {
+  float *ln1w, *ln1b, *ln2w, *ln2b, *bqkv, *bo, *b1, *b2;
+  bf16 *wqkv, *wo, *w1, *w2;
+};
+
+constexpr int PATCH_K = 640;  // 14*14*3 = 588 padded to a multiple of 64
+constexpr int QDIM = Q_HEADS * HEAD_DIM;
+constexpr int QKV = (Q_HEADS + 2) * HEAD_DIM;
+
+struct Model {
+  oxy_pi05_config c{};
+  int sms = 148;
+  std::vector<Tensor> tensors;
+  void *wmem = nullptr;
+  // handles into wmem
+  bf16 *embed = nullptr, *lm_head = nullptr;
+  float *final_norm = nullptr;
+  std::vector<LayerW> L;
+  std::vector<ExpertW> E;
+  std::vector<VitW> V;
+  bf16 *e_in, *e_out, *t1, *t2, *wmod, *vpatch, *vproj;
+  float *e_in_b, *e_out_b, *t1_b, *t2_b, *bmod, *vpatch_b, *vpos, *vln_w, *vln_b, *vproj_b;
+  int n_mod = 0;
+  // pool
+  bf16 *pool = nullptr;
+  int NB = 0;
+  size_t kv_stride = 0, layer_stride = 0;
+  // denoise constants
+  float *noise = nullptr;           // [H, A]
+  int mod_S = -1;
+  DevBuf mod;                        // [S, n_mod] f32
+  // scratch
+  DevBuf x, y, qkv, q, o, hmid, ws, ints, kd, vd, attn_groups, attn_ws, attn_ml, logits, amv, ami,
+      vit_h, vit_y, vit_qkv, vit_o, vit_m, patches, act, act_bf, vel, xe, dec_ws, host_img;
+  cudaEvent_t ev = nullptr;
+
+  bf16 *kpool(int l) { return pool + l * layer_stride; }
+  bf16 *vpool(int l) { return pool + l * layer_stride + kv_stride; }
+
+  ~Model() {
+    cudaFree(wmem);
+    cudaFree(pool);
+    cudaFree(noise);
+    for (DevBuf *b : {&mod, &x, &y, &qkv, &q, &o, &hmid, &ws, &ints, &kd, &vd, &attn_groups, &attn_ws,
+                      &attn_ml, &logits, &amv, &ami, &vit_h, &vit_y, &vit_qkv, &vit_o, &vit_m, &patches,
+                      &act, &act_bf, &vel, &xe, &dec_ws, &host_img})
+      b->release();
+  }
+
+  // ------------------------------------------------------------ weights
+  uint64_t next_offset = 0;
+  void add(const std::string &name, int64_t rows, int64_t cols, int dtype, float bound, float center = 0.f) {
+    Tensor t{name, rows, cols, dtype, bound, center, next_offset, nullptr};
+    next_offset += (uint64_t)(rows * cols);
+    tensors.push_back(t);
+  }
+  static float mat_bound(int64_t fan_in) { return (float)std::sqrt(3.0 / (double)fan_in); }
+  // action vectors are padded to 8 lanes so the in-projection's K stride is 16-byte aligned
+  int apad() const { return (c.action_dim + 7) / 8 * 8; }
+
+  void declare() {
+    const int W = c.width, We = c.expert_width, Dv = c.vit_width;
+    add("embed", c.vocab, W, 0, mat_bound(W));
+    for (int l = 0; l < c.depth; ++l) {
+      std::string p = "llm." + std::to_string(l) + ".";
+      add(p + "ln1", 1, W, 1, 0.1f);
+      add(p + "wqkv", QKV, W, 0, mat_bound(W));
+      add(p + "wo", W, QDIM, 0, mat_bound(QDIM));
+      add(p + "ln2", 1, W, 1, 0.1f);
+      add(p + "wgu", 2 * c.mlp, W, 0, mat_bound(W));
+      add(p + "wd", W, c.mlp, 0, mat_bound(c.mlp));
+    }
+    add("final_norm", 1, W, 1, 0.1f);
+    // untied LM head: with random weights a tied head echoes its input, so
+    // EOS-as-BOS (kvweaver/backend.py:30-32) would end every request at once
+    add("lm_head", c.vocab, W, 0, mat_bound(W));
+    for (int l = 0; l < c.depth; ++l) {
+      std::string p = "expert." + std::to_string(l) + ".";
+      add(p + "wqkv", QKV, We, 0, mat_bound(We));
+      add(p + "wo", We, QDIM, 0, mat_bound(QDIM));
+      add(p + "wgu", 2 * c.expert_mlp, We, 0, mat_bound(We));
+      add(p + "wd", We, c.expert_mlp, 0, mat_bound(c.expert_mlp));
+    }
+    n_mod = c.depth * 6 * We + 2 * We;
+    add("action_in", We, apad(), 0, mat_bound(c.action_dim));
+    add("action_in.b", 1, We, 1, 0.02f);
+    add("action_out", c.action_dim, We, 0, mat_bound(We));
+    add("action_out.b", 1, c.action_dim, 1, 0.02f);
+    add("time1", We, We, 0, mat_bound(We));
+    add("time1.b", 1, We, 1, 0.02f);
+    add("time2", We, We, 0, mat_bound(We));
+    add("time2.b", 1, We, 1, 0.02f);
+    add("mod", n_mod, We, 0, 0.1f * mat_bound(We));
+    add("mod.b", 1, n_mod, 1, 0.02f);
+    if (c.vit_depth > 0) {
+      add("vit.patch", Dv, PATCH_K, 0, mat_bound(588));
+      add("vit.patch.b", 1, Dv, 1, 0.02f);
+      add("vit.pos", 256, Dv, 1, 0.02f);
+      for (int l = 0; l < c.vit_depth; ++l) {
+        std::string p = "vit." + std::to_string(l) + ".";
+        add(p + "ln1.w", 1, Dv, 1, 0.1f, 1.f);
+        add(p + "ln1.b", 1, Dv, 1, 0.02f);
+        add(p + "wqkv", 3 * Dv, Dv, 0, mat_bound(Dv));
+        add(p + "bqkv", 1, 3 * Dv, 1, 0.02f);
+        add(p + "wo", Dv, Dv, 0, mat_bound(Dv));
+        add(p + "bo", 1, Dv, 1, 0.02f);
+        add(p + "ln2.w", 1, Dv, 1, 0.1f, 1.f);
+        add(p + "ln2.b", 1, Dv, 1, 0.02f);
+        add(p + "w1", c.vit_mlp, Dv, 0, mat_bound(Dv));
+        add(p + "b1", 1, c.vit_mlp, 1, 0.02f);
+        add(p + "w2", Dv, c.vit_mlp, 0, mat_bound(c.vit_mlp));
+        add(p + "b2", 1, Dv, 1, 0.02f);
+      }
+      add("vit.ln.w", 1, Dv, 1, 0.1f, 1.f);
+      add("vit.ln.b", 1, Dv, 1, 0.02f);
+      add("vit.proj", W, Dv, 0, mat_bound(Dv));
+      add("vit.proj.b", 1, W, 1, 0.02f);
+    }
+  }
+
+  void materialise(cudaStream_t st) {
+    size_t bytes = 0;
+    for (auto &t : tensors) {
+      bytes = (bytes + 255) / 256 * 256;
+      t.ptr = reinterpret_cast<void *>(bytes);
+      bytes += t.numel() * (t.dtype == 0 ? 2 : 4);
+    }
+    OXY_CUDA(cudaMalloc(&wmem, bytes));
+    for (auto &t : tensors) {
+      t.ptr = static_cast<char *>(wmem) + reinterpret_cast<size_t>(t.ptr);
+      if (t.dtype == 0)
+        init_uniform_bf16(static_cast<bf16 *>(t.ptr), t.numel(), c.seed, t.offset, t.bound, st);
+      else
+        init_uniform_f32(static_cast<float *>(t.ptr), t.numel(), c.seed, t.offset, t.bound, t.center, st);
+    }
+    {
+      Tensor &ai = find("action_in");
+      if (apad() > c.action_dim)
+        OXY_CUDA(cudaMemset2DAsync(static_cast<bf16 *>(ai.ptr) + c.action_dim, apad() * 2, 0,
+                                   (apad() - c.action_dim) * 2, ai.rows, st));
+    }
+    if (c.vit_depth > 0) {  // patch columns 588..639 multiply zero padding; keep them zero
+      Tensor &pt = find("vit.patch");
+      OXY_CUDA(cudaMemset2DAsync(static_cast<bf16 *>(pt.ptr) + 588, PATCH_K * 2, 0, (PATCH_K - 588) * 2,
+                                 pt.rows, st));
+    }
+    size_t i = 0;
+    auto nb = [&]() { return static_cast<bf16 *>(tensors[i++].ptr); };
+    auto nf = [&]() { return static_cast<float *>(tensors[i++].ptr); };
+    embed = nb();
+    for (int l = 0; l < c.depth; ++l) {
+      LayerW w;
+      w.ln1 = nf(); w.wqkv = nb(); w.wo = nb(); w.ln2 = nf(); w.wgu = nb(); w.wd = nb();
+      L.push_back(w);
+    }
+    final_norm = nf();
+    lm_head = nb();
+    for (int l = 0; l < c.depth; ++l) {
+      ExpertW w;
+      w.wqkv = nb(); w.wo = nb(); w.wgu = nb(); w.wd = nb();
+      E.push_back(w);
+    }
+    e_in = nb(); e_in_b = nf(); e_out = nb(); e_out_b = nf();
+    t1 = nb(); t1_b = nf(); t2 = nb(); t2_b = nf(); wmod = nb(); bmod = nf();
+    if (c.vit_depth > 0) {
+      vpatch = nb(); vpatch_b = nf(); vpos = nf();
+      for (int l = 0; l < c.vit_depth; ++l) {
+        VitW w;
+        w.ln1w = nf(); w.ln1b = nf(); w.wqkv = nb(); w.bqkv = nf(); w.wo = nb(); w.bo = nf();
+        w.ln2w = nf(); w.ln2b = nf(); w.w1 = nb(); w.b1 = nf(); w.w2 = nb(); w.b2 = nf();
+        V.push_back(w);
+      }
+      vln_w = nf(); vln_b = nf(); vproj = nb(); vproj_b = nf();
+    }
+  }
+
+  Tensor &find(const std::string &n) {
+    for (auto &t : tensors)
+      if (t.name == n) return t;
+    fail(OXY_EINVAL, "no tensor %s", n.c_str());
+  }
+
+  void create(const oxy_pi05_config &cfg, int num_blocks, cudaStream_t st) {
+    c = cfg;
+    int dev = 0;
+    OXY_CUDA(cudaGetDevice(&dev));
+    OXY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    declare();
+    materialise(st);
+    NB = num_blocks;
+    kv_stride = (size_t)NB * KV_BLOCK * HEAD_DIM;
+    layer_stride = 2 * kv_stride;
+    OXY_CUDA(cudaMalloc(&pool, (size_t)c.depth * layer_stride * sizeof(bf16)));
+    OXY_CUDA(cudaMemsetAsync(pool, 0, (size_t)c.depth * layer_stride * sizeof(bf16), st));
+    // noise [H, apad] (pad lanes zero) from H*A standard normals
+    OXY_CUDA(cudaMalloc(&noise, (size_t)c.H * apad() * sizeof(float)));
+    OXY_CUDA(cudaMemsetAsync(noise, 0, (size_t)c.H * apad() * sizeof(float), st));
+    float *tmp = vel.as<float>((size_t)c.H * c.action_dim);
+    normal_noise(tmp, (int64_t)c.H * c.action_dim, c.seed ^ 0x6E6F697365ull, st);  // "noise"
+    OXY_CUDA(cudaMemcpy2DAsync(noise, apad() * sizeof(float), tmp, c.action_dim * sizeof(float),
+                               c.action_dim * sizeof(float), c.H, cudaMemcpyDeviceToDevice, st));
+  }
+
+  // ------------------------------------------------------------ helpers
+  void gemm(cudaStream_t st, const bf16 *w, const bf16 *xin, int n_out, int k, int t, int mode, void *out,
+            int ldo, const float *bias = nullptr, const float *gate = nullptr) {
+    if (t <= 0) return;
+    gemm::Plan plan = gemm::make_plan(n_out, k, t, sms);
+    float *wsp = plan.splits > 1 ? ws.as<float>((size_t)plan.splits * t * n_out) : nullptr;
+    EpiParams e{mode, out, ldo, bias, nullptr, 0, gate};
+    gemm::launch(w, xin, n_out, k, t, e, plan, wsp, st);
+  }
+
+  // attention over groups already laid out on the host
+  void attend(cudaStream_t st, std::vector<AttnGroup> &groups, int head_dim, const bf16 *kp, const bf16 *vp) {
+    if (groups.empty()) return;
+    int max_nq = 0, max_tiles = 0, rows = 0;
+    for (auto &g : groups) {
+      g.wrow0 = rows;
+      rows += g.nq;
+      max_nq = std::max(max_nq, g.nq);
+      max_tiles = std::max(max_tiles, (g.nka + 63) / 64 + (g.nkb + 63) / 64);
+    }
+    const int q_tiles = (max_nq + 63) / 64;
+    const int ctas = (int)groups.size() * q_tiles;
+    int splits = 1;
+    if (ctas < sms && max_tiles > 1) splits = std::min(max_tiles, std::max(1, (2 * sms) / ctas));
+    AttnGroup *gd = attn_groups.as<AttnGroup>(groups.size());
+    OXY_CUDA(cudaMemcpyAsync(gd, groups.data(), groups.size() * sizeof(AttnGroup), cudaMemcpyHostToDevice, st));
+    float *wo = nullptr, *wml = nullptr;
+    const int hdp = head_dim == 256 ? 256 : 80;
+    if (splits > 1) {
+      wo = attn_ws.as<float>((size_t)splits * rows * hdp);
+      wml = attn_ml.as<float>((size_t)splits * rows * 2);
+    }
+    flash_attention(gd, (int)groups.size(), q_tiles, head_dim, kp, vp, 1.f / std::sqrt((float)head_dim),
+                    splits, max_tiles, wo, wml, rows, st);
+  }
+
+  // host staging for small int arrays: one H2D copy
+  int *upload_ints(cudaStream_t st, const std::vector<int> &h) {
+    int *d = ints.as<int>(h.size());
+    OXY_CUDA(cudaMemcpyAsync(d, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    return d;
+  }
+
+  // ------------------------------------------------------------ vision
+  // images_d: uint8 [n_img, 224, 224, 3]; writes projected tokens to out (f32, ld W)
+  void vision(cudaStream_t st, const uint8_t *images_d, int n_img, float *out_rows, const int *dst_row,
+              int n_obs, const int *imgs_per_obs) {
+    const int Dv = c.vit_width, T = n_img * 256, W = c.width, nh = c.vit_heads, hd = Dv / nh;
+    bf16 *pt = patches.as<bf16>((size_t)T * PATCH_K);
+    patchify(images_d, n_img, pt, PATCH_K, st);
+    float *h = vit_h.as<float>((size_t)T * Dv);
+    bf16 *yv = vit_y.as<bf16>((size_t)T * Dv);
+    bf16 *qkvv = vit_qkv.as<bf16>((size_t)T * 3 * Dv);
+    bf16 *ov = vit_o.as<bf16>((size_t)T * Dv);
+    bf16 *mv = vit_m.as<bf16>((size_t)T * c.vit_mlp);
+    tile_rows(h, Dv, vpos, Dv, T, 256, Dv, st);
+    gemm(st, vpatch, pt, Dv, PATCH_K, T, gemm::EPI_ADD_F32, h, Dv, vpatch_b);
+    std::vector<AttnGroup> groups;
+    for (int im = 0; im < n_img; ++im)
+      for (int hh = 0; hh < nh; ++hh) {
+        AttnGroup g{};
+        g.q = qkvv + (size_t)im * 256 * 3 * Dv + hh * hd;
+        g.ldq = 3 * Dv;
+        g.o = ov + (size_t)im * 256 * Dv + hh * hd;
+        g.ldo = Dv;
+        g.nq = 256;
+        g.kb = g.q + Dv;
+        g.vb = g.q + 2 * Dv;
+        g.ldkv = 3 * Dv;
+        g.nkb = 256;
+        groups.push_back(g);
+      }
+    for (int l = 0; l < c.vit_depth; ++l) {
+      const VitW &w = V[l];
+      layernorm(h, Dv, yv, Dv, w.ln1w, w.ln1b, T, Dv, 1e-6f, st);
+      gemm(st, w.wqkv, yv, 3 * Dv, Dv, T, gemm::EPI_BF16, qkvv, 3 * Dv, w.bqkv);
+      std::vector<AttnGroup> gs = groups;
+      attend(st, gs, hd, nullptr, nullptr);
+      gemm(st, w.wo, ov, Dv, Dv, T, gemm::EPI_ADD_F32, h, Dv, w.bo);
+      layernorm(h, Dv, yv, Dv, w.ln2w, w.ln2b, T, Dv, 1e-6f, st);
+      gemm(st, w.w1, yv, c.vit_mlp, Dv, T, gemm::EPI_GELU_BF16, mv, c.vit_mlp, w.b1);
+      gemm(st, w.w2, mv, Dv, c.vit_mlp, T, gemm::EPI_ADD_F32, h, Dv, w.b2);
+    }
+    layernorm(h, Dv, yv, Dv, vln_w, vln_b, T, Dv, 1e-6f, st);
+    int img0 = 0;
+    for (int i = 0; i < n_obs; ++i) {
+      const int ni = imgs_per_obs[i];
+      if (ni > 0)
+        gemm(st, vproj, yv + (size_t)img0 * 256 * Dv, W, Dv, ni * 256, gemm::EPI_F32,
+             out_rows + (size_t)dst_row[i] * W, W, vproj_b);
+      img0 += ni;
+    }
+  }
+
+  // ------------------------------------------------------------ prefill
+  // n_obs observations; obs i has n_img[i] images (in images_d order) and
+  // n_txt[i] text tokens (concatenated in tokens_h); prefix = [images; text].
+  // blocks_h: per obs ceil(P_i/64) block ids, concatenated.
+  void prefill(cudaStream_t st, int n_obs, const int *n_img, const int *n_txt, const int *tokens_h,
+               const uint8_t *images_d, const int *blocks_h) {
+    const int W = c.width;
+    std::vector<int> P(n_obs), off(n_obs), boff(n_obs);
+    int T = 0, nb = 0, n_images = 0, n_tok = 0;
+    for (int i = 0; i < n_obs; ++i) {
+      OXY_REQUIRE(n_img[i] >= 0 && n_txt[i] >= 0, "negative prefix part");
+      OXY_REQUIRE(n_img[i] == 0 || c.vit_depth > 0, "this model has no vision tower");
+      P[i] = n_img[i] * 256 + n_txt[i];
+      OXY_REQUIRE(P[i] >= 1, "observation needs at least one token");
+      off[i] = T;
+      boff[i] = nb;
+      T += P[i];
+      nb += (P[i] + KV_BLOCK - 1) / KV_BLOCK;
+      n_images += n_img[i];
+      n_tok += n_txt[i];
+    }
+    for (int i = 0; i < n_tok; ++i)
+      OXY_REQUIRE(tokens_h[i] >= 0 && tokens_h[i] < c.vocab, "observation token %d outside vocab of %d",
+                  tokens_h[i], c.vocab);
+    // ints: tokens(per row, -1 for image rows) | pos | slot | block tables
+    std::vector<int> h(3 * (size_t)T + nb);
+    int *tok = h.data(), *pos = tok + T, *slot = pos + T, *bt = slot + T;
+    std::memcpy(bt, blocks_h, nb * sizeof(int));
+    int ti = 0;
+    for (int i = 0; i < n_obs; ++i)
+      for (int p = 0; p < P[i]; ++p) {
+        const int r = off[i] + p;
+        tok[r] = p < n_img[i] * 256 ? -1 : tokens_h[ti++];
+        pos[r] = p;
+        slot[r] = blocks_h[boff[i] + p / KV_BLOCK] * KV_BLOCK + p % KV_BLOCK;
+      }
+    int *dints = upload_ints(st, h);
+    int *d_pos = dints + T, *d_slot = dints + 2 * T, *d_bt = dints + 3 * T;
+    float *X = x.as<float>((size_t)T * W);
+    bf16 *Y = y.as<bf16>((size_t)T * W);
+    float *QKVf = qkv.as<float>((size_t)T * QKV);
+    bf16 *Qb = q.as<bf16>((size_t)T * QDIM);
+    bf16 *Ob = o.as<bf16>((size_t)T * QDIM);
+    bf16 *Hm = hmid.as<bf16>((size_t)T * c.mlp);
+    // text embeddings (rows with tok >= 0), image tokens from the vision tower
+    for (int i = 0; i < n_obs; ++i) {
+      const int r0 = off[i] + n_img[i] * 256;
+      embed_rows(X + (size_t)r0 * W, W, embed, dints + r0, nullptr, n_txt[i], W, std::sqrt((float)W), st);
+    }
+    if (n_images > 0) vision(st, images_d, n_images, X, off.data(), n_obs, n_img);
+    std::vector<AttnGroup> groups(n_obs);
+    for (int i = 0; i < n_obs; ++i) {
+      AttnGroup g{};
+      g.q = Qb + (size_t)off[i] * QDIM;
+      g.ldq = HEAD_DIM;
+      g.o = Ob + (size_t)off[i] * QDIM;
+      g.ldo = HEAD_DIM;
+      g.nq = P[i] * Q_HEADS;
+      g.bt = d_bt + boff[i];
+      g.nka = P[i];
+      groups[i] = g;
+    }
+    for (int l = 0; l < c.depth; ++l) {
+      const LayerW &w = L[l];
+      rmsnorm(X, W, Y, W, w.ln1, nullptr, nullptr, T, W, 1e-6f, st);
+      gemm(st, w.wqkv, Y, QKV, W, T, gemm::EPI_F32, QKVf, QKV);
+      rope_split(QKVf, T, Q_HEADS, d_pos, d_slot, nullptr, Qb, kpool(l), vpool(l), nullptr, nullptr,
+                 10000.f, st);
+      if (l == c.depth - 1) break;  // the last block's output is not cached
+      std::vector<AttnGroup> gs = groups;
+      attend(st, gs, HEAD_DIM, kpool(l), vpool(l));
+      gemm(st, w.wo, Ob, W, QDIM, T, gemm::EPI_ADD_F32, X, W);
+      rmsnorm(X, W, Y, W, w.ln2, nullptr, nullptr, T, W, 1e-6f, st);
+      gemm(st, w.wgu, Y, 2 * c.mlp, W, T, gemm::EPI_GEGLU_BF16, Hm, c.mlp);
+      gemm(st, w.wd, Hm, W, c.mlp, T, gemm::EPI_ADD_F32, X, W);
+    }
+  }
+
+  // ------------------------------------------------------------ action expert
+  void ensure_mod(cudaStream_t st, int S) {
+    if (mod_S == S) return;
+    const int We = c.expert_width;
+    // time embedding of t_s = 1 - s/S (openpi posemb_sincos: periods 4e-3 .. 4)
+    std::vector<float> temb((size_t)S * We);
+    const int half = We / 2;
+    for (int s = 0; s < S; ++s) {
+      const double t = 1.0 - (double)s / S;
+      for (int i = 0; i < half; ++i) {
+        const double frac = half > 1 ? (double)i / (half - 1) : 0.0;
+        const double period = 4e-3 * std::pow(4.0 / 4e-3, frac);
+        const double ang = t / period * 2.0 * M_PI;
+        temb[(size_t)s * We + i] = (float)std::sin(ang);
+        temb[(size_t)s * We + half + i] = (float)std::cos(ang);
+      }
+    }
+    float *tf = xe.as<float>((size_t)S * We * 2);
+    OXY_CUDA(cudaMemcpyAsync(tf, temb.data(), temb.size() * sizeof(float), cudaMemcpyHostToDevice, st));
+    bf16 *tb = act_bf.as<bf16>((size_t)S * We * 3);
+    bf16 *h1 = tb + (size_t)S * We, *h2 = h1 + (size_t)S * We;
+    f32_to_bf16(tf, tb, (int64_t)S * We, st);
+    gemm(st, t1, tb, We, We, S, gemm::EPI_SWISH_BF16, h1, We, t1_b);
+    gemm(st, t2, h1, We, We, S, gemm::EPI_SWISH_BF16, h2, We, t2_b);
+    float *m = mod.as<float>((size_t)S * n_mod);
+    gemm(st, wmod, h2, n_mod, We, S, gemm::EPI_F32, m, n_mod, bmod);
+    mod_S = S;
+  }
+
+  // n streams; stream i's prefix has P[i] positions in blocks (concatenated).
+  void denoise(cudaStream_t st, int n, const int *P, const int *blocks_h, int S, float *actions_out_d) {
+    OXY_REQUIRE(S >= 1, "denoise step count must be >= 1, got %d", S);
+    const int We = c.expert_width, H = c.H, A = c.action_dim, T = n * H;
+    ensure_mod(st, S);
+    int nb = 0;
+    for (int i = 0; i < n; ++i) nb += (P[i] + KV_BLOCK - 1) / KV_BLOCK;
+    std::vector<int> h((size_t)T + nb);
+    int *pos = h.data(), *bt = pos + T;
+    std::memcpy(bt, blocks_h, nb * sizeof(int));
+    std::vector<int> boff(n);
+    for (int i = 0, b = 0; i < n; ++i) {
+      boff[i] = b;
+      b += (P[i] + KV_BLOCK - 1) / KV_BLOCK;
+      for (int j = 0; j < H; ++j) pos[i * H + j] = P[i] + j;
+    }
+    int *dints = upload_ints(st, h);
+    int *d_pos = dints, *d_bt = dints + T;
+    const int AP = apad();
+    float *a = act.as<float>((size_t)T * AP);
+    bf16 *ab = act_bf.as<bf16>((size_t)T * AP);
+    for (int i = 0; i < n; ++i)
+      OXY_CUDA(cudaMemcpyAsync(a + (size_t)i * H * AP, noise, (size_t)H * AP * sizeof(float),
+                               cudaMemcpyDeviceToDevice, st));
+    f32_to_bf16(a, ab, (int64_t)T * AP, st);
+    float *X = xe.as<float>((size_t)T * We);
+    bf16 *Y = y.as<bf16>((size_t)T * std::max(We, QDIM));
+    float *QKVf = qkv.as<float>((size_t)T * QKV);
+    bf16 *Qb = q.as<bf16>((size_t)T * QDIM);
+    bf16 *Ob = o.as<bf16>((size_t)T * QDIM);
+    bf16 *Kd = kd.as<bf16>((size_t)T * HEAD_DIM), *Vd = vd.as<bf16>((size_t)T * HEAD_DIM);
+    bf16 *Hm = hmid.as<bf16>((size_t)T * c.expert_mlp);
+    float *vel_d = vel.as<float>((size_t)T * AP);
+    OXY_CUDA(cudaMemsetAsync(vel_d, 0, (size_t)T * AP * sizeof(float), st));
+    std::vector<AttnGroup> groups(n);
+    for (int i = 0; i < n; ++i) {
+      AttnGroup g{};
+      g.q = Qb + (size_t)i * H * QDIM;
+      g.ldq = HEAD_DIM;
+      g.o = Ob + (size_t)i * H * QDIM;
+      g.ldo = HEAD_DIM;
+      g.nq = H * Q_HEADS;
+      g.bt = d_bt + boff[i];
+      g.nka = P[i];
+      g.kb = Kd + (size_t)i * H * HEAD_DIM;
+      g.vb = Vd + (size_t)i * H * HEAD_DIM;
+      g.ldkv = HEAD_DIM;
+      g.nkb = H;
+      groups[i] = g;
+    }
+    const float dt = -1.f / (float)S;
+    for (int s = 0; s < S; ++s) {
+      const float *ms = mod.as<float>(0) + (size_t)s * n_mod;
+      gemm(st, e_in, ab, We, AP, T, gemm::EPI_F32, X, We, e_in_b);
+      for (int l = 0; l < c.depth; ++l) {
+        const ExpertW &w = E[l];
+        const float *m = ms + (size_t)l * 6 * We;
+        rmsnorm(X, We, Y, We, nullptr, m, m + We, T, We, 1e-6f, st);
+        gemm(st, w.wqkv, Y, QKV, We, T, gemm::EPI_F32, QKVf, QKV);
+        rope_split(QKVf, T, Q_HEADS, d_pos, nullptr, nullptr, Qb, nullptr, nullptr, Kd, Vd, 10000.f, st);
+        std::vector<AttnGroup> gs = groups;
+        attend(st, gs, HEAD_DIM, kpool(l), vpool(l));
+        gemm(st, w.wo, Ob, We, QDIM, T, gemm::EPI_ADD_GATED_F32, X, We, nullptr, m + 2 * We);
+        rmsnorm(X, We, Y, We, nullptr, m + 3 * We, m + 4 * We, T, We, 1e-6f, st);
+        gemm(st, w.wgu, Y, 2 * c.expert_mlp, We, T, gemm::EPI_GEGLU_BF16, Hm, c.expert_mlp);
+        gemm(st, w.wd, Hm, We, c.expert_mlp, T, gemm::EPI_ADD_GATED_F32, X, We, nullptr, m + 5 * We);
+      }
+      const float *mf = ms + (size_t)c.depth * 6 * We;
+      rmsnorm(X, We, Y, We, nullptr, mf, mf + We, T, We, 1e-6f, st);
+      gemm(st, e_out, Y, A, We, T, gemm::EPI_F32, vel_d, AP, e_out_b);
+      euler_step(a, vel_d, ab, (int64_t)T * AP, dt, st);
+    }
+    OXY_CUDA(cudaMemcpy2DAsync(actions_out_d, A * sizeof(float), a, AP * sizeof(float), A * sizeof(float), T,
+                               cudaMemcpyDeviceToDevice, st));
+  }
+
+  // ------------------------------------------------------------ decode
+  void decode(cudaStream_t st, int rows, int k, const int *bt_h, int maxb, const int *seq_h, const int *last_h,
+              const int *budget_h, const int *cow_h, int *out_tok_h, int *out_cnt_h, float *logits_h) {
+    const int W = c.width;
+    const size_t n_bt = (size_t)rows * maxb, n_out = (size_t)rows * k;
+    std::vector<int> h(n_bt + 3 * (size_t)rows + 6 * (size_t)rows + n_out, 0);
+    int *hp = h.data();
+    std::memcpy(hp, bt_h, n_bt * sizeof(int));
+    std::memcpy(hp + n_bt, cow_h, 3 * rows * sizeof(int));
+    int *h_active = hp + n_bt + 3 * rows, *h_tok = h_active + rows, *h_pos = h_tok + rows,
+        *h_cnt = h_pos + rows, *h_bud = h_cnt + rows;
+    int max_pos = 0;
+    for (int r = 0; r < rows; ++r) {
+      OXY_REQUIRE(last_h[r] >= 0 && last_h[r] < c.vocab, "token %d outside vocab", last_h[r]);
+      h_active[r] = 1;
+      h_tok[r] = last_h[r];
+      h_pos[r] = seq_h[r];
+      h_bud[r] = budget_h[r];
+      max_pos = std::max(max_pos, seq_h[r] + k);
+    }
+    OXY_REQUIRE((max_pos + KV_BLOCK - 1) / KV_BLOCK <= maxb, "block table too short for %d positions", max_pos);
+    int *dv = upload_ints(st, h);
+    int *d_bt = dv, *d_cow = dv + n_bt, *d_active = d_cow + 3 * rows, *d_tok = d_active + rows,
+        *d_pos = d_tok + rows, *d_cnt = d_pos + rows, *d_bud = d_cnt + rows, *d_slot = d_bud + rows,
+        *d_out = d_slot + rows;
+    cow_blocks(pool, d_cow, rows, c.depth, layer_stride, kv_stride, st);
+    float *X = x.as<float>((size_t)rows * W);
+    bf16 *Y = y.as<bf16>((size_t)rows * W);
+    float *QKVf = qkv.as<float>((size_t)rows * QKV);
+    bf16 *Qb = q.as<bf16>((size_t)rows * QDIM);
+    bf16 *Ob = o.as<bf16>((size_t)rows * QDIM);
+    bf16 *Hm = hmid.as<bf16>((size_t)rows * c.mlp);
+    float *LG = logits.as<float>((size_t)rows * c.vocab);
+    float *pv = amv.as<float>((size_t)rows * 64);
+    int *pi = ami.as<int>((size_t)rows * 64);
+    float *dws = dec_ws.as<float>((size_t)rows * maxb * Q_HEADS * (HEAD_DIM + 2));
+    const float scale = 1.f / 16.f;  // 1/sqrt(256)
+    for (int s = 0; s < k; ++s) {
+      embed_rows(X, W, embed, d_tok, nullptr, rows, W, std::sqrt((float)W), st);
+      next_slots(d_slot, d_pos, d_active, d_bt, maxb, rows, st);
+      for (int l = 0; l < c.depth; ++l) {
+        const LayerW &w = L[l];
+        rmsnorm(X, W, Y, W, w.ln1, nullptr, nullptr, rows, W, 1e-6f, st);
+        gemm(st, w.wqkv, Y, QKV, W, rows, gemm::EPI_F32, QKVf, QKV);
+        rope_split(QKVf, rows, Q_HEADS, d_pos, d_slot, d_active, Qb, kpool(l), vpool(l), nullptr, nullptr,
+                   10000.f, st);
+        decode_attention(Qb, Ob, kpool(l), vpool(l), d_bt, maxb, d_pos, d_active, rows, maxb, scale, dws, st);
+        gemm(st, w.wo, Ob, W, QDIM, rows, gemm::EPI_ADD_F32, X, W);
+        rmsnorm(X, W, Y, W, w.ln2, nullptr, nullptr, rows, W, 1e-6f, st);
+        gemm(st, w.wgu, Y, 2 * c.mlp, W, rows, gemm::EPI_GEGLU_BF16, Hm, c.mlp);
+        gemm(st, w.wd, Hm, W, c.mlp, rows, gemm::EPI_ADD_F32, X, W);
+      }
+      rmsnorm(X, W, Y, W, final_norm, nullptr, nullptr, rows, W, 1e-6f, st);
+      gemm(st, lm_head, Y, c.vocab, W, rows, gemm::EPI_F32, LG, c.vocab);
+      if (logits_h)
+        OXY_CUDA(cudaMemcpyAsync(logits_h + (size_t)s * rows * c.vocab, LG, (size_t)rows * c.vocab * sizeof(float),
+                                 cudaMemcpyDeviceToHost, st));
+      argmax_update(LG, rows, c.vocab, s, k, c.eos_token, d_active, d_tok, d_pos, d_cnt, d_bud, d_out, pv, pi, st);
+    }
+    OXY_CUDA(cudaMemcpyAsync(out_tok_h, d_out, n_out * sizeof(int), cudaMemcpyDeviceToHost, st));
+    OXY_CUDA(cudaMemcpyAsync(out_cnt_h, d_cnt, rows * sizeof(int), cudaMemcpyDeviceToHost, st));
+    OXY_CUDA(cudaStreamSynchronize(st));
+  }
+};
+
+__global__ void gather_kv_f32(float *kout, float *vout, const bf16 *kp, const bf16 *vp, const int *blocks,
+                              int seq_len) {
+  const int t = blockIdx.x;
+  const size_t s = (size_t)blocks[t / KV_BLOCK] * KV_BLOCK + t % KV_BLOCK;
+  for (int j = threadIdx.x; j < HEAD_DIM; j += blockDim.x) {
+    kout[(size_t)t * HEAD_DIM + j] = __bfloat162float(kp[s * HEAD_DIM + j]);
+    vout[(size_t)t * HEAD_DIM + j] = __bfloat162float(vp[s * HEAD_DIM + j]);
+  }
+}
+
+}  // namespace pi05
+}  // namespace oxy
+
+struct oxy_pi05 {
+  oxy::pi05::Model m;
+};
+
+extern "C" {
+
+int oxy_pi05_create(const oxy_pi05_config *cfg, int32_t num_blocks, void *stream, oxy_pi05 **out) {
+  OXY_API_BEGIN
+  OXY_REQUIRE(cfg && cfg->width % 64 == 0 && cfg->expert_width % 64 == 0 && cfg->mlp % 64 == 0 &&
+                  cfg->expert_mlp % 64 == 0 && cfg->depth >= 1 && cfg->vocab >= 2,
+              "invalid pi05 config (widths must be multiples of 64)");
+  OXY_REQUIRE(cfg->vit_depth == 0 || (cfg->vit_heads > 0 && cfg->vit_width == 72 * cfg->vit_heads &&
+                                      cfg->vit_mlp % 8 == 0),
+              "vision tower needs head dim 72 and vit_mlp % 8 == 0");
+  OXY_REQUIRE(cfg->eos_token >= 0 && cfg->eos_token < cfg->vocab, "eos outside vocab");
+  OXY_REQUIRE(num_blocks > 0, "pool needs blocks");
+  auto *p = new oxy_pi05;
+  try {
+    p->m.create(*cfg, num_blocks, oxy::as_stream(stream));
+    OXY_CUDA(cudaStreamSynchronize(oxy::as_stream(stream)));
+  } catch (...) {
+    delete p;
+    throw;
+  }
+  *out = p;
+  OXY_API_END
+}
+
+int oxy_pi05_destroy(oxy_pi05 *p) {
+  delete p;
+  return OXY_OK;
+}
+
+int oxy_pi05_num_tensors(oxy_pi05 *p, int32_t *n) {
+  *n = (int32_t)p->m.tensors.size();
+  return OXY_OK;
+}
+
+int oxy_pi05_tensor_info(oxy_pi05 *p, int32_t i, char *name64, int64_t *shape2, int32_t *dtype,
+                         uint64_t *offset, float *bound, float *center) {
+  OXY_API_BEGIN
+  OXY_REQUIRE(i >= 0 && i < (int32_t)p->m.tensors.size(), "tensor index out of range");
+  const auto &t = p->m.tensors[i];
+  std::snprintf(name64, 64, "%s", t.name.c_str());
+  shape2[0] = t.rows;
+  shape2[1] = t.cols;
+  *dtype = t.dtype;
+  *offset = t.offset;
+  *bound = t.bound;
+  *center = t.center;
+  OXY_API_END
+}
+
+int oxy_pi05_tensor_read(oxy_pi05 *p, int32_t i, void *host, int64_t nbytes, void *stream) {
+  OXY_API_BEGIN
+  OXY_REQUIRE(i >= 0 && i < (int32_t)p->m.tensors.size(), "tensor index out of range");
+  const auto &t = p->m.tensors[i];
+  OXY_REQUIRE(nbytes == t.numel() * (t.dtype == 0 ? 2 : 4), "tensor %s byte count mismatch", t.name.c_str());
+  auto st = oxy::as_stream(stream);
+  OXY_CUDA(cudaMemcpyAsync(host, t.ptr, nbytes, cudaMemcpyDeviceToHost, st));
+  OXY_CUDA(cudaStreamSynchronize(st));
+  OXY_API_END
+}
+
+int oxy_pi05_prefill(oxy_pi05 *p, int32_t n_obs, const int32_t *n_img_h, const int32_t *n_txt_h,
+                     const int32_t *tokens_h, const uint8_t *images_d, const int32_t *blocks_h, void *stream) {
+  OXY_API_BEGIN
+  OXY_REQUIRE(n_obs >= 1, "prefill needs at least one observation");
+  p->m.prefill(oxy::as_stream(stream), n_obs, n_img_h, n_txt_h, tokens_h, images_d, blocks_h);
+  OXY_API_END
+}
+
+int oxy_pi05_denoise(oxy_pi05 *p, int32_t n, const int32_t *prefix_lens_h, const int32_t *blocks_h, int32_t S,
+                     float *actions_d, void *stream) {
+  OXY_API_BEGIN
+  OXY_REQUIRE(n >= 1, "denoise needs at least one stream");
+  p->m.denoise(oxy::as_stream(stream), n, prefix_lens_h, blocks_h, S, actions_d);
+  OXY_API_END
+}
+
+int oxy_pi05_decode(oxy_pi05 *p, int32_t rows, int32_t k, const int32_t *block_tables_h, int32_t max_blocks,
+                    const int32_t *seq_lens_h, const int32_t *last_tokens_h, const int32_t *budgets_h,
+                    const int32_t *cow_h, int32_t *out_tokens_h, int32_t *out_count_h, float *logits_h,
+                    void *stream) {
+  OXY_API_BEGIN
+  OXY_REQUIRE(rows >= 1, "decode needs at least one row");
+  OXY_REQUIRE(k >= 1, "decode step count must be >= 1, got %d", k);
+  p->m.decode(oxy::as_stream(stream), rows, k, block_tables_h, max_blocks, seq_lens_h, last_tokens_h, budgets_h,
+              cow_h, out_tokens_h, out_count_h, logits_h);
+  OXY_API_END
+}
+
+int oxy_pi05_read_kv(oxy_pi05 *p, const int32_t *blocks_h, int32_t seq_len, int32_t layer, float *keys_h,
+                     float *values_h, void *stream) {
+  OXY_API_BEGIN
+  auto &m = p->m;
+  OXY_REQUIRE(layer >= 0 && layer < m.c.depth, "layer %d out of range", layer);
+  if (seq_len == 0) return OXY_OK;
+  auto st = oxy::as_stream(stream);
+  const int nb = (seq_len + 63) / 64;
+  int *bd = m.ints.as<int>(nb);
+  OXY_CUDA(cudaMemcpyAsync(bd, blocks_h, nb * sizeof(int), cudaMemcpyHostToDevice, st));
+  float *ko = m.qkv.as<float>((size_t)2 * seq_len * 256);
+  oxy::pi05::gather_kv_f32<<<seq_len, 256, 0, st>>>(ko, ko + (size_t)seq_len * 256, m.kpool(layer), m.vpool(layer),
+                                                    bd, seq_len);
+  OXY_LAUNCH_CHECK();
+  OXY_CUDA(cudaMemcpyAsync(keys_h, ko, (size_t)seq_len * 256 * 4, cudaMemcpyDeviceToHost, st));
+  OXY_CUDA(cudaMemcpyAsync(values_h, ko + (size_t)seq_len * 256, (size_t)seq_len * 256 * 4, cudaMemcpyDeviceToHost, st));
+  OXY_CUDA(cudaStreamSynchronize(st));
+  OXY_API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,359 @@
+"""F2 backend: a pi0.5-shaped Mixture-of-Transformers VLA on the B200.
+
+Same protocol as the reference backends (``kvweaver/backend.py:163-201``):
+``prefill`` writes the shared observation prefix (3 SigLIP cameras + prompt)
+into the unified paged KV pool ONCE; ``action_denoise`` runs the
+flow-matching action expert whose suffix attends to that same paged prefix
+(cross-task KV sharing, ``PAPER.md:217-238``); ``batched_language_decode``
+continues language requests from the same handles, continuously batched
+across frames.  ``admit_many`` batches the prefill and denoise of r
+lock-stepped robot streams (``Uniform(r)`` arrivals).
+
+Shapes (``Pi05Config``) follow the public openpi pi0.5 configuration
+(SURVEY.md Appendix B); weights are random (splitmix64 counter draws,
+U(+-sqrt(3/fan_in))), which the reference cannot pin: this family's layer
+arithmetic is checked against ``oracle/pi05_ref.py`` (torch fp32), parity
+unpinned by the reference itself.  Compute is bf16 on tcgen05 with fp32
+accumulation and an fp32 residual stream.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .backend import ActionChunk, CostModelParams, Observation, PricedBackend
+from .kv_manager import BatchedState, GenerationState, KvLayer
+from .paged import BlockAllocator, PagedKvCache
+from .timing import StageMeter
+
+__all__ = ["Pi05Config", "Pi05Observation", "Pi05Backend", "TINY", "smoke"]
+
+KV_BLOCK = 64
+HEAD_DIM = 256
+_BIG_BUDGET = 1 << 30
+
+
+class OxyPi05Config(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in (
+        "width", "depth", "mlp", "vocab", "expert_width", "expert_mlp", "vit_width", "vit_depth",
+        "vit_mlp", "vit_heads", "H", "action_dim", "eos_token")] + [("seed", C.c_uint64)]
+
+
+@dataclass(frozen=True, slots=True)
+class Pi05Config:
+    """pi0.5 shape.  Defaults: Gemma-2B + Gemma-300M expert + SigLIP So400m/14."""
+
+    width: int = 2048
+    depth: int = 18
+    mlp: int = 16384
+    vocab: int = 257152
+    expert_width: int = 1024
+    expert_mlp: int = 4096
+    vit_width: int = 1152
+    vit_depth: int = 27
+    vit_mlp: int = 4304
+    vit_heads: int = 16
+    H: int = 50
+    action_dim: int = 32
+    S: int = 10
+    eos_token: int = 1
+    seed: int = 7
+    n_cams: int = 3
+
+    def __post_init__(self):
+        for name in ("width", "expert_width", "mlp", "expert_mlp"):
+            if getattr(self, name) % 64:
+                raise ValueError(f"{name} must be a multiple of 64")
+        if self.vit_depth and self.vit_width != 72 * self.vit_heads:
+            raise ValueError("vision head dim must be 72 (vit_width = 72 * vit_heads)")
+        if not 0 <= self.eos_token < self.vocab:
+            raise ValueError(f"eos_token {self.eos_token} outside vocab of {self.vocab}")
+        if self.H < 1 or self.S < 1 or self.action_dim < 1:
+            raise ValueError("action_dim, H and S must be positive")
+
+    @property
+    def L(self) -> int:
+        return self.depth
+
+    def to_c(self) -> OxyPi05Config:
+        return OxyPi05Config(self.width, self.depth, self.mlp, self.vocab, self.expert_width,
+                             self.expert_mlp, self.vit_width, self.vit_depth, self.vit_mlp,
+                             self.vit_heads, self.H, self.action_dim, self.eos_token,
+                             self.seed & ((1 << 64) - 1))
+
+
+# reduced shape with the same code paths (parity tests against the CPU oracle)
+TINY = Pi05Config(width=256, depth=2, mlp=512, vocab=1000, expert_width=128, expert_mlp=256,
+                  vit_width=144, vit_depth=2, vit_mlp=288, vit_heads=2, H=10, action_dim=8,
+                  S=4, eos_token=1, seed=3, n_cams=2)
+
+
+@dataclass(frozen=True, slots=True, eq=False)
+class Pi05Observation:
+    """Observation with camera images: uint8 [n_cams, 224, 224, 3] on host
+    (numpy) or device (torch CUDA tensor), plus prompt token ids."""
+
+    obs_tokens: tuple
+    frame: int
+    images: object = None
+
+    def __post_init__(self):
+        object.__setattr__(self, "obs_tokens", tuple(self.obs_tokens))
+        n = 0 if self.images is None else int(self.images.shape[0])
+        if n == 0 and not self.obs_tokens:
+            raise ValueError("observation needs at least one token")
+        if n and tuple(self.images.shape[1:]) != (224, 224, 3):
+            raise ValueError(f"images must be [n, 224, 224, 3], got {tuple(self.images.shape)}")
+
+    @property
+    def n_images(self) -> int:
+        return 0 if self.images is None else int(self.images.shape[0])
+
+    @property
+    def prefix_len(self) -> int:
+        return 256 * self.n_images + len(self.obs_tokens)
+
+
+def _as_pi05(cfg) -> Pi05Config:
+    if cfg is None:
+        return Pi05Config()
+    if isinstance(cfg, Pi05Config):
+        return cfg
+    # a reference BackendConfig: keep the protocol fields, pi0.5 shape otherwise
+    return Pi05Config(H=cfg.H, S=cfg.S, action_dim=cfg.action_dim, seed=cfg.seed,
+                      vocab=max(cfg.vocab, 2), eos_token=cfg.eos_token, width=256, depth=2,
+                      mlp=512, expert_width=128, expert_mlp=256, vit_depth=0)
+
+
+class Pi05Backend(PricedBackend):
+    def __init__(self, config=None, cost: CostModelParams | None = None, num_blocks: int = 2048,
+                 measure: bool = False):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("Pi05Backend needs a CUDA device (no CPU fallback)")
+        self.config = c = _as_pi05(config)
+        self.cost = cost or CostModelParams.zero()
+        self.kind = "Pi05"
+        self.backend_tag = (f"pi05/w{c.width}-d{c.depth}-e{c.expert_width}-v{c.vocab}"
+                            f"-vit{c.vit_depth}-s{c.seed}")
+        self.num_layers = c.depth
+        self.block_size = KV_BLOCK
+        self.allocator = BlockAllocator(num_blocks, KV_BLOCK)
+        self.meter = StageMeter() if measure else None
+        h = C.c_void_p()
+        _lib.call("oxy_pi05_create", C.byref(c.to_c()), C.c_int32(num_blocks), _lib.stream_ptr(),
+                  C.byref(h))
+        self._h = h
+        self._torch = torch
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                _lib.lib().oxy_pi05_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    # ---------------------------------------------------------------- utils
+
+    def _span(self, stage):
+        import contextlib
+        return self.meter.span(stage) if self.meter is not None else contextlib.nullcontext()
+
+    def tensors(self) -> list[dict]:
+        n = C.c_int32()
+        _lib.call("oxy_pi05_num_tensors", self._h, C.byref(n))
+        out = []
+        for i in range(n.value):
+            name = C.create_string_buffer(64)
+            shape = (C.c_int64 * 2)()
+            dt, off = C.c_int32(), C.c_uint64()
+            bound, center = C.c_float(), C.c_float()
+            _lib.call("oxy_pi05_tensor_info", self._h, C.c_int32(i), name, shape, C.byref(dt),
+                      C.byref(off), C.byref(bound), C.byref(center))
+            out.append(dict(index=i, name=name.value.decode(), shape=(shape[0], shape[1]),
+                            dtype="bf16" if dt.value == 0 else "f32", offset=off.value,
+                            bound=bound.value, center=center.value))
+        return out
+
+    def read_tensor(self, info: dict):
+        """Weight tensor as a torch CPU tensor (bf16 or f32)."""
+        torch = self._torch
+        dtype = torch.bfloat16 if info["dtype"] == "bf16" else torch.float32
+        t = torch.empty(info["shape"], dtype=dtype)
+        _lib.call("oxy_pi05_tensor_read", self._h, C.c_int32(info["index"]),
+                  C.c_void_p(t.data_ptr()), C.c_int64(t.numel() * t.element_size()),
+                  _lib.stream_ptr())
+        return t
+
+    def read_kv(self, kv: PagedKvCache, layer: int):
+        keys = np.empty((kv.seq_len, HEAD_DIM), np.float32)
+        vals = np.empty((kv.seq_len, HEAD_DIM), np.float32)
+        b = _lib.as_i32(kv.blocks)
+        _lib.call("oxy_pi05_read_kv", self._h, _lib.ptr_i32(b), C.c_int32(kv.seq_len),
+                  C.c_int32(layer), keys.ctypes.data_as(C.c_void_p),
+                  vals.ctypes.data_as(C.c_void_p), _lib.stream_ptr())
+        return keys.astype(np.float64), vals.astype(np.float64)
+
+    def _own(self, kv) -> PagedKvCache:
+        self._check_tag(kv)
+        if not isinstance(kv, PagedKvCache) or kv.owner is not self:
+            raise ValueError(f"cache from backend {kv.backend_tag!r} is not resident in this "
+                             f"backend's KV pool")
+        return kv
+
+    def _check_obs(self, obs) -> None:
+        v = self.config.vocab
+        for t in obs.obs_tokens:
+            if not 0 <= t < v:
+                raise ValueError(f"observation token {t} outside vocab of {v}")
+
+    def _images_device(self, obs_list):
+        torch = self._torch
+        imgs = [o.images for o in obs_list if getattr(o, "images", None) is not None
+                and o.images.shape[0] > 0]
+        if not imgs:
+            return None, None
+        if all(isinstance(i, torch.Tensor) and i.is_cuda for i in imgs):
+            dev = imgs[0] if len(imgs) == 1 else torch.cat(imgs)
+        else:
+            host = np.concatenate([np.asarray(i.cpu() if isinstance(i, torch.Tensor) else i,
+                                              dtype=np.uint8) for i in imgs])
+            pinned = torch.from_numpy(host).pin_memory()
+            dev = pinned.to("cuda", non_blocking=True)
+        return dev.contiguous(), C.c_void_p(dev.data_ptr())
+
+    # ---------------------------------------------------------------- protocol
+
+    def prefill_many(self, obs_list) -> list[PagedKvCache]:
+        for o in obs_list:
+            self._check_obs(o)
+        n_img = _lib.as_i32([getattr(o, "n_images", 0) for o in obs_list])
+        n_txt = _lib.as_i32([len(o.obs_tokens) for o in obs_list])
+        toks = _lib.as_i32([t for o in obs_list for t in o.obs_tokens] or [0])
+        handles = []
+        for o, ni, nt in zip(obs_list, n_img, n_txt):
+            p = 256 * int(ni) + int(nt)
+            handles.append(PagedKvCache(self, self.allocator.alloc_seq(p), p))
+        blocks = _lib.as_i32([b for h in handles for b in h.blocks])
+        with self._span("prefill"):
+            keep, img_ptr = self._images_device(obs_list)
+            _lib.call("oxy_pi05_prefill", self._h, C.c_int32(len(obs_list)), _lib.ptr_i32(n_img),
+                      _lib.ptr_i32(n_txt), _lib.ptr_i32(toks), img_ptr, _lib.ptr_i32(blocks),
+                      _lib.stream_ptr())
+        del keep
+        return handles
+
+    def prefill(self, obs) -> PagedKvCache:
+        return self.prefill_many([obs])[0]
+
+    def denoise_many(self, kvs, S: int) -> list[ActionChunk]:
+        if S < 1:
+            raise ValueError(f"denoise step count must be >= 1, got {S}")
+        kvs = [self._own(kv) for kv in kvs]
+        c = self.config
+        torch = self._torch
+        out = torch.empty((len(kvs), c.H, c.action_dim), dtype=torch.float32, device="cuda")
+        lens = _lib.as_i32([kv.seq_len for kv in kvs])
+        blocks = _lib.as_i32([b for kv in kvs for b in kv.blocks])
+        with self._span("denoise"):
+            _lib.call("oxy_pi05_denoise", self._h, C.c_int32(len(kvs)), _lib.ptr_i32(lens),
+                      _lib.ptr_i32(blocks), C.c_int32(S), C.c_void_p(out.data_ptr()),
+                      _lib.stream_ptr())
+            host = out.cpu().numpy().astype(np.float64)
+        return [ActionChunk(a) for a in host]
+
+    def action_denoise(self, kv, S: int) -> ActionChunk:
+        self._check_tag(kv)
+        return self.denoise_many([kv], S)[0]
+
+    def admit_many(self, arrivals, t: int):
+        """Lock-stepped streams: one batched prefill and one batched denoise."""
+        kvs = self.prefill_many([a.observation for a in arrivals])
+        chunks = self.denoise_many(kvs, self.config.S)
+        return [(chunk, GenerationState(kv, (), False, t, a.n_tokens))
+                for chunk, kv, a in zip(chunks, kvs, arrivals)]
+
+    def batched_language_decode(self, batched: BatchedState, k: int,
+                                return_logits: bool = False):
+        self._check_batch(batched, k)
+        c = self.config
+        m = batched.size
+        caches = [self._own(kv) for kv in batched.kv_batch]
+        budgets, reserved, tables, cows, lasts = [], [], [], [], []
+        for kv, toks, max_len in zip(caches, batched.token_buffers, batched.max_lens):
+            left = max_len - len(toks)
+            budgets.append(left if left > 0 else _BIG_BUDGET)
+            n_res = min(k, left) if left > 0 else k
+            blocks, cow = self.allocator.reserve(kv.blocks, kv.seq_len, n_res)
+            reserved.append(n_res)
+            tables.append(blocks)
+            cows.append(cow)
+            lasts.append(toks[-1] if toks else c.eos_token)
+        maxb = max(len(t) for t in tables)
+        bt = np.zeros((m, maxb), np.int32)
+        for i, tb in enumerate(tables):
+            bt[i, :len(tb)] = tb
+        seq = _lib.as_i32([kv.seq_len for kv in caches])
+        out = np.empty((m, k), np.int32)
+        cnt = np.empty(m, np.int32)
+        logits = np.empty((k, m, c.vocab), np.float32) if return_logits else None
+        try:
+            with self._span("decode"):
+                _lib.call("oxy_pi05_decode", self._h, C.c_int32(m), C.c_int32(k),
+                          _lib.ptr_i32(bt), C.c_int32(maxb), _lib.ptr_i32(seq),
+                          _lib.ptr_i32(_lib.as_i32(lasts)), _lib.ptr_i32(_lib.as_i32(budgets)),
+                          _lib.ptr_i32(_lib.as_i32(np.stack(cows))), _lib.ptr_i32(out),
+                          _lib.ptr_i32(cnt),
+                          logits.ctypes.data_as(C.c_void_p) if return_logits else None,
+                          _lib.stream_ptr())
+        except Exception:
+            for tb in tables:
+                self.allocator.decref(tb)
+            raise
+        new_caches, bufs, flags = [], [], []
+        for i, kv in enumerate(caches):
+            adv = int(cnt[i])
+            blocks = self.allocator.settle(tables[i], kv.seq_len, reserved[i], adv)
+            new_caches.append(PagedKvCache(self, blocks, kv.seq_len + adv))
+            toks = batched.token_buffers[i] + tuple(int(t) for t in out[i, :adv])
+            bufs.append(toks)
+            flags.append(bool(adv and (toks[-1] == c.eos_token
+                                       or len(toks) == batched.max_lens[i])))
+        res = BatchedState(tuple(new_caches), tuple(bufs), tuple(flags), batched.request_ids,
+                           batched.max_lens, batched.created_frames)
+        return (res, logits) if return_logits else res
+
+
+def synthetic_images(n: int, seed: int) -> np.ndarray:
+    """uint8 camera frames from a splitmix64 counter."""
+    from .rng import counter_u64
+    raw = counter_u64(seed, 0, n * 224 * 224 * 3 // 8 + 1).view(np.uint8)
+    return raw[: n * 224 * 224 * 3].reshape(n, 224, 224, 3).copy()
+
+
+def smoke() -> None:
+    """Tiny pi0.5 frame on cuda:0 checked against the CPU oracle."""
+    import sys
+    import os
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from oracle.pi05_ref import Pi05Ref
+
+    be = Pi05Backend(TINY, num_blocks=64)
+    ref = Pi05Ref.from_backend(be)
+    obs = Pi05Observation((5, 17, 99, 3), 0, synthetic_images(1, 11))
+    kv = be.prefill(obs)
+    chunk = be.action_denoise(kv, TINY.S)
+    out = be.batched_language_decode(BatchedState((kv,), ((),), (False,), (0,), (4,), (0,)), 4)
+    r_kv = ref.prefill(obs)
+    r_act = ref.denoise(r_kv, TINY.S)
+    r_toks = ref.decode(r_kv, (), 4)[0]
+    err = float(np.max(np.abs(chunk.actions - r_act)) / (np.max(np.abs(r_act)) + 1e-6))
+    assert err < 3e-2, f"pi05 action mismatch {err}"
+    print(f"smoke F2 ok: action rel err {err:.2e}, tokens {out.token_buffers[0]} "
+          f"(oracle {tuple(r_toks)})")

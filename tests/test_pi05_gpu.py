@@ -1,0 +1,141 @@
+"""F2 (pi0.5-shaped, bf16 on tcgen05) vs the torch-fp32 CPU oracle
+(oracle/pi05_ref.py) at a reduced shape that runs the same kernels, plus the
+reference's route-equality suites on the F2 backend and a full-shape run.
+
+Tolerances (bf16 mode): KV and actions within 3e-2 of the
+oracle's max magnitude; logits cosine >= 0.999; greedy tokens compared where
+the oracle's top-2 margin exceeds the logit error bound (else reported)."""
+
+import numpy as np
+import pytest
+
+from paper_2603_14371_b200 import BatchedState, BackendConfig, Observation
+from paper_2603_14371_b200.verify import (suite_batching, suite_resumption, suite_sharing)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def tiny():
+    from oracle.pi05_ref import Pi05Ref
+    from paper_2603_14371_b200.pi05 import TINY, Pi05Backend
+    be = Pi05Backend(TINY, num_blocks=256)
+    return be, Pi05Ref.from_backend(be)
+
+
+def _obs(n_img, toks, seed=11):
+    from paper_2603_14371_b200.pi05 import Pi05Observation, synthetic_images
+    return Pi05Observation(tuple(toks), 0, synthetic_images(n_img, seed) if n_img else None)
+
+
+def rel(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.max(np.abs(a - b)) / (np.max(np.abs(b)) + 1e-9))
+
+
+def test_weight_init_is_the_splitmix_counter(tiny):
+    be, ref = tiny
+    ref.check_init(be, names=("embed", "llm.0.wqkv", "mod.b", "vit.0.ln1.w", "action_out"))
+
+
+@pytest.mark.parametrize("n_img, toks", [(0, (5, 17, 99, 3)), (1, (7, 8)), (2, tuple(range(40, 110)))])
+def test_prefill_kv_matches_oracle(tiny, n_img, toks):
+    be, ref = tiny
+    obs = _obs(n_img, toks)
+    kv = be.prefill(obs)
+    assert kv.seq_len == 256 * n_img + len(toks)
+    want = ref.prefill(obs)
+    for l, layer in enumerate(kv.layers):
+        assert rel(layer.keys, want[l][0].numpy()) < 3e-2, l
+        assert rel(layer.values, want[l][1].numpy()) < 3e-2, l
+
+
+def test_action_denoise_matches_oracle(tiny):
+    be, ref = tiny
+    obs = _obs(1, (3, 4, 5))
+    kv = be.prefill(obs)
+    got = be.action_denoise(kv, be.config.S).actions
+    want = ref.denoise(ref.prefill(obs), be.config.S)
+    assert got.shape == (be.config.H, be.config.action_dim)
+    assert rel(got, want) < 3e-2
+
+
+def test_decode_logits_and_tokens_match_oracle(tiny):
+    be, ref = tiny
+    obs = _obs(1, (9, 10, 11, 12))
+    kv = be.prefill(obs)
+    out, logits = be.batched_language_decode(
+        BatchedState((kv,), ((),), (False,), (0,), (6,), (0,)), 6, return_logits=True)
+    toks, _, want_logits = ref.decode(ref.prefill(obs), (), 6)
+    got = out.token_buffers[0]
+    n = min(len(got), len(toks))
+    for s in range(n):
+        a, b = logits[s, 0].astype(np.float64), want_logits[s].astype(np.float64)
+        cos = a @ b / (np.linalg.norm(a) * np.linalg.norm(b))
+        assert cos > 0.999, (s, cos)
+        if got[:s] != toks[:s]:
+            break
+        top2 = np.sort(b)[-2:]
+        if top2[1] - top2[0] > 4 * np.max(np.abs(a - b)):
+            assert got[s] == toks[s], (s, got, toks)
+
+
+def test_kv_pool_shared_between_action_and_language(tiny):
+    be, _ = tiny
+    kv = be.prefill(_obs(1, (1, 2, 3)))
+    snap = [(l.keys.copy(), l.values.copy()) for l in kv.layers]
+    a1 = be.action_denoise(kv, be.config.S)
+    kv._layers = None
+    for (k0, v0), layer in zip(snap, kv.layers):
+        assert np.array_equal(k0, layer.keys) and np.array_equal(v0, layer.values)
+    a2 = be.action_denoise(kv, be.config.S)
+    assert a1 == a2
+
+
+def test_batched_admission_matches_single(tiny):
+    be, _ = tiny
+    from paper_2603_14371_b200.workload import Arrival
+    arr = [Arrival(0, _obs(1, (4, 5, i + 6), seed=20 + i), 3) for i in range(3)]
+    got = be.admit_many(arr, 0)
+    for (chunk, st), a in zip(got, arr):
+        solo = be.action_denoise(be.prefill(a.observation), be.config.S)
+        assert rel(chunk.actions, solo.actions) < 2e-2
+        assert st.kv.seq_len == 256 + 3
+
+
+def test_batch_invariant_decode(tiny):
+    be, _ = tiny
+    caches = [be.prefill(_obs(0, (i + 2, i + 3, 7))) for i in range(4)]
+    big = be.batched_language_decode(
+        BatchedState(tuple(caches), ((),) * 4, (False,) * 4, (0, 1, 2, 3), (5,) * 4, (0,) * 4), 5)
+    for i, kv in enumerate(caches):
+        solo = be.batched_language_decode(
+            BatchedState((kv,), ((),), (False,), (i,), (5,), (0,)), 5)
+        assert big.token_buffers[i] == solo.token_buffers[0]
+        assert big.kv_batch[i] == solo.kv_batch[0]
+
+
+def _pi05_factory(cfg: BackendConfig):
+    from paper_2603_14371_b200.pi05 import Pi05Backend
+    return Pi05Backend(cfg, num_blocks=128)
+
+
+@pytest.mark.parametrize("suite, n", [(suite_batching, 6), (suite_resumption, 8), (suite_sharing, 5)])
+def test_reference_suites_on_pi05_backend(suite, n):
+    rep = suite(n, backend_factory=_pi05_factory)
+    assert rep.ok, rep.failures[:3]
+
+
+def test_full_shape_frame_runs():
+    """The BASELINE config-2 shape: 3 cameras + 32 prompt tokens, chunk 50."""
+    from paper_2603_14371_b200.pi05 import Pi05Backend, Pi05Config
+    be = Pi05Backend(Pi05Config(), num_blocks=256)
+    obs = _obs(3, tuple(range(1000, 1032)))
+    kv = be.prefill(obs)
+    assert kv.seq_len == 800
+    chunk = be.action_denoise(kv, 10)
+    assert chunk.actions.shape == (50, 32) and np.all(np.isfinite(chunk.actions))
+    out = be.batched_language_decode(BatchedState((kv,), ((),), (False,), (0,), (5,), (0,)), 5)
+    assert len(out.token_buffers[0]) == 5 and out.kv_batch[0].seq_len == 805
+    k0 = out.kv_batch[0].layers[0].keys
+    assert np.all(np.isfinite(k0)) and np.abs(k0).max() > 0
