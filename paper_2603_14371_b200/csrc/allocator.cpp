@@ -24,6 +24,7 @@ namespace oxy {
 
 static thread_local std::string g_err;
 unsigned long long g_launches = 0;
+unsigned long long g_devbuf_reallocs = 0;
 
 void set_error(const char *fmt, ...) {
   char buf[1024];

@@ -15,6 +15,8 @@
 namespace oxy {
 // kernels launched by this library (read by bench.py as gpu_launches)
 extern unsigned long long g_launches;
+// scratch reallocations (invalidates captured CUDA graphs)
+extern unsigned long long g_devbuf_reallocs;
 }
 
 #define OXY_LAUNCH_CHECK()                                  \
@@ -46,6 +48,7 @@ struct DevBuf {
   size_t bytes = 0;
   void *get(size_t need) {
     if (need > bytes) {
+      ++g_devbuf_reallocs;
       if (ptr) cudaFree(ptr);
       size_t cap = need + need / 2 + 256;
       OXY_CUDA(cudaMalloc(&ptr, cap));

@@ -670,13 +670,156 @@ __global__ void decode_merge_kernel(const float *ws, bf16 *out, const int *pos, 
   out[(size_t)r * Q_HEADS * HEAD_DIM + h * HEAD_DIM + d] = __float2bfloat16(acc / L);
 }
 
+// Tensor-core variant (used): CTA = (row, 64-key block), 4 warps.  The
+// block's K and V (2 x 32 KB, one pool block per layer) are staged in smem
+// with 16-byte cp.async; the 8 query heads are the 16-row MMA A tile (rows
+// 8..15 zero); warp w owns keys 16w..16w+15: S = Q K^T (16 MMAs x 2), online
+// softmax in registers, O = P V (32 MMAs), then the 4 warps' (m, l, O) are
+// merged in smem into one partial per block.  HBM-bound: 64 KB per CTA.
+constexpr int DM_LDS = HEAD_DIM + 8;
+constexpr size_t DM_SMEM = (size_t)(16 + 2 * KV_BLOCK) * DM_LDS * sizeof(bf16);
+
+__global__ void __launch_bounds__(128)
+    decode_attn_mma_kernel(const bf16 *q, const bf16 *kpool, const bf16 *vpool, const int *bt, int bt_stride,
+                           const int *pos, const int *active, int max_blocks, float scale_log2, float *ws) {
+  extern __shared__ __align__(16) unsigned char dm_smem[];
+  bf16 *sQ = reinterpret_cast<bf16 *>(dm_smem);
+  bf16 *sK = sQ + 16 * DM_LDS;
+  bf16 *sV = sK + KV_BLOCK * DM_LDS;
+  const int r = blockIdx.x, blk = blockIdx.y;
+  if (active && !active[r]) return;
+  const int n_keys = pos[r] + 1;
+  const int k0 = blk * KV_BLOCK;
+  if (k0 >= n_keys) return;
+  const int nvalid = min(KV_BLOCK, n_keys - k0);
+  const int b = bt[(size_t)r * bt_stride + blk];
+  const bf16 *kb = kpool + (size_t)b * KV_BLOCK * HEAD_DIM;
+  const bf16 *vb = vpool + (size_t)b * KV_BLOCK * HEAD_DIM;
+  const bf16 *qr = q + (size_t)r * Q_HEADS * HEAD_DIM;
+  for (int i = threadIdx.x; i < KV_BLOCK * 32; i += 128) {
+    const int row = i >> 5, ch = i & 31;
+    if (row < nvalid) {
+      cp_async16(smem_addr(sK + row * DM_LDS + ch * 8), kb + (size_t)row * HEAD_DIM + ch * 8);
+      cp_async16(smem_addr(sV + row * DM_LDS + ch * 8), vb + (size_t)row * HEAD_DIM + ch * 8);
+    } else {
+      *reinterpret_cast<int4 *>(sK + row * DM_LDS + ch * 8) = make_int4(0, 0, 0, 0);
+      *reinterpret_cast<int4 *>(sV + row * DM_LDS + ch * 8) = make_int4(0, 0, 0, 0);
+    }
+  }
+  for (int i = threadIdx.x; i < 16 * 32; i += 128) {
+    const int row = i >> 5, ch = i & 31;
+    if (row < Q_HEADS) cp_async16(smem_addr(sQ + row * DM_LDS + ch * 8), qr + (size_t)row * HEAD_DIM + ch * 8);
+    else *reinterpret_cast<int4 *>(sQ + row * DM_LDS + ch * 8) = make_int4(0, 0, 0, 0);
+  }
+  cp_commit();
+  cp_wait<0>();
+  __syncthreads();
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+  const uint32_t qa = smem_addr(sQ + (lane & 15) * DM_LDS + (lane >> 4) * 8);
+  const int kkey = warp * 16 + (lane & 7) + ((lane >> 4) << 3);
+  const uint32_t ka = smem_addr(sK + kkey * DM_LDS + ((lane >> 3) & 1) * 8);
+#pragma unroll
+  for (int kk = 0; kk < HEAD_DIM / 16; ++kk) {
+    uint32_t a0, a1, a2, a3, b0, b1, b2, b3;
+    ldsm_x4(qa + kk * 32, a0, a1, a2, a3);
+    ldsm_x4(ka + kk * 32, b0, b1, b2, b3);
+    mma16816(s[0], a0, a1, a2, a3, b0, b1);
+    mma16816(s[1], a0, a1, a2, a3, b2, b3);
+  }
+  // softmax over this warp's 16 keys for query row g = lane >> 2 (heads; rows 8..15 pad)
+  float mx = -INFINITY;
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int key = warp * 16 + nt * 8 + (lane & 3) * 2 + (e & 1);
+      float v = s[nt][e] * scale_log2;
+      if (key >= nvalid) v = -INFINITY;
+      s[nt][e] = v;
+      if (e < 2) mx = fmaxf(mx, v);
+    }
+  mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+  mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+  float l = 0.f;
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float p = (e < 2 && mx != -INFINITY) ? exp2f(s[nt][e] - mx) : 0.f;
+      s[nt][e] = p;
+      l += p;
+    }
+  l += __shfl_xor_sync(0xffffffffu, l, 1);
+  l += __shfl_xor_sync(0xffffffffu, l, 2);
+  const uint32_t pa0 = pack_bf16(s[0][0], s[0][1]), pa1 = pack_bf16(s[0][2], s[0][3]);
+  const uint32_t pa2 = pack_bf16(s[1][0], s[1][1]), pa3 = pack_bf16(s[1][2], s[1][3]);
+  float o[32][4];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  const uint32_t va = smem_addr(sV + (warp * 16 + (lane & 15)) * DM_LDS + (lane >> 4) * 8);
+#pragma unroll
+  for (int np = 0; np < 16; ++np) {
+    uint32_t b0, b1, b2, b3;
+    ldsm_x4_t(va + np * 32, b0, b1, b2, b3);
+    mma16816(o[2 * np], pa0, pa1, pa2, pa3, b0, b1);
+    mma16816(o[2 * np + 1], pa0, pa1, pa2, pa3, b2, b3);
+  }
+  __syncthreads();  // K/V smem is reused for the cross-warp merge
+  float *sO = reinterpret_cast<float *>(sK);                  // [4][8][256]
+  float *sM = reinterpret_cast<float *>(sQ);                  // [4][8] m, then [4][8] l
+  const int g = lane >> 2;
+#pragma unroll
+  for (int nt = 0; nt < 32; ++nt) {
+    const int c = nt * 8 + (lane & 3) * 2;
+    sO[(warp * 8 + g) * HEAD_DIM + c] = o[nt][0];
+    sO[(warp * 8 + g) * HEAD_DIM + c + 1] = o[nt][1];
+  }
+  if ((lane & 3) == 0) {
+    sM[warp * 8 + g] = mx;
+    sM[32 + warp * 8 + g] = l;
+  }
+  __syncthreads();
+  float *part = ws + ((size_t)r * max_blocks + blk) * DA_PART;
+  for (int i = threadIdx.x; i < Q_HEADS * HEAD_DIM; i += 128) {
+    const int h = i / HEAD_DIM, d = i % HEAD_DIM;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) M = fmaxf(M, sM[w * 8 + h]);
+    float acc = 0.f;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const float mw = sM[w * 8 + h];
+      if (mw != -INFINITY) acc += sO[(w * 8 + h) * HEAD_DIM + d] * exp2f(mw - M);
+    }
+    part[h * (HEAD_DIM + 2) + d] = acc;
+    if (d == 0) {
+      float L = 0.f;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const float mw = sM[w * 8 + h];
+        if (mw != -INFINITY) L += sM[32 + w * 8 + h] * exp2f(mw - M);
+      }
+      part[h * (HEAD_DIM + 2) + HEAD_DIM] = M;
+      part[h * (HEAD_DIM + 2) + HEAD_DIM + 1] = L;
+    }
+  }
+}
+
 void decode_attention(const bf16 *q, bf16 *out, const bf16 *kpool, const bf16 *vpool, const int *bt,
                       int bt_stride, const int *pos, const int *active, int rows, int max_blocks,
                       float scale, float *ws, cudaStream_t st) {
   if (rows <= 0) return;
+  static bool attr = false;
+  if (!attr) {
+    OXY_CUDA(cudaFuncSetAttribute(decode_attn_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)DM_SMEM));
+    attr = true;
+  }
   const float sl2 = scale * 1.4426950408889634f;
-  decode_attn_kernel<<<dim3(rows, max_blocks), DA_THREADS, 0, st>>>(q, kpool, vpool, bt, bt_stride, pos,
-                                                                    active, max_blocks, sl2, ws);
+  decode_attn_mma_kernel<<<dim3(rows, max_blocks), 128, DM_SMEM, st>>>(q, kpool, vpool, bt, bt_stride, pos,
+                                                                       active, max_blocks, sl2, ws);
   OXY_LAUNCH_CHECK();
   decode_merge_kernel<<<dim3(rows, Q_HEADS), HEAD_DIM, 0, st>>>(ws, out, pos, active, max_blocks);
   OXY_LAUNCH_CHECK();

@@ -16,6 +16,7 @@
 // splitmix64 counter draws, U(+-sqrt(3/fan_in)) for matrices.
 #include <cmath>
 #include <cstring>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -79,19 +80,20 @@ struct Model {
   DevBuf mod;                        // [S, n_mod] f32
   // scratch
   DevBuf x, y, qkv, q, o, hmid, ws, ints, kd, vd, attn_groups, attn_ws, attn_ml, logits, amv, ami,
-      vit_h, vit_y, vit_qkv, vit_o, vit_m, patches, act, act_bf, vel, xe, dec_ws, host_img;
+      vit_h, vit_y, vit_qkv, vit_o, vit_m, patches, act, act_bf, vel, xe, dec_ws, kvread_i, kvread_f;
   cudaEvent_t ev = nullptr;
 
   bf16 *kpool(int l) { return pool + l * layer_stride; }
   bf16 *vpool(int l) { return pool + l * layer_stride + kv_stride; }
 
   ~Model() {
+    destroy_exec();
     cudaFree(wmem);
     cudaFree(pool);
     cudaFree(noise);
     for (DevBuf *b : {&mod, &x, &y, &qkv, &q, &o, &hmid, &ws, &ints, &kd, &vd, &attn_groups, &attn_ws,
                       &attn_ml, &logits, &amv, &ami, &vit_h, &vit_y, &vit_qkv, &vit_o, &vit_m, &patches,
-                      &act, &act_bf, &vel, &xe, &dec_ws, &host_img})
+                      &act, &act_bf, &vel, &xe, &dec_ws, &kvread_i, &kvread_f})
       b->release();
   }
 
@@ -247,111 +249,177 @@ struct Model {
     normal_noise(tmp, (int64_t)c.H * c.action_dim, c.seed ^ 0x6E6F697365ull, st);  // "noise"
     OXY_CUDA(cudaMemcpy2DAsync(noise, apad() * sizeof(float), tmp, c.action_dim * sizeof(float),
                                c.action_dim * sizeof(float), c.H, cudaMemcpyDeviceToDevice, st));
+    OXY_CUDA(cudaStreamSynchronize(st));
+    init_exec();
   }
 
-  // ------------------------------------------------------------ helpers
-  void gemm(cudaStream_t st, const bf16 *w, const bf16 *xin, int n_out, int k, int t, int mode, void *out,
-            int ldo, const float *bias = nullptr, const float *gate = nullptr) {
+  // ------------------------------------------------------------ execution
+  // Every call = host planning (all per-call integers and attention
+  // descriptors packed into one stable device arena, uploaded with a single
+  // H2D copy) + a kernel-only body.  The body runs eagerly the first time a
+  // shape is seen (sizing the grow-only scratch), is captured into a CUDA
+  // graph the second time and replayed from then on.  Any scratch regrowth
+  // bumps a generation counter that invalidates captured graphs.
+  cudaStream_t mst = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  uint8_t *arena_d = nullptr;
+  std::vector<uint8_t> arena_h;
+  size_t arena_cap = 0, arena_used = 0;
+  struct Graph {
+    cudaGraphExec_t exec = nullptr;
+    unsigned long long gen = 0;
+    int seen = 0;
+  };
+  std::map<std::string, Graph> graphs;
+  bool use_graphs = true;
+
+  void init_exec() {
+    OXY_CUDA(cudaStreamCreateWithFlags(&mst, cudaStreamNonBlocking));
+    OXY_CUDA(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
+    OXY_CUDA(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
+    arena_cap = 8u << 20;
+    OXY_CUDA(cudaMalloc(&arena_d, arena_cap));
+    arena_h.resize(arena_cap);
+  }
+  void destroy_exec() {
+    for (auto &kv : graphs)
+      if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    if (mst) cudaStreamDestroy(mst);
+    if (ev_in) cudaEventDestroy(ev_in);
+    if (ev_out) cudaEventDestroy(ev_out);
+    cudaFree(arena_d);
+  }
+  void enter(cudaStream_t caller) {
+    OXY_CUDA(cudaEventRecord(ev_in, caller));
+    OXY_CUDA(cudaStreamWaitEvent(mst, ev_in, 0));
+  }
+  void leave(cudaStream_t caller) {
+    OXY_CUDA(cudaEventRecord(ev_out, mst));
+    OXY_CUDA(cudaStreamWaitEvent(caller, ev_out, 0));
+  }
+  template <typename T>
+  T *arena_put(const T *src, size_t n) {
+    const size_t off = (arena_used + 15) & ~static_cast<size_t>(15);
+    const size_t bytes = n * sizeof(T);
+    if (off + bytes > arena_cap) fail(OXY_EINVAL, "call too large for the planning arena (%zu bytes)", off + bytes);
+    if (src) std::memcpy(arena_h.data() + off, src, bytes);
+    else std::memset(arena_h.data() + off, 0, bytes);
+    arena_used = off + bytes;
+    return reinterpret_cast<T *>(arena_d + off);
+  }
+  void arena_upload() {
+    if (arena_used)
+      OXY_CUDA(cudaMemcpyAsync(arena_d, arena_h.data(), arena_used, cudaMemcpyHostToDevice, mst));
+  }
+
+  template <typename F>
+  void run_body(const std::string &key, bool allow_graph, F &&body) {
+    if (!use_graphs || !allow_graph) {
+      body();
+      return;
+    }
+    Graph &g = graphs[key];
+    if (g.exec && g.gen == g_devbuf_reallocs) {
+      OXY_CUDA(cudaGraphLaunch(g.exec, mst));
+      return;
+    }
+    if (g.exec) {
+      cudaGraphExecDestroy(g.exec);
+      g.exec = nullptr;
+    }
+    if (g.seen++ == 0) {
+      body();
+      return;
+    }
+    const unsigned long long gen0 = g_devbuf_reallocs;
+    cudaGraph_t graph = nullptr;
+    OXY_CUDA(cudaStreamBeginCapture(mst, cudaStreamCaptureModeThreadLocal));
+    try {
+      body();
+    } catch (...) {
+      cudaStreamEndCapture(mst, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      throw;
+    }
+    OXY_CUDA(cudaStreamEndCapture(mst, &graph));
+    if (g_devbuf_reallocs != gen0) fail(OXY_ESTATE, "scratch reallocated during graph capture");
+    OXY_CUDA(cudaGraphInstantiate(&g.exec, graph, 0));
+    cudaGraphDestroy(graph);
+    g.gen = g_devbuf_reallocs;
+    OXY_CUDA(cudaGraphLaunch(g.exec, mst));
+  }
+
+  // split-K workspace is reserved by plan_gemm(); gemm() only fetches it
+  size_t ws_need = 0;
+  void plan_gemm(int n_out, int k, int t) {
+    if (t <= 0) return;
+    gemm::Plan p = gemm::make_plan(n_out, k, t, sms);
+    if (p.splits > 1) ws_need = std::max(ws_need, (size_t)p.splits * t * n_out);
+  }
+  void gemm(const bf16 *w, const bf16 *xin, int n_out, int k, int t, int mode, void *out, int ldo,
+            const float *bias = nullptr, const float *gate = nullptr) {
     if (t <= 0) return;
     gemm::Plan plan = gemm::make_plan(n_out, k, t, sms);
     float *wsp = plan.splits > 1 ? ws.as<float>((size_t)plan.splits * t * n_out) : nullptr;
     EpiParams e{mode, out, ldo, bias, nullptr, 0, gate};
-    gemm::launch(w, xin, n_out, k, t, e, plan, wsp, st);
+    gemm::launch(w, xin, n_out, k, t, e, plan, wsp, mst);
   }
 
-  // attention over groups already laid out on the host
-  void attend(cudaStream_t st, std::vector<AttnGroup> &groups, int head_dim, const bf16 *kp, const bf16 *vp) {
-    if (groups.empty()) return;
-    int max_nq = 0, max_tiles = 0, rows = 0;
+  struct AttnPlan {
+    AttnGroup *groups = nullptr;
+    int n = 0, q_tiles = 0, splits = 1, hd = 256, rows = 0, max_tiles = 0;
+  };
+  size_t attn_ws_need = 0, attn_ml_need = 0;
+  // pass 1: shapes only (reserve workspace); pass 2 (after scratch is final): upload descriptors
+  AttnPlan shape_attention(std::vector<AttnGroup> &groups, int head_dim) {
+    AttnPlan p;
+    p.n = (int)groups.size();
+    p.hd = head_dim;
+    int max_nq = 0;
     for (auto &g : groups) {
-      g.wrow0 = rows;
-      rows += g.nq;
+      g.wrow0 = p.rows;
+      p.rows += g.nq;
       max_nq = std::max(max_nq, g.nq);
-      max_tiles = std::max(max_tiles, (g.nka + 63) / 64 + (g.nkb + 63) / 64);
+      p.max_tiles = std::max(p.max_tiles, (g.nka + 63) / 64 + (g.nkb + 63) / 64);
     }
-    const int q_tiles = (max_nq + 63) / 64;
-    const int ctas = (int)groups.size() * q_tiles;
-    int splits = 1;
-    if (ctas < sms && max_tiles > 1) splits = std::min(max_tiles, std::max(1, (2 * sms) / ctas));
-    AttnGroup *gd = attn_groups.as<AttnGroup>(groups.size());
-    OXY_CUDA(cudaMemcpyAsync(gd, groups.data(), groups.size() * sizeof(AttnGroup), cudaMemcpyHostToDevice, st));
+    p.q_tiles = (max_nq + 63) / 64;
+    const int ctas = p.n * p.q_tiles;
+    if (ctas < sms && p.max_tiles > 1) p.splits = std::min(p.max_tiles, std::max(1, (2 * sms) / ctas));
+    if (p.splits > 1) {
+      const int hdp = head_dim == 256 ? 256 : 80;
+      attn_ws_need = std::max(attn_ws_need, (size_t)p.splits * p.rows * hdp);
+      attn_ml_need = std::max(attn_ml_need, (size_t)p.splits * p.rows * 2);
+    }
+    return p;
+  }
+  void attend(const AttnPlan &p, const bf16 *kp, const bf16 *vp) {
+    if (!p.n) return;
     float *wo = nullptr, *wml = nullptr;
-    const int hdp = head_dim == 256 ? 256 : 80;
-    if (splits > 1) {
-      wo = attn_ws.as<float>((size_t)splits * rows * hdp);
-      wml = attn_ml.as<float>((size_t)splits * rows * 2);
+    if (p.splits > 1) {
+      const int hdp = p.hd == 256 ? 256 : 80;
+      wo = attn_ws.as<float>((size_t)p.splits * p.rows * hdp);
+      wml = attn_ml.as<float>((size_t)p.splits * p.rows * 2);
     }
-    flash_attention(gd, (int)groups.size(), q_tiles, head_dim, kp, vp, 1.f / std::sqrt((float)head_dim),
-                    splits, max_tiles, wo, wml, rows, st);
+    flash_attention(p.groups, p.n, p.q_tiles, p.hd, kp, vp, 1.f / std::sqrt((float)p.hd), p.splits, p.max_tiles,
+                    wo, wml, p.rows, mst);
   }
-
-  // host staging for small int arrays: one H2D copy
-  int *upload_ints(cudaStream_t st, const std::vector<int> &h) {
-    int *d = ints.as<int>(h.size());
-    OXY_CUDA(cudaMemcpyAsync(d, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-    return d;
-  }
-
-  // ------------------------------------------------------------ vision
-  // images_d: uint8 [n_img, 224, 224, 3]; writes projected tokens to out (f32, ld W)
-  void vision(cudaStream_t st, const uint8_t *images_d, int n_img, float *out_rows, const int *dst_row,
-              int n_obs, const int *imgs_per_obs) {
-    const int Dv = c.vit_width, T = n_img * 256, W = c.width, nh = c.vit_heads, hd = Dv / nh;
-    bf16 *pt = patches.as<bf16>((size_t)T * PATCH_K);
-    patchify(images_d, n_img, pt, PATCH_K, st);
-    float *h = vit_h.as<float>((size_t)T * Dv);
-    bf16 *yv = vit_y.as<bf16>((size_t)T * Dv);
-    bf16 *qkvv = vit_qkv.as<bf16>((size_t)T * 3 * Dv);
-    bf16 *ov = vit_o.as<bf16>((size_t)T * Dv);
-    bf16 *mv = vit_m.as<bf16>((size_t)T * c.vit_mlp);
-    tile_rows(h, Dv, vpos, Dv, T, 256, Dv, st);
-    gemm(st, vpatch, pt, Dv, PATCH_K, T, gemm::EPI_ADD_F32, h, Dv, vpatch_b);
-    std::vector<AttnGroup> groups;
-    for (int im = 0; im < n_img; ++im)
-      for (int hh = 0; hh < nh; ++hh) {
-        AttnGroup g{};
-        g.q = qkvv + (size_t)im * 256 * 3 * Dv + hh * hd;
-        g.ldq = 3 * Dv;
-        g.o = ov + (size_t)im * 256 * Dv + hh * hd;
-        g.ldo = Dv;
-        g.nq = 256;
-        g.kb = g.q + Dv;
-        g.vb = g.q + 2 * Dv;
-        g.ldkv = 3 * Dv;
-        g.nkb = 256;
-        groups.push_back(g);
-      }
-    for (int l = 0; l < c.vit_depth; ++l) {
-      const VitW &w = V[l];
-      layernorm(h, Dv, yv, Dv, w.ln1w, w.ln1b, T, Dv, 1e-6f, st);
-      gemm(st, w.wqkv, yv, 3 * Dv, Dv, T, gemm::EPI_BF16, qkvv, 3 * Dv, w.bqkv);
-      std::vector<AttnGroup> gs = groups;
-      attend(st, gs, hd, nullptr, nullptr);
-      gemm(st, w.wo, ov, Dv, Dv, T, gemm::EPI_ADD_F32, h, Dv, w.bo);
-      layernorm(h, Dv, yv, Dv, w.ln2w, w.ln2b, T, Dv, 1e-6f, st);
-      gemm(st, w.w1, yv, c.vit_mlp, Dv, T, gemm::EPI_GELU_BF16, mv, c.vit_mlp, w.b1);
-      gemm(st, w.w2, mv, Dv, c.vit_mlp, T, gemm::EPI_ADD_F32, h, Dv, w.b2);
-    }
-    layernorm(h, Dv, yv, Dv, vln_w, vln_b, T, Dv, 1e-6f, st);
-    int img0 = 0;
-    for (int i = 0; i < n_obs; ++i) {
-      const int ni = imgs_per_obs[i];
-      if (ni > 0)
-        gemm(st, vproj, yv + (size_t)img0 * 256 * Dv, W, Dv, ni * 256, gemm::EPI_F32,
-             out_rows + (size_t)dst_row[i] * W, W, vproj_b);
-      img0 += ni;
-    }
+  void reserve_common() {
+    if (ws_need) ws.as<float>(ws_need);
+    if (attn_ws_need) attn_ws.as<float>(attn_ws_need);
+    if (attn_ml_need) attn_ml.as<float>(attn_ml_need);
+    ws_need = attn_ws_need = attn_ml_need = 0;
   }
 
   // ------------------------------------------------------------ prefill
   // n_obs observations; obs i has n_img[i] images (in images_d order) and
   // n_txt[i] text tokens (concatenated in tokens_h); prefix = [images; text].
   // blocks_h: per obs ceil(P_i/64) block ids, concatenated.
-  void prefill(cudaStream_t st, int n_obs, const int *n_img, const int *n_txt, const int *tokens_h,
+  void prefill(cudaStream_t caller, int n_obs, const int *n_img, const int *n_txt, const int *tokens_h,
                const uint8_t *images_d, const int *blocks_h) {
-    const int W = c.width;
+    const int W = c.width, Dv = c.vit_width, nh = c.vit_heads, hd = nh ? Dv / nh : 72;
     std::vector<int> P(n_obs), off(n_obs), boff(n_obs);
     int T = 0, nb = 0, n_images = 0, n_tok = 0;
+    std::string key = "prefill";
     for (int i = 0; i < n_obs; ++i) {
       OXY_REQUIRE(n_img[i] >= 0 && n_txt[i] >= 0, "negative prefix part");
       OXY_REQUIRE(n_img[i] == 0 || c.vit_depth > 0, "this model has no vision tower");
@@ -363,66 +431,146 @@ struct Model {
       nb += (P[i] + KV_BLOCK - 1) / KV_BLOCK;
       n_images += n_img[i];
       n_tok += n_txt[i];
+      key += "/" + std::to_string(n_img[i]) + "," + std::to_string(n_txt[i]);
     }
     for (int i = 0; i < n_tok; ++i)
       OXY_REQUIRE(tokens_h[i] >= 0 && tokens_h[i] < c.vocab, "observation token %d outside vocab of %d",
                   tokens_h[i], c.vocab);
-    // ints: tokens(per row, -1 for image rows) | pos | slot | block tables
-    std::vector<int> h(3 * (size_t)T + nb);
-    int *tok = h.data(), *pos = tok + T, *slot = pos + T, *bt = slot + T;
-    std::memcpy(bt, blocks_h, nb * sizeof(int));
+    const int Tv = n_images * 256;
+    // ---- plan pass 1: reserve scratch
+    x.as<float>((size_t)T * W);
+    y.as<bf16>((size_t)T * W);
+    qkv.as<float>((size_t)T * QKV);
+    q.as<bf16>((size_t)T * QDIM);
+    o.as<bf16>((size_t)T * QDIM);
+    hmid.as<bf16>((size_t)T * c.mlp);
+    arena_used = 0;
+    plan_gemm(QKV, W, T);
+    plan_gemm(W, QDIM, T);
+    plan_gemm(2 * c.mlp, W, T);
+    plan_gemm(W, c.mlp, T);
+    std::vector<AttnGroup> g_llm(n_obs), g_vit;
+    for (int i = 0; i < n_obs; ++i) {
+      g_llm[i] = AttnGroup{};
+      g_llm[i].nq = P[i] * Q_HEADS;
+      g_llm[i].nka = P[i];
+    }
+    AttnPlan a_llm = shape_attention(g_llm, HEAD_DIM), a_vit;
+    if (Tv) {
+      patches.as<bf16>((size_t)Tv * PATCH_K);
+      vit_h.as<float>((size_t)Tv * Dv);
+      vit_y.as<bf16>((size_t)Tv * Dv);
+      vit_qkv.as<bf16>((size_t)Tv * 3 * Dv);
+      vit_o.as<bf16>((size_t)Tv * Dv);
+      vit_m.as<bf16>((size_t)Tv * c.vit_mlp);
+      plan_gemm(Dv, PATCH_K, Tv);
+      plan_gemm(3 * Dv, Dv, Tv);
+      plan_gemm(Dv, Dv, Tv);
+      plan_gemm(c.vit_mlp, Dv, Tv);
+      plan_gemm(Dv, c.vit_mlp, Tv);
+      for (int i = 0; i < n_obs; ++i) plan_gemm(W, Dv, n_img[i] * 256);
+      g_vit.resize((size_t)n_images * nh);
+      for (auto &g : g_vit) {
+        g = AttnGroup{};
+        g.nq = 256;
+        g.nkb = 256;
+      }
+      a_vit = shape_attention(g_vit, hd);
+    }
+    reserve_common();
+    // ---- plan pass 2: pointers are final; build the arena
+    float *X = x.as<float>(0);
+    bf16 *Y = y.as<bf16>(0), *Qb = q.as<bf16>(0), *Ob = o.as<bf16>(0), *Hm = hmid.as<bf16>(0);
+    float *QKVf = qkv.as<float>(0);
+    std::vector<int> tok(T), pos(T), slot(T);
     int ti = 0;
     for (int i = 0; i < n_obs; ++i)
       for (int p = 0; p < P[i]; ++p) {
         const int r = off[i] + p;
-        tok[r] = p < n_img[i] * 256 ? -1 : tokens_h[ti++];
+        tok[r] = p < n_img[i] * 256 ? 0 : tokens_h[ti++];
         pos[r] = p;
         slot[r] = blocks_h[boff[i] + p / KV_BLOCK] * KV_BLOCK + p % KV_BLOCK;
       }
-    int *dints = upload_ints(st, h);
-    int *d_pos = dints + T, *d_slot = dints + 2 * T, *d_bt = dints + 3 * T;
-    float *X = x.as<float>((size_t)T * W);
-    bf16 *Y = y.as<bf16>((size_t)T * W);
-    float *QKVf = qkv.as<float>((size_t)T * QKV);
-    bf16 *Qb = q.as<bf16>((size_t)T * QDIM);
-    bf16 *Ob = o.as<bf16>((size_t)T * QDIM);
-    bf16 *Hm = hmid.as<bf16>((size_t)T * c.mlp);
-    // text embeddings (rows with tok >= 0), image tokens from the vision tower
+    int *d_tok = arena_put(tok.data(), T), *d_pos = arena_put(pos.data(), T), *d_slot = arena_put(slot.data(), T);
+    int *d_bt = arena_put(blocks_h, nb);
     for (int i = 0; i < n_obs; ++i) {
-      const int r0 = off[i] + n_img[i] * 256;
-      embed_rows(X + (size_t)r0 * W, W, embed, dints + r0, nullptr, n_txt[i], W, std::sqrt((float)W), st);
-    }
-    if (n_images > 0) vision(st, images_d, n_images, X, off.data(), n_obs, n_img);
-    std::vector<AttnGroup> groups(n_obs);
-    for (int i = 0; i < n_obs; ++i) {
-      AttnGroup g{};
+      AttnGroup &g = g_llm[i];
       g.q = Qb + (size_t)off[i] * QDIM;
       g.ldq = HEAD_DIM;
       g.o = Ob + (size_t)off[i] * QDIM;
       g.ldo = HEAD_DIM;
-      g.nq = P[i] * Q_HEADS;
       g.bt = d_bt + boff[i];
-      g.nka = P[i];
-      groups[i] = g;
     }
-    for (int l = 0; l < c.depth; ++l) {
-      const LayerW &w = L[l];
-      rmsnorm(X, W, Y, W, w.ln1, nullptr, nullptr, T, W, 1e-6f, st);
-      gemm(st, w.wqkv, Y, QKV, W, T, gemm::EPI_F32, QKVf, QKV);
-      rope_split(QKVf, T, Q_HEADS, d_pos, d_slot, nullptr, Qb, kpool(l), vpool(l), nullptr, nullptr,
-                 10000.f, st);
-      if (l == c.depth - 1) break;  // the last block's output is not cached
-      std::vector<AttnGroup> gs = groups;
-      attend(st, gs, HEAD_DIM, kpool(l), vpool(l));
-      gemm(st, w.wo, Ob, W, QDIM, T, gemm::EPI_ADD_F32, X, W);
-      rmsnorm(X, W, Y, W, w.ln2, nullptr, nullptr, T, W, 1e-6f, st);
-      gemm(st, w.wgu, Y, 2 * c.mlp, W, T, gemm::EPI_GEGLU_BF16, Hm, c.mlp);
-      gemm(st, w.wd, Hm, W, c.mlp, T, gemm::EPI_ADD_F32, X, W);
+    a_llm.groups = arena_put(g_llm.data(), g_llm.size());
+    bf16 *pt = nullptr, *yv = nullptr, *qkvv = nullptr, *ov = nullptr, *mv = nullptr;
+    float *hv = nullptr;
+    if (Tv) {
+      pt = patches.as<bf16>(0);
+      hv = vit_h.as<float>(0);
+      yv = vit_y.as<bf16>(0);
+      qkvv = vit_qkv.as<bf16>(0);
+      ov = vit_o.as<bf16>(0);
+      mv = vit_m.as<bf16>(0);
+      for (int im = 0, gi = 0; im < n_images; ++im)
+        for (int hh = 0; hh < nh; ++hh, ++gi) {
+          AttnGroup &g = g_vit[gi];
+          g.q = qkvv + (size_t)im * 256 * 3 * Dv + hh * hd;
+          g.ldq = 3 * Dv;
+          g.o = ov + (size_t)im * 256 * Dv + hh * hd;
+          g.ldo = Dv;
+          g.kb = g.q + Dv;
+          g.vb = g.q + 2 * Dv;
+          g.ldkv = 3 * Dv;
+        }
+      a_vit.groups = arena_put(g_vit.data(), g_vit.size());
     }
+    enter(caller);
+    arena_upload();
+    if (Tv) patchify(images_d, n_images, pt, PATCH_K, mst);  // caller's buffer: outside the graph
+    auto body = [&]() {
+      for (int i = 0; i < n_obs; ++i) {
+        const int r0 = off[i] + n_img[i] * 256;
+        embed_rows(X + (size_t)r0 * W, W, embed, d_tok + r0, nullptr, n_txt[i], W, std::sqrt((float)W), mst);
+      }
+      if (Tv) {
+        tile_rows(hv, Dv, vpos, Dv, Tv, 256, Dv, mst);
+        gemm(vpatch, pt, Dv, PATCH_K, Tv, gemm::EPI_ADD_F32, hv, Dv, vpatch_b);
+        for (int l = 0; l < c.vit_depth; ++l) {
+          const VitW &w = V[l];
+          layernorm(hv, Dv, yv, Dv, w.ln1w, w.ln1b, Tv, Dv, 1e-6f, mst);
+          gemm(w.wqkv, yv, 3 * Dv, Dv, Tv, gemm::EPI_BF16, qkvv, 3 * Dv, w.bqkv);
+          attend(a_vit, nullptr, nullptr);
+          gemm(w.wo, ov, Dv, Dv, Tv, gemm::EPI_ADD_F32, hv, Dv, w.bo);
+          layernorm(hv, Dv, yv, Dv, w.ln2w, w.ln2b, Tv, Dv, 1e-6f, mst);
+          gemm(w.w1, yv, c.vit_mlp, Dv, Tv, gemm::EPI_GELU_BF16, mv, c.vit_mlp, w.b1);
+          gemm(w.w2, mv, Dv, c.vit_mlp, Tv, gemm::EPI_ADD_F32, hv, Dv, w.b2);
+        }
+        layernorm(hv, Dv, yv, Dv, vln_w, vln_b, Tv, Dv, 1e-6f, mst);
+        for (int i = 0, img0 = 0; i < n_obs; img0 += n_img[i], ++i)
+          if (n_img[i] > 0)
+            gemm(vproj, yv + (size_t)img0 * 256 * Dv, W, Dv, n_img[i] * 256, gemm::EPI_F32,
+                 X + (size_t)off[i] * W, W, vproj_b);
+      }
+      for (int l = 0; l < c.depth; ++l) {
+        const LayerW &w = L[l];
+        rmsnorm(X, W, Y, W, w.ln1, nullptr, nullptr, T, W, 1e-6f, mst);
+        gemm(w.wqkv, Y, QKV, W, T, gemm::EPI_F32, QKVf, QKV);
+        rope_split(QKVf, T, Q_HEADS, d_pos, d_slot, nullptr, Qb, kpool(l), vpool(l), nullptr, nullptr, 10000.f,
+                   mst);
+        if (l == c.depth - 1) break;  // the last block's output is not cached
+        attend(a_llm, kpool(l), vpool(l));
+        gemm(w.wo, Ob, W, QDIM, T, gemm::EPI_ADD_F32, X, W);
+        rmsnorm(X, W, Y, W, w.ln2, nullptr, nullptr, T, W, 1e-6f, mst);
+        gemm(w.wgu, Y, 2 * c.mlp, W, T, gemm::EPI_GEGLU_BF16, Hm, c.mlp);
+        gemm(w.wd, Hm, W, c.mlp, T, gemm::EPI_ADD_F32, X, W);
+      }
+    };
+    run_body(key, true, body);
+    leave(caller);
   }
 
   // ------------------------------------------------------------ action expert
-  void ensure_mod(cudaStream_t st, int S) {
+  void ensure_mod(int S) {
     if (mod_S == S) return;
     const int We = c.expert_width;
     // time embedding of t_s = 1 - s/S (openpi posemb_sincos: periods 4e-3 .. 4)
@@ -438,156 +586,201 @@ struct Model {
         temb[(size_t)s * We + half + i] = (float)std::cos(ang);
       }
     }
+    plan_gemm(We, We, S);
+    plan_gemm(n_mod, We, S);
+    reserve_common();
     float *tf = xe.as<float>((size_t)S * We * 2);
-    OXY_CUDA(cudaMemcpyAsync(tf, temb.data(), temb.size() * sizeof(float), cudaMemcpyHostToDevice, st));
     bf16 *tb = act_bf.as<bf16>((size_t)S * We * 3);
-    bf16 *h1 = tb + (size_t)S * We, *h2 = h1 + (size_t)S * We;
-    f32_to_bf16(tf, tb, (int64_t)S * We, st);
-    gemm(st, t1, tb, We, We, S, gemm::EPI_SWISH_BF16, h1, We, t1_b);
-    gemm(st, t2, h1, We, We, S, gemm::EPI_SWISH_BF16, h2, We, t2_b);
     float *m = mod.as<float>((size_t)S * n_mod);
-    gemm(st, wmod, h2, n_mod, We, S, gemm::EPI_F32, m, n_mod, bmod);
+    bf16 *h1 = tb + (size_t)S * We, *h2 = h1 + (size_t)S * We;
+    OXY_CUDA(cudaMemcpyAsync(tf, temb.data(), temb.size() * sizeof(float), cudaMemcpyHostToDevice, mst));
+    f32_to_bf16(tf, tb, (int64_t)S * We, mst);
+    gemm(t1, tb, We, We, S, gemm::EPI_SWISH_BF16, h1, We, t1_b);
+    gemm(t2, h1, We, We, S, gemm::EPI_SWISH_BF16, h2, We, t2_b);
+    gemm(wmod, h2, n_mod, We, S, gemm::EPI_F32, m, n_mod, bmod);
+    OXY_CUDA(cudaStreamSynchronize(mst));
     mod_S = S;
   }
 
   // n streams; stream i's prefix has P[i] positions in blocks (concatenated).
-  void denoise(cudaStream_t st, int n, const int *P, const int *blocks_h, int S, float *actions_out_d) {
+  void denoise(cudaStream_t caller, int n, const int *P, const int *blocks_h, int S, float *actions_out_d) {
     OXY_REQUIRE(S >= 1, "denoise step count must be >= 1, got %d", S);
-    const int We = c.expert_width, H = c.H, A = c.action_dim, T = n * H;
-    ensure_mod(st, S);
+    const int We = c.expert_width, H = c.H, A = c.action_dim, T = n * H, AP = apad();
+    ensure_mod(S);
+    std::string key = "denoise/" + std::to_string(S);
     int nb = 0;
-    for (int i = 0; i < n; ++i) nb += (P[i] + KV_BLOCK - 1) / KV_BLOCK;
-    std::vector<int> h((size_t)T + nb);
-    int *pos = h.data(), *bt = pos + T;
-    std::memcpy(bt, blocks_h, nb * sizeof(int));
+    for (int i = 0; i < n; ++i) {
+      nb += (P[i] + KV_BLOCK - 1) / KV_BLOCK;
+      key += "," + std::to_string(P[i]);
+    }
+    // ---- plan pass 1
+    arena_used = 0;
+    act.as<float>((size_t)T * AP);
+    act_bf.as<bf16>((size_t)T * AP);
+    xe.as<float>((size_t)T * We);
+    y.as<bf16>((size_t)T * std::max(We, QDIM));
+    qkv.as<float>((size_t)T * QKV);
+    q.as<bf16>((size_t)T * QDIM);
+    o.as<bf16>((size_t)T * QDIM);
+    kd.as<bf16>((size_t)T * HEAD_DIM);
+    vd.as<bf16>((size_t)T * HEAD_DIM);
+    hmid.as<bf16>((size_t)T * c.expert_mlp);
+    vel.as<float>((size_t)T * AP);
+    plan_gemm(We, AP, T);
+    plan_gemm(QKV, We, T);
+    plan_gemm(We, QDIM, T);
+    plan_gemm(2 * c.expert_mlp, We, T);
+    plan_gemm(We, c.expert_mlp, T);
+    plan_gemm(A, We, T);
+    std::vector<AttnGroup> groups(n);
+    for (int i = 0; i < n; ++i) {
+      groups[i] = AttnGroup{};
+      groups[i].nq = H * Q_HEADS;
+      groups[i].nka = P[i];
+      groups[i].nkb = H;
+    }
+    AttnPlan ap = shape_attention(groups, HEAD_DIM);
+    reserve_common();
+    // ---- plan pass 2
+    float *a = act.as<float>(0), *X = xe.as<float>(0), *QKVf = qkv.as<float>(0), *vel_d = vel.as<float>(0);
+    bf16 *ab = act_bf.as<bf16>(0), *Y = y.as<bf16>(0), *Qb = q.as<bf16>(0), *Ob = o.as<bf16>(0),
+         *Kd = kd.as<bf16>(0), *Vd = vd.as<bf16>(0), *Hm = hmid.as<bf16>(0);
+    const float *modp = mod.as<float>(0);
+    std::vector<int> pos(T);
     std::vector<int> boff(n);
     for (int i = 0, b = 0; i < n; ++i) {
       boff[i] = b;
       b += (P[i] + KV_BLOCK - 1) / KV_BLOCK;
       for (int j = 0; j < H; ++j) pos[i * H + j] = P[i] + j;
     }
-    int *dints = upload_ints(st, h);
-    int *d_pos = dints, *d_bt = dints + T;
-    const int AP = apad();
-    float *a = act.as<float>((size_t)T * AP);
-    bf16 *ab = act_bf.as<bf16>((size_t)T * AP);
-    for (int i = 0; i < n; ++i)
-      OXY_CUDA(cudaMemcpyAsync(a + (size_t)i * H * AP, noise, (size_t)H * AP * sizeof(float),
-                               cudaMemcpyDeviceToDevice, st));
-    f32_to_bf16(a, ab, (int64_t)T * AP, st);
-    float *X = xe.as<float>((size_t)T * We);
-    bf16 *Y = y.as<bf16>((size_t)T * std::max(We, QDIM));
-    float *QKVf = qkv.as<float>((size_t)T * QKV);
-    bf16 *Qb = q.as<bf16>((size_t)T * QDIM);
-    bf16 *Ob = o.as<bf16>((size_t)T * QDIM);
-    bf16 *Kd = kd.as<bf16>((size_t)T * HEAD_DIM), *Vd = vd.as<bf16>((size_t)T * HEAD_DIM);
-    bf16 *Hm = hmid.as<bf16>((size_t)T * c.expert_mlp);
-    float *vel_d = vel.as<float>((size_t)T * AP);
-    OXY_CUDA(cudaMemsetAsync(vel_d, 0, (size_t)T * AP * sizeof(float), st));
-    std::vector<AttnGroup> groups(n);
+    int *d_pos = arena_put(pos.data(), T);
+    int *d_bt = arena_put(blocks_h, nb);
     for (int i = 0; i < n; ++i) {
-      AttnGroup g{};
+      AttnGroup &g = groups[i];
       g.q = Qb + (size_t)i * H * QDIM;
       g.ldq = HEAD_DIM;
       g.o = Ob + (size_t)i * H * QDIM;
       g.ldo = HEAD_DIM;
-      g.nq = H * Q_HEADS;
       g.bt = d_bt + boff[i];
-      g.nka = P[i];
       g.kb = Kd + (size_t)i * H * HEAD_DIM;
       g.vb = Vd + (size_t)i * H * HEAD_DIM;
       g.ldkv = HEAD_DIM;
-      g.nkb = H;
-      groups[i] = g;
     }
-    const float dt = -1.f / (float)S;
-    for (int s = 0; s < S; ++s) {
-      const float *ms = mod.as<float>(0) + (size_t)s * n_mod;
-      gemm(st, e_in, ab, We, AP, T, gemm::EPI_F32, X, We, e_in_b);
-      for (int l = 0; l < c.depth; ++l) {
-        const ExpertW &w = E[l];
-        const float *m = ms + (size_t)l * 6 * We;
-        rmsnorm(X, We, Y, We, nullptr, m, m + We, T, We, 1e-6f, st);
-        gemm(st, w.wqkv, Y, QKV, We, T, gemm::EPI_F32, QKVf, QKV);
-        rope_split(QKVf, T, Q_HEADS, d_pos, nullptr, nullptr, Qb, nullptr, nullptr, Kd, Vd, 10000.f, st);
-        std::vector<AttnGroup> gs = groups;
-        attend(st, gs, HEAD_DIM, kpool(l), vpool(l));
-        gemm(st, w.wo, Ob, We, QDIM, T, gemm::EPI_ADD_GATED_F32, X, We, nullptr, m + 2 * We);
-        rmsnorm(X, We, Y, We, nullptr, m + 3 * We, m + 4 * We, T, We, 1e-6f, st);
-        gemm(st, w.wgu, Y, 2 * c.expert_mlp, We, T, gemm::EPI_GEGLU_BF16, Hm, c.expert_mlp);
-        gemm(st, w.wd, Hm, We, c.expert_mlp, T, gemm::EPI_ADD_GATED_F32, X, We, nullptr, m + 5 * We);
+    ap.groups = arena_put(groups.data(), groups.size());
+    enter(caller);
+    arena_upload();
+    auto body = [&]() {
+      for (int i = 0; i < n; ++i)
+        OXY_CUDA(cudaMemcpyAsync(a + (size_t)i * H * AP, noise, (size_t)H * AP * sizeof(float),
+                                 cudaMemcpyDeviceToDevice, mst));
+      OXY_CUDA(cudaMemsetAsync(vel_d, 0, (size_t)T * AP * sizeof(float), mst));
+      f32_to_bf16(a, ab, (int64_t)T * AP, mst);
+      const float dt = -1.f / (float)S;
+      for (int s = 0; s < S; ++s) {
+        const float *ms = modp + (size_t)s * n_mod;
+        gemm(e_in, ab, We, AP, T, gemm::EPI_F32, X, We, e_in_b);
+        for (int l = 0; l < c.depth; ++l) {
+          const ExpertW &w = E[l];
+          const float *m = ms + (size_t)l * 6 * We;
+          rmsnorm(X, We, Y, We, nullptr, m, m + We, T, We, 1e-6f, mst);
+          gemm(w.wqkv, Y, QKV, We, T, gemm::EPI_F32, QKVf, QKV);
+          rope_split(QKVf, T, Q_HEADS, d_pos, nullptr, nullptr, Qb, nullptr, nullptr, Kd, Vd, 10000.f, mst);
+          attend(ap, kpool(l), vpool(l));
+          gemm(w.wo, Ob, We, QDIM, T, gemm::EPI_ADD_GATED_F32, X, We, nullptr, m + 2 * We);
+          rmsnorm(X, We, Y, We, nullptr, m + 3 * We, m + 4 * We, T, We, 1e-6f, mst);
+          gemm(w.wgu, Y, 2 * c.expert_mlp, We, T, gemm::EPI_GEGLU_BF16, Hm, c.expert_mlp);
+          gemm(w.wd, Hm, We, c.expert_mlp, T, gemm::EPI_ADD_GATED_F32, X, We, nullptr, m + 5 * We);
+        }
+        const float *mf = ms + (size_t)c.depth * 6 * We;
+        rmsnorm(X, We, Y, We, nullptr, mf, mf + We, T, We, 1e-6f, mst);
+        gemm(e_out, Y, A, We, T, gemm::EPI_F32, vel_d, AP, e_out_b);
+        euler_step(a, vel_d, ab, (int64_t)T * AP, dt, mst);
       }
-      const float *mf = ms + (size_t)c.depth * 6 * We;
-      rmsnorm(X, We, Y, We, nullptr, mf, mf + We, T, We, 1e-6f, st);
-      gemm(st, e_out, Y, A, We, T, gemm::EPI_F32, vel_d, AP, e_out_b);
-      euler_step(a, vel_d, ab, (int64_t)T * AP, dt, st);
-    }
+    };
+    run_body(key, true, body);
     OXY_CUDA(cudaMemcpy2DAsync(actions_out_d, A * sizeof(float), a, AP * sizeof(float), A * sizeof(float), T,
-                               cudaMemcpyDeviceToDevice, st));
+                               cudaMemcpyDeviceToDevice, mst));
+    leave(caller);
   }
 
   // ------------------------------------------------------------ decode
-  void decode(cudaStream_t st, int rows, int k, const int *bt_h, int maxb, const int *seq_h, const int *last_h,
+  void decode(cudaStream_t caller, int rows, int k, const int *bt_h, int maxb, const int *seq_h, const int *last_h,
               const int *budget_h, const int *cow_h, int *out_tok_h, int *out_cnt_h, float *logits_h) {
     const int W = c.width;
-    const size_t n_bt = (size_t)rows * maxb, n_out = (size_t)rows * k;
-    std::vector<int> h(n_bt + 3 * (size_t)rows + 6 * (size_t)rows + n_out, 0);
-    int *hp = h.data();
-    std::memcpy(hp, bt_h, n_bt * sizeof(int));
-    std::memcpy(hp + n_bt, cow_h, 3 * rows * sizeof(int));
-    int *h_active = hp + n_bt + 3 * rows, *h_tok = h_active + rows, *h_pos = h_tok + rows,
-        *h_cnt = h_pos + rows, *h_bud = h_cnt + rows;
     int max_pos = 0;
     for (int r = 0; r < rows; ++r) {
       OXY_REQUIRE(last_h[r] >= 0 && last_h[r] < c.vocab, "token %d outside vocab", last_h[r]);
-      h_active[r] = 1;
-      h_tok[r] = last_h[r];
-      h_pos[r] = seq_h[r];
-      h_bud[r] = budget_h[r];
       max_pos = std::max(max_pos, seq_h[r] + k);
     }
     OXY_REQUIRE((max_pos + KV_BLOCK - 1) / KV_BLOCK <= maxb, "block table too short for %d positions", max_pos);
-    int *dv = upload_ints(st, h);
-    int *d_bt = dv, *d_cow = dv + n_bt, *d_active = d_cow + 3 * rows, *d_tok = d_active + rows,
-        *d_pos = d_tok + rows, *d_cnt = d_pos + rows, *d_bud = d_cnt + rows, *d_slot = d_bud + rows,
-        *d_out = d_slot + rows;
-    cow_blocks(pool, d_cow, rows, c.depth, layer_stride, kv_stride, st);
-    float *X = x.as<float>((size_t)rows * W);
-    bf16 *Y = y.as<bf16>((size_t)rows * W);
-    float *QKVf = qkv.as<float>((size_t)rows * QKV);
-    bf16 *Qb = q.as<bf16>((size_t)rows * QDIM);
-    bf16 *Ob = o.as<bf16>((size_t)rows * QDIM);
-    bf16 *Hm = hmid.as<bf16>((size_t)rows * c.mlp);
-    float *LG = logits.as<float>((size_t)rows * c.vocab);
-    float *pv = amv.as<float>((size_t)rows * 64);
-    int *pi = ami.as<int>((size_t)rows * 64);
-    float *dws = dec_ws.as<float>((size_t)rows * maxb * Q_HEADS * (HEAD_DIM + 2));
+    // ---- plan pass 1
+    arena_used = 0;
+    x.as<float>((size_t)rows * W);
+    y.as<bf16>((size_t)rows * W);
+    qkv.as<float>((size_t)rows * QKV);
+    q.as<bf16>((size_t)rows * QDIM);
+    o.as<bf16>((size_t)rows * QDIM);
+    hmid.as<bf16>((size_t)rows * c.mlp);
+    logits.as<float>((size_t)rows * c.vocab);
+    amv.as<float>((size_t)rows * 64);
+    ami.as<int>((size_t)rows * 64);
+    dec_ws.as<float>((size_t)rows * maxb * Q_HEADS * (HEAD_DIM + 2));
+    plan_gemm(QKV, W, rows);
+    plan_gemm(W, QDIM, rows);
+    plan_gemm(2 * c.mlp, W, rows);
+    plan_gemm(W, c.mlp, rows);
+    plan_gemm(c.vocab, W, rows);
+    reserve_common();
+    // ---- plan pass 2
+    float *X = x.as<float>(0), *QKVf = qkv.as<float>(0), *LG = logits.as<float>(0), *pv = amv.as<float>(0),
+          *dws = dec_ws.as<float>(0);
+    bf16 *Y = y.as<bf16>(0), *Qb = q.as<bf16>(0), *Ob = o.as<bf16>(0), *Hm = hmid.as<bf16>(0);
+    int *pi = ami.as<int>(0);
+    std::vector<int> ones(rows, 1), zeros((size_t)rows * k, 0);
+    int *d_bt = arena_put(bt_h, (size_t)rows * maxb);
+    int *d_cow = arena_put(cow_h, (size_t)rows * 3);
+    int *d_active = arena_put(ones.data(), rows);
+    int *d_tok = arena_put(last_h, rows);
+    int *d_pos = arena_put(seq_h, rows);
+    int *d_cnt = arena_put(zeros.data(), rows);
+    int *d_bud = arena_put(budget_h, rows);
+    int *d_slot = arena_put(zeros.data(), rows);
+    int *d_out = arena_put(zeros.data(), (size_t)rows * k);
     const float scale = 1.f / 16.f;  // 1/sqrt(256)
-    for (int s = 0; s < k; ++s) {
-      embed_rows(X, W, embed, d_tok, nullptr, rows, W, std::sqrt((float)W), st);
-      next_slots(d_slot, d_pos, d_active, d_bt, maxb, rows, st);
-      for (int l = 0; l < c.depth; ++l) {
-        const LayerW &w = L[l];
-        rmsnorm(X, W, Y, W, w.ln1, nullptr, nullptr, rows, W, 1e-6f, st);
-        gemm(st, w.wqkv, Y, QKV, W, rows, gemm::EPI_F32, QKVf, QKV);
-        rope_split(QKVf, rows, Q_HEADS, d_pos, d_slot, d_active, Qb, kpool(l), vpool(l), nullptr, nullptr,
-                   10000.f, st);
-        decode_attention(Qb, Ob, kpool(l), vpool(l), d_bt, maxb, d_pos, d_active, rows, maxb, scale, dws, st);
-        gemm(st, w.wo, Ob, W, QDIM, rows, gemm::EPI_ADD_F32, X, W);
-        rmsnorm(X, W, Y, W, w.ln2, nullptr, nullptr, rows, W, 1e-6f, st);
-        gemm(st, w.wgu, Y, 2 * c.mlp, W, rows, gemm::EPI_GEGLU_BF16, Hm, c.mlp);
-        gemm(st, w.wd, Hm, W, c.mlp, rows, gemm::EPI_ADD_F32, X, W);
+    enter(caller);
+    arena_upload();
+    auto body = [&]() {
+      cow_blocks(pool, d_cow, rows, c.depth, layer_stride, kv_stride, mst);
+      for (int s = 0; s < k; ++s) {
+        embed_rows(X, W, embed, d_tok, nullptr, rows, W, std::sqrt((float)W), mst);
+        next_slots(d_slot, d_pos, d_active, d_bt, maxb, rows, mst);
+        for (int l = 0; l < c.depth; ++l) {
+          const LayerW &w = L[l];
+          rmsnorm(X, W, Y, W, w.ln1, nullptr, nullptr, rows, W, 1e-6f, mst);
+          gemm(w.wqkv, Y, QKV, W, rows, gemm::EPI_F32, QKVf, QKV);
+          rope_split(QKVf, rows, Q_HEADS, d_pos, d_slot, d_active, Qb, kpool(l), vpool(l), nullptr, nullptr,
+                     10000.f, mst);
+          decode_attention(Qb, Ob, kpool(l), vpool(l), d_bt, maxb, d_pos, d_active, rows, maxb, scale, dws, mst);
+          gemm(w.wo, Ob, W, QDIM, rows, gemm::EPI_ADD_F32, X, W);
+          rmsnorm(X, W, Y, W, w.ln2, nullptr, nullptr, rows, W, 1e-6f, mst);
+          gemm(w.wgu, Y, 2 * c.mlp, W, rows, gemm::EPI_GEGLU_BF16, Hm, c.mlp);
+          gemm(w.wd, Hm, W, c.mlp, rows, gemm::EPI_ADD_F32, X, W);
+        }
+        rmsnorm(X, W, Y, W, final_norm, nullptr, nullptr, rows, W, 1e-6f, mst);
+        gemm(lm_head, Y, c.vocab, W, rows, gemm::EPI_F32, LG, c.vocab);
+        if (logits_h)
+          OXY_CUDA(cudaMemcpyAsync(logits_h + (size_t)s * rows * c.vocab, LG, (size_t)rows * c.vocab * sizeof(float),
+                                   cudaMemcpyDeviceToHost, mst));
+        argmax_update(LG, rows, c.vocab, s, k, c.eos_token, d_active, d_tok, d_pos, d_cnt, d_bud, d_out, pv, pi,
+                      mst);
       }
-      rmsnorm(X, W, Y, W, final_norm, nullptr, nullptr, rows, W, 1e-6f, st);
-      gemm(st, lm_head, Y, c.vocab, W, rows, gemm::EPI_F32, LG, c.vocab);
-      if (logits_h)
-        OXY_CUDA(cudaMemcpyAsync(logits_h + (size_t)s * rows * c.vocab, LG, (size_t)rows * c.vocab * sizeof(float),
-                                 cudaMemcpyDeviceToHost, st));
-      argmax_update(LG, rows, c.vocab, s, k, c.eos_token, d_active, d_tok, d_pos, d_cnt, d_bud, d_out, pv, pi, st);
-    }
-    OXY_CUDA(cudaMemcpyAsync(out_tok_h, d_out, n_out * sizeof(int), cudaMemcpyDeviceToHost, st));
-    OXY_CUDA(cudaMemcpyAsync(out_cnt_h, d_cnt, rows * sizeof(int), cudaMemcpyDeviceToHost, st));
-    OXY_CUDA(cudaStreamSynchronize(st));
+    };
+    const std::string key = "decode/" + std::to_string(rows) + "," + std::to_string(k) + "," + std::to_string(maxb);
+    run_body(key, logits_h == nullptr, body);
+    OXY_CUDA(cudaMemcpyAsync(out_tok_h, d_out, (size_t)rows * k * sizeof(int), cudaMemcpyDeviceToHost, mst));
+    OXY_CUDA(cudaMemcpyAsync(out_cnt_h, d_cnt, rows * sizeof(int), cudaMemcpyDeviceToHost, mst));
+    OXY_CUDA(cudaStreamSynchronize(mst));
+    leave(caller);
   }
 };
 
@@ -704,9 +897,9 @@ int oxy_pi05_read_kv(oxy_pi05 *p, const int32_t *blocks_h, int32_t seq_len, int3
   if (seq_len == 0) return OXY_OK;
   auto st = oxy::as_stream(stream);
   const int nb = (seq_len + 63) / 64;
-  int *bd = m.ints.as<int>(nb);
+  int *bd = m.kvread_i.as<int>(nb);
   OXY_CUDA(cudaMemcpyAsync(bd, blocks_h, nb * sizeof(int), cudaMemcpyHostToDevice, st));
-  float *ko = m.qkv.as<float>((size_t)2 * seq_len * 256);
+  float *ko = m.kvread_f.as<float>((size_t)2 * seq_len * 256);
   oxy::pi05::gather_kv_f32<<<seq_len, 256, 0, st>>>(ko, ko + (size_t)seq_len * 256, m.kpool(layer), m.vpool(layer),
                                                     bd, seq_len);
   OXY_LAUNCH_CHECK();

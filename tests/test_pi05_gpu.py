@@ -115,6 +115,22 @@ def test_batch_invariant_decode(tiny):
         assert big.kv_batch[i] == solo.kv_batch[0]
 
 
+def test_cuda_graph_replay_is_bit_identical(tiny):
+    """Calls 1 (eager), 2 (captured) and 3+ (replayed) of one shape agree exactly."""
+    be, _ = tiny
+    obs = _obs(1, (21, 22, 23))
+    kvs = [be.prefill(obs) for _ in range(4)]
+    for kv in kvs[1:]:
+        assert kv == kvs[0]
+    acts = [be.action_denoise(kvs[0], be.config.S) for _ in range(4)]
+    assert all(a == acts[0] for a in acts)
+    outs = [be.batched_language_decode(
+        BatchedState((kv,), ((),), (False,), (0,), (7,), (0,)), 7) for kv in kvs]
+    for out in outs[1:]:
+        assert out.token_buffers == outs[0].token_buffers
+        assert out.kv_batch[0] == outs[0].kv_batch[0]
+
+
 def _pi05_factory(cfg: BackendConfig):
     from paper_2603_14371_b200.pi05 import Pi05Backend
     return Pi05Backend(cfg, num_blocks=128)
