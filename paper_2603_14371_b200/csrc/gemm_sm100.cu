@@ -145,6 +145,7 @@ struct KParams {
   int n_out, k, t, bn, stages, kb_total, splits, kb_per_split;
   EpiParams epi;
   float *ws;
+  int *counters;  // one per (m, n) tile; self-resetting
 };
 
 __global__ void __launch_bounds__(192, 1)
@@ -161,7 +162,9 @@ __global__ void __launch_bounds__(192, 1)
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * MAX_STAGES + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * bn, split = blockIdx.z;
+  // token tiles fastest: the CTAs sharing one weight tile run in the same wave
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * bn, split = blockIdx.z;
+  __shared__ int s_last;
   const int kb0 = split * p.kb_per_split;
   const int nkb = min(p.kb_total, kb0 + p.kb_per_split) - kb0;
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + MAX_STAGES),
@@ -190,6 +193,7 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // prologue above overlaps the previous kernel; operands are read below
 
   if (warp == 0) {
     if (lane == 0) {
@@ -243,6 +247,28 @@ __global__ void __launch_bounds__(192, 1)
           epilogue_store(p.epi, t, f, p.n_out, acc, pair);
       }
     }
+    if (split_out) {
+      // Deterministic split-K fix-up: the last CTA of this tile to arrive sums
+      // the partials in split order 0..S-1 and applies the epilogue.
+      __threadfence();
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      const int tile = blockIdx.y * gridDim.x + blockIdx.x;
+      if (threadIdx.x == 64) s_last = atomicAdd(p.counters + tile, 1) == p.splits - 1;
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (s_last) {
+        __threadfence();
+        for (int c = 0; c < bn; ++c) {
+          const int t = n0 + c;
+          if (t >= p.t) break;
+          float acc = 0.f;
+          if (f < p.n_out)
+            for (int s = 0; s < p.splits; ++s) acc += __ldcg(p.ws + ((size_t)s * p.t + t) * p.n_out + f);
+          const float pair = __shfl_xor_sync(0xffffffffu, acc, 1);
+          if (f < p.n_out) epilogue_store(p.epi, t, f, p.n_out, acc, pair);
+        }
+        if (threadIdx.x == 64) p.counters[tile] = 0;
+      }
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -251,23 +277,6 @@ __global__ void __launch_bounds__(192, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols)
                  : "memory");
   }
-}
-
-// Fixed-order split-K reduction + epilogue; one thread per feature pair.
-__global__ void splitk_reduce_kernel(const float *ws, int splits, int t_rows, int n_out,
-                                     EpiParams e) {
-  const int pairs = (n_out + 1) >> 1;
-  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (idx >= (int64_t)t_rows * pairs) return;
-  const int t = (int)(idx / pairs), f = (int)(idx % pairs) * 2;
-  float a0 = 0.f, a1 = 0.f;
-  for (int s = 0; s < splits; ++s) {
-    const float *row = ws + ((size_t)s * t_rows + t) * n_out;
-    a0 += row[f];
-    if (f + 1 < n_out) a1 += row[f + 1];
-  }
-  epilogue_store(e, t, f, n_out, a0, a1);
-  if (f + 1 < n_out) epilogue_store(e, t, f + 1, n_out, a1, a0);
 }
 
 // ------------------------------------------------------------------ host
@@ -332,7 +341,7 @@ static size_t smem_bytes(const Plan &p) {
 }
 
 void launch(const void *w, const void *x, int n_out, int k, int t, const EpiParams &epi,
-            const Plan &plan, float *ws, cudaStream_t st) {
+            const Plan &plan, float *ws, int *counters, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
     OXY_CUDA(cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -340,7 +349,8 @@ void launch(const void *w, const void *x, int n_out, int k, int t, const EpiPara
     attr_set = true;
   }
   if (t <= 0) return;
-  if (plan.splits > 1 && !ws) fail(OXY_EINVAL, "split-K GEMM needs a workspace");
+  if (plan.splits > 1 && (!ws || !counters)) fail(OXY_EINVAL, "split-K GEMM needs a workspace");
+  if (plan.splits > 1 && plan.m_tiles * plan.n_tiles > MAX_TILES) fail(OXY_EINVAL, "too many split-K tiles");
   CUtensorMap ma = make_map(w, n_out, k, BM);
   CUtensorMap mb = make_map(x, t, k, plan.bn);
   KParams kp;
@@ -354,14 +364,18 @@ void launch(const void *w, const void *x, int n_out, int k, int t, const EpiPara
   kp.kb_per_split = (plan.kb_total + plan.splits - 1) / plan.splits;
   kp.epi = epi;
   kp.ws = ws;
-  dim3 grid(plan.m_tiles, plan.n_tiles, plan.splits);
-  gemm_kernel<<<grid, 192, smem_bytes(plan), st>>>(ma, mb, kp);
-  OXY_LAUNCH_CHECK();
-  if (plan.splits > 1) {
-    const int64_t n = (int64_t)t * ((n_out + 1) / 2);
-    splitk_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ws, plan.splits, t, n_out, epi);
-    OXY_LAUNCH_CHECK();
+  kp.counters = counters;
+  dim3 grid(plan.n_tiles, plan.m_tiles, plan.splits);
+  launch_pdl(gemm_kernel, grid, dim3(192), smem_bytes(plan), st, ma, mb, kp);
+}
+
+int *counters_for_abi() {
+  static int *c = nullptr;
+  if (!c) {
+    OXY_CUDA(cudaMalloc(&c, MAX_TILES * sizeof(int)));
+    OXY_CUDA(cudaMemset(c, 0, MAX_TILES * sizeof(int)));
   }
+  return c;
 }
 
 }  // namespace gemm
@@ -383,7 +397,8 @@ extern "C" int oxy_gemm_bf16(const void *w_d, const void *x_d, int32_t n_out, in
                 "split-K workspace too small (%lld floats needed)",
                 (long long)plan.splits * t * n_out);
   oxy::gemm::EpiParams e{mode, out_d, ldo, bias_d, res_d, ldr, nullptr};
-  oxy::gemm::launch(w_d, x_d, n_out, k, t, e, plan, ws_d, oxy::as_stream(stream));
+  oxy::gemm::launch(w_d, x_d, n_out, k, t, e, plan, ws_d, oxy::gemm::counters_for_abi(),
+                    oxy::as_stream(stream));
   OXY_API_END
 }
 

@@ -46,6 +46,7 @@ constexpr int MAX_BN = 256;
 constexpr int MAX_STAGES = 8;
 constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
 constexpr int SMEM_BUDGET = 200 * 1024;
+constexpr int MAX_TILES = 1 << 16;  // split-K tile counters
 
 struct Plan {
   int bn, n_tiles, m_tiles, splits, stages, kb_total;
@@ -56,7 +57,9 @@ Plan make_plan(int n_out, int k, int t, int sms, int force_splits = 0);
 
 // Host: launch.  ws must hold splits * T * N_out floats when splits > 1.
 void launch(const void *w, const void *x, int n_out, int k, int t, const EpiParams &epi,
-            const Plan &plan, float *ws, cudaStream_t st);
+            const Plan &plan, float *ws, int *counters, cudaStream_t st);
+// self-resetting split-K tile counters for launches made through the C ABI
+int *counters_for_abi();
 
 }  // namespace gemm
 }  // namespace oxy

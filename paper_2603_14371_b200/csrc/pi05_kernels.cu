@@ -12,6 +12,7 @@ namespace pi05 {
 
 __global__ void rmsnorm_kernel(const float *x, int ldx, bf16 *y, int ldy, const float *w,
                                const float *ms, const float *mb, int D, float eps) {
+  pdl_wait();
   __shared__ float red[32];
   const float *xr = x + (size_t)blockIdx.x * ldx;
   bf16 *yr = y + (size_t)blockIdx.x * ldy;
@@ -39,12 +40,12 @@ __global__ void rmsnorm_kernel(const float *x, int ldx, bf16 *y, int ldy, const 
 void rmsnorm(const float *x, int ldx, bf16 *y, int ldy, const float *w, const float *ms,
              const float *mb, int rows, int D, float eps, cudaStream_t st) {
   if (rows <= 0) return;
-  rmsnorm_kernel<<<rows, 256, 0, st>>>(x, ldx, y, ldy, w, ms, mb, D, eps);
-  OXY_LAUNCH_CHECK();
+  launch_pdl(rmsnorm_kernel, dim3(rows), dim3(256), 0, st, x, ldx, y, ldy, w, ms, mb, D, eps);
 }
 
 __global__ void layernorm_kernel(const float *x, int ldx, bf16 *y, int ldy, const float *w,
                                  const float *b, int D, float eps) {
+  pdl_wait();
   __shared__ float red[32];
   const float *xr = x + (size_t)blockIdx.x * ldx;
   bf16 *yr = y + (size_t)blockIdx.x * ldy;
@@ -64,12 +65,12 @@ __global__ void layernorm_kernel(const float *x, int ldx, bf16 *y, int ldy, cons
 void layernorm(const float *x, int ldx, bf16 *y, int ldy, const float *w, const float *b, int rows,
                int D, float eps, cudaStream_t st) {
   if (rows <= 0) return;
-  layernorm_kernel<<<rows, 256, 0, st>>>(x, ldx, y, ldy, w, b, D, eps);
-  OXY_LAUNCH_CHECK();
+  launch_pdl(layernorm_kernel, dim3(rows), dim3(256), 0, st, x, ldx, y, ldy, w, b, D, eps);
 }
 
 __global__ void embed_kernel(float *x, int ldx, const bf16 *table, const int *tok,
                              const int *active, int D, float scale) {
+  pdl_wait();
   const int r = blockIdx.x;
   if (active && !active[r]) return;
   const bf16 *row = table + (size_t)tok[r] * D;
@@ -80,20 +81,29 @@ __global__ void embed_kernel(float *x, int ldx, const bf16 *table, const int *to
 void embed_rows(float *x, int ldx, const bf16 *table, const int *tok, const int *active, int rows,
                 int D, float scale, cudaStream_t st) {
   if (rows <= 0) return;
-  embed_kernel<<<rows, 256, 0, st>>>(x, ldx, table, tok, active, D, scale);
-  OXY_LAUNCH_CHECK();
+  launch_pdl(embed_kernel, dim3(rows), dim3(256), 0, st, x, ldx, table, tok, active, D, scale);
+}
+
+// RoPE inverse frequencies theta^(-2i/256), computed in double on the host.
+__constant__ float c_rope_inv[128];
+
+void set_rope_theta(float theta) {
+  float inv[128];
+  for (int i = 0; i < 128; ++i) inv[i] = (float)std::pow((double)theta, -2.0 * (double)i / (double)HEAD_DIM);
+  OXY_CUDA(cudaMemcpyToSymbol(c_rope_inv, inv, sizeof(inv)));
 }
 
 // One CTA per token; thread i < 128 owns rotary pair (i, i+128) of every head.
 __global__ void rope_split_kernel(const float *qkv, int n_qh, const int *pos, const int *slot,
                                   const int *active, bf16 *q_out, bf16 *kpool, bf16 *vpool,
                                   bf16 *k_dense, bf16 *v_dense, float theta) {
+  pdl_wait();
   const int t = blockIdx.x;
   if (active && !active[t]) return;
   const int ld = (n_qh + 2) * HEAD_DIM;
   const float *row = qkv + (size_t)t * ld;
   const int i = threadIdx.x;  // 0..127
-  const float inv = (float)pow((double)theta, -2.0 * (double)i / (double)HEAD_DIM);
+  const float inv = c_rope_inv[i];
   float sn, cs;
   sincosf((float)pos[t] * inv, &sn, &cs);
   const int s = slot ? slot[t] : -1;
@@ -120,12 +130,11 @@ void rope_split(const float *qkv, int T, int n_qh, const int *pos, const int *sl
                 const int *active, bf16 *q_out, bf16 *kpool, bf16 *vpool, bf16 *k_dense,
                 bf16 *v_dense, float theta, cudaStream_t st) {
   if (T <= 0) return;
-  rope_split_kernel<<<T, 128, 0, st>>>(qkv, n_qh, pos, slot, active, q_out, kpool, vpool, k_dense,
-                                       v_dense, theta);
-  OXY_LAUNCH_CHECK();
+  launch_pdl(rope_split_kernel, dim3(T), dim3(128), 0, st, qkv, n_qh, pos, slot, active, q_out, kpool, vpool, k_dense, v_dense, theta);
 }
 
 __global__ void patchify_kernel(const uint8_t *img, bf16 *patches, int kpad) {
+  pdl_wait();
   const int p = blockIdx.x;  // image * 256 + patch
   const int im = p >> 8, py = (p & 255) >> 4, px = p & 15;
   const uint8_t *base = img + (size_t)im * 224 * 224 * 3;
@@ -142,11 +151,11 @@ __global__ void patchify_kernel(const uint8_t *img, bf16 *patches, int kpad) {
 
 void patchify(const uint8_t *img, int n, bf16 *patches, int kpad, cudaStream_t st) {
   if (n <= 0) return;
-  patchify_kernel<<<n * 256, 128, 0, st>>>(img, patches, kpad);
-  OXY_LAUNCH_CHECK();
+  launch_pdl(patchify_kernel, dim3(n * 256), dim3(128), 0, st, img, patches, kpad);
 }
 
 __global__ void tile_rows_kernel(float *dst, int ld, const float *src, int ld_src, int period, int D) {
+  pdl_wait();
   const int r = blockIdx.x;
   const float *s = src + (size_t)(r % period) * ld_src;
   for (int j = threadIdx.x; j < D; j += blockDim.x) dst[(size_t)r * ld + j] = s[j];
@@ -155,11 +164,11 @@ __global__ void tile_rows_kernel(float *dst, int ld, const float *src, int ld_sr
 void tile_rows(float *dst, int ld, const float *src, int ld_src, int rows, int period, int D,
                cudaStream_t st) {
   if (rows <= 0) return;
-  tile_rows_kernel<<<rows, 256, 0, st>>>(dst, ld, src, ld_src, period, D);
-  OXY_LAUNCH_CHECK();
+  launch_pdl(tile_rows_kernel, dim3(rows), dim3(256), 0, st, dst, ld, src, ld_src, period, D);
 }
 
 __global__ void f32_to_bf16_kernel(const float *x, bf16 *y, int64_t n) {
+  pdl_wait();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     y[i] = __float2bfloat16(x[i]);
 }
@@ -171,6 +180,7 @@ void f32_to_bf16(const float *x, bf16 *y, int64_t n, cudaStream_t st) {
 }
 
 __global__ void euler_kernel(float *a, const float *v, bf16 *ab, int64_t n, float dt) {
+  pdl_wait();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const float x = a[i] + dt * v[i];
     a[i] = x;
@@ -185,6 +195,7 @@ void euler_step(float *a, const float *v, bf16 *ab, int64_t n, float dt, cudaStr
 
 // Box-Muller on consecutive splitmix64 uniforms: pair i uses draws 2i, 2i+1.
 __global__ void noise_kernel(float *out, int64_t n, uint64_t seed) {
+  pdl_wait();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; 2 * i < n; i += (int64_t)gridDim.x * blockDim.x) {
     double u1 = splitmix_uniform(seed, 2 * i), u2 = splitmix_uniform(seed, 2 * i + 1);
     double r = sqrt(-2.0 * log(1.0 - u1)), th = 6.283185307179586 * u2;
@@ -199,6 +210,7 @@ void normal_noise(float *out, int64_t n, uint64_t seed, cudaStream_t st) {
 }
 
 __global__ void init_bf16_kernel(bf16 *out, int64_t n, uint64_t seed, uint64_t offset, float bound) {
+  pdl_wait();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     double u = splitmix_uniform(seed, offset + (uint64_t)i);
     out[i] = __float2bfloat16((float)((2.0 * u - 1.0) * (double)bound));
@@ -211,6 +223,7 @@ void init_uniform_bf16(bf16 *out, int64_t n, uint64_t seed, uint64_t offset, flo
 }
 
 __global__ void init_f32_kernel(float *out, int64_t n, uint64_t seed, uint64_t offset, float bound, float center) {
+  pdl_wait();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     double u = splitmix_uniform(seed, offset + (uint64_t)i);
     out[i] = (float)((double)center + (2.0 * u - 1.0) * (double)bound);
@@ -224,6 +237,7 @@ void init_uniform_f32(float *out, int64_t n, uint64_t seed, uint64_t offset, flo
 }
 
 __global__ void cow_kernel(bf16 *pool, const int *cow, size_t layer_stride, size_t kv_stride) {
+  pdl_wait();
   const int r = blockIdx.x, l = blockIdx.y;
   const int src = cow[r * 3], dst = cow[r * 3 + 1], n = cow[r * 3 + 2];
   if (src < 0) return;
@@ -246,6 +260,7 @@ void cow_blocks(bf16 *pool, const int *cow, int rows, int L, size_t layer_stride
 
 __global__ void next_slot_kernel(int *slot, const int *pos, const int *active, const int *bt,
                                  int bt_stride, int rows) {
+  pdl_wait();
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= rows) return;
   if (!active[r]) { slot[r] = -1; return; }
@@ -255,8 +270,7 @@ __global__ void next_slot_kernel(int *slot, const int *pos, const int *active, c
 
 void next_slots(int *slot, const int *pos, const int *active, const int *bt, int bt_stride, int rows,
                 cudaStream_t st) {
-  next_slot_kernel<<<(rows + 127) / 128, 128, 0, st>>>(slot, pos, active, bt, bt_stride, rows);
-  OXY_LAUNCH_CHECK();
+  launch_pdl(next_slot_kernel, dim3((rows + 127) / 128), dim3(128), 0, st, slot, pos, active, bt, bt_stride, rows);
 }
 
 // ============================================================ flash attention
@@ -328,6 +342,7 @@ template <int HD>
 __global__ void __launch_bounds__(128)
     flash_attn_kernel(const AttnGroup *groups, int max_q_tiles, const bf16 *kpool, const bf16 *vpool,
                       float scale_log2, int splits, float *ws_o, float *ws_ml, int ws_rows) {
+  pdl_wait();
   using C = FaCfg<HD>;
   constexpr int NT = C::HDP / 8;  // output n-tiles per warp
   extern __shared__ __align__(16) unsigned char fa_smem[];
@@ -504,30 +519,38 @@ __global__ void __launch_bounds__(128)
   }
 }
 
-// Combine split-KV partials in split order (log2 domain).
+// Combine split-KV partials in split order (log2 domain); one warp per row.
 template <int HD>
-__global__ void fa_merge_kernel(const AttnGroup *groups, int max_rows, int splits, const float *ws_o,
-                                const float *ws_ml, int ws_rows) {
+__global__ void fa_merge_kernel(const AttnGroup *groups, int splits, const float *ws_o, const float *ws_ml,
+                                int ws_rows) {
+  pdl_wait();
   using C = FaCfg<HD>;
   const AttnGroup g = groups[blockIdx.y];
-  const int r = blockIdx.x;
+  const int r = blockIdx.x * 4 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (r >= g.nq) return;
+  const size_t row0 = (size_t)g.wrow0 + r;
   float M = -INFINITY;
-  for (int s = 0; s < splits; ++s) M = fmaxf(M, ws_ml[((size_t)s * ws_rows + g.wrow0 + r) * 2]);
+  for (int s = lane; s < splits; s += 32) M = fmaxf(M, ws_ml[((size_t)s * ws_rows + row0) * 2]);
+  M = warp_max(M);
   float L = 0.f;
-  for (int s = 0; s < splits; ++s) {
-    const size_t wr = (size_t)s * ws_rows + g.wrow0 + r;
-    const float m = ws_ml[wr * 2];
-    if (m != -INFINITY) L += ws_ml[wr * 2 + 1] * exp2f(m - M);
+  for (int s = lane; s < splits; s += 32) {
+    const float m = ws_ml[((size_t)s * ws_rows + row0) * 2];
+    if (m != -INFINITY) L += ws_ml[((size_t)s * ws_rows + row0) * 2 + 1] * exp2f(m - M);
   }
-  for (int c = threadIdx.x; c < HD; c += blockDim.x) {
-    float acc = 0.f;
+  L = warp_sum(L);
+  const float inv = L > 0.f ? 1.f / L : 0.f;
+  for (int c = lane * 2; c < HD; c += 64) {
+    float a0 = 0.f, a1 = 0.f;
     for (int s = 0; s < splits; ++s) {
-      const size_t wr = (size_t)s * ws_rows + g.wrow0 + r;
+      const size_t wr = (size_t)s * ws_rows + row0;
       const float m = ws_ml[wr * 2];
-      if (m != -INFINITY) acc += ws_o[wr * C::HDP + c] * exp2f(m - M);
+      if (m == -INFINITY) continue;
+      const float w = exp2f(m - M);
+      const float2 v = *reinterpret_cast<const float2 *>(ws_o + wr * C::HDP + c);
+      a0 += v.x * w;
+      a1 += v.y * w;
     }
-    g.o[(size_t)r * g.ldo + c] = __float2bfloat16(L > 0.f ? acc / L : 0.f);
+    *reinterpret_cast<__nv_bfloat162 *>(g.o + (size_t)r * g.ldo + c) = __floats2bfloat162_rn(a0 * inv, a1 * inv);
   }
 }
 
@@ -544,13 +567,10 @@ static void flash_launch(const AttnGroup *groups_d, int n_groups, int max_q_tile
   }
   const float scale_log2 = scale * 1.4426950408889634f;
   dim3 grid(n_groups * max_q_tiles, splits);
-  flash_attn_kernel<HD><<<grid, 128, C::SMEM, st>>>(groups_d, max_q_tiles, kpool, vpool, scale_log2,
-                                                    splits, ws_o, ws_ml, ws_rows);
-  OXY_LAUNCH_CHECK();
+  launch_pdl(flash_attn_kernel<HD>, dim3(grid), dim3(128), C::SMEM, st, groups_d, max_q_tiles, kpool, vpool, scale_log2, splits, ws_o, ws_ml, ws_rows);
   if (splits > 1) {
-    fa_merge_kernel<HD><<<dim3(max_q_tiles * FA_BQ, n_groups), 128, 0, st>>>(groups_d, max_q_tiles * FA_BQ,
-                                                                             splits, ws_o, ws_ml, ws_rows);
-    OXY_LAUNCH_CHECK();
+    launch_pdl(fa_merge_kernel<HD>, dim3(max_q_tiles * FA_BQ / 4, n_groups), dim3(128), 0, st, groups_d, splits,
+               ws_o, ws_ml, ws_rows);
   }
 }
 
@@ -569,91 +589,11 @@ void flash_attention(const AttnGroup *groups_d, int n_groups, int max_q_tiles, i
 
 // ============================================================ decode attention
 
-// CTA = (row, key block).  8 warps; warp w scores keys 8w..8w+7 of the block
-// for all 8 query heads (16-byte vector loads: lane holds 8 dims of a key),
-// then warp h runs the softmax of head h and all 256 threads do P.V with one
-// output dim each (coalesced 512-byte V rows).  Partials merged in order.
-constexpr int DA_THREADS = 256;
 constexpr int DA_PART = Q_HEADS * (HEAD_DIM + 2);
-
-__global__ void __launch_bounds__(DA_THREADS)
-    decode_attn_kernel(const bf16 *q, const bf16 *kpool, const bf16 *vpool, const int *bt, int bt_stride,
-                       const int *pos, const int *active, int max_blocks, float scale_log2, float *ws) {
-  __shared__ float qs[Q_HEADS][HEAD_DIM];
-  __shared__ float sc[Q_HEADS][KV_BLOCK];
-  __shared__ float mh[Q_HEADS], lh[Q_HEADS];
-  const int r = blockIdx.x, blk = blockIdx.y;
-  if (active && !active[r]) return;
-  const int n_keys = pos[r] + 1;
-  const int k0 = blk * KV_BLOCK;
-  float *part = ws + ((size_t)r * max_blocks + blk) * DA_PART;
-  if (k0 >= n_keys) return;
-  const int nvalid = min(KV_BLOCK, n_keys - k0);
-  const int b = bt[(size_t)r * bt_stride + blk];
-  const bf16 *kb = kpool + (size_t)b * KV_BLOCK * HEAD_DIM;
-  const bf16 *vb = vpool + (size_t)b * KV_BLOCK * HEAD_DIM;
-  for (int i = threadIdx.x; i < Q_HEADS * HEAD_DIM; i += DA_THREADS)
-    qs[i / HEAD_DIM][i % HEAD_DIM] = __bfloat162float(q[(size_t)r * Q_HEADS * HEAD_DIM + i]);
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float qreg[Q_HEADS][8];
-#pragma unroll
-  for (int h = 0; h < Q_HEADS; ++h)
-#pragma unroll
-    for (int e = 0; e < 8; ++e) qreg[h][e] = qs[h][lane * 8 + e];
-#pragma unroll
-  for (int kk = 0; kk < 8; ++kk) {
-    const int j = warp * 8 + kk;
-    float acc[Q_HEADS];
-#pragma unroll
-    for (int h = 0; h < Q_HEADS; ++h) acc[h] = 0.f;
-    if (j < nvalid) {
-      const int4 raw = *reinterpret_cast<const int4 *>(kb + (size_t)j * HEAD_DIM + lane * 8);
-      const bf16 *kv = reinterpret_cast<const bf16 *>(&raw);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const float kf = __bfloat162float(kv[e]);
-#pragma unroll
-        for (int h = 0; h < Q_HEADS; ++h) acc[h] = fmaf(qreg[h][e], kf, acc[h]);
-      }
-    }
-#pragma unroll
-    for (int h = 0; h < Q_HEADS; ++h) {
-      const float v = warp_sum(acc[h]);
-      if (lane == 0) sc[h][j] = j < nvalid ? v * scale_log2 : -INFINITY;
-    }
-  }
-  __syncthreads();
-  {  // softmax of head `warp` over this block (2 keys per lane)
-    const int h = warp;
-    const float s0 = sc[h][lane], s1 = sc[h][lane + 32];
-    const float m = warp_max(fmaxf(s0, s1));
-    const float p0 = s0 == -INFINITY ? 0.f : exp2f(s0 - m), p1 = s1 == -INFINITY ? 0.f : exp2f(s1 - m);
-    sc[h][lane] = p0;
-    sc[h][lane + 32] = p1;
-    const float l = warp_sum(p0 + p1);
-    if (lane == 0) { mh[h] = m; lh[h] = l; }
-  }
-  __syncthreads();
-  const int d = threadIdx.x;  // one output dim per thread
-  float acc[Q_HEADS];
-#pragma unroll
-  for (int h = 0; h < Q_HEADS; ++h) acc[h] = 0.f;
-  for (int j = 0; j < nvalid; ++j) {
-    const float vf = __bfloat162float(vb[(size_t)j * HEAD_DIM + d]);
-#pragma unroll
-    for (int h = 0; h < Q_HEADS; ++h) acc[h] = fmaf(sc[h][j], vf, acc[h]);
-  }
-#pragma unroll
-  for (int h = 0; h < Q_HEADS; ++h) part[h * (HEAD_DIM + 2) + d] = acc[h];
-  if (d < Q_HEADS) {
-    part[d * (HEAD_DIM + 2) + HEAD_DIM] = mh[d];
-    part[d * (HEAD_DIM + 2) + HEAD_DIM + 1] = lh[d];
-  }
-}
 
 __global__ void decode_merge_kernel(const float *ws, bf16 *out, const int *pos, const int *active,
                                     int max_blocks) {
+  pdl_wait();
   const int r = blockIdx.x, h = blockIdx.y, d = threadIdx.x;
   if (active && !active[r]) return;
   const int nb = (pos[r] + 1 + KV_BLOCK - 1) / KV_BLOCK;
@@ -670,7 +610,7 @@ __global__ void decode_merge_kernel(const float *ws, bf16 *out, const int *pos, 
   out[(size_t)r * Q_HEADS * HEAD_DIM + h * HEAD_DIM + d] = __float2bfloat16(acc / L);
 }
 
-// Tensor-core variant (used): CTA = (row, 64-key block), 4 warps.  The
+// CTA = (row, 64-key block), 4 warps.  The
 // block's K and V (2 x 32 KB, one pool block per layer) are staged in smem
 // with 16-byte cp.async; the 8 query heads are the 16-row MMA A tile (rows
 // 8..15 zero); warp w owns keys 16w..16w+15: S = Q K^T (16 MMAs x 2), online
@@ -682,6 +622,7 @@ constexpr size_t DM_SMEM = (size_t)(16 + 2 * KV_BLOCK) * DM_LDS * sizeof(bf16);
 __global__ void __launch_bounds__(128)
     decode_attn_mma_kernel(const bf16 *q, const bf16 *kpool, const bf16 *vpool, const int *bt, int bt_stride,
                            const int *pos, const int *active, int max_blocks, float scale_log2, float *ws) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char dm_smem[];
   bf16 *sQ = reinterpret_cast<bf16 *>(dm_smem);
   bf16 *sK = sQ + 16 * DM_LDS;
@@ -818,11 +759,9 @@ void decode_attention(const bf16 *q, bf16 *out, const bf16 *kpool, const bf16 *v
     attr = true;
   }
   const float sl2 = scale * 1.4426950408889634f;
-  decode_attn_mma_kernel<<<dim3(rows, max_blocks), 128, DM_SMEM, st>>>(q, kpool, vpool, bt, bt_stride, pos,
-                                                                       active, max_blocks, sl2, ws);
-  OXY_LAUNCH_CHECK();
-  decode_merge_kernel<<<dim3(rows, Q_HEADS), HEAD_DIM, 0, st>>>(ws, out, pos, active, max_blocks);
-  OXY_LAUNCH_CHECK();
+  launch_pdl(decode_attn_mma_kernel, dim3(rows, max_blocks), dim3(128), DM_SMEM, st, q, kpool, vpool, bt,
+             bt_stride, pos, active, max_blocks, sl2, ws);
+  launch_pdl(decode_merge_kernel, dim3(rows, Q_HEADS), dim3(HEAD_DIM), 0, st, ws, out, pos, active, max_blocks);
 }
 
 // ============================================================ argmax
@@ -834,6 +773,7 @@ __device__ __forceinline__ void better(float &bv, int &bi, float v, int i) {
 }
 
 __global__ void argmax_partial_kernel(const float *logits, int V, const int *active, float *pv, int *pi) {
+  pdl_wait();
   __shared__ float sv[32];
   __shared__ int si[32];
   const int r = blockIdx.x, c = blockIdx.y;
@@ -862,6 +802,7 @@ __global__ void argmax_partial_kernel(const float *logits, int V, const int *act
 __global__ void argmax_final_kernel(int rows, const float *pv, const int *pi, int step, int k, int eos,
                                     int *active, int *tok, int *pos, int *count, const int *budget,
                                     int *out_tokens, int *plain_out) {
+  pdl_wait();
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= rows) return;
   if (active && !active[r]) return;
@@ -880,19 +821,14 @@ __global__ void argmax_final_kernel(int rows, const float *pv, const int *pi, in
 void argmax_update(const float *logits, int rows, int V, int step, int k, int eos, int *active, int *tok,
                    int *pos, int *count, const int *budget, int *out_tokens, float *pv, int *pi,
                    cudaStream_t st) {
-  argmax_partial_kernel<<<dim3(rows, AM_CHUNKS), 256, 0, st>>>(logits, V, active, pv, pi);
-  OXY_LAUNCH_CHECK();
-  argmax_final_kernel<<<(rows + 63) / 64, 64, 0, st>>>(rows, pv, pi, step, k, eos, active, tok, pos, count,
-                                                       budget, out_tokens, nullptr);
-  OXY_LAUNCH_CHECK();
+  launch_pdl(argmax_partial_kernel, dim3(rows, AM_CHUNKS), dim3(256), 0, st, logits, V, active, pv, pi);
+  launch_pdl(argmax_final_kernel, dim3((rows + 63) / 64), dim3(64), 0, st, rows, pv, pi, step, k, eos, active, tok, pos, count, budget, out_tokens, nullptr);
 }
 
 void argmax_rows(const float *logits, int rows, int V, int *out, float *pv, int *pi, cudaStream_t st) {
   argmax_partial_kernel<<<dim3(rows, AM_CHUNKS), 256, 0, st>>>(logits, V, nullptr, pv, pi);
   OXY_LAUNCH_CHECK();
-  argmax_final_kernel<<<(rows + 63) / 64, 64, 0, st>>>(rows, pv, pi, 0, 1, -1, nullptr, nullptr, nullptr,
-                                                       nullptr, nullptr, nullptr, out);
-  OXY_LAUNCH_CHECK();
+  launch_pdl(argmax_final_kernel, dim3((rows + 63) / 64), dim3(64), 0, st, rows, pv, pi, 0, 1, -1, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, out);
 }
 
 }  // namespace pi05

@@ -26,6 +26,8 @@ void layernorm(const float *x, int ldx, bf16 *y, int ldy, const float *w, const 
 // x[r] = float(table[tok[r]]) * scale (rows with active[r]==0 skipped if active)
 void embed_rows(float *x, int ldx, const bf16 *table, const int *tok, const int *active, int rows,
                 int D, float scale, cudaStream_t st);
+// RoPE inverse-frequency table (constant memory), set once per process
+void set_rope_theta(float theta);
 // RoPE on q (n_qh heads) and k from fp32 qkv [T, (n_qh+2)*256]; q -> q_out bf16 [T, n_qh*256];
 // k, v -> pool rows at slot[t] (layer base pointers) or dense rows (k_dense/v_dense, ld 256).
 void rope_split(const float *qkv, int T, int n_qh, const int *pos, const int *slot,

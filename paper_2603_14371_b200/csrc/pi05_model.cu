@@ -237,6 +237,7 @@ struct Model {
     OXY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     declare();
     materialise(st);
+    set_rope_theta(10000.f);
     NB = num_blocks;
     kv_stride = (size_t)NB * KV_BLOCK * HEAD_DIM;
     layer_stride = 2 * kv_stride;
@@ -273,7 +274,10 @@ struct Model {
   std::map<std::string, Graph> graphs;
   bool use_graphs = true;
 
+  int *gemm_counters = nullptr;
   void init_exec() {
+    OXY_CUDA(cudaMalloc(&gemm_counters, gemm::MAX_TILES * sizeof(int)));
+    OXY_CUDA(cudaMemset(gemm_counters, 0, gemm::MAX_TILES * sizeof(int)));
     OXY_CUDA(cudaStreamCreateWithFlags(&mst, cudaStreamNonBlocking));
     OXY_CUDA(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
     OXY_CUDA(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
@@ -288,6 +292,7 @@ struct Model {
     if (ev_in) cudaEventDestroy(ev_in);
     if (ev_out) cudaEventDestroy(ev_out);
     cudaFree(arena_d);
+    cudaFree(gemm_counters);
   }
   void enter(cudaStream_t caller) {
     OXY_CUDA(cudaEventRecord(ev_in, caller));
@@ -362,7 +367,7 @@ struct Model {
     gemm::Plan plan = gemm::make_plan(n_out, k, t, sms);
     float *wsp = plan.splits > 1 ? ws.as<float>((size_t)plan.splits * t * n_out) : nullptr;
     EpiParams e{mode, out, ldo, bias, nullptr, 0, gate};
-    gemm::launch(w, xin, n_out, k, t, e, plan, wsp, mst);
+    gemm::launch(w, xin, n_out, k, t, e, plan, wsp, gemm_counters, mst);
   }
 
   struct AttnPlan {
