@@ -257,14 +257,29 @@ __global__ void __launch_bounds__(192, 1)
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (s_last) {
         __threadfence();
-        for (int c = 0; c < bn; ++c) {
-          const int t = n0 + c;
-          if (t >= p.t) break;
-          float acc = 0.f;
-          if (f < p.n_out)
-            for (int s = 0; s < p.splits; ++s) acc += __ldcg(p.ws + ((size_t)s * p.t + t) * p.n_out + f);
-          const float pair = __shfl_xor_sync(0xffffffffu, acc, 1);
-          if (f < p.n_out) epilogue_store(p.epi, t, f, p.n_out, acc, pair);
+        const int ncols = min(bn, p.t - n0);
+        const bool fok = f < p.n_out;
+        for (int c0 = 0; c0 < ncols; c0 += 4) {
+          float acc[4] = {0.f, 0.f, 0.f, 0.f};
+          for (int s0 = 0; s0 < p.splits; s0 += 8) {
+            float v[8][4];  // 32 independent L2 loads in flight per thread
+#pragma unroll
+            for (int s = 0; s < 8; ++s)
+#pragma unroll
+              for (int j = 0; j < 4; ++j)
+                v[s][j] = (fok && s0 + s < p.splits && c0 + j < ncols)
+                              ? __ldcg(p.ws + ((size_t)(s0 + s) * p.t + n0 + c0 + j) * p.n_out + f)
+                              : 0.f;
+#pragma unroll
+            for (int s = 0; s < 8; ++s)
+#pragma unroll
+              for (int j = 0; j < 4; ++j) acc[j] += v[s][j];  // split order 0..S-1
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float pair = __shfl_xor_sync(0xffffffffu, acc[j], 1);
+            if (fok && c0 + j < ncols) epilogue_store(p.epi, n0 + c0 + j, f, p.n_out, acc[j], pair);
+          }
         }
         if (threadIdx.x == 64) p.counters[tile] = 0;
       }
@@ -318,15 +333,18 @@ static CUtensorMap make_map(const void *ptr, int rows, int k, int box_rows) {
 Plan make_plan(int n_out, int k, int t, int sms, int force_splits) {
   Plan p{};
   p.kb_total = (k + BK - 1) / BK;
+  p.m_tiles = (n_out + BM - 1) / BM;
   p.n_tiles = (t + MAX_BN - 1) / MAX_BN;
+  // wide token dims (prefill): narrower token tiles until the grid fills the SMs
+  while (t > 64 && p.m_tiles * p.n_tiles < sms && (t + p.n_tiles) / (p.n_tiles + 1) >= 48) ++p.n_tiles;
   int per = (t + p.n_tiles - 1) / p.n_tiles;
   p.bn = std::max(16, (per + 15) / 16 * 16);
-  p.m_tiles = (n_out + BM - 1) / BM;
+  p.n_tiles = (t + p.bn - 1) / p.bn;
   const int base = p.m_tiles * p.n_tiles;
   int splits = 1;
   if (force_splits > 0) {
     splits = force_splits;
-  } else if (base < sms) {
+  } else if (base < sms && t <= 64) {  // skinny (decode / denoise): split K, tiny fix-up
     splits = std::max(1, std::min(sms / base, p.kb_total / 4));
   }
   splits = std::max(1, std::min(splits, p.kb_total));
