@@ -7,6 +7,8 @@
 // releases a stage when the MMAs that read it retire.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
+#include <string>
 
 #include "cuda_util.cuh"
 #include "gemm_sm100.cuh"
@@ -146,9 +148,42 @@ struct KParams {
   EpiParams epi;
   float *ws;
   int *counters;  // one per (m, n) tile; self-resetting
+  int fixup;      // 1: last-arriving split CTA reduces; 0: separate reduce kernel
 };
 
-__global__ void __launch_bounds__(192, 1)
+// Launch-time knobs (env, read once): OXY_SPLITK=fixup|kernel, OXY_PDL=0|1,
+// OXY_GEMM_SMEM_KB=<per-CTA smem budget>.  Used for A/B measurements.
+struct Knobs {
+  int fixup = 0, pdl = 1, smem_kb = 200;
+  Knobs() {
+    if (const char *s = getenv("OXY_SPLITK")) fixup = std::string(s) == "fixup";
+    if (const char *s = getenv("OXY_PDL")) pdl = atoi(s);
+    if (const char *s = getenv("OXY_GEMM_SMEM_KB")) smem_kb = std::max(64, std::min(200, atoi(s)));
+  }
+};
+static const Knobs &knobs() {
+  static Knobs k;
+  return k;
+}
+
+// Fixed-order split-K reduction + epilogue; one thread per feature pair.
+__global__ void splitk_reduce_kernel(const float *ws, int splits, int t_rows, int n_out, EpiParams e) {
+  pdl_wait();
+  const int pairs = (n_out + 1) >> 1;
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)t_rows * pairs) return;
+  const int t = (int)(idx / pairs), f = (int)(idx % pairs) * 2;
+  float a0 = 0.f, a1 = 0.f;
+  for (int s = 0; s < splits; ++s) {
+    const float *row = ws + ((size_t)s * t_rows + t) * n_out;
+    a0 += row[f];
+    if (f + 1 < n_out) a1 += row[f + 1];
+  }
+  epilogue_store(e, t, f, n_out, a0, a1);
+  if (f + 1 < n_out) epilogue_store(e, t, f + 1, n_out, a1, a0);
+}
+
+__global__ void __launch_bounds__(192, 2)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 KParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -247,7 +282,7 @@ __global__ void __launch_bounds__(192, 1)
           epilogue_store(p.epi, t, f, p.n_out, acc, pair);
       }
     }
-    if (split_out) {
+    if (split_out && p.fixup) {
       // Deterministic split-K fix-up: the last CTA of this tile to arrive sums
       // the partials in split order 0..S-1 and applies the epilogue.
       __threadfence();
@@ -350,7 +385,7 @@ Plan make_plan(int n_out, int k, int t, int sms, int force_splits) {
   splits = std::max(1, std::min(splits, p.kb_total));
   const int per_split = (p.kb_total + splits - 1) / splits;
   p.splits = (p.kb_total + per_split - 1) / per_split;
-  p.stages = std::min(MAX_STAGES, SMEM_BUDGET / (A_STAGE_BYTES + p.bn * BK * 2));
+  p.stages = std::max(2, std::min(MAX_STAGES, knobs().smem_kb * 1024 / (A_STAGE_BYTES + p.bn * BK * 2)));
   return p;
 }
 
@@ -383,8 +418,24 @@ void launch(const void *w, const void *x, int n_out, int k, int t, const EpiPara
   kp.epi = epi;
   kp.ws = ws;
   kp.counters = counters;
+  kp.fixup = knobs().fixup;
   dim3 grid(plan.n_tiles, plan.m_tiles, plan.splits);
-  launch_pdl(gemm_kernel, grid, dim3(192), smem_bytes(plan), st, ma, mb, kp);
+  if (knobs().pdl) {
+    launch_pdl(gemm_kernel, grid, dim3(192), smem_bytes(plan), st, ma, mb, kp);
+  } else {
+    gemm_kernel<<<grid, 192, smem_bytes(plan), st>>>(ma, mb, kp);
+    OXY_LAUNCH_CHECK();
+  }
+  if (plan.splits > 1 && !kp.fixup) {
+    const int64_t n = (int64_t)t * ((n_out + 1) / 2);
+    if (knobs().pdl) {
+      launch_pdl(splitk_reduce_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, ws, plan.splits, t,
+                 n_out, epi);
+    } else {
+      splitk_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ws, plan.splits, t, n_out, epi);
+      OXY_LAUNCH_CHECK();
+    }
+  }
 }
 
 int *counters_for_abi() {
