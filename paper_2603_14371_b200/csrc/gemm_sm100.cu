@@ -154,7 +154,7 @@ struct KParams {
 // Launch-time knobs (env, read once): OXY_SPLITK=fixup|kernel, OXY_PDL=0|1,
 // OXY_GEMM_SMEM_KB=<per-CTA smem budget>.  Used for A/B measurements.
 struct Knobs {
-  int fixup = 0, pdl = 1, smem_kb = 200;
+  int fixup = 0, pdl = 1, smem_kb = 100;  // 2 CTAs per SM (measured best)
   Knobs() {
     if (const char *s = getenv("OXY_SPLITK")) fixup = std::string(s) == "fixup";
     if (const char *s = getenv("OXY_PDL")) pdl = atoi(s);

@@ -94,8 +94,8 @@ void set_rope_theta(float theta) {
 }
 
 // One CTA per token; thread i < 128 owns rotary pair (i, i+128) of every head.
-__global__ void rope_split_kernel(const float *qkv, int n_qh, const int *pos, const int *slot,
-                                  const int *active, bf16 *q_out, bf16 *kpool, bf16 *vpool,
+__global__ void rope_split_kernel(const float *__restrict__ qkv, int n_qh, const int *pos, const int *slot,
+                                  const int *active, bf16 *__restrict__ q_out, bf16 *kpool, bf16 *vpool,
                                   bf16 *k_dense, bf16 *v_dense, float theta) {
   pdl_wait();
   const int t = blockIdx.x;
@@ -109,20 +109,23 @@ __global__ void rope_split_kernel(const float *qkv, int n_qh, const int *pos, co
   const int s = slot ? slot[t] : -1;
   bf16 *kdst = s >= 0 ? kpool + (size_t)s * HEAD_DIM : (k_dense ? k_dense + (size_t)t * HEAD_DIM : nullptr);
   bf16 *vdst = s >= 0 ? vpool + (size_t)s * HEAD_DIM : (v_dense ? v_dense + (size_t)t * HEAD_DIM : nullptr);
-  for (int h = 0; h <= n_qh; ++h) {
-    const float *src = row + h * HEAD_DIM;
-    const float x1 = src[i], x2 = src[i + 128];
-    const float o1 = x1 * cs - x2 * sn, o2 = x2 * cs + x1 * sn;
-    bf16 *dst = h < n_qh ? q_out + (size_t)t * n_qh * HEAD_DIM + h * HEAD_DIM : kdst;
+  float x1[Q_HEADS + 2], x2[Q_HEADS + 2];  // all loads first (n_qh == Q_HEADS)
+#pragma unroll
+  for (int h = 0; h < Q_HEADS + 2; ++h) {
+    x1[h] = __ldg(row + h * HEAD_DIM + i);
+    x2[h] = __ldg(row + h * HEAD_DIM + i + 128);
+  }
+#pragma unroll
+  for (int h = 0; h <= Q_HEADS; ++h) {
+    bf16 *dst = h < Q_HEADS ? q_out + (size_t)t * Q_HEADS * HEAD_DIM + h * HEAD_DIM : kdst;
     if (dst) {
-      dst[i] = __float2bfloat16(o1);
-      dst[i + 128] = __float2bfloat16(o2);
+      dst[i] = __float2bfloat16(x1[h] * cs - x2[h] * sn);
+      dst[i + 128] = __float2bfloat16(x2[h] * cs + x1[h] * sn);
     }
   }
   if (vdst) {
-    const float *src = row + (n_qh + 1) * HEAD_DIM;
-    vdst[i] = __float2bfloat16(src[i]);
-    vdst[i + 128] = __float2bfloat16(src[i + 128]);
+    vdst[i] = __float2bfloat16(x1[Q_HEADS + 1]);
+    vdst[i + 128] = __float2bfloat16(x2[Q_HEADS + 1]);
   }
 }
 
@@ -519,39 +522,43 @@ __global__ void __launch_bounds__(128)
   }
 }
 
-// Combine split-KV partials in split order (log2 domain); one warp per row.
+// Combine split-KV partials in split order (log2 domain).  CTA = one query
+// row, thread = one column pair; split loads unrolled for memory parallelism.
 template <int HD>
 __global__ void fa_merge_kernel(const AttnGroup *groups, int splits, const float *ws_o, const float *ws_ml,
                                 int ws_rows) {
   pdl_wait();
   using C = FaCfg<HD>;
   const AttnGroup g = groups[blockIdx.y];
-  const int r = blockIdx.x * 4 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  const int r = blockIdx.x;
   if (r >= g.nq) return;
   const size_t row0 = (size_t)g.wrow0 + r;
+  const float *ml = ws_ml + row0 * 2;
+  const size_t mstride = (size_t)ws_rows * 2;
   float M = -INFINITY;
-  for (int s = lane; s < splits; s += 32) M = fmaxf(M, ws_ml[((size_t)s * ws_rows + row0) * 2]);
-  M = warp_max(M);
+#pragma unroll 8
+  for (int s = 0; s < splits; ++s) M = fmaxf(M, ml[s * mstride]);
   float L = 0.f;
-  for (int s = lane; s < splits; s += 32) {
-    const float m = ws_ml[((size_t)s * ws_rows + row0) * 2];
-    if (m != -INFINITY) L += ws_ml[((size_t)s * ws_rows + row0) * 2 + 1] * exp2f(m - M);
+#pragma unroll 8
+  for (int s = 0; s < splits; ++s) {
+    const float m = ml[s * mstride];
+    L += m == -INFINITY ? 0.f : ml[s * mstride + 1] * exp2f(m - M);
   }
-  L = warp_sum(L);
   const float inv = L > 0.f ? 1.f / L : 0.f;
-  for (int c = lane * 2; c < HD; c += 64) {
-    float a0 = 0.f, a1 = 0.f;
-    for (int s = 0; s < splits; ++s) {
-      const size_t wr = (size_t)s * ws_rows + row0;
-      const float m = ws_ml[wr * 2];
-      if (m == -INFINITY) continue;
-      const float w = exp2f(m - M);
-      const float2 v = *reinterpret_cast<const float2 *>(ws_o + wr * C::HDP + c);
-      a0 += v.x * w;
-      a1 += v.y * w;
-    }
-    *reinterpret_cast<__nv_bfloat162 *>(g.o + (size_t)r * g.ldo + c) = __floats2bfloat162_rn(a0 * inv, a1 * inv);
+  const int c = threadIdx.x * 2;
+  if (c >= HD) return;
+  const float *o = ws_o + row0 * C::HDP + c;
+  const size_t ostride = (size_t)ws_rows * C::HDP;
+  float a0 = 0.f, a1 = 0.f;
+#pragma unroll 8
+  for (int s = 0; s < splits; ++s) {
+    const float m = ml[s * mstride];
+    const float w = m == -INFINITY ? 0.f : exp2f(m - M);
+    const float2 v = *reinterpret_cast<const float2 *>(o + s * ostride);
+    a0 += v.x * w;
+    a1 += v.y * w;
   }
+  *reinterpret_cast<__nv_bfloat162 *>(g.o + (size_t)r * g.ldo + c) = __floats2bfloat162_rn(a0 * inv, a1 * inv);
 }
 
 template <int HD>
@@ -569,8 +576,8 @@ static void flash_launch(const AttnGroup *groups_d, int n_groups, int max_q_tile
   dim3 grid(n_groups * max_q_tiles, splits);
   launch_pdl(flash_attn_kernel<HD>, dim3(grid), dim3(128), C::SMEM, st, groups_d, max_q_tiles, kpool, vpool, scale_log2, splits, ws_o, ws_ml, ws_rows);
   if (splits > 1) {
-    launch_pdl(fa_merge_kernel<HD>, dim3(max_q_tiles * FA_BQ / 4, n_groups), dim3(128), 0, st, groups_d, splits,
-               ws_o, ws_ml, ws_rows);
+    launch_pdl(fa_merge_kernel<HD>, dim3(max_q_tiles * FA_BQ, n_groups), dim3((HD / 2 + 31) / 32 * 32), 0, st,
+               groups_d, splits, ws_o, ws_ml, ws_rows);
   }
 }
 

@@ -270,6 +270,7 @@ struct Model {
     cudaGraphExec_t exec = nullptr;
     unsigned long long gen = 0;
     int seen = 0;
+    unsigned long long kernels = 0;  // kernel nodes, counted per replay
   };
   std::map<std::string, Graph> graphs;
   bool use_graphs = true;
@@ -326,6 +327,7 @@ struct Model {
     Graph &g = graphs[key];
     if (g.exec && g.gen == g_devbuf_reallocs) {
       OXY_CUDA(cudaGraphLaunch(g.exec, mst));
+      __atomic_fetch_add(&g_launches, g.kernels, __ATOMIC_RELAXED);
       return;
     }
     if (g.exec) {
@@ -338,6 +340,7 @@ struct Model {
     }
     const unsigned long long gen0 = g_devbuf_reallocs;
     cudaGraph_t graph = nullptr;
+    const unsigned long long k0 = g_launches;
     OXY_CUDA(cudaStreamBeginCapture(mst, cudaStreamCaptureModeThreadLocal));
     try {
       body();
@@ -351,6 +354,7 @@ struct Model {
     OXY_CUDA(cudaGraphInstantiate(&g.exec, graph, 0));
     cudaGraphDestroy(graph);
     g.gen = g_devbuf_reallocs;
+    g.kernels = g_launches - k0;  // counted once here for the launch just below
     OXY_CUDA(cudaGraphLaunch(g.exec, mst));
   }
 
