@@ -47,6 +47,9 @@ def args_parse():
     p.add_argument("--warmup", type=int, default=8)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--streams", type=int, default=1, help="lock-stepped robot streams per GPU")
+    p.add_argument("--total-streams", type=int, default=0,
+                   help="shard this many streams over the ranks (stream s -> rank s mod N); "
+                        "overrides --streams (BASELINE configs[4]: 64)")
     p.add_argument("--k", type=int, default=5, help="decode tokens per frame")
     p.add_argument("--budget", type=int, default=30, help="language tokens per request (N)")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -322,6 +325,9 @@ def ours(a, ws, rank, local):
     import torch
     from paper_2603_14371_b200.pi05 import Pi05Backend, Pi05Config
     cfg = Pi05Config()
+    if a.total_streams:
+        from paper_2603_14371_b200.sharding import streams_for_rank
+        a.streams = max(1, len(streams_for_rank(a.total_streams, ws, rank)))
     r, k, budget = a.streams, a.k, a.budget
     steady_m = r * -(-budget // k)
     n_frames = a.warmup + a.steps

@@ -755,6 +755,242 @@ __global__ void __launch_bounds__(128)
   }
 }
 
+// ---- v2: chunked, pipelined, self-merging -----------------------------------
+// CTA = (row, chunk of up to `cb` pool blocks).  Blocks stream through a
+// 2-stage cp.async ring of unpadded, XOR-swizzled 32 KB K and V tiles (16-byte
+// chunk c of key row r lives at c ^ (r & 7): conflict-free ldmatrix).  Warp w
+// owns keys 16w..16w+15 of every block and keeps a running (m, l, O) across
+// the chunk; the 4 warps merge once at the end.  A row's chunks are merged by
+// the last-arriving CTA in chunk order (deterministic, no extra launch).
+constexpr int DV_ROW = HEAD_DIM * 2;                 // 512 B per key row
+constexpr int DV_TILE = KV_BLOCK * DV_ROW;           // 32 KB
+constexpr size_t DV_SMEM = 16 * DV_ROW + 2 * 2 * DV_TILE + 64;
+
+__device__ __forceinline__ uint32_t swz(uint32_t base, int row, int chunk) {
+  return base + row * DV_ROW + ((chunk ^ (row & 7)) << 4);
+}
+
+__global__ void __launch_bounds__(128, 1)
+    decode_attn_v2_kernel(const bf16 *q, const bf16 *kpool, const bf16 *vpool, const int *bt, int bt_stride,
+                          const int *pos, const int *active, int cb, int max_chunks, float scale_log2,
+                          float *ws, int *counters, bf16 *out) {
+  pdl_wait();
+  extern __shared__ __align__(128) unsigned char dv_smem[];
+  const uint32_t sQ = smem_addr(dv_smem);
+  const uint32_t sKV = sQ + 16 * DV_ROW;  // stage s: K at sKV + s*2*DV_TILE, V after it
+  __shared__ int s_last;
+  const int r = blockIdx.x, chunk = blockIdx.y;
+  if (active && !active[r]) return;
+  const int n_keys = pos[r] + 1;
+  const int nb = (n_keys + KV_BLOCK - 1) / KV_BLOCK;
+  const int n_chunks = (nb + cb - 1) / cb;
+  if (chunk >= n_chunks) return;
+  const int b0 = chunk * cb, b1 = min(nb, b0 + cb);
+  const int *btr = bt + (size_t)r * bt_stride;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  auto load_block = [&](int b, int stage) {
+    const int blk = btr[b];
+    const int nvalid = min(KV_BLOCK, n_keys - b * KV_BLOCK);
+    const bf16 *kb = kpool + (size_t)blk * KV_BLOCK * HEAD_DIM;
+    const bf16 *vb = vpool + (size_t)blk * KV_BLOCK * HEAD_DIM;
+    const uint32_t kbase = sKV + stage * 2 * DV_TILE, vbase = kbase + DV_TILE;
+    for (int i = threadIdx.x; i < KV_BLOCK * 32; i += 128) {
+      const int row = i >> 5, ch = i & 31;
+      if (row < nvalid) {
+        cp_async16(swz(kbase, row, ch), kb + (size_t)row * HEAD_DIM + ch * 8);
+        cp_async16(swz(vbase, row, ch), vb + (size_t)row * HEAD_DIM + ch * 8);
+      } else {  // zero rows: masked scores, and V must not hold NaN garbage
+        asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(swz(kbase, row, ch)), "r"(0));
+        asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(swz(vbase, row, ch)), "r"(0));
+      }
+    }
+  };
+  // group 0: Q (8 heads, rows 8..15 zero) + first block; group 1: second block
+  const bf16 *qr = q + (size_t)r * Q_HEADS * HEAD_DIM;
+  for (int i = threadIdx.x; i < 16 * 32; i += 128) {
+    const int row = i >> 5, ch = i & 31;
+    if (row < Q_HEADS) cp_async16(swz(sQ, row, ch), qr + (size_t)row * HEAD_DIM + ch * 8);
+    else asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(swz(sQ, row, ch)), "r"(0));
+  }
+  load_block(b0, 0);
+  cp_commit();
+  if (b0 + 1 < b1) load_block(b0 + 1, 1);
+  cp_commit();
+
+  float o[32][4];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float m_run = -INFINITY, l_run = 0.f;  // query row g = lane >> 2 (rows 8..15 are padding)
+  for (int b = b0; b < b1; ++b) {
+    const int stage = (b - b0) & 1;
+    cp_wait<1>();
+    __syncthreads();
+    const uint32_t kbase = sKV + stage * 2 * DV_TILE, vbase = kbase + DV_TILE;
+    float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+    const int krow = warp * 16 + (lane & 7) + ((lane >> 4) << 3);
+#pragma unroll
+    for (int kk = 0; kk < HEAD_DIM / 16; ++kk) {
+      uint32_t a0, a1, a2, a3, k0, k1, k2, k3;
+      ldsm_x4(swz(sQ, lane & 15, kk * 2 + (lane >> 4)), a0, a1, a2, a3);
+      ldsm_x4(swz(kbase, krow, kk * 2 + ((lane >> 3) & 1)), k0, k1, k2, k3);
+      mma16816(s[0], a0, a1, a2, a3, k0, k1);
+      mma16816(s[1], a0, a1, a2, a3, k2, k3);
+    }
+    float mx = m_run;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int key = b * KV_BLOCK + warp * 16 + nt * 8 + (lane & 3) * 2 + (e & 1);
+        float v = s[nt][e] * scale_log2;
+        if (key >= n_keys) v = -INFINITY;
+        s[nt][e] = v;
+        if (e < 2) mx = fmaxf(mx, v);
+      }
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    const float corr = (mx == -INFINITY) ? 1.f : exp2f(m_run - mx);
+    float ls = 0.f;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float p = (e < 2 && mx != -INFINITY) ? exp2f(s[nt][e] - mx) : 0.f;
+        s[nt][e] = p;
+        ls += p;
+      }
+    ls += __shfl_xor_sync(0xffffffffu, ls, 1);
+    ls += __shfl_xor_sync(0xffffffffu, ls, 2);
+    l_run = l_run * corr + ls;
+    m_run = mx;
+#pragma unroll
+    for (int nt = 0; nt < 32; ++nt) {
+      o[nt][0] *= corr;
+      o[nt][1] *= corr;
+    }
+    const uint32_t pa0 = pack_bf16(s[0][0], s[0][1]), pa1 = pack_bf16(s[0][2], s[0][3]);
+    const uint32_t pa2 = pack_bf16(s[1][0], s[1][1]), pa3 = pack_bf16(s[1][2], s[1][3]);
+    const int vrow = warp * 16 + (lane & 15);
+#pragma unroll
+    for (int np = 0; np < 16; ++np) {
+      uint32_t v0, v1, v2, v3;
+      ldsm_x4_t(swz(vbase, vrow, np * 2 + (lane >> 4)), v0, v1, v2, v3);
+      mma16816(o[2 * np], pa0, pa1, pa2, pa3, v0, v1);
+      mma16816(o[2 * np + 1], pa0, pa1, pa2, pa3, v2, v3);
+    }
+    __syncthreads();  // everyone is done with this stage
+    if (b + 2 < b1) load_block(b + 2, stage);
+    cp_commit();
+  }
+  cp_wait<0>();
+  // ---- merge the 4 warps (stage buffers reused) -> chunk partial (m, l, O[8][256])
+  float *sO = reinterpret_cast<float *>(dv_smem + 16 * DV_ROW);   // [4][8][256]
+  float *sM = sO + 4 * 8 * HEAD_DIM;                               // [4][8] m, [4][8] l
+  const int g = lane >> 2;
+#pragma unroll
+  for (int nt = 0; nt < 32; ++nt) {
+    const int c = nt * 8 + (lane & 3) * 2;
+    *reinterpret_cast<float2 *>(sO + (warp * 8 + g) * HEAD_DIM + c) = make_float2(o[nt][0], o[nt][1]);
+  }
+  if ((lane & 3) == 0) {
+    sM[warp * 8 + g] = m_run;
+    sM[32 + warp * 8 + g] = l_run;
+  }
+  __syncthreads();
+  float pm[Q_HEADS], pl[Q_HEADS];
+#pragma unroll
+  for (int h = 0; h < Q_HEADS; ++h) {
+    float M = -INFINITY, L = 0.f;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) M = fmaxf(M, sM[w * 8 + h]);
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const float mw = sM[w * 8 + h];
+      if (mw != -INFINITY) L += sM[32 + w * 8 + h] * exp2f(mw - M);
+    }
+    pm[h] = M;
+    pl[h] = L;
+  }
+  // thread owns 16 of the 8 x 256 outputs: (h, d) = (i / 256, i % 256) for i = tid + 128 j
+  float po[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int i = threadIdx.x + 128 * j, h = i >> 8, d = i & 255;
+    float acc = 0.f;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const float mw = sM[w * 8 + h];
+      if (mw != -INFINITY) acc += sO[(w * 8 + h) * HEAD_DIM + d] * exp2f(mw - pm[h]);
+    }
+    po[j] = acc;
+  }
+  bf16 *orow = out + (size_t)r * Q_HEADS * HEAD_DIM;
+  if (n_chunks == 1) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int i = threadIdx.x + 128 * j;
+      orow[i] = __float2bfloat16(po[j] / pl[i >> 8]);
+    }
+    return;
+  }
+  float *part = ws + ((size_t)r * max_chunks + chunk) * DA_PART;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int i = threadIdx.x + 128 * j;
+    part[(i >> 8) * (HEAD_DIM + 2) + (i & 255)] = po[j];
+  }
+  if (threadIdx.x < Q_HEADS) {
+    part[threadIdx.x * (HEAD_DIM + 2) + HEAD_DIM] = pm[threadIdx.x];
+    part[threadIdx.x * (HEAD_DIM + 2) + HEAD_DIM + 1] = pl[threadIdx.x];
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(counters + r, 1) == n_chunks - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const float *base = ws + (size_t)r * max_chunks * DA_PART;
+#pragma unroll 1
+  for (int j = 0; j < 16; ++j) {
+    const int i = threadIdx.x + 128 * j, h = i >> 8, d = i & 255;
+    float M = -INFINITY;
+    for (int c = 0; c < n_chunks; ++c) M = fmaxf(M, __ldcg(base + (size_t)c * DA_PART + h * (HEAD_DIM + 2) + HEAD_DIM));
+    float L = 0.f, acc = 0.f;
+#pragma unroll 4
+    for (int c = 0; c < n_chunks; ++c) {
+      const float *p = base + (size_t)c * DA_PART + h * (HEAD_DIM + 2);
+      const float w = exp2f(__ldcg(p + HEAD_DIM) - M);
+      L += __ldcg(p + HEAD_DIM + 1) * w;
+      acc += __ldcg(p + d) * w;
+    }
+    orow[i] = __float2bfloat16(acc / L);
+  }
+  if (threadIdx.x == 0) counters[r] = 0;
+}
+
+int decode_chunk_blocks(int rows, int max_blocks, int sms) {
+  // enough CTAs for ~2 per SM, at least 2 blocks per CTA so the ring pipelines
+  int cb = std::max(1, (rows * max_blocks + 2 * sms - 1) / (2 * sms));
+  return std::min(cb, max_blocks);
+}
+
+void decode_attention_v2(const bf16 *q, bf16 *out, const bf16 *kpool, const bf16 *vpool, const int *bt,
+                         int bt_stride, const int *pos, const int *active, int rows, int max_blocks, float scale,
+                         float *ws, int *counters, int sms, cudaStream_t st) {
+  if (rows <= 0) return;
+  static bool attr = false;
+  if (!attr) {
+    OXY_CUDA(cudaFuncSetAttribute(decode_attn_v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)DV_SMEM));
+    attr = true;
+  }
+  const int cb = decode_chunk_blocks(rows, max_blocks, sms);
+  const int max_chunks = (max_blocks + cb - 1) / cb;
+  launch_pdl(decode_attn_v2_kernel, dim3(rows, max_chunks), dim3(128), DV_SMEM, st, q, kpool, vpool, bt,
+             bt_stride, pos, active, cb, max_chunks, scale * 1.4426950408889634f, ws, counters, out);
+}
+
 void decode_attention(const bf16 *q, bf16 *out, const bf16 *kpool, const bf16 *vpool, const int *bt,
                       int bt_stride, const int *pos, const int *active, int rows, int max_blocks,
                       float scale, float *ws, cudaStream_t st) {
@@ -848,9 +1084,18 @@ extern "C" int oxy_paged_decode_attention(const void *q_d, void *out_d, const vo
   OXY_API_BEGIN
   OXY_REQUIRE(rows >= 1 && max_blocks >= 1 && bt_stride >= max_blocks, "bad decode-attention shape");
   using oxy::pi05::bf16;
-  oxy::pi05::decode_attention(static_cast<const bf16 *>(q_d), static_cast<bf16 *>(out_d),
-                              static_cast<const bf16 *>(kpool_d), static_cast<const bf16 *>(vpool_d), bt_d,
-                              bt_stride, pos_d, nullptr, rows, max_blocks, 1.f / 16.f, ws_d,
-                              oxy::as_stream(stream));
+  OXY_REQUIRE(rows <= 8192, "at most 8192 decode rows per call");
+  static int *counters = nullptr;
+  if (!counters) {
+    OXY_CUDA(cudaMalloc(&counters, 8192 * sizeof(int)));
+    OXY_CUDA(cudaMemset(counters, 0, 8192 * sizeof(int)));
+  }
+  int dev = 0, sms = 148;
+  OXY_CUDA(cudaGetDevice(&dev));
+  OXY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  oxy::pi05::decode_attention_v2(static_cast<const bf16 *>(q_d), static_cast<bf16 *>(out_d),
+                                 static_cast<const bf16 *>(kpool_d), static_cast<const bf16 *>(vpool_d), bt_d,
+                                 bt_stride, pos_d, nullptr, rows, max_blocks, 1.f / 16.f, ws_d, counters, sms,
+                                 oxy::as_stream(stream));
   OXY_API_END
 }

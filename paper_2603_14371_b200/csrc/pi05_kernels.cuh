@@ -79,6 +79,13 @@ void decode_attention(const bf16 *q, bf16 *out, const bf16 *kpool, const bf16 *v
                       const int *bt, int bt_stride, const int *pos, const int *active, int rows,
                       int max_blocks, float scale, float *ws, cudaStream_t st);
 
+// v2 (used): chunked + pipelined, last-arriving chunk merges (counters: one per row,
+// zero-initialised, self-resetting).  ws: rows*max_blocks*8*(256+2) floats.
+void decode_attention_v2(const bf16 *q, bf16 *out, const bf16 *kpool, const bf16 *vpool, const int *bt,
+                         int bt_stride, const int *pos, const int *active, int rows, int max_blocks, float scale,
+                         float *ws, int *counters, int sms, cudaStream_t st);
+int decode_chunk_blocks(int rows, int max_blocks, int sms);
+
 // Greedy token + continuous-batching state update over logits [rows, V].
 // part: rows * 64 (val, idx) scratch.
 void argmax_update(const float *logits, int rows, int V, int step, int k, int eos, int *active,

@@ -55,6 +55,7 @@ struct VitW {
 constexpr int PATCH_K = 640;  // 14*14*3 = 588 padded to a multiple of 64
 constexpr int QDIM = Q_HEADS * HEAD_DIM;
 constexpr int QKV = (Q_HEADS + 2) * HEAD_DIM;
+constexpr int MAX_DECODE_ROWS = 8192;
 
 struct Model {
   oxy_pi05_config c{};
@@ -276,9 +277,12 @@ struct Model {
   bool use_graphs = true;
 
   int *gemm_counters = nullptr;
+  int *dec_counters = nullptr;  // per decode row, for the self-merging attention
   void init_exec() {
     OXY_CUDA(cudaMalloc(&gemm_counters, gemm::MAX_TILES * sizeof(int)));
     OXY_CUDA(cudaMemset(gemm_counters, 0, gemm::MAX_TILES * sizeof(int)));
+    OXY_CUDA(cudaMalloc(&dec_counters, MAX_DECODE_ROWS * sizeof(int)));
+    OXY_CUDA(cudaMemset(dec_counters, 0, MAX_DECODE_ROWS * sizeof(int)));
     OXY_CUDA(cudaStreamCreateWithFlags(&mst, cudaStreamNonBlocking));
     OXY_CUDA(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
     OXY_CUDA(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
@@ -294,6 +298,7 @@ struct Model {
     if (ev_out) cudaEventDestroy(ev_out);
     cudaFree(arena_d);
     cudaFree(gemm_counters);
+    cudaFree(dec_counters);
   }
   void enter(cudaStream_t caller) {
     OXY_CUDA(cudaEventRecord(ev_in, caller));
@@ -769,7 +774,8 @@ struct Model {
           gemm(w.wqkv, Y, QKV, W, rows, gemm::EPI_F32, QKVf, QKV);
           rope_split(QKVf, rows, Q_HEADS, d_pos, d_slot, d_active, Qb, kpool(l), vpool(l), nullptr, nullptr,
                      10000.f, mst);
-          decode_attention(Qb, Ob, kpool(l), vpool(l), d_bt, maxb, d_pos, d_active, rows, maxb, scale, dws, mst);
+          decode_attention_v2(Qb, Ob, kpool(l), vpool(l), d_bt, maxb, d_pos, d_active, rows, maxb, scale, dws,
+                              dec_counters, sms, mst);
           gemm(w.wo, Ob, W, QDIM, rows, gemm::EPI_ADD_F32, X, W);
           rmsnorm(X, W, Y, W, w.ln2, nullptr, nullptr, rows, W, 1e-6f, mst);
           gemm(w.wgu, Y, 2 * c.mlp, W, rows, gemm::EPI_GEGLU_BF16, Hm, c.mlp);
@@ -892,6 +898,8 @@ int oxy_pi05_decode(oxy_pi05 *p, int32_t rows, int32_t k, const int32_t *block_t
                     void *stream) {
   OXY_API_BEGIN
   OXY_REQUIRE(rows >= 1, "decode needs at least one row");
+  OXY_REQUIRE(rows <= oxy::pi05::MAX_DECODE_ROWS, "at most %d decode rows per call",
+              oxy::pi05::MAX_DECODE_ROWS);
   OXY_REQUIRE(k >= 1, "decode step count must be >= 1, got %d", k);
   p->m.decode(oxy::as_stream(stream), rows, k, block_tables_h, max_blocks, seq_lens_h, last_tokens_h, budgets_h,
               cow_h, out_tokens_h, out_count_h, logits_h);
