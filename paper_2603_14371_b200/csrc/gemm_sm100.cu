@@ -140,6 +140,27 @@ __device__ __forceinline__ void epilogue_store(const EpiParams &e, int t, int f,
       static_cast<__nv_bfloat16 *>(e.out)[(size_t)t * e.ldo + f] =
           __float2bfloat16(acc / (1.f + __expf(-acc)));
       break;
+    case EPI_QKV_ROPE: {
+      const QkvRope &r = e.rope;
+      const int h = f >> 8, j = f & 255, i = j >> 1;
+      if (h < 9) {  // q heads 0..7, k head 8: rotate the (x1, x2) pair
+        float sn, cs;
+        sincosf((float)r.pos[t] * r.inv_freq[i], &sn, &cs);
+        const bool second = j & 1;  // this lane holds x2 (dim i + 128)
+        const float v = second ? acc * cs + pair * sn : acc * cs - pair * sn;
+        const int dim = second ? i + 128 : i;
+        if (h < 8) {
+          r.q_out[(size_t)t * 2048 + h * 256 + dim] = __float2bfloat16(v);
+        } else {
+          const int s = r.slot ? r.slot[t] : t;
+          if (s >= 0) r.k_dst[(size_t)s * 256 + dim] = __float2bfloat16(v);
+        }
+      } else {  // v head
+        const int s = r.slot ? r.slot[t] : t;
+        if (s >= 0) r.v_dst[(size_t)s * 256 + j] = __float2bfloat16(acc);
+      }
+      break;
+    }
   }
 }
 
@@ -168,6 +189,7 @@ static const Knobs &knobs() {
 
 // Fixed-order split-K reduction + epilogue; one thread per feature pair.
 __global__ void splitk_reduce_kernel(const float *ws, int splits, int t_rows, int n_out, EpiParams e) {
+  pdl_trigger();
   pdl_wait();
   const int pairs = (n_out + 1) >> 1;
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -228,11 +250,21 @@ __global__ void __launch_bounds__(192, 2)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  pdl_wait();  // prologue above overlaps the previous kernel; operands are read below
+  pdl_trigger();  // let the next kernel launch (and prefetch its weights) once we are resident
 
   if (warp == 0) {
     if (lane == 0) {
-      for (int i = 0; i < nkb; ++i) {
+      // Weights never depend on the previous kernel: stream the first ring of
+      // weight tiles before waiting on it, activations after.
+      const int pre = min(nkb, stages);
+      for (int i = 0; i < pre; ++i) {
+        mbar_expect_tx(full0 + 8 * i, A_STAGE_BYTES + b_bytes);
+        tma_load_2d(&tmA, full0 + 8 * i, smem_u32(sA + i * A_STAGE_BYTES), (kb0 + i) * BK, m0);
+      }
+      pdl_wait();
+      for (int i = 0; i < pre; ++i)
+        tma_load_2d(&tmB, full0 + 8 * i, smem_u32(sB + i * b_bytes), (kb0 + i) * BK, n0);
+      for (int i = pre; i < nkb; ++i) {
         const int s = i % stages;
         const uint32_t ph = (i / stages) & 1;
         mbar_wait(empty0 + 8 * s, ph ^ 1);
@@ -262,6 +294,7 @@ __global__ void __launch_bounds__(192, 2)
     }
     __syncwarp();
   } else {
+    pdl_wait();  // the epilogue reads bias/residual/gates and writes outputs
     mbar_wait(done, 0);
     tc_fence_after();
     const int q = warp & 3;

@@ -28,6 +28,17 @@ enum Epi : int {
   EPI_ADD_BF16 = 5,   // out_bf16[t, f] = bf16(acc + bias + res_f32[t, f])  (no in-place)
   EPI_ADD_GATED_F32 = 6,  // out_f32[t, f] += gate[f] * (acc + bias)     adaRMS gated residual
   EPI_SWISH_BF16 = 7,     // out_bf16[t, f] = swish(acc + bias)
+  EPI_QKV_ROPE = 8,       // fused QKV projection: RoPE on q/k (rotary pairs interleaved in the
+                          // weight rows), q -> bf16 [T, 2048], k/v -> pool slot rows or dense rows
+};
+
+// Extra state of EPI_QKV_ROPE (8 q heads + 1 k + 1 v head of 256).
+struct QkvRope {
+  const float *inv_freq;  // [128]
+  const int *pos;         // [T]
+  const int *slot;        // [T] pool slot (<0: skip k/v) or null: dense k/v rows
+  __nv_bfloat16 *q_out;   // [T, 2048]
+  __nv_bfloat16 *k_dst, *v_dst;  // pool layer base (slot rows) or dense [T, 256]
 };
 
 struct EpiParams {
@@ -38,7 +49,16 @@ struct EpiParams {
   const float *res;     // EPI_ADD_BF16 residual input [T, ldr]
   int ldr;
   const float *gate;    // EPI_ADD_GATED_F32 per-feature gate [N]
+  QkvRope rope;         // EPI_QKV_ROPE
 };
+
+// Row permutation that puts rotary pair (i, i + 128) of every q/k head at rows
+// (2i, 2i + 1): new row -> canonical row.  V rows (f >= 2304) are unchanged.
+__host__ __device__ inline int qkv_rope_row(int f) {
+  if (f >= 9 * 256) return f;
+  const int h = f >> 8, j = f & 255;
+  return (h << 8) + ((j & 1) ? (j >> 1) + 128 : (j >> 1));
+}
 
 constexpr int BM = 128;        // weight rows per tile (UMMA M)
 constexpr int BK = 64;         // K per stage: 64 bf16 = one 128-byte swizzle row

@@ -3,6 +3,7 @@
 #include <cmath>
 
 #include "cuda_util.cuh"
+#include "gemm_sm100.cuh"
 #include "pi05_kernels.cuh"
 
 namespace oxy {
@@ -12,6 +13,7 @@ namespace pi05 {
 
 __global__ void rmsnorm_kernel(const float *x, int ldx, bf16 *y, int ldy, const float *w,
                                const float *ms, const float *mb, int D, float eps) {
+  pdl_trigger();
   pdl_wait();
   __shared__ float red[32];
   const float *xr = x + (size_t)blockIdx.x * ldx;
@@ -45,6 +47,7 @@ void rmsnorm(const float *x, int ldx, bf16 *y, int ldy, const float *w, const fl
 
 __global__ void layernorm_kernel(const float *x, int ldx, bf16 *y, int ldy, const float *w,
                                  const float *b, int D, float eps) {
+  pdl_trigger();
   pdl_wait();
   __shared__ float red[32];
   const float *xr = x + (size_t)blockIdx.x * ldx;
@@ -70,6 +73,7 @@ void layernorm(const float *x, int ldx, bf16 *y, int ldy, const float *w, const 
 
 __global__ void embed_kernel(float *x, int ldx, const bf16 *table, const int *tok,
                              const int *active, int D, float scale) {
+  pdl_trigger();
   pdl_wait();
   const int r = blockIdx.x;
   if (active && !active[r]) return;
@@ -82,6 +86,17 @@ void embed_rows(float *x, int ldx, const bf16 *table, const int *tok, const int 
                 int D, float scale, cudaStream_t st) {
   if (rows <= 0) return;
   launch_pdl(embed_kernel, dim3(rows), dim3(256), 0, st, x, ldx, table, tok, active, D, scale);
+}
+
+__global__ void permute_rows_kernel(bf16 *dst, const bf16 *src, int cols) {
+  const int f = blockIdx.x;
+  const bf16 *s = src + (size_t)gemm::qkv_rope_row(f) * cols;
+  for (int j = threadIdx.x; j < cols; j += blockDim.x) dst[(size_t)f * cols + j] = s[j];
+}
+
+void permute_rows(bf16 *dst, const bf16 *src, int rows, int cols, cudaStream_t st) {
+  permute_rows_kernel<<<rows, 256, 0, st>>>(dst, src, cols);
+  OXY_LAUNCH_CHECK();
 }
 
 // RoPE inverse frequencies theta^(-2i/256), computed in double on the host.
@@ -97,6 +112,7 @@ void set_rope_theta(float theta) {
 __global__ void rope_split_kernel(const float *__restrict__ qkv, int n_qh, const int *pos, const int *slot,
                                   const int *active, bf16 *__restrict__ q_out, bf16 *kpool, bf16 *vpool,
                                   bf16 *k_dense, bf16 *v_dense, float theta) {
+  pdl_trigger();
   pdl_wait();
   const int t = blockIdx.x;
   if (active && !active[t]) return;
@@ -137,6 +153,7 @@ void rope_split(const float *qkv, int T, int n_qh, const int *pos, const int *sl
 }
 
 __global__ void patchify_kernel(const uint8_t *img, bf16 *patches, int kpad) {
+  pdl_trigger();
   pdl_wait();
   const int p = blockIdx.x;  // image * 256 + patch
   const int im = p >> 8, py = (p & 255) >> 4, px = p & 15;
@@ -158,6 +175,7 @@ void patchify(const uint8_t *img, int n, bf16 *patches, int kpad, cudaStream_t s
 }
 
 __global__ void tile_rows_kernel(float *dst, int ld, const float *src, int ld_src, int period, int D) {
+  pdl_trigger();
   pdl_wait();
   const int r = blockIdx.x;
   const float *s = src + (size_t)(r % period) * ld_src;
@@ -171,6 +189,7 @@ void tile_rows(float *dst, int ld, const float *src, int ld_src, int rows, int p
 }
 
 __global__ void f32_to_bf16_kernel(const float *x, bf16 *y, int64_t n) {
+  pdl_trigger();
   pdl_wait();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     y[i] = __float2bfloat16(x[i]);
@@ -183,6 +202,7 @@ void f32_to_bf16(const float *x, bf16 *y, int64_t n, cudaStream_t st) {
 }
 
 __global__ void euler_kernel(float *a, const float *v, bf16 *ab, int64_t n, float dt) {
+  pdl_trigger();
   pdl_wait();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const float x = a[i] + dt * v[i];
@@ -198,6 +218,7 @@ void euler_step(float *a, const float *v, bf16 *ab, int64_t n, float dt, cudaStr
 
 // Box-Muller on consecutive splitmix64 uniforms: pair i uses draws 2i, 2i+1.
 __global__ void noise_kernel(float *out, int64_t n, uint64_t seed) {
+  pdl_trigger();
   pdl_wait();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; 2 * i < n; i += (int64_t)gridDim.x * blockDim.x) {
     double u1 = splitmix_uniform(seed, 2 * i), u2 = splitmix_uniform(seed, 2 * i + 1);
@@ -213,6 +234,7 @@ void normal_noise(float *out, int64_t n, uint64_t seed, cudaStream_t st) {
 }
 
 __global__ void init_bf16_kernel(bf16 *out, int64_t n, uint64_t seed, uint64_t offset, float bound) {
+  pdl_trigger();
   pdl_wait();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     double u = splitmix_uniform(seed, offset + (uint64_t)i);
@@ -226,6 +248,7 @@ void init_uniform_bf16(bf16 *out, int64_t n, uint64_t seed, uint64_t offset, flo
 }
 
 __global__ void init_f32_kernel(float *out, int64_t n, uint64_t seed, uint64_t offset, float bound, float center) {
+  pdl_trigger();
   pdl_wait();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     double u = splitmix_uniform(seed, offset + (uint64_t)i);
@@ -240,6 +263,7 @@ void init_uniform_f32(float *out, int64_t n, uint64_t seed, uint64_t offset, flo
 }
 
 __global__ void cow_kernel(bf16 *pool, const int *cow, size_t layer_stride, size_t kv_stride) {
+  pdl_trigger();
   pdl_wait();
   const int r = blockIdx.x, l = blockIdx.y;
   const int src = cow[r * 3], dst = cow[r * 3 + 1], n = cow[r * 3 + 2];
@@ -263,6 +287,7 @@ void cow_blocks(bf16 *pool, const int *cow, int rows, int L, size_t layer_stride
 
 __global__ void next_slot_kernel(int *slot, const int *pos, const int *active, const int *bt,
                                  int bt_stride, int rows) {
+  pdl_trigger();
   pdl_wait();
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= rows) return;
@@ -345,6 +370,7 @@ template <int HD>
 __global__ void __launch_bounds__(128)
     flash_attn_kernel(const AttnGroup *groups, int max_q_tiles, const bf16 *kpool, const bf16 *vpool,
                       float scale_log2, int splits, float *ws_o, float *ws_ml, int ws_rows) {
+  pdl_trigger();
   pdl_wait();
   using C = FaCfg<HD>;
   constexpr int NT = C::HDP / 8;  // output n-tiles per warp
@@ -527,6 +553,7 @@ __global__ void __launch_bounds__(128)
 template <int HD>
 __global__ void fa_merge_kernel(const AttnGroup *groups, int splits, const float *ws_o, const float *ws_ml,
                                 int ws_rows) {
+  pdl_trigger();
   pdl_wait();
   using C = FaCfg<HD>;
   const AttnGroup g = groups[blockIdx.y];
@@ -600,6 +627,7 @@ constexpr int DA_PART = Q_HEADS * (HEAD_DIM + 2);
 
 __global__ void decode_merge_kernel(const float *ws, bf16 *out, const int *pos, const int *active,
                                     int max_blocks) {
+  pdl_trigger();
   pdl_wait();
   const int r = blockIdx.x, h = blockIdx.y, d = threadIdx.x;
   if (active && !active[r]) return;
@@ -629,6 +657,7 @@ constexpr size_t DM_SMEM = (size_t)(16 + 2 * KV_BLOCK) * DM_LDS * sizeof(bf16);
 __global__ void __launch_bounds__(128)
     decode_attn_mma_kernel(const bf16 *q, const bf16 *kpool, const bf16 *vpool, const int *bt, int bt_stride,
                            const int *pos, const int *active, int max_blocks, float scale_log2, float *ws) {
+  pdl_trigger();
   pdl_wait();
   extern __shared__ __align__(16) unsigned char dm_smem[];
   bf16 *sQ = reinterpret_cast<bf16 *>(dm_smem);
@@ -774,6 +803,7 @@ __global__ void __launch_bounds__(128, 1)
     decode_attn_v2_kernel(const bf16 *q, const bf16 *kpool, const bf16 *vpool, const int *bt, int bt_stride,
                           const int *pos, const int *active, int cb, int max_chunks, float scale_log2,
                           float *ws, int *counters, bf16 *out) {
+  pdl_trigger();
   pdl_wait();
   extern __shared__ __align__(128) unsigned char dv_smem[];
   const uint32_t sQ = smem_addr(dv_smem);
@@ -1016,6 +1046,7 @@ __device__ __forceinline__ void better(float &bv, int &bi, float v, int i) {
 }
 
 __global__ void argmax_partial_kernel(const float *logits, int V, const int *active, float *pv, int *pi) {
+  pdl_trigger();
   pdl_wait();
   __shared__ float sv[32];
   __shared__ int si[32];
@@ -1045,6 +1076,7 @@ __global__ void argmax_partial_kernel(const float *logits, int V, const int *act
 __global__ void argmax_final_kernel(int rows, const float *pv, const int *pi, int step, int k, int eos,
                                     int *active, int *tok, int *pos, int *count, const int *budget,
                                     int *out_tokens, int *plain_out) {
+  pdl_trigger();
   pdl_wait();
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= rows) return;

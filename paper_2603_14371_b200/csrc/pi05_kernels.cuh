@@ -26,6 +26,8 @@ void layernorm(const float *x, int ldx, bf16 *y, int ldy, const float *w, const 
 // x[r] = float(table[tok[r]]) * scale (rows with active[r]==0 skipped if active)
 void embed_rows(float *x, int ldx, const bf16 *table, const int *tok, const int *active, int rows,
                 int D, float scale, cudaStream_t st);
+// dst[f, :] = src[gemm::qkv_rope_row(f), :] (rotary-pair interleaved QKV weights)
+void permute_rows(bf16 *dst, const bf16 *src, int rows, int cols, cudaStream_t st);
 // RoPE inverse-frequency table (constant memory), set once per process
 void set_rope_theta(float theta);
 // RoPE on q (n_qh heads) and k from fp32 qkv [T, (n_qh+2)*256]; q -> q_out bf16 [T, n_qh*256];

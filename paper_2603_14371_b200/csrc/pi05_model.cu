@@ -92,6 +92,7 @@ struct Model {
     cudaFree(wmem);
     cudaFree(pool);
     cudaFree(noise);
+    cudaFree(rope_inv);
     for (DevBuf *b : {&mod, &x, &y, &qkv, &q, &o, &hmid, &ws, &ints, &kd, &vd, &attn_groups, &attn_ws,
                       &attn_ml, &logits, &amv, &ami, &vit_h, &vit_y, &vit_qkv, &vit_o, &vit_m, &patches,
                       &act, &act_bf, &vel, &xe, &dec_ws, &kvread_i, &kvread_f})
@@ -106,6 +107,12 @@ struct Model {
     tensors.push_back(t);
   }
   static float mat_bound(int64_t fan_in) { return (float)std::sqrt(3.0 / (double)fan_in); }
+  // Gemma/expert QKV weights are stored with rotary pairs interleaved (gemm::qkv_rope_row)
+  static bool is_rope_qkv(const std::string &n) {
+    return (n.rfind("llm.", 0) == 0 || n.rfind("expert.", 0) == 0) && n.size() > 5 &&
+           n.compare(n.size() - 5, 5, ".wqkv") == 0;
+  }
+  float *rope_inv = nullptr;
   // action vectors are padded to 8 lanes so the in-projection's K stride is 16-byte aligned
   int apad() const { return (c.action_dim + 7) / 8 * 8; }
 
@@ -239,6 +246,22 @@ struct Model {
     declare();
     materialise(st);
     set_rope_theta(10000.f);
+    {  // device RoPE table for the fused QKV epilogue, and the rotary-pair row order
+      float inv[128];
+      for (int i = 0; i < 128; ++i) inv[i] = (float)std::pow(10000.0, -2.0 * i / 256.0);
+      OXY_CUDA(cudaMalloc(&rope_inv, sizeof(inv)));
+      OXY_CUDA(cudaMemcpyAsync(rope_inv, inv, sizeof(inv), cudaMemcpyHostToDevice, st));
+      bf16 *tmp = nullptr;
+      const int kmax = std::max(c.width, c.expert_width);
+      OXY_CUDA(cudaMalloc(&tmp, (size_t)QKV * kmax * sizeof(bf16)));
+      for (auto &t : tensors)
+        if (is_rope_qkv(t.name)) {
+          OXY_CUDA(cudaMemcpyAsync(tmp, t.ptr, t.numel() * 2, cudaMemcpyDeviceToDevice, st));
+          permute_rows(static_cast<bf16 *>(t.ptr), tmp, (int)t.rows, (int)t.cols, st);
+        }
+      OXY_CUDA(cudaStreamSynchronize(st));
+      cudaFree(tmp);
+    }
     NB = num_blocks;
     kv_stride = (size_t)NB * KV_BLOCK * HEAD_DIM;
     layer_stride = 2 * kv_stride;
@@ -375,8 +398,18 @@ struct Model {
     if (t <= 0) return;
     gemm::Plan plan = gemm::make_plan(n_out, k, t, sms);
     float *wsp = plan.splits > 1 ? ws.as<float>((size_t)plan.splits * t * n_out) : nullptr;
-    EpiParams e{mode, out, ldo, bias, nullptr, 0, gate};
+    EpiParams e{mode, out, ldo, bias, nullptr, 0, gate, {}};
     gemm::launch(w, xin, n_out, k, t, e, plan, wsp, gemm_counters, mst);
+  }
+  // fused QKV projection + RoPE + K/V append (slot == null: dense k/v rows)
+  void gemm_qkv(const bf16 *w, const bf16 *xin, int k, int t, const int *pos, const int *slot, bf16 *q_out,
+                bf16 *k_dst, bf16 *v_dst) {
+    if (t <= 0) return;
+    gemm::Plan plan = gemm::make_plan(QKV, k, t, sms);
+    float *wsp = plan.splits > 1 ? ws.as<float>((size_t)plan.splits * t * QKV) : nullptr;
+    EpiParams e{gemm::EPI_QKV_ROPE, nullptr, 0, nullptr, nullptr, 0, nullptr,
+                gemm::QkvRope{rope_inv, pos, slot, q_out, k_dst, v_dst}};
+    gemm::launch(w, xin, QKV, k, t, e, plan, wsp, gemm_counters, mst);
   }
 
   struct AttnPlan {
@@ -568,9 +601,7 @@ struct Model {
       for (int l = 0; l < c.depth; ++l) {
         const LayerW &w = L[l];
         rmsnorm(X, W, Y, W, w.ln1, nullptr, nullptr, T, W, 1e-6f, mst);
-        gemm(w.wqkv, Y, QKV, W, T, gemm::EPI_F32, QKVf, QKV);
-        rope_split(QKVf, T, Q_HEADS, d_pos, d_slot, nullptr, Qb, kpool(l), vpool(l), nullptr, nullptr, 10000.f,
-                   mst);
+        gemm_qkv(w.wqkv, Y, W, T, d_pos, d_slot, Qb, kpool(l), vpool(l));
         if (l == c.depth - 1) break;  // the last block's output is not cached
         attend(a_llm, kpool(l), vpool(l));
         gemm(w.wo, Ob, W, QDIM, T, gemm::EPI_ADD_F32, X, W);
@@ -697,8 +728,7 @@ struct Model {
           const ExpertW &w = E[l];
           const float *m = ms + (size_t)l * 6 * We;
           rmsnorm(X, We, Y, We, nullptr, m, m + We, T, We, 1e-6f, mst);
-          gemm(w.wqkv, Y, QKV, We, T, gemm::EPI_F32, QKVf, QKV);
-          rope_split(QKVf, T, Q_HEADS, d_pos, nullptr, nullptr, Qb, nullptr, nullptr, Kd, Vd, 10000.f, mst);
+          gemm_qkv(w.wqkv, Y, We, T, d_pos, nullptr, Qb, Kd, Vd);
           attend(ap, kpool(l), vpool(l));
           gemm(w.wo, Ob, We, QDIM, T, gemm::EPI_ADD_GATED_F32, X, We, nullptr, m + 2 * We);
           rmsnorm(X, We, Y, We, nullptr, m + 3 * We, m + 4 * We, T, We, 1e-6f, mst);
@@ -771,9 +801,7 @@ struct Model {
         for (int l = 0; l < c.depth; ++l) {
           const LayerW &w = L[l];
           rmsnorm(X, W, Y, W, w.ln1, nullptr, nullptr, rows, W, 1e-6f, mst);
-          gemm(w.wqkv, Y, QKV, W, rows, gemm::EPI_F32, QKVf, QKV);
-          rope_split(QKVf, rows, Q_HEADS, d_pos, d_slot, d_active, Qb, kpool(l), vpool(l), nullptr, nullptr,
-                     10000.f, mst);
+          gemm_qkv(w.wqkv, Y, W, rows, d_pos, d_slot, Qb, kpool(l), vpool(l));
           decode_attention_v2(Qb, Ob, kpool(l), vpool(l), d_bt, maxb, d_pos, d_active, rows, maxb, scale, dws,
                               dec_counters, sms, mst);
           gemm(w.wo, Ob, W, QDIM, rows, gemm::EPI_ADD_F32, X, W);
@@ -873,6 +901,13 @@ int oxy_pi05_tensor_read(oxy_pi05 *p, int32_t i, void *host, int64_t nbytes, voi
   auto st = oxy::as_stream(stream);
   OXY_CUDA(cudaMemcpyAsync(host, t.ptr, nbytes, cudaMemcpyDeviceToHost, st));
   OXY_CUDA(cudaStreamSynchronize(st));
+  if (oxy::pi05::Model::is_rope_qkv(t.name)) {  // return the canonical row order
+    std::vector<uint16_t> dev(static_cast<uint16_t *>(host), static_cast<uint16_t *>(host) + t.numel());
+    uint16_t *out = static_cast<uint16_t *>(host);
+    for (int64_t f = 0; f < t.rows; ++f)
+      std::memcpy(out + (size_t)oxy::gemm::qkv_rope_row((int)f) * t.cols, dev.data() + (size_t)f * t.cols,
+                  t.cols * 2);
+  }
   OXY_API_END
 }
 
