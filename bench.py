@@ -285,7 +285,7 @@ def kernel_rooflines(backend, m_decode):
     ob = torch.empty_like(q)
     wsd = torch.empty(rows * (ctx // blk) * 8 * 258, device="cuda", dtype=torch.float32)
     args = (C.c_void_p(q.data_ptr()), C.c_void_p(ob.data_ptr()), C.c_void_p(kp.data_ptr()),
-            C.c_void_p(vp.data_ptr()), C.c_void_p(bt.data_ptr()), C.c_int32(ctx // blk),
+            C.c_void_p(vp.data_ptr()), C.c_int32(nb), C.c_void_p(bt.data_ptr()), C.c_int32(ctx // blk),
             C.c_void_p(pos.data_ptr()), C.c_int32(rows), C.c_int32(ctx // blk),
             C.c_void_p(wsd.data_ptr()), C.c_void_p(st.cuda_stream))
     sec = time_launches(lambda: _lib.call("oxy_paged_decode_attention", *args))

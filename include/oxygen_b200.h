@@ -130,11 +130,11 @@ int oxy_gemm_plan(int32_t n_out, int32_t k, int32_t t, int32_t splits, int32_t *
  * heads (q_d bf16 [rows, 2048]) over 1 KV head of dim 256 read through the
  * block table from one layer's pool (bf16 [num_blocks, 64, 256] K and V),
  * keys [0, pos[r]]; out_d bf16 [rows, 2048].  ws_d: rows*max_blocks*8*258
- * floats.  Device pointers; scale 1/16. */
+ * floats.  Device pointers; scale 1/16.  Pools hold num_blocks blocks. */
 int oxy_paged_decode_attention(const void *q_d, void *out_d, const void *kpool_d,
-                               const void *vpool_d, const int32_t *bt_d, int32_t bt_stride,
-                               const int32_t *pos_d, int32_t rows, int32_t max_blocks,
-                               float *ws_d, void *stream);
+                               const void *vpool_d, int32_t num_blocks, const int32_t *bt_d,
+                               int32_t bt_stride, const int32_t *pos_d, int32_t rows,
+                               int32_t max_blocks, float *ws_d, void *stream);
 
 /* kernels launched by this library so far (process-wide counter) */
 int64_t oxy_launch_count(void);

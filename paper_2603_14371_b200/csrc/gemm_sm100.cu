@@ -250,8 +250,6 @@ __global__ void __launch_bounds__(192, 2)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  pdl_trigger();  // let the next kernel launch (and prefetch its weights) once we are resident
-
   if (warp == 0) {
     if (lane == 0) {
       // Weights never depend on the previous kernel: stream the first ring of
@@ -273,6 +271,9 @@ __global__ void __launch_bounds__(192, 2)
         tma_load_2d(&tmA, full0 + 8 * s, smem_u32(sA + s * A_STAGE_BYTES), kc, m0);
         tma_load_2d(&tmB, full0 + 8 * s, smem_u32(sB + s * b_bytes), kc, n0);
       }
+      // all operand loads are in flight: let the next kernel start its
+      // prologue and weight prefetch while this CTA drains
+      pdl_trigger();
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -382,7 +383,7 @@ static EncodeTiledFn encode_fn() {
 }
 
 // rows x k bf16 row-major, box (64 x box_rows), 128-byte swizzle
-static CUtensorMap make_map(const void *ptr, int rows, int k, int box_rows) {
+CUtensorMap make_map(const void *ptr, int rows, int k, int box_rows) {
   if ((k * 2) % 16 != 0) fail(OXY_EINVAL, "GEMM K=%d: row stride must be a multiple of 16 bytes", k);
   if (reinterpret_cast<uintptr_t>(ptr) % 16 != 0) fail(OXY_EINVAL, "GEMM operand not 16-byte aligned");
   CUtensorMap map;

@@ -78,6 +78,8 @@ Plan make_plan(int n_out, int k, int t, int sms, int force_splits = 0);
 // Host: launch.  ws must hold splits * T * N_out floats when splits > 1.
 void launch(const void *w, const void *x, int n_out, int k, int t, const EpiParams &epi,
             const Plan &plan, float *ws, int *counters, cudaStream_t st);
+// 2-D TMA map over a row-major bf16 [rows, k] matrix, box (64 cols x box_rows), 128-byte swizzle
+CUtensorMap make_map(const void *ptr, int rows, int k, int box_rows);
 // self-resetting split-K tile counters for launches made through the C ABI
 int *counters_for_abi();
 

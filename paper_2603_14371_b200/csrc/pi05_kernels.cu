@@ -784,7 +784,263 @@ __global__ void __launch_bounds__(128)
   }
 }
 
-// ---- v2: chunked, pipelined, self-merging -----------------------------------
+// ---- v3 (used): TMA-fed, chunked, pipelined ----------------------------------
+// CTA = (row, chunk of `cb` pool blocks), 4 warps, 1 CTA/SM.  One thread
+// streams each block's K and V (2 x 32 KB) with 8 TMA tensor copies (64-column
+// sub-tiles, 128-byte swizzle) into a 3-stage mbarrier ring, so the SM keeps up
+// to 192 KB of KV in flight with a handful of instructions.  Warp w owns keys
+// 16w..16w+15 of every block (S = QK^T and O = PV on mma.sync bf16, online
+// softmax in registers); the 4 warps merge once per chunk; chunks of a row are
+// merged by decode_merge3_kernel in chunk order (deterministic).
+constexpr int D3_STAGES = 3;
+constexpr int D3_SUB = KV_BLOCK * 128;              // one 64-row x 64-col bf16 sub-tile: 8 KB
+constexpr int D3_STAGE_BYTES = 8 * D3_SUB;          // K (4 sub-tiles) + V (4 sub-tiles)
+constexpr size_t D3_SMEM = 1024 + 4 * 16 * 128 + D3_STAGES * D3_STAGE_BYTES + 64;
+
+// 16-byte chunk c (0..31) of row `row` in a tile of 4 swizzled 64-col sub-tiles
+__device__ __forceinline__ uint32_t tile16(uint32_t base, int rows_per_sub, int row, int c) {
+  return base + (c >> 3) * (rows_per_sub * 128) + row * 128 + (((c & 7) ^ (row & 7)) << 4);
+}
+
+__device__ __forceinline__ void d3_mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void d3_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void d3_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tLAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE;\n\tbra LAB_WAIT;\n\tDONE:\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void d3_tma(const CUtensorMap *map, uint32_t bar, uint32_t dst, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::
+          "r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(128, 1)
+    decode_attn_v3_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
+                          const bf16 *q, const int *bt, int bt_stride, const int *pos, const int *active, int cb,
+                          int max_chunks, float scale_log2, float *ws, bf16 *out) {
+  pdl_trigger();
+  extern __shared__ unsigned char d3_raw[];
+  unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(d3_raw) + 1023) &
+                                                          ~static_cast<uintptr_t>(1023));
+  const uint32_t sQ = smem_addr(smem);                    // 4 sub-tiles x 16 rows x 128 B
+  const uint32_t sKV = sQ + 4 * 16 * 128;                 // stages
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + 4 * 16 * 128 + D3_STAGES * D3_STAGE_BYTES);
+  const uint32_t full0 = smem_addr(bars);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < D3_STAGES; ++s) d3_mbar_init(full0 + 8 * s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&kmap)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&vmap)) : "memory");
+  }
+  __syncthreads();
+  pdl_wait();
+  const int r = blockIdx.x, chunk = blockIdx.y;
+  if (active && !active[r]) return;
+  const int n_keys = pos[r] + 1;
+  const int nb = (n_keys + KV_BLOCK - 1) / KV_BLOCK;
+  const int n_chunks = (nb + cb - 1) / cb;
+  if (chunk >= n_chunks) return;
+  const int b0 = chunk * cb, nblk = min(nb, b0 + cb) - b0;
+  const int *btr = bt + (size_t)r * bt_stride + b0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  auto issue = [&](int i) {  // block i of the chunk -> stage i % 3 (thread 0 only)
+    const int s = i % D3_STAGES, row0 = btr[i] * KV_BLOCK;
+    const uint32_t bar = full0 + 8 * s, kb = sKV + s * D3_STAGE_BYTES, vb = kb + 4 * D3_SUB;
+    d3_expect_tx(bar, D3_STAGE_BYTES);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      d3_tma(&kmap, bar, kb + j * D3_SUB, 64 * j, row0);
+      d3_tma(&vmap, bar, vb + j * D3_SUB, 64 * j, row0);
+    }
+  };
+  if (threadIdx.x == 0)
+    for (int i = 0; i < min(nblk, D3_STAGES); ++i) issue(i);
+  // Q: the 8 heads as MMA rows 0..7 (rows 8..15 zero)
+  const bf16 *qr = q + (size_t)r * Q_HEADS * HEAD_DIM;
+  for (int i = threadIdx.x; i < 16 * 32; i += 128) {
+    const int row = i >> 5, c = i & 31;
+    const uint32_t dst = tile16(sQ, 16, row, c);
+    if (row < Q_HEADS) cp_async16(dst, qr + (size_t)row * HEAD_DIM + c * 8);
+    else asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(dst), "r"(0));
+  }
+  cp_commit();
+  cp_wait<0>();
+  __syncthreads();
+
+  float o[32][4];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float m_run = -INFINITY, l_run = 0.f;
+  const int krow = warp * 16 + (lane & 7) + ((lane >> 4) << 3);
+  const int vrow = warp * 16 + (lane & 15);
+  for (int i = 0; i < nblk; ++i) {
+    const int s = i % D3_STAGES;
+    d3_wait(full0 + 8 * s, (i / D3_STAGES) & 1);
+    const uint32_t kb = sKV + s * D3_STAGE_BYTES, vb = kb + 4 * D3_SUB;
+    float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+    for (int kk = 0; kk < HEAD_DIM / 16; ++kk) {
+      uint32_t a0, a1, a2, a3, k0, k1, k2, k3;
+      ldsm_x4(tile16(sQ, 16, lane & 15, kk * 2 + (lane >> 4)), a0, a1, a2, a3);
+      ldsm_x4(tile16(kb, 64, krow, kk * 2 + ((lane >> 3) & 1)), k0, k1, k2, k3);
+      mma16816(sc[0], a0, a1, a2, a3, k0, k1);
+      mma16816(sc[1], a0, a1, a2, a3, k2, k3);
+    }
+    const int kbase = (b0 + i) * KV_BLOCK + warp * 16 + (lane & 3) * 2;
+    float mx = m_run;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        float v = sc[nt][e] * scale_log2;
+        if (kbase + nt * 8 + e >= n_keys) v = -INFINITY;
+        sc[nt][e] = v;
+        mx = fmaxf(mx, v);
+      }
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    const float corr = (mx == -INFINITY) ? 1.f : exp2f(m_run - mx);
+    float ls = 0.f;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const float p = mx == -INFINITY ? 0.f : exp2f(sc[nt][e] - mx);
+        sc[nt][e] = p;
+        ls += p;
+      }
+    ls += __shfl_xor_sync(0xffffffffu, ls, 1);
+    ls += __shfl_xor_sync(0xffffffffu, ls, 2);
+    l_run = l_run * corr + ls;
+    m_run = mx;
+#pragma unroll
+    for (int nt = 0; nt < 32; ++nt) {
+      o[nt][0] *= corr;
+      o[nt][1] *= corr;
+    }
+    // P rows 8..15 (padding) are zero
+    const uint32_t pa0 = pack_bf16(sc[0][0], sc[0][1]), pa2 = pack_bf16(sc[1][0], sc[1][1]);
+#pragma unroll
+    for (int np = 0; np < 16; ++np) {
+      uint32_t v0, v1, v2, v3;
+      ldsm_x4_t(tile16(vb, 64, vrow, np * 2 + (lane >> 4)), v0, v1, v2, v3);
+      mma16816(o[2 * np], pa0, 0u, pa2, 0u, v0, v1);
+      mma16816(o[2 * np + 1], pa0, 0u, pa2, 0u, v2, v3);
+    }
+    __syncthreads();  // stage s fully consumed
+    if (threadIdx.x == 0 && i + D3_STAGES < nblk) issue(i + D3_STAGES);
+  }
+  // ---- merge the 4 warps (stage memory reused) -> chunk result
+  float *sO = reinterpret_cast<float *>(smem + 4 * 16 * 128);   // [4][8][256]
+  float *sM = sO + 4 * 8 * HEAD_DIM;                             // [4][8] m, [4][8] l
+  const int g = lane >> 2;
+#pragma unroll
+  for (int nt = 0; nt < 32; ++nt)
+    *reinterpret_cast<float2 *>(sO + (warp * 8 + g) * HEAD_DIM + nt * 8 + (lane & 3) * 2) =
+        make_float2(o[nt][0], o[nt][1]);
+  if ((lane & 3) == 0) {
+    sM[warp * 8 + g] = m_run;
+    sM[32 + warp * 8 + g] = l_run;
+  }
+  __syncthreads();
+  bf16 *orow = out + (size_t)r * Q_HEADS * HEAD_DIM;
+  float *part = ws + ((size_t)r * max_chunks + chunk) * DA_PART;
+  for (int i = threadIdx.x; i < Q_HEADS * HEAD_DIM; i += 128) {
+    const int h = i >> 8, d = i & 255;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) M = fmaxf(M, sM[w * 8 + h]);
+    float acc = 0.f, L = 0.f;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const float mw = sM[w * 8 + h];
+      if (mw == -INFINITY) continue;
+      const float e = exp2f(mw - M);
+      acc += sO[(w * 8 + h) * HEAD_DIM + d] * e;
+      L += sM[32 + w * 8 + h] * e;
+    }
+    if (n_chunks == 1) {
+      orow[i] = __float2bfloat16(acc / L);
+    } else {
+      part[h * (HEAD_DIM + 2) + d] = acc;
+      if (d == 0) {
+        part[h * (HEAD_DIM + 2) + HEAD_DIM] = M;
+        part[h * (HEAD_DIM + 2) + HEAD_DIM + 1] = L;
+      }
+    }
+  }
+}
+
+// chunk merge: CTA = (row, head), thread = output dim; chunk order fixed
+__global__ void decode_merge3_kernel(const float *ws, bf16 *out, const int *pos, const int *active, int cb,
+                                     int max_chunks) {
+  pdl_trigger();
+  pdl_wait();
+  const int r = blockIdx.x, h = blockIdx.y, d = threadIdx.x;
+  if (active && !active[r]) return;
+  const int nb = (pos[r] + KV_BLOCK) / KV_BLOCK;
+  const int n_chunks = (nb + cb - 1) / cb;
+  if (n_chunks == 1) return;  // written directly by the attention kernel
+  const float *base = ws + (size_t)r * max_chunks * DA_PART + h * (HEAD_DIM + 2);
+  float M = -INFINITY;
+  for (int c = 0; c < n_chunks; ++c) M = fmaxf(M, base[(size_t)c * DA_PART + HEAD_DIM]);
+  float L = 0.f, acc = 0.f;
+#pragma unroll 4
+  for (int c = 0; c < n_chunks; ++c) {
+    const float *p = base + (size_t)c * DA_PART;
+    const float w = exp2f(p[HEAD_DIM] - M);
+    L += p[HEAD_DIM + 1] * w;
+    acc += p[d] * w;
+  }
+  out[(size_t)r * Q_HEADS * HEAD_DIM + h * HEAD_DIM + d] = __float2bfloat16(acc / L);
+}
+
+int decode_chunk_blocks3(int rows, int max_blocks, int sms) {
+  // minimise the makespan ceil(ctas / sms) * cb (in block loads), prefer longer chunks on ties
+  int best = 1;
+  long best_span = -1;
+  for (int cb = 1; cb <= max_blocks; ++cb) {
+    const long ctas = (long)rows * ((max_blocks + cb - 1) / cb);
+    const long span = ((ctas + sms - 1) / sms) * cb;
+    if (best_span < 0 || span <= best_span) {
+      best_span = span;
+      best = cb;
+    }
+  }
+  return best;
+}
+
+void decode_attention_v3(const CUtensorMap &kmap, const CUtensorMap &vmap, const bf16 *q, bf16 *out, const int *bt,
+                         int bt_stride, const int *pos, const int *active, int rows, int max_blocks, float scale,
+                         float *ws, int sms, cudaStream_t st) {
+  if (rows <= 0) return;
+  static bool attr = false;
+  if (!attr) {
+    OXY_CUDA(cudaFuncSetAttribute(decode_attn_v3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)D3_SMEM));
+    attr = true;
+  }
+  const int cb = decode_chunk_blocks3(rows, max_blocks, sms);
+  const int max_chunks = (max_blocks + cb - 1) / cb;
+  launch_pdl(decode_attn_v3_kernel, dim3(rows, max_chunks), dim3(128), D3_SMEM, st, kmap, vmap, q, bt, bt_stride,
+             pos, active, cb, max_chunks, scale * 1.4426950408889634f, ws, out);
+  if (max_chunks > 1)
+    launch_pdl(decode_merge3_kernel, dim3(rows, Q_HEADS), dim3(HEAD_DIM), 0, st, ws, out, pos, active, cb,
+               max_chunks);
+}
+
+// ---- v2: chunked, pipelined, self-merging (superseded by v3) ----------------
 // CTA = (row, chunk of up to `cb` pool blocks).  Blocks stream through a
 // 2-stage cp.async ring of unpadded, XOR-swizzled 32 KB K and V tiles (16-byte
 // chunk c of key row r lives at c ^ (r & 7): conflict-free ldmatrix).  Warp w
@@ -1110,24 +1366,22 @@ void argmax_rows(const float *logits, int rows, int V, int *out, float *pv, int 
 }  // namespace oxy
 
 extern "C" int oxy_paged_decode_attention(const void *q_d, void *out_d, const void *kpool_d,
-                                          const void *vpool_d, const int32_t *bt_d, int32_t bt_stride,
-                                          const int32_t *pos_d, int32_t rows, int32_t max_blocks,
-                                          float *ws_d, void *stream) {
+                                          const void *vpool_d, int32_t num_blocks, const int32_t *bt_d,
+                                          int32_t bt_stride, const int32_t *pos_d, int32_t rows,
+                                          int32_t max_blocks, float *ws_d, void *stream) {
   OXY_API_BEGIN
-  OXY_REQUIRE(rows >= 1 && max_blocks >= 1 && bt_stride >= max_blocks, "bad decode-attention shape");
+  OXY_REQUIRE(rows >= 1 && max_blocks >= 1 && bt_stride >= max_blocks && num_blocks >= 1,
+              "bad decode-attention shape");
   using oxy::pi05::bf16;
-  OXY_REQUIRE(rows <= 8192, "at most 8192 decode rows per call");
-  static int *counters = nullptr;
-  if (!counters) {
-    OXY_CUDA(cudaMalloc(&counters, 8192 * sizeof(int)));
-    OXY_CUDA(cudaMemset(counters, 0, 8192 * sizeof(int)));
-  }
   int dev = 0, sms = 148;
   OXY_CUDA(cudaGetDevice(&dev));
   OXY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  oxy::pi05::decode_attention_v2(static_cast<const bf16 *>(q_d), static_cast<bf16 *>(out_d),
-                                 static_cast<const bf16 *>(kpool_d), static_cast<const bf16 *>(vpool_d), bt_d,
-                                 bt_stride, pos_d, nullptr, rows, max_blocks, 1.f / 16.f, ws_d, counters, sms,
+  const CUtensorMap km = oxy::gemm::make_map(kpool_d, num_blocks * oxy::pi05::KV_BLOCK, oxy::pi05::HEAD_DIM,
+                                             oxy::pi05::KV_BLOCK);
+  const CUtensorMap vm = oxy::gemm::make_map(vpool_d, num_blocks * oxy::pi05::KV_BLOCK, oxy::pi05::HEAD_DIM,
+                                             oxy::pi05::KV_BLOCK);
+  oxy::pi05::decode_attention_v3(km, vm, static_cast<const bf16 *>(q_d), static_cast<bf16 *>(out_d), bt_d,
+                                 bt_stride, pos_d, nullptr, rows, max_blocks, 1.f / 16.f, ws_d, sms,
                                  oxy::as_stream(stream));
   OXY_API_END
 }

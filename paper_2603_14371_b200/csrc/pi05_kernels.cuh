@@ -1,6 +1,7 @@
 // F2 (pi0.5-shaped) kernels other than the GEMM.  See pi05_kernels.cu.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -81,7 +82,14 @@ void decode_attention(const bf16 *q, bf16 *out, const bf16 *kpool, const bf16 *v
                       const int *bt, int bt_stride, const int *pos, const int *active, int rows,
                       int max_blocks, float scale, float *ws, cudaStream_t st);
 
-// v2 (used): chunked + pipelined, last-arriving chunk merges (counters: one per row,
+// v3 (used): TMA-fed 3-stage ring over chunks of pool blocks + ordered chunk merge.
+// kmap/vmap: 2-D tensor maps over one layer's K / V pool viewed as [num_blocks*64, 256]
+// (box 64 x 64, 128-byte swizzle; gemm::make_map).  ws: rows*max_blocks*8*(256+2) floats.
+void decode_attention_v3(const CUtensorMap &kmap, const CUtensorMap &vmap, const bf16 *q, bf16 *out, const int *bt,
+                         int bt_stride, const int *pos, const int *active, int rows, int max_blocks, float scale,
+                         float *ws, int sms, cudaStream_t st);
+int decode_chunk_blocks3(int rows, int max_blocks, int sms);
+// v2 (superseded): chunked + pipelined, last-arriving chunk merges (counters: one per row,
 // zero-initialised, self-resetting).  ws: rows*max_blocks*8*(256+2) floats.
 void decode_attention_v2(const bf16 *q, bf16 *out, const bf16 *kpool, const bf16 *vpool, const int *bt,
                          int bt_stride, const int *pos, const int *active, int rows, int max_blocks, float scale,

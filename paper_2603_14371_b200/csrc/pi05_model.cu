@@ -73,6 +73,7 @@ struct Model {
   int n_mod = 0;
   // pool
   bf16 *pool = nullptr;
+  std::vector<CUtensorMap> kv_maps;  // per layer: K, V
   int NB = 0;
   size_t kv_stride = 0, layer_stride = 0;
   // denoise constants
@@ -266,6 +267,10 @@ struct Model {
     kv_stride = (size_t)NB * KV_BLOCK * HEAD_DIM;
     layer_stride = 2 * kv_stride;
     OXY_CUDA(cudaMalloc(&pool, (size_t)c.depth * layer_stride * sizeof(bf16)));
+    for (int l = 0; l < c.depth; ++l) {  // TMA views of each layer's K and V pool: [NB*64, 256]
+      kv_maps.push_back(gemm::make_map(kpool(l), NB * KV_BLOCK, HEAD_DIM, KV_BLOCK));
+      kv_maps.push_back(gemm::make_map(vpool(l), NB * KV_BLOCK, HEAD_DIM, KV_BLOCK));
+    }
     OXY_CUDA(cudaMemsetAsync(pool, 0, (size_t)c.depth * layer_stride * sizeof(bf16), st));
     // noise [H, apad] (pad lanes zero) from H*A standard normals
     OXY_CUDA(cudaMalloc(&noise, (size_t)c.H * apad() * sizeof(float)));
@@ -802,8 +807,8 @@ struct Model {
           const LayerW &w = L[l];
           rmsnorm(X, W, Y, W, w.ln1, nullptr, nullptr, rows, W, 1e-6f, mst);
           gemm_qkv(w.wqkv, Y, W, rows, d_pos, d_slot, Qb, kpool(l), vpool(l));
-          decode_attention_v2(Qb, Ob, kpool(l), vpool(l), d_bt, maxb, d_pos, d_active, rows, maxb, scale, dws,
-                              dec_counters, sms, mst);
+          decode_attention_v3(kv_maps[2 * l], kv_maps[2 * l + 1], Qb, Ob, d_bt, maxb, d_pos, d_active, rows, maxb,
+                              scale, dws, sms, mst);
           gemm(w.wo, Ob, W, QDIM, rows, gemm::EPI_ADD_F32, X, W);
           rmsnorm(X, W, Y, W, w.ln2, nullptr, nullptr, rows, W, 1e-6f, mst);
           gemm(w.wgu, Y, 2 * c.mlp, W, rows, gemm::EPI_GEGLU_BF16, Hm, c.mlp);

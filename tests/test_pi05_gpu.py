@@ -151,7 +151,7 @@ def test_paged_decode_attention_matches_torch(rows, ctxs):
     ws = torch.empty(rows * maxb * 8 * 258, dtype=torch.float32, device="cuda")
     for _ in range(2):  # second call reuses the self-resetting merge counters
         _lib.call("oxy_paged_decode_attention", C.c_void_p(q.data_ptr()), C.c_void_p(out.data_ptr()),
-                  C.c_void_p(kp.data_ptr()), C.c_void_p(vp.data_ptr()), C.c_void_p(bt.data_ptr()),
+                  C.c_void_p(kp.data_ptr()), C.c_void_p(vp.data_ptr()), C.c_int32(nb), C.c_void_p(bt.data_ptr()),
                   C.c_int32(maxb), C.c_void_p(pos.data_ptr()), C.c_int32(rows), C.c_int32(maxb),
                   C.c_void_p(ws.data_ptr()), _lib.stream_ptr())
         torch.cuda.synchronize()

@@ -42,7 +42,7 @@ def decode_attention(rows, ctx, reps=5):
     ws = torch.empty(rows * (ctx // blk) * 8 * 258, device="cuda", dtype=torch.float32)
     for _ in range(reps):
         _lib.call("oxy_paged_decode_attention", C.c_void_p(q.data_ptr()), C.c_void_p(ob.data_ptr()),
-                  C.c_void_p(kp.data_ptr()), C.c_void_p(vp.data_ptr()), C.c_void_p(bt.data_ptr()),
+                  C.c_void_p(kp.data_ptr()), C.c_void_p(vp.data_ptr()), C.c_int32(nb), C.c_void_p(bt.data_ptr()),
                   C.c_int32(ctx // blk), C.c_void_p(pos.data_ptr()), C.c_int32(rows),
                   C.c_int32(ctx // blk), C.c_void_p(ws.data_ptr()), C.c_void_p(st.cuda_stream))
     torch.cuda.synchronize()
