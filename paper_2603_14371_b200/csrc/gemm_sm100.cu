@@ -170,13 +170,19 @@ struct KParams {
   float *ws;
   int *counters;  // one per (m, n) tile; self-resetting
   int fixup;      // 1: last-arriving split CTA reduces; 0: separate reduce kernel
+  int prefetch;   // 1: issue the first ring of weight tiles before griddepcontrol.wait
+  int trigger;    // 1: launch_dependents once all operand loads are issued
 };
 
 // Launch-time knobs (env, read once): OXY_SPLITK=fixup|kernel, OXY_PDL=0|1,
 // OXY_GEMM_SMEM_KB=<per-CTA smem budget>.  Used for A/B measurements.
 struct Knobs {
   int fixup = 0, pdl = 1, smem_kb = 100;  // 2 CTAs per SM (measured best)
+  // early PDL (weight prefetch + trigger) for skinny / wide GEMMs: -1 = default policy
+  int early_skinny = 1, early_wide = 0;
   Knobs() {
+    if (const char *s = getenv("OXY_PDL_EARLY_SKINNY")) early_skinny = atoi(s);
+    if (const char *s = getenv("OXY_PDL_EARLY_WIDE")) early_wide = atoi(s);
     if (const char *s = getenv("OXY_SPLITK")) fixup = std::string(s) == "fixup";
     if (const char *s = getenv("OXY_PDL")) pdl = atoi(s);
     if (const char *s = getenv("OXY_GEMM_SMEM_KB")) smem_kb = std::max(64, std::min(200, atoi(s)));
@@ -254,7 +260,7 @@ __global__ void __launch_bounds__(192, 2)
     if (lane == 0) {
       // Weights never depend on the previous kernel: stream the first ring of
       // weight tiles before waiting on it, activations after.
-      const int pre = min(nkb, stages);
+      const int pre = p.prefetch ? min(nkb, stages) : 0;
       for (int i = 0; i < pre; ++i) {
         mbar_expect_tx(full0 + 8 * i, A_STAGE_BYTES + b_bytes);
         tma_load_2d(&tmA, full0 + 8 * i, smem_u32(sA + i * A_STAGE_BYTES), (kb0 + i) * BK, m0);
@@ -273,7 +279,7 @@ __global__ void __launch_bounds__(192, 2)
       }
       // all operand loads are in flight: let the next kernel start its
       // prologue and weight prefetch while this CTA drains
-      pdl_trigger();
+      if (p.trigger) pdl_trigger();
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -453,6 +459,7 @@ void launch(const void *w, const void *x, int n_out, int k, int t, const EpiPara
   kp.ws = ws;
   kp.counters = counters;
   kp.fixup = knobs().fixup;
+  kp.prefetch = kp.trigger = t <= 64 ? knobs().early_skinny : knobs().early_wide;
   dim3 grid(plan.n_tiles, plan.m_tiles, plan.splits);
   if (knobs().pdl) {
     launch_pdl(gemm_kernel, grid, dim3(192), smem_bytes(plan), st, ma, mb, kp);
