@@ -105,11 +105,13 @@ __device__ __forceinline__ float gelu_tanh(float x) {
   return 0.5f * x * (1.f + tanhf(c * (x + 0.044715f * x * x * x)));
 }
 
-// Shared epilogue.  `pair` is the accumulator of feature f^1 (GeGLU).
+// Shared epilogue.  `pair` is the accumulator of feature f^1 (GeGLU, RoPE).
+// MODE >= 0 fixes the mode at compile time; MODE < 0 dispatches on e.mode.
+template <int MODE = -1>
 __device__ __forceinline__ void epilogue_store(const EpiParams &e, int t, int f, int n_out, float acc,
                                                float pair) {
   if (e.bias) acc += e.bias[f];
-  switch (e.mode) {
+  switch (MODE >= 0 ? MODE : e.mode) {
     case EPI_F32:
       static_cast<float *>(e.out)[(size_t)t * e.ldo + f] = acc;
       break;
@@ -173,6 +175,27 @@ struct KParams {
   int prefetch;   // 1: issue the first ring of weight tiles before griddepcontrol.wait
   int trigger;    // 1: launch_dependents once all operand loads are issued
 };
+
+// Epilogue over this thread's output feature f and the tile's BN token columns
+// (TMEM lane = f).  MODE < 0 writes split-K partials.
+template <int MODE>
+__device__ __forceinline__ void epi_loop(const KParams &p, uint32_t trow, int bn, int n0, int f, int split) {
+  const bool fok = f < p.n_out;
+  for (int c = 0; c < bn; c += 16) {
+    uint32_t v[16];
+    tmem_ld16(trow + (uint32_t)c, v);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int t = n0 + c + j;
+      const float acc = __uint_as_float(v[j]);
+      float pair = 0.f;
+      if (MODE == EPI_GEGLU_BF16 || MODE == EPI_QKV_ROPE) pair = __shfl_xor_sync(0xffffffffu, acc, 1);
+      if (t >= p.t || !fok) continue;
+      if (MODE < 0) p.ws[((size_t)split * p.t + t) * p.n_out + f] = acc;
+      else epilogue_store<(MODE < 0 ? 0 : MODE)>(p.epi, t, f, p.n_out, acc, pair);
+    }
+  }
+}
 
 // Launch-time knobs (env, read once): OXY_SPLITK=fixup|kernel, OXY_PDL=0|1,
 // OXY_GEMM_SMEM_KB=<per-CTA smem budget>.  Used for A/B measurements.
@@ -307,20 +330,19 @@ __global__ void __launch_bounds__(192, 2)
     const int q = warp & 3;
     const int f = m0 + q * 32 + lane;
     const bool split_out = p.splits > 1;
-    for (int c = 0; c < bn; c += 16) {
-      uint32_t v[16];
-      tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c, v);
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int t = n0 + c + j;
-        const float acc = __uint_as_float(v[j]);
-        const float pair = __shfl_xor_sync(0xffffffffu, acc, 1);
-        if (t >= p.t || f >= p.n_out) continue;
-        if (split_out)
-          p.ws[((size_t)split * p.t + t) * p.n_out + f] = acc;
-        else
-          epilogue_store(p.epi, t, f, p.n_out, acc, pair);
-      }
+    const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
+    // the mode switch sits outside the column loop: one tight loop per epilogue
+    switch (split_out ? -1 : p.epi.mode) {
+      case -1: epi_loop<-1>(p, trow, bn, n0, f, split); break;
+      case EPI_F32: epi_loop<EPI_F32>(p, trow, bn, n0, f, split); break;
+      case EPI_BF16: epi_loop<EPI_BF16>(p, trow, bn, n0, f, split); break;
+      case EPI_ADD_F32: epi_loop<EPI_ADD_F32>(p, trow, bn, n0, f, split); break;
+      case EPI_GEGLU_BF16: epi_loop<EPI_GEGLU_BF16>(p, trow, bn, n0, f, split); break;
+      case EPI_GELU_BF16: epi_loop<EPI_GELU_BF16>(p, trow, bn, n0, f, split); break;
+      case EPI_ADD_BF16: epi_loop<EPI_ADD_BF16>(p, trow, bn, n0, f, split); break;
+      case EPI_ADD_GATED_F32: epi_loop<EPI_ADD_GATED_F32>(p, trow, bn, n0, f, split); break;
+      case EPI_SWISH_BF16: epi_loop<EPI_SWISH_BF16>(p, trow, bn, n0, f, split); break;
+      case EPI_QKV_ROPE: epi_loop<EPI_QKV_ROPE>(p, trow, bn, n0, f, split); break;
     }
     if (split_out && p.fixup) {
       // Deterministic split-K fix-up: the last CTA of this tile to arrive sums
