@@ -30,7 +30,16 @@ enum Epi : int {
   EPI_SWISH_BF16 = 7,     // out_bf16[t, f] = swish(acc + bias)
   EPI_QKV_ROPE = 8,       // fused QKV projection: RoPE on q/k (rotary pairs interleaved in the
                           // weight rows), q -> bf16 [T, 2048], k/v -> pool slot rows or dense rows
+  EPI_PARTIALS = 9,       // split-K partials only; the caller launches its own fused reduction
 };
+
+// Fused split-K reduction + residual + RMSNorm (one CTA per token row):
+//   x[t, :] += (gate ? gate : 1) * sum_s ws[s, t, :]          (fixed split order)
+//   y[t, :] = bf16( x * rsqrt(mean(x^2) + eps) * (1 + w) )       (w != null)
+//           = bf16( x * rsqrt(...) * (1 + mod_scale) + mod_shift ) (adaRMS)
+void splitk_residual_norm(const float *ws, int splits, int t, int n, const float *gate, float *x, int ldx,
+                          __nv_bfloat16 *y, int ldy, const float *w, const float *mod_scale,
+                          const float *mod_shift, float eps, cudaStream_t st);
 
 // Extra state of EPI_QKV_ROPE (8 q heads + 1 k + 1 v head of 256).
 struct QkvRope {

@@ -406,6 +406,23 @@ struct Model {
     EpiParams e{mode, out, ldo, bias, nullptr, 0, gate, {}};
     gemm::launch(w, xin, n_out, k, t, e, plan, wsp, gemm_counters, mst);
   }
+  // residual projection (x += [gate *] W h) followed by the next RMSNorm/adaRMS (-> y).
+  // Split-K: partials + one fused reduce/residual/norm kernel; else GEMM epilogue + norm.
+  void gemm_res_norm(const bf16 *w, const bf16 *xin, int n_out, int k, int t, const float *gate, float *X, bf16 *Y,
+                     const float *norm_w, const float *mod_scale, const float *mod_shift) {
+    if (t <= 0) return;
+    gemm::Plan plan = gemm::make_plan(n_out, k, t, sms);
+    if (plan.splits > 1 && n_out <= 2048) {
+      float *wsp = ws.as<float>((size_t)plan.splits * t * n_out);
+      EpiParams e{gemm::EPI_PARTIALS, nullptr, 0, nullptr, nullptr, 0, nullptr, {}};
+      gemm::launch(w, xin, n_out, k, t, e, plan, wsp, gemm_counters, mst);
+      gemm::splitk_residual_norm(wsp, plan.splits, t, n_out, gate, X, n_out, Y, n_out, norm_w, mod_scale,
+                                 mod_shift, 1e-6f, mst);
+      return;
+    }
+    gemm(w, xin, n_out, k, t, gate ? gemm::EPI_ADD_GATED_F32 : gemm::EPI_ADD_F32, X, n_out, nullptr, gate);
+    rmsnorm(X, n_out, Y, n_out, norm_w, mod_scale, mod_shift, t, n_out, 1e-6f, mst);
+  }
   // fused QKV projection + RoPE + K/V append (slot == null: dense k/v rows)
   void gemm_qkv(const bf16 *w, const bf16 *xin, int k, int t, const int *pos, const int *slot, bf16 *q_out,
                 bf16 *k_dst, bf16 *v_dst) {
@@ -729,19 +746,18 @@ struct Model {
       for (int s = 0; s < S; ++s) {
         const float *ms = modp + (size_t)s * n_mod;
         gemm(e_in, ab, We, AP, T, gemm::EPI_F32, X, We, e_in_b);
+        rmsnorm(X, We, Y, We, nullptr, ms, ms + We, T, We, 1e-6f, mst);
+        const float *mf = ms + (size_t)c.depth * 6 * We;
         for (int l = 0; l < c.depth; ++l) {
           const ExpertW &w = E[l];
           const float *m = ms + (size_t)l * 6 * We;
-          rmsnorm(X, We, Y, We, nullptr, m, m + We, T, We, 1e-6f, mst);
+          const float *mn = l + 1 < c.depth ? m + 6 * We : mf;  // the norm that follows this layer
           gemm_qkv(w.wqkv, Y, We, T, d_pos, nullptr, Qb, Kd, Vd);
           attend(ap, kpool(l), vpool(l));
-          gemm(w.wo, Ob, We, QDIM, T, gemm::EPI_ADD_GATED_F32, X, We, nullptr, m + 2 * We);
-          rmsnorm(X, We, Y, We, nullptr, m + 3 * We, m + 4 * We, T, We, 1e-6f, mst);
+          gemm_res_norm(w.wo, Ob, We, QDIM, T, m + 2 * We, X, Y, nullptr, m + 3 * We, m + 4 * We);
           gemm(w.wgu, Y, 2 * c.expert_mlp, We, T, gemm::EPI_GEGLU_BF16, Hm, c.expert_mlp);
-          gemm(w.wd, Hm, We, c.expert_mlp, T, gemm::EPI_ADD_GATED_F32, X, We, nullptr, m + 5 * We);
+          gemm_res_norm(w.wd, Hm, We, c.expert_mlp, T, m + 5 * We, X, Y, nullptr, mn, mn + We);
         }
-        const float *mf = ms + (size_t)c.depth * 6 * We;
-        rmsnorm(X, We, Y, We, nullptr, mf, mf + We, T, We, 1e-6f, mst);
         gemm(e_out, Y, A, We, T, gemm::EPI_F32, vel_d, AP, e_out_b);
         euler_step(a, vel_d, ab, (int64_t)T * AP, dt, mst);
       }
@@ -803,18 +819,17 @@ struct Model {
       for (int s = 0; s < k; ++s) {
         embed_rows(X, W, embed, d_tok, nullptr, rows, W, std::sqrt((float)W), mst);
         next_slots(d_slot, d_pos, d_active, d_bt, maxb, rows, mst);
+        rmsnorm(X, W, Y, W, L[0].ln1, nullptr, nullptr, rows, W, 1e-6f, mst);
         for (int l = 0; l < c.depth; ++l) {
           const LayerW &w = L[l];
-          rmsnorm(X, W, Y, W, w.ln1, nullptr, nullptr, rows, W, 1e-6f, mst);
+          const float *next_norm = l + 1 < c.depth ? L[l + 1].ln1 : final_norm;
           gemm_qkv(w.wqkv, Y, W, rows, d_pos, d_slot, Qb, kpool(l), vpool(l));
           decode_attention_v3(kv_maps[2 * l], kv_maps[2 * l + 1], Qb, Ob, d_bt, maxb, d_pos, d_active, rows, maxb,
                               scale, dws, sms, mst);
-          gemm(w.wo, Ob, W, QDIM, rows, gemm::EPI_ADD_F32, X, W);
-          rmsnorm(X, W, Y, W, w.ln2, nullptr, nullptr, rows, W, 1e-6f, mst);
+          gemm_res_norm(w.wo, Ob, W, QDIM, rows, nullptr, X, Y, w.ln2, nullptr, nullptr);
           gemm(w.wgu, Y, 2 * c.mlp, W, rows, gemm::EPI_GEGLU_BF16, Hm, c.mlp);
-          gemm(w.wd, Hm, W, c.mlp, rows, gemm::EPI_ADD_F32, X, W);
+          gemm_res_norm(w.wd, Hm, W, c.mlp, rows, nullptr, X, Y, next_norm, nullptr, nullptr);
         }
-        rmsnorm(X, W, Y, W, final_norm, nullptr, nullptr, rows, W, 1e-6f, mst);
         gemm(lm_head, Y, c.vocab, W, rows, gemm::EPI_F32, LG, c.vocab);
         if (logits_h)
           OXY_CUDA(cudaMemcpyAsync(logits_h + (size_t)s * rows * c.vocab, LG, (size_t)rows * c.vocab * sizeof(float),
