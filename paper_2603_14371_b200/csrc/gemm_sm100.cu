@@ -501,32 +501,31 @@ void launch(const void *w, const void *x, int n_out, int k, int t, const EpiPara
   }
 }
 
-// one CTA per token row; thread owns features tid, tid+256, ... (coalesced)
-__global__ void splitk_residual_norm_kernel(const float *ws, int splits, int t_rows, int n, const float *gate,
-                                            float *x, int ldx, __nv_bfloat16 *y, int ldy, const float *w,
-                                            const float *ms, const float *mb, float eps) {
+// one 1024-thread CTA per token row (memory-level parallelism for the skinny
+// decode/denoise rows); thread owns features tid, tid+1024 (coalesced)
+constexpr int RN_THREADS = 1024, RN_MAXV = 2;  // n <= 2048
+__global__ void __launch_bounds__(RN_THREADS)
+    splitk_residual_norm_kernel(const float *ws, int splits, int t_rows, int n, const float *gate, float *x,
+                                int ldx, __nv_bfloat16 *y, int ldy, const float *w, const float *ms,
+                                const float *mb, float eps) {
   pdl_trigger();
   pdl_wait();
   __shared__ float red[32];
-  constexpr int MAXV = 8;  // n <= 2048
   const int t = blockIdx.x;
-  float v[MAXV];
-#pragma unroll
-  for (int i = 0; i < MAXV; ++i) v[i] = 0.f;
-  // split order 0..S-1 per element; MAXV x 4 independent loads in flight
-#pragma unroll 4
-  for (int s = 0; s < splits; ++s) {
+  float v[RN_MAXV] = {0.f, 0.f};
+#pragma unroll 8
+  for (int s = 0; s < splits; ++s) {  // split order 0..S-1 per element
     const float *row = ws + ((size_t)s * t_rows + t) * n;
 #pragma unroll
-    for (int i = 0; i < MAXV; ++i) {
-      const int f = threadIdx.x + i * 256;
+    for (int i = 0; i < RN_MAXV; ++i) {
+      const int f = threadIdx.x + i * RN_THREADS;
       if (f < n) v[i] += row[f];
     }
   }
   float ss = 0.f;
 #pragma unroll
-  for (int i = 0; i < MAXV; ++i) {
-    const int f = threadIdx.x + i * 256;
+  for (int i = 0; i < RN_MAXV; ++i) {
+    const int f = threadIdx.x + i * RN_THREADS;
     if (f < n) {
       float xv = x[(size_t)t * ldx + f];
       xv += gate ? gate[f] * v[i] : v[i];
@@ -538,8 +537,8 @@ __global__ void splitk_residual_norm_kernel(const float *ws, int splits, int t_r
   ss = block_sum(ss, red);
   const float inv = rsqrtf(ss / (float)n + eps);
 #pragma unroll
-  for (int i = 0; i < MAXV; ++i) {
-    const int f = threadIdx.x + i * 256;
+  for (int i = 0; i < RN_MAXV; ++i) {
+    const int f = threadIdx.x + i * RN_THREADS;
     if (f < n) {
       const float o = w ? v[i] * inv * (1.f + w[f]) : v[i] * inv * (1.f + ms[f]) + mb[f];
       y[(size_t)t * ldy + f] = __float2bfloat16(o);
@@ -551,8 +550,8 @@ void splitk_residual_norm(const float *ws, int splits, int t, int n, const float
                           __nv_bfloat16 *y, int ldy, const float *w, const float *mod_scale,
                           const float *mod_shift, float eps, cudaStream_t st) {
   if (t <= 0) return;
-  if (n > 8 * 256) fail(OXY_EINVAL, "fused residual norm supports rows of at most 2048");
-  launch_pdl(splitk_residual_norm_kernel, dim3(t), dim3(256), 0, st, ws, splits, t, n, gate, x, ldx, y, ldy, w,
+  if (n > RN_THREADS * RN_MAXV) fail(OXY_EINVAL, "fused residual norm supports rows of at most 2048");
+  launch_pdl(splitk_residual_norm_kernel, dim3(t), dim3(RN_THREADS), 0, st, ws, splits, t, n, gate, x, ldx, y, ldy, w,
              mod_scale, mod_shift, eps);
 }
 
