@@ -556,36 +556,37 @@ __global__ void fa_merge_kernel(const AttnGroup *groups, int splits, const float
   pdl_trigger();
   pdl_wait();
   using C = FaCfg<HD>;
+  __shared__ float wsh[32];
+  __shared__ float s_inv;
   const AttnGroup g = groups[blockIdx.y];
   const int r = blockIdx.x;
   if (r >= g.nq) return;
   const size_t row0 = (size_t)g.wrow0 + r;
-  const float *ml = ws_ml + row0 * 2;
   const size_t mstride = (size_t)ws_rows * 2;
-  float M = -INFINITY;
-#pragma unroll 8
-  for (int s = 0; s < splits; ++s) M = fmaxf(M, ml[s * mstride]);
-  float L = 0.f;
-#pragma unroll 8
-  for (int s = 0; s < splits; ++s) {
-    const float m = ml[s * mstride];
-    L += m == -INFINITY ? 0.f : ml[s * mstride + 1] * exp2f(m - M);
+  if (threadIdx.x < 32) {  // warp 0: split weights once (splits <= 32), lane s owns split s
+    const int s = threadIdx.x;
+    const float m = s < splits ? ws_ml[row0 * 2 + s * mstride] : -INFINITY;
+    const float l = s < splits ? ws_ml[row0 * 2 + s * mstride + 1] : 0.f;
+    const float M = warp_max(m);
+    const float w = m == -INFINITY ? 0.f : exp2f(m - M);
+    const float L = warp_sum(l * w);
+    wsh[s] = w;
+    if (s == 0) s_inv = L > 0.f ? 1.f / L : 0.f;
   }
-  const float inv = L > 0.f ? 1.f / L : 0.f;
+  __syncthreads();
   const int c = threadIdx.x * 2;
   if (c >= HD) return;
   const float *o = ws_o + row0 * C::HDP + c;
   const size_t ostride = (size_t)ws_rows * C::HDP;
   float a0 = 0.f, a1 = 0.f;
 #pragma unroll 8
-  for (int s = 0; s < splits; ++s) {
-    const float m = ml[s * mstride];
-    const float w = m == -INFINITY ? 0.f : exp2f(m - M);
+  for (int s = 0; s < splits; ++s) {  // split order; independent loads
     const float2 v = *reinterpret_cast<const float2 *>(o + s * ostride);
-    a0 += v.x * w;
-    a1 += v.y * w;
+    a0 += v.x * wsh[s];
+    a1 += v.y * wsh[s];
   }
-  *reinterpret_cast<__nv_bfloat162 *>(g.o + (size_t)r * g.ldo + c) = __floats2bfloat162_rn(a0 * inv, a1 * inv);
+  *reinterpret_cast<__nv_bfloat162 *>(g.o + (size_t)r * g.ldo + c) =
+      __floats2bfloat162_rn(a0 * s_inv, a1 * s_inv);
 }
 
 template <int HD>
@@ -993,28 +994,37 @@ __global__ void decode_merge3_kernel(const float *ws, bf16 *out, const int *pos,
   const int n_chunks = (nb + cb - 1) / cb;
   if (n_chunks == 1) return;  // written directly by the attention kernel
   const float *base = ws + (size_t)r * max_chunks * DA_PART + h * (HEAD_DIM + 2);
-  float M = -INFINITY;
-  for (int c = 0; c < n_chunks; ++c) M = fmaxf(M, base[(size_t)c * DA_PART + HEAD_DIM]);
-  float L = 0.f, acc = 0.f;
-#pragma unroll 4
-  for (int c = 0; c < n_chunks; ++c) {
-    const float *p = base + (size_t)c * DA_PART;
-    const float w = exp2f(p[HEAD_DIM] - M);
-    L += p[HEAD_DIM + 1] * w;
-    acc += p[d] * w;
+  __shared__ float wsh[64];
+  __shared__ float s_inv;
+  if (threadIdx.x < 32) {  // warp 0: chunk weights once (chunks <= 64)
+    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+    const int c0 = threadIdx.x, c1 = threadIdx.x + 32;
+    if (c0 < n_chunks) { m0 = base[(size_t)c0 * DA_PART + HEAD_DIM]; l0 = base[(size_t)c0 * DA_PART + HEAD_DIM + 1]; }
+    if (c1 < n_chunks) { m1 = base[(size_t)c1 * DA_PART + HEAD_DIM]; l1 = base[(size_t)c1 * DA_PART + HEAD_DIM + 1]; }
+    const float M = warp_max(fmaxf(m0, m1));
+    const float w0 = c0 < n_chunks ? exp2f(m0 - M) : 0.f, w1 = c1 < n_chunks ? exp2f(m1 - M) : 0.f;
+    const float L = warp_sum(l0 * w0 + l1 * w1);
+    wsh[c0] = w0;
+    wsh[c1] = w1;
+    if (threadIdx.x == 0) s_inv = 1.f / L;
   }
-  out[(size_t)r * Q_HEADS * HEAD_DIM + h * HEAD_DIM + d] = __float2bfloat16(acc / L);
+  __syncthreads();
+  float acc = 0.f;
+#pragma unroll 8
+  for (int c = 0; c < n_chunks; ++c) acc += base[(size_t)c * DA_PART + d] * wsh[c];  // chunk order
+  out[(size_t)r * Q_HEADS * HEAD_DIM + h * HEAD_DIM + d] = __float2bfloat16(acc * s_inv);
 }
 
 int decode_chunk_blocks3(int rows, int max_blocks, int sms) {
-  // minimise the makespan ceil(ctas / sms) * cb (in block loads), prefer longer chunks on ties
-  int best = 1;
-  long best_span = -1;
-  for (int cb = 1; cb <= max_blocks; ++cb) {
-    const long ctas = (long)rows * ((max_blocks + cb - 1) / cb);
-    const long span = ((ctas + sms - 1) / sms) * cb;
-    if (best_span < 0 || span <= best_span) {
-      best_span = span;
+  // cost in block-load units: waves x (pipeline fill ~2 + cb) + 2 if a merge pass is needed
+  int best = std::max(1, (max_blocks + 63) / 64);  // the merge handles <= 64 chunks
+  long best_cost = -1;
+  for (int cb = best; cb <= max_blocks; ++cb) {
+    const int chunks = (max_blocks + cb - 1) / cb;
+    const long ctas = (long)rows * chunks;
+    const long cost = ((ctas + sms - 1) / sms) * (cb + 2) + (chunks > 1 ? 2 : 0);
+    if (best_cost < 0 || cost < best_cost) {
+      best_cost = cost;
       best = cb;
     }
   }
