@@ -14,6 +14,7 @@
 //     the same pool, LM head + lowest-id argmax, per-row stop on device.
 // Weight values are the builder's choice (random init, stated in DESIGN.md):
 // splitmix64 counter draws, U(+-sqrt(3/fan_in)) for matrices.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <map>
