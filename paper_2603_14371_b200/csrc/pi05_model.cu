@@ -454,9 +454,8 @@ struct Model {
     }
     p.q_tiles = (max_nq + 63) / 64;
     const int ctas = p.n * p.q_tiles;
-    // split-KV only while the partials stay small next to the KV itself (measured: the
-    // merge of 14 splits x 400 rows cost more than the attention)
-    if (ctas < sms && p.max_tiles > 1) p.splits = std::min({p.max_tiles, 4, std::max(1, (2 * sms) / ctas)});
+    // split-KV to fill the SMs (the merge kernel handles <= 32 splits)
+    if (ctas < sms && p.max_tiles > 1) p.splits = std::min({p.max_tiles, 32, std::max(1, (2 * sms) / ctas)});
     if (p.splits > 1) {
       const int hdp = head_dim == 256 ? 256 : 80;
       attn_ws_need = std::max(attn_ws_need, (size_t)p.splits * p.rows * hdp);
