@@ -365,6 +365,14 @@ def ours(a, ws, rank, local):
         "clocks": clocks,
     }
     if not a.no_extras:
+        # the same frames with the stages run back to back (no denoise/decode overlap)
+        backend.admit_overlapped = None
+        s_ms, s_traces, _, _ = timed(ws, backend, frames_dev, a.warmup, k)
+        del backend.admit_overlapped
+        line["stage_serial"] = {
+            "frame_ms": s_ms / a.steps, "value": H_REPORT * frames_all / (s_ms / 1e3),
+            "stage_ms": {k_: round(statistics.mean(getattr(t, k_) for t in s_traces) / 1e3, 3)
+                         for k_ in ("prefill_us", "denoise_us", "decode_us")}}
         frames_host = build_frames(cfg, r, n_frames, budget, device=False)
         backend.meter = None
         e_ms, e_traces, _, _ = timed(ws, backend, frames_host, a.warmup, k)

@@ -173,6 +173,17 @@ int oxy_pi05_prefill(oxy_pi05 *m, int32_t n_obs, const int32_t *n_img_h,
  * n streams reading each stream's prefix blocks; actions_d f32 [n, H, A]. */
 int oxy_pi05_denoise(oxy_pi05 *m, int32_t n, const int32_t *prefix_lens_h,
                      const int32_t *blocks_h, int32_t S, float *actions_d, void *stream);
+/* Same as oxy_pi05_denoise but enqueued on the model's action-expert lane
+ * without making `stream` wait for it, so a following oxy_pi05_decode on
+ * `stream` overlaps it (OxyGen's cross-task parallelism inside a frame,
+ * kvweaver/scheduler.py:117-171 runs the two stages back to back).
+ * actions_d is valid only after oxy_pi05_join(stream). */
+int oxy_pi05_denoise_async(oxy_pi05 *m, int32_t n, const int32_t *prefix_lens_h,
+                           const int32_t *blocks_h, int32_t S, float *actions_d, void *stream);
+/* make `stream` wait for the last oxy_pi05_denoise(_async) */
+int oxy_pi05_join(oxy_pi05 *m, void *stream);
+/* device time of the last denoise (waits for it to finish) */
+int oxy_pi05_denoise_elapsed_us(oxy_pi05 *m, double *us);
 /* continuous-batched greedy decode (batched_language_decode,
  * kvweaver/backend.py:334-420); same contract as oxy_toy_decode; logits_h
  * (optional) receives [k, rows, vocab] f32. */

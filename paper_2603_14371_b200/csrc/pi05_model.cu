@@ -307,11 +307,46 @@ struct Model {
 
   int *gemm_counters = nullptr;
   int *dec_counters = nullptr;  // per decode row, for the self-merging attention
-  void init_exec() {
+
+  // ---- execution lanes.  The members above (stream, events, arena, graph
+  // cache, split-K counters) and the per-call scratch describe the ACTIVE lane.
+  // Lane 0 runs prefill and language decode; lane 1 (`alt`) runs the action
+  // expert, so a frame's denoise can overlap its decode (they share no
+  // writable memory: denoise reads prefix slots [0, P), decode appends >= P).
+  // LaneSwap exchanges the two sets around an enqueue (host calls are serial).
+  struct LaneState {
+    cudaStream_t mst = nullptr;
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr, t0 = nullptr, t1 = nullptr;
+    uint8_t *arena_d = nullptr;
+    std::vector<uint8_t> arena_h;
+    size_t arena_cap = 0, arena_used = 0;
+    std::map<std::string, Graph> graphs;
+    int *gemm_counters = nullptr;
+    DevBuf y, q, o, hmid, ws, kd, vd, attn_ws, attn_ml;
+  } alt;
+  void swap_lane(LaneState &s) {
+    std::swap(mst, s.mst);
+    std::swap(ev_in, s.ev_in);
+    std::swap(ev_out, s.ev_out);
+    std::swap(arena_d, s.arena_d);
+    std::swap(arena_h, s.arena_h);
+    std::swap(arena_cap, s.arena_cap);
+    std::swap(arena_used, s.arena_used);
+    std::swap(graphs, s.graphs);
+    std::swap(gemm_counters, s.gemm_counters);
+    for (auto [a, b] : {std::pair<DevBuf *, DevBuf *>{&y, &s.y}, {&q, &s.q}, {&o, &s.o}, {&hmid, &s.hmid},
+                        {&ws, &s.ws}, {&kd, &s.kd}, {&vd, &s.vd}, {&attn_ws, &s.attn_ws}, {&attn_ml, &s.attn_ml}})
+      std::swap(*a, *b);
+  }
+  struct LaneSwap {
+    Model &m;
+    explicit LaneSwap(Model &mm) : m(mm) { m.swap_lane(m.alt); }
+    ~LaneSwap() { m.swap_lane(m.alt); }
+  };
+
+  void init_lane() {
     OXY_CUDA(cudaMalloc(&gemm_counters, gemm::MAX_TILES * sizeof(int)));
     OXY_CUDA(cudaMemset(gemm_counters, 0, gemm::MAX_TILES * sizeof(int)));
-    OXY_CUDA(cudaMalloc(&dec_counters, MAX_DECODE_ROWS * sizeof(int)));
-    OXY_CUDA(cudaMemset(dec_counters, 0, MAX_DECODE_ROWS * sizeof(int)));
     OXY_CUDA(cudaStreamCreateWithFlags(&mst, cudaStreamNonBlocking));
     OXY_CUDA(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
     OXY_CUDA(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
@@ -319,7 +354,7 @@ struct Model {
     OXY_CUDA(cudaMalloc(&arena_d, arena_cap));
     arena_h.resize(arena_cap);
   }
-  void destroy_exec() {
+  void destroy_lane() {
     for (auto &kv : graphs)
       if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
     if (mst) cudaStreamDestroy(mst);
@@ -327,7 +362,37 @@ struct Model {
     if (ev_out) cudaEventDestroy(ev_out);
     cudaFree(arena_d);
     cudaFree(gemm_counters);
+  }
+  void init_exec() {
+    OXY_CUDA(cudaMalloc(&dec_counters, MAX_DECODE_ROWS * sizeof(int)));
+    OXY_CUDA(cudaMemset(dec_counters, 0, MAX_DECODE_ROWS * sizeof(int)));
+    init_lane();
+    {
+      LaneSwap g(*this);
+      init_lane();
+    }
+    OXY_CUDA(cudaEventCreate(&alt.t0));
+    OXY_CUDA(cudaEventCreate(&alt.t1));
+  }
+  void destroy_exec() {
+    destroy_lane();
+    {
+      LaneSwap g(*this);
+      destroy_lane();
+    }
+    if (alt.t0) cudaEventDestroy(alt.t0);
+    if (alt.t1) cudaEventDestroy(alt.t1);
     cudaFree(dec_counters);
+    for (DevBuf *b : {&alt.y, &alt.q, &alt.o, &alt.hmid, &alt.ws, &alt.kd, &alt.vd, &alt.attn_ws, &alt.attn_ml})
+      b->release();
+  }
+  // the action-expert lane's last denoise: make `caller` wait for it
+  void join_alt(cudaStream_t caller) { OXY_CUDA(cudaStreamWaitEvent(caller, alt.ev_out, 0)); }
+  float alt_elapsed_ms() {
+    OXY_CUDA(cudaEventSynchronize(alt.t1));
+    float ms = 0.f;
+    OXY_CUDA(cudaEventElapsedTime(&ms, alt.t0, alt.t1));
+    return ms;
   }
   void enter(cudaStream_t caller) {
     OXY_CUDA(cudaEventRecord(ev_in, caller));
@@ -672,8 +737,12 @@ struct Model {
   }
 
   // n streams; stream i's prefix has P[i] positions in blocks (concatenated).
-  void denoise(cudaStream_t caller, int n, const int *P, const int *blocks_h, int S, float *actions_out_d) {
+  // Runs on the action-expert lane.  join = false leaves the caller stream
+  // free (decode may be enqueued behind it and overlap); join_alt() syncs.
+  void denoise(cudaStream_t caller, int n, const int *P, const int *blocks_h, int S, float *actions_out_d,
+               bool join = true) {
     OXY_REQUIRE(S >= 1, "denoise step count must be >= 1, got %d", S);
+    LaneSwap lane(*this);
     const int We = c.expert_width, H = c.H, A = c.action_dim, T = n * H, AP = apad();
     ensure_mod(S);
     std::string key = "denoise/" + std::to_string(S);
@@ -688,7 +757,6 @@ struct Model {
     act_bf.as<bf16>((size_t)T * AP);
     xe.as<float>((size_t)T * We);
     y.as<bf16>((size_t)T * std::max(We, QDIM));
-    qkv.as<float>((size_t)T * QKV);
     q.as<bf16>((size_t)T * QDIM);
     o.as<bf16>((size_t)T * QDIM);
     kd.as<bf16>((size_t)T * HEAD_DIM);
@@ -711,7 +779,7 @@ struct Model {
     AttnPlan ap = shape_attention(groups, HEAD_DIM);
     reserve_common();
     // ---- plan pass 2
-    float *a = act.as<float>(0), *X = xe.as<float>(0), *QKVf = qkv.as<float>(0), *vel_d = vel.as<float>(0);
+    float *a = act.as<float>(0), *X = xe.as<float>(0), *vel_d = vel.as<float>(0);
     bf16 *ab = act_bf.as<bf16>(0), *Y = y.as<bf16>(0), *Qb = q.as<bf16>(0), *Ob = o.as<bf16>(0),
          *Kd = kd.as<bf16>(0), *Vd = vd.as<bf16>(0), *Hm = hmid.as<bf16>(0);
     const float *modp = mod.as<float>(0);
@@ -737,6 +805,7 @@ struct Model {
     }
     ap.groups = arena_put(groups.data(), groups.size());
     enter(caller);
+    OXY_CUDA(cudaEventRecord(alt.t0, mst));
     arena_upload();
     auto body = [&]() {
       for (int i = 0; i < n; ++i)
@@ -767,7 +836,9 @@ struct Model {
     run_body(key, true, body);
     OXY_CUDA(cudaMemcpy2DAsync(actions_out_d, A * sizeof(float), a, AP * sizeof(float), A * sizeof(float), T,
                                cudaMemcpyDeviceToDevice, mst));
-    leave(caller);
+    OXY_CUDA(cudaEventRecord(alt.t1, mst));
+    if (join) leave(caller);
+    else OXY_CUDA(cudaEventRecord(ev_out, mst));
   }
 
   // ------------------------------------------------------------ decode
@@ -946,6 +1017,27 @@ int oxy_pi05_denoise(oxy_pi05 *p, int32_t n, const int32_t *prefix_lens_h, const
   OXY_API_BEGIN
   OXY_REQUIRE(n >= 1, "denoise needs at least one stream");
   p->m.denoise(oxy::as_stream(stream), n, prefix_lens_h, blocks_h, S, actions_d);
+  OXY_API_END
+}
+
+int oxy_pi05_denoise_async(oxy_pi05 *p, int32_t n, const int32_t *prefix_lens_h, const int32_t *blocks_h,
+                           int32_t S, float *actions_d, void *stream) {
+  OXY_API_BEGIN
+  OXY_REQUIRE(n >= 1, "denoise needs at least one stream");
+  p->m.denoise(oxy::as_stream(stream), n, prefix_lens_h, blocks_h, S, actions_d, false);
+  OXY_API_END
+}
+
+int oxy_pi05_join(oxy_pi05 *p, void *stream) {
+  OXY_API_BEGIN
+  p->m.join_alt(oxy::as_stream(stream));
+  OXY_API_END
+}
+
+int oxy_pi05_denoise_elapsed_us(oxy_pi05 *p, double *us) {
+  OXY_API_BEGIN
+  OXY_REQUIRE(us != nullptr, "null output pointer");
+  *us = 1e3 * (double)p->m.alt_elapsed_ms();
   OXY_API_END
 }
 

@@ -131,7 +131,7 @@ def _as_pi05(cfg) -> Pi05Config:
 
 class Pi05Backend(PricedBackend):
     def __init__(self, config=None, cost: CostModelParams | None = None, num_blocks: int = 2048,
-                 measure: bool = False):
+                 measure: bool = False, overlap: bool = True):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("Pi05Backend needs a CUDA device (no CPU fallback)")
@@ -144,6 +144,8 @@ class Pi05Backend(PricedBackend):
         self.block_size = KV_BLOCK
         self.allocator = BlockAllocator(num_blocks, KV_BLOCK)
         self.meter = StageMeter() if measure else None
+        if not overlap:   # stage-serial frames (the reference's order, scheduler.py:117-171)
+            self.admit_overlapped = None
         h = C.c_void_p()
         _lib.call("oxy_pi05_create", C.byref(c.to_c()), C.c_int32(num_blocks), _lib.stream_ptr(),
                   C.byref(h))
@@ -278,6 +280,42 @@ class Pi05Backend(PricedBackend):
         chunks = self.denoise_many(kvs, self.config.S)
         return [(chunk, GenerationState(kv, (), False, t, a.n_tokens))
                 for chunk, kv, a in zip(chunks, kvs, arrivals)]
+
+    def admit_overlapped(self, arrivals, t: int):
+        """Prefill now; denoise on the model's action-expert lane without
+        blocking the backend stream, so the frame's batched decode (enqueued
+        next) runs concurrently with it.  Returns ``(states, join)``:
+        ``join()`` orders the backend stream after the denoise and starts the
+        action copy-out; the callable it returns yields the ActionChunks.
+        """
+        kvs = self.prefill_many([a.observation for a in arrivals])
+        c = self.config
+        torch = self._torch
+        n = len(kvs)
+        out = torch.empty((n, c.H, c.action_dim), dtype=torch.float32, device="cuda")
+        lens = _lib.as_i32([kv.seq_len for kv in kvs])
+        blocks = _lib.as_i32([b for kv in kvs for b in kv.blocks])
+        _lib.call("oxy_pi05_denoise_async", self._h, C.c_int32(n), _lib.ptr_i32(lens),
+                  _lib.ptr_i32(blocks), C.c_int32(c.S), C.c_void_p(out.data_ptr()),
+                  _lib.stream_ptr())
+        states = [GenerationState(kv, (), False, t, a.n_tokens) for kv, a in zip(kvs, arrivals)]
+
+        def join():
+            _lib.call("oxy_pi05_join", self._h, _lib.stream_ptr())
+            host = torch.empty(out.shape, dtype=torch.float32, pin_memory=True)
+            host.copy_(out, non_blocking=True)
+            done = torch.cuda.Event()
+            done.record()
+
+            def chunks():
+                done.synchronize()
+                if self.meter is not None:
+                    us = C.c_double()
+                    _lib.call("oxy_pi05_denoise_elapsed_us", self._h, C.byref(us))
+                    self.meter.put("denoise", us.value)
+                return [ActionChunk(a) for a in host.numpy().astype(np.float64)]
+            return chunks
+        return states, join
 
     def batched_language_decode(self, batched: BatchedState, k: int,
                                 return_logits: bool = False):

@@ -15,6 +15,8 @@ import contextlib
 class StageMeter:
     def __init__(self):
         self._spans: dict[str, list] = {}
+        self._extra: dict[str, float] = {}
+        self._open: dict[str, object] = {}
 
     @contextlib.contextmanager
     def span(self, stage: str):
@@ -27,12 +29,30 @@ class StageMeter:
             e.record()
             self._spans.setdefault(stage, []).append((s, e))
 
+    def begin(self, stage: str) -> None:
+        import torch
+        s = torch.cuda.Event(enable_timing=True)
+        s.record()
+        self._open[stage] = s
+
+    def end(self, stage: str) -> None:
+        import torch
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        self._spans.setdefault(stage, []).append((self._open.pop(stage), e))
+
+    def put(self, stage: str, us: float) -> None:
+        """Add a duration timed elsewhere (e.g. on the action-expert lane)."""
+        self._extra[stage] = self._extra.get(stage, 0.0) + us
+
     def take(self, stage: str) -> int:
         spans = self._spans.pop(stage, [])
-        if not spans:
-            return 0
-        spans[-1][1].synchronize()
-        return int(round(sum(s.elapsed_time(e) for s, e in spans) * 1000.0))
+        extra = self._extra.pop(stage, 0.0)
+        if spans:
+            spans[-1][1].synchronize()
+        return int(round(sum(s.elapsed_time(e) for s, e in spans) * 1000.0 + extra))
 
     def clear(self) -> None:
         self._spans.clear()
+        self._extra.clear()
+        self._open.clear()

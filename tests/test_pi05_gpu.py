@@ -188,3 +188,25 @@ def test_full_shape_frame_runs():
     assert len(out.token_buffers[0]) == 5 and out.kv_batch[0].seq_len == 805
     k0 = out.kv_batch[0].layers[0].keys
     assert np.all(np.isfinite(k0)) and np.abs(k0).max() > 0
+
+
+@pytest.mark.parametrize("pattern", ["OnePerFrame", "Poisson"])
+def test_overlapped_frames_match_stage_serial(pattern):
+    """Denoise on the action-expert lane overlapping the batched decode gives
+    the same transcript (actions, tokens, completion frames) as running the
+    stages back to back, and the measured frame time is no more than the sum."""
+    from paper_2603_14371_b200.pi05 import TINY, Pi05Backend
+    from paper_2603_14371_b200.sim_engine import SimConfig, run_simulation, transcript_to_json
+    from paper_2603_14371_b200.workload import WorkloadSpec
+    cfg = SimConfig(backend_kind="Pi05", backend_config=BackendConfig(vocab=TINY.vocab),
+                    workload=WorkloadSpec(pattern=pattern, default_N=9, obs_len=24, num_frames=8,
+                                          seed=5, lam=1.5),
+                    k=3)
+    runs = {}
+    for overlap in (False, True):
+        be = Pi05Backend(TINY, num_blocks=256, measure=True, overlap=overlap)
+        runs[overlap] = run_simulation(cfg, backend=be)
+    assert transcript_to_json(runs[True]) == transcript_to_json(runs[False])
+    for tr in runs[True].traces:
+        if tr.arrival_count:
+            assert 0 < tr.total_us <= sum(tr.latency_components) + 2000, tr
