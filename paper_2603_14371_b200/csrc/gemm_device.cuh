@@ -1,0 +1,297 @@
+// Device-side building blocks of the tcgen05 GEMM shared by the stand-alone
+// kernels (gemm_sm100.cu) and the persistent layer kernel (megakernel.cu):
+// PTX wrappers (mbarrier, TMA, tcgen05, cluster), the fused epilogues, and the
+// deterministic split-K fix-up.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "cuda_util.cuh"
+#include "gemm_sm100.cuh"
+
+namespace oxy {
+namespace gemm {
+
+// ------------------------------------------------------------------ PTX
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred P1;\n\t"
+      "LAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE;\n\t"
+      "bra LAB_WAIT;\n\t"
+      "DONE:\n\t"
+      "}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap *map, uint32_t bar, uint32_t dst,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+
+// K-major, 128-byte swizzle: 8-row atoms of 1024 B (SBO), version 1 (sm100).
+__device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)1 << 16;            // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;  // SBO
+  d |= (uint64_t)1 << 46;            // descriptor version
+  d |= (uint64_t)2 << 61;            // SWIZZLE_128B
+  return d;
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+      "}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accum)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   bar)
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// ---- cluster / CTA-pair helpers (cta_group::2)
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same smem offset in CTA `rank` of this cluster
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_local(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+// pair TMA: the bytes land in this CTA's smem, completion is counted on the
+// leader CTA's barrier (bar_leader = shared::cluster address in CTA 0)
+__device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap *map, uint32_t bar_leader, uint32_t dst, int c0,
+                                                 int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_leader), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void mma_bf16_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                              uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t"
+      "}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accum)
+      : "memory");
+}
+// arrive on the barrier at this smem offset in both CTAs of the pair
+__device__ __forceinline__ void mma_commit_pair(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+__device__ __forceinline__ float gelu_tanh(float x) {
+  const float c = 0.7978845608028654f;  // sqrt(2/pi)
+  return 0.5f * x * (1.f + tanhf(c * (x + 0.044715f * x * x * x)));
+}
+
+// Shared epilogue.  `pair` is the accumulator of feature f^1 (GeGLU, RoPE).
+// MODE >= 0 fixes the mode at compile time; MODE < 0 dispatches on e.mode.
+template <int MODE = -1>
+__device__ __forceinline__ void epilogue_store(const EpiParams &e, int t, int f, int n_out, float acc,
+                                               float pair) {
+  if (e.bias) acc += e.bias[f];
+  switch (MODE >= 0 ? MODE : e.mode) {
+    case EPI_F32:
+      static_cast<float *>(e.out)[(size_t)t * e.ldo + f] = acc;
+      break;
+    case EPI_BF16:
+      static_cast<__nv_bfloat16 *>(e.out)[(size_t)t * e.ldo + f] = __float2bfloat16(acc);
+      break;
+    case EPI_ADD_F32:
+      static_cast<float *>(e.out)[(size_t)t * e.ldo + f] += acc;
+      break;
+    case EPI_GEGLU_BF16:
+      if ((f & 1) == 0) {
+        float up = pair + (e.bias ? e.bias[f + 1] : 0.f);
+        static_cast<__nv_bfloat16 *>(e.out)[(size_t)t * e.ldo + (f >> 1)] =
+            __float2bfloat16(gelu_tanh(acc) * up);
+      }
+      break;
+    case EPI_GELU_BF16:
+      static_cast<__nv_bfloat16 *>(e.out)[(size_t)t * e.ldo + f] = __float2bfloat16(gelu_tanh(acc));
+      break;
+    case EPI_ADD_BF16:
+      static_cast<__nv_bfloat16 *>(e.out)[(size_t)t * e.ldo + f] =
+          __float2bfloat16(acc + e.res[(size_t)t * e.ldr + f]);
+      break;
+    case EPI_ADD_GATED_F32:
+      static_cast<float *>(e.out)[(size_t)t * e.ldo + f] += e.gate[f] * acc;
+      break;
+    case EPI_SWISH_BF16:
+      static_cast<__nv_bfloat16 *>(e.out)[(size_t)t * e.ldo + f] =
+          __float2bfloat16(acc / (1.f + __expf(-acc)));
+      break;
+    case EPI_QKV_ROPE: {
+      const QkvRope &r = e.rope;
+      const int h = f >> 8, j = f & 255, i = j >> 1;
+      if (h < 9) {  // q heads 0..7, k head 8: rotate the (x1, x2) pair
+        float sn, cs;
+        sincosf((float)r.pos[t] * r.inv_freq[i], &sn, &cs);
+        const bool second = j & 1;  // this lane holds x2 (dim i + 128)
+        const float v = second ? acc * cs + pair * sn : acc * cs - pair * sn;
+        const int dim = second ? i + 128 : i;
+        if (h < 8) {
+          r.q_out[(size_t)t * 2048 + h * 256 + dim] = __float2bfloat16(v);
+        } else {
+          const int s = r.slot ? r.slot[t] : t;
+          if (s >= 0) r.k_dst[(size_t)s * 256 + dim] = __float2bfloat16(v);
+        }
+      } else {  // v head
+        const int s = r.slot ? r.slot[t] : t;
+        if (s >= 0) r.v_dst[(size_t)s * 256 + j] = __float2bfloat16(acc);
+      }
+      break;
+    }
+  }
+}
+
+// Epilogue over this thread's output feature f and the tile's BN token columns
+// (TMEM lane = f).  MODE < 0 writes split-K partials.
+template <int MODE, typename P>
+__device__ __forceinline__ void epi_loop(const P &p, uint32_t trow, int bn, int n0, int f, int split) {
+  const bool fok = f < p.n_out;
+  for (int c = 0; c < bn; c += 16) {
+    uint32_t v[16];
+    tmem_ld16(trow + (uint32_t)c, v);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int t = n0 + c + j;
+      const float acc = __uint_as_float(v[j]);
+      float pair = 0.f;
+      if (MODE == EPI_GEGLU_BF16 || MODE == EPI_QKV_ROPE) pair = __shfl_xor_sync(0xffffffffu, acc, 1);
+      if (t >= p.t || !fok) continue;
+      if (MODE < 0) p.ws[((size_t)split * p.t + t) * p.n_out + f] = acc;
+      else epilogue_store<(MODE < 0 ? 0 : MODE)>(p.epi, t, f, p.n_out, acc, pair);
+    }
+  }
+}
+
+// the mode switch sits outside the column loop: one tight loop per epilogue
+template <typename P>
+__device__ __forceinline__ void epi_tile(const P &p, uint32_t trow, int bn, int n0, int f, int split, bool split_out) {
+  switch (split_out ? -1 : p.epi.mode) {
+    case -1: epi_loop<-1>(p, trow, bn, n0, f, split); break;
+    case EPI_F32: epi_loop<EPI_F32>(p, trow, bn, n0, f, split); break;
+    case EPI_BF16: epi_loop<EPI_BF16>(p, trow, bn, n0, f, split); break;
+    case EPI_ADD_F32: epi_loop<EPI_ADD_F32>(p, trow, bn, n0, f, split); break;
+    case EPI_GEGLU_BF16: epi_loop<EPI_GEGLU_BF16>(p, trow, bn, n0, f, split); break;
+    case EPI_GELU_BF16: epi_loop<EPI_GELU_BF16>(p, trow, bn, n0, f, split); break;
+    case EPI_ADD_BF16: epi_loop<EPI_ADD_BF16>(p, trow, bn, n0, f, split); break;
+    case EPI_ADD_GATED_F32: epi_loop<EPI_ADD_GATED_F32>(p, trow, bn, n0, f, split); break;
+    case EPI_SWISH_BF16: epi_loop<EPI_SWISH_BF16>(p, trow, bn, n0, f, split); break;
+    case EPI_QKV_ROPE: epi_loop<EPI_QKV_ROPE>(p, trow, bn, n0, f, split); break;
+  }
+}
+
+// Deterministic split-K fix-up, run by the 4 epilogue warps (named barrier 1)
+// after they wrote this CTA's partials: the last CTA of the tile to arrive sums
+// the partials in split order 0..S-1 and applies the epilogue.
+template <typename P>
+__device__ __forceinline__ void splitk_fixup(const P &p, int tile, int n0, int bn, int f, int &s_last) {
+  __threadfence();
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  if (threadIdx.x == 64) s_last = atomicAdd(p.counters + tile, 1) == p.splits - 1;
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  if (s_last) {
+    __threadfence();
+    const int ncols = min(bn, p.t - n0);
+    const bool fok = f < p.n_out;
+    for (int c0 = 0; c0 < ncols; c0 += 4) {
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int s0 = 0; s0 < p.splits; s0 += 8) {
+        float v[8][4];  // 32 independent L2 loads in flight per thread
+#pragma unroll
+        for (int s = 0; s < 8; ++s)
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            v[s][j] = (fok && s0 + s < p.splits && c0 + j < ncols)
+                          ? __ldcg(p.ws + ((size_t)(s0 + s) * p.t + n0 + c0 + j) * p.n_out + f)
+                          : 0.f;
+#pragma unroll
+        for (int s = 0; s < 8; ++s)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[j] += v[s][j];  // split order 0..S-1
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float pair = __shfl_xor_sync(0xffffffffu, acc[j], 1);
+        if (fok && c0 + j < ncols) epilogue_store(p.epi, n0 + c0 + j, f, p.n_out, acc[j], pair);
+      }
+    }
+    if (threadIdx.x == 64) p.counters[tile] = 0;
+  }
+  asm volatile("bar.sync 1, 128;" ::: "memory");  // s_last is reused by the next tile
+}
+
+}  // namespace gemm
+}  // namespace oxy

@@ -12,159 +12,10 @@
 
 #include "cuda_util.cuh"
 #include "gemm_sm100.cuh"
+#include "gemm_device.cuh"
 
 namespace oxy {
 namespace gemm {
-
-// ------------------------------------------------------------------ PTX
-
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t"
-      ".reg .pred P1;\n\t"
-      "LAB_WAIT:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@P1 bra DONE;\n\t"
-      "bra LAB_WAIT;\n\t"
-      "DONE:\n\t"
-      "}" ::"r"(bar),
-      "r"(parity)
-      : "memory");
-}
-
-__device__ __forceinline__ void tma_load_2d(const CUtensorMap *map, uint32_t bar, uint32_t dst,
-                                            int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
-      "%4}], [%2];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
-      : "memory");
-}
-
-__device__ __forceinline__ void tc_fence_after() {
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_before() {
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-
-// K-major, 128-byte swizzle: 8-row atoms of 1024 B (SBO), version 1 (sm100).
-__device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
-  d |= (uint64_t)1 << 16;            // LBO (unused for swizzled K-major)
-  d |= (uint64_t)(1024 >> 4) << 32;  // SBO
-  d |= (uint64_t)1 << 46;            // descriptor version
-  d |= (uint64_t)2 << 61;            // SWIZZLE_128B
-  return d;
-}
-
-__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
-                                         uint32_t accum) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
-      "}" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(idesc), "r"(accum)
-      : "memory");
-}
-
-__device__ __forceinline__ void mma_commit(uint32_t bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   bar)
-               : "memory");
-}
-
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
-      "%12, %13, %14, %15}, [%16];"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-        "=r"(v[14]), "=r"(v[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
-
-__device__ __forceinline__ float gelu_tanh(float x) {
-  const float c = 0.7978845608028654f;  // sqrt(2/pi)
-  return 0.5f * x * (1.f + tanhf(c * (x + 0.044715f * x * x * x)));
-}
-
-// Shared epilogue.  `pair` is the accumulator of feature f^1 (GeGLU, RoPE).
-// MODE >= 0 fixes the mode at compile time; MODE < 0 dispatches on e.mode.
-template <int MODE = -1>
-__device__ __forceinline__ void epilogue_store(const EpiParams &e, int t, int f, int n_out, float acc,
-                                               float pair) {
-  if (e.bias) acc += e.bias[f];
-  switch (MODE >= 0 ? MODE : e.mode) {
-    case EPI_F32:
-      static_cast<float *>(e.out)[(size_t)t * e.ldo + f] = acc;
-      break;
-    case EPI_BF16:
-      static_cast<__nv_bfloat16 *>(e.out)[(size_t)t * e.ldo + f] = __float2bfloat16(acc);
-      break;
-    case EPI_ADD_F32:
-      static_cast<float *>(e.out)[(size_t)t * e.ldo + f] += acc;
-      break;
-    case EPI_GEGLU_BF16:
-      if ((f & 1) == 0) {
-        float up = pair + (e.bias ? e.bias[f + 1] : 0.f);
-        static_cast<__nv_bfloat16 *>(e.out)[(size_t)t * e.ldo + (f >> 1)] =
-            __float2bfloat16(gelu_tanh(acc) * up);
-      }
-      break;
-    case EPI_GELU_BF16:
-      static_cast<__nv_bfloat16 *>(e.out)[(size_t)t * e.ldo + f] = __float2bfloat16(gelu_tanh(acc));
-      break;
-    case EPI_ADD_BF16:
-      static_cast<__nv_bfloat16 *>(e.out)[(size_t)t * e.ldo + f] =
-          __float2bfloat16(acc + e.res[(size_t)t * e.ldr + f]);
-      break;
-    case EPI_ADD_GATED_F32:
-      static_cast<float *>(e.out)[(size_t)t * e.ldo + f] += e.gate[f] * acc;
-      break;
-    case EPI_SWISH_BF16:
-      static_cast<__nv_bfloat16 *>(e.out)[(size_t)t * e.ldo + f] =
-          __float2bfloat16(acc / (1.f + __expf(-acc)));
-      break;
-    case EPI_QKV_ROPE: {
-      const QkvRope &r = e.rope;
-      const int h = f >> 8, j = f & 255, i = j >> 1;
-      if (h < 9) {  // q heads 0..7, k head 8: rotate the (x1, x2) pair
-        float sn, cs;
-        sincosf((float)r.pos[t] * r.inv_freq[i], &sn, &cs);
-        const bool second = j & 1;  // this lane holds x2 (dim i + 128)
-        const float v = second ? acc * cs + pair * sn : acc * cs - pair * sn;
-        const int dim = second ? i + 128 : i;
-        if (h < 8) {
-          r.q_out[(size_t)t * 2048 + h * 256 + dim] = __float2bfloat16(v);
-        } else {
-          const int s = r.slot ? r.slot[t] : t;
-          if (s >= 0) r.k_dst[(size_t)s * 256 + dim] = __float2bfloat16(v);
-        }
-      } else {  // v head
-        const int s = r.slot ? r.slot[t] : t;
-        if (s >= 0) r.v_dst[(size_t)s * 256 + j] = __float2bfloat16(acc);
-      }
-      break;
-    }
-  }
-}
 
 struct KParams {
   int n_out, k, t, bn, stages, kb_total, splits, kb_per_split;
@@ -176,34 +27,18 @@ struct KParams {
   int trigger;    // 1: launch_dependents once all operand loads are issued
 };
 
-// Epilogue over this thread's output feature f and the tile's BN token columns
-// (TMEM lane = f).  MODE < 0 writes split-K partials.
-template <int MODE>
-__device__ __forceinline__ void epi_loop(const KParams &p, uint32_t trow, int bn, int n0, int f, int split) {
-  const bool fok = f < p.n_out;
-  for (int c = 0; c < bn; c += 16) {
-    uint32_t v[16];
-    tmem_ld16(trow + (uint32_t)c, v);
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int t = n0 + c + j;
-      const float acc = __uint_as_float(v[j]);
-      float pair = 0.f;
-      if (MODE == EPI_GEGLU_BF16 || MODE == EPI_QKV_ROPE) pair = __shfl_xor_sync(0xffffffffu, acc, 1);
-      if (t >= p.t || !fok) continue;
-      if (MODE < 0) p.ws[((size_t)split * p.t + t) * p.n_out + f] = acc;
-      else epilogue_store<(MODE < 0 ? 0 : MODE)>(p.epi, t, f, p.n_out, acc, pair);
-    }
-  }
-}
-
 // Launch-time knobs (env, read once): OXY_SPLITK=fixup|kernel, OXY_PDL=0|1,
 // OXY_GEMM_SMEM_KB=<per-CTA smem budget>.  Used for A/B measurements.
 struct Knobs {
   int fixup = 0, pdl = 1, smem_kb = 100;  // 2 CTAs per SM (measured best)
   // early PDL (weight prefetch + trigger) for skinny / wide GEMMs: -1 = default policy
   int early_skinny = 1, early_wide = 0;
+  // persistent wide kernel for T > 64: -1 auto (cost model), 0 off, 1 / 2 force CTA group
+  int wide = 0, wide_bn = 0, wide_splits = 0;  // off: measured slower in-frame (profiles/r01_gemm_wide.md)
   Knobs() {
+    if (const char *s = getenv("OXY_GEMM_WIDE")) wide = atoi(s);
+    if (const char *s = getenv("OXY_GEMM_WIDE_BN")) wide_bn = atoi(s);
+    if (const char *s = getenv("OXY_GEMM_WIDE_SPLITS")) wide_splits = atoi(s);
     if (const char *s = getenv("OXY_PDL_EARLY_SKINNY")) early_skinny = atoi(s);
     if (const char *s = getenv("OXY_PDL_EARLY_WIDE")) early_wide = atoi(s);
     if (const char *s = getenv("OXY_SPLITK")) fixup = std::string(s) == "fixup";
@@ -331,56 +166,8 @@ __global__ void __launch_bounds__(192, 2)
     const int f = m0 + q * 32 + lane;
     const bool split_out = p.splits > 1;
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
-    // the mode switch sits outside the column loop: one tight loop per epilogue
-    switch (split_out ? -1 : p.epi.mode) {
-      case -1: epi_loop<-1>(p, trow, bn, n0, f, split); break;
-      case EPI_F32: epi_loop<EPI_F32>(p, trow, bn, n0, f, split); break;
-      case EPI_BF16: epi_loop<EPI_BF16>(p, trow, bn, n0, f, split); break;
-      case EPI_ADD_F32: epi_loop<EPI_ADD_F32>(p, trow, bn, n0, f, split); break;
-      case EPI_GEGLU_BF16: epi_loop<EPI_GEGLU_BF16>(p, trow, bn, n0, f, split); break;
-      case EPI_GELU_BF16: epi_loop<EPI_GELU_BF16>(p, trow, bn, n0, f, split); break;
-      case EPI_ADD_BF16: epi_loop<EPI_ADD_BF16>(p, trow, bn, n0, f, split); break;
-      case EPI_ADD_GATED_F32: epi_loop<EPI_ADD_GATED_F32>(p, trow, bn, n0, f, split); break;
-      case EPI_SWISH_BF16: epi_loop<EPI_SWISH_BF16>(p, trow, bn, n0, f, split); break;
-      case EPI_QKV_ROPE: epi_loop<EPI_QKV_ROPE>(p, trow, bn, n0, f, split); break;
-    }
-    if (split_out && p.fixup) {
-      // Deterministic split-K fix-up: the last CTA of this tile to arrive sums
-      // the partials in split order 0..S-1 and applies the epilogue.
-      __threadfence();
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      const int tile = blockIdx.y * gridDim.x + blockIdx.x;
-      if (threadIdx.x == 64) s_last = atomicAdd(p.counters + tile, 1) == p.splits - 1;
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (s_last) {
-        __threadfence();
-        const int ncols = min(bn, p.t - n0);
-        const bool fok = f < p.n_out;
-        for (int c0 = 0; c0 < ncols; c0 += 4) {
-          float acc[4] = {0.f, 0.f, 0.f, 0.f};
-          for (int s0 = 0; s0 < p.splits; s0 += 8) {
-            float v[8][4];  // 32 independent L2 loads in flight per thread
-#pragma unroll
-            for (int s = 0; s < 8; ++s)
-#pragma unroll
-              for (int j = 0; j < 4; ++j)
-                v[s][j] = (fok && s0 + s < p.splits && c0 + j < ncols)
-                              ? __ldcg(p.ws + ((size_t)(s0 + s) * p.t + n0 + c0 + j) * p.n_out + f)
-                              : 0.f;
-#pragma unroll
-            for (int s = 0; s < 8; ++s)
-#pragma unroll
-              for (int j = 0; j < 4; ++j) acc[j] += v[s][j];  // split order 0..S-1
-          }
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const float pair = __shfl_xor_sync(0xffffffffu, acc[j], 1);
-            if (fok && c0 + j < ncols) epilogue_store(p.epi, n0 + c0 + j, f, p.n_out, acc[j], pair);
-          }
-        }
-        if (threadIdx.x == 64) p.counters[tile] = 0;
-      }
-    }
+    epi_tile(p, trow, bn, n0, f, split, split_out);
+    if (split_out && p.fixup) splitk_fixup(p, blockIdx.y * gridDim.x + blockIdx.x, n0, bn, f, s_last);
   }
   tc_fence_before();
   __syncthreads();
@@ -388,6 +175,181 @@ __global__ void __launch_bounds__(192, 2)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols)
                  : "memory");
+  }
+}
+
+// ------------------------------------------------------------------ wide (prefill) GEMM
+//
+// Persistent, one CTA per SM (or one CTA pair per TPC with CG = 2), static
+// tile schedule with the token tiles of one weight tile adjacent (they run in
+// the same wave and share the weight tile through L2).  Two TMEM accumulators:
+// the epilogue of tile i overlaps the mainloop of tile i+1.  With CG = 2 the
+// pair computes a 256-feature x BN-token tile with tcgen05.mma.cta_group::2:
+// each CTA stages its 128 weight rows and BN/2 token rows per stage, so the
+// smem/L2 bytes per MAC halve against the 1-CTA tile.
+struct WParams {
+  int n_out, k, t, bn, stages, kb_total;
+  int m_tiles, n_tiles, splits, kb_per_split, tiles;
+  EpiParams epi;
+  float *ws;
+  int *counters;  // one per (tile, CTA of the pair); self-resetting
+};
+
+template <int CG>
+__global__ void __launch_bounds__(192, 1)
+    gemm_wide_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, WParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                              ~static_cast<uintptr_t>(1023));
+  const int bn = p.bn, stages = p.stages;
+  const int b_rows = bn / CG;
+  const int b_bytes = b_rows * BK * 2;
+  uint8_t *sA = smem;
+  uint8_t *sB = smem + stages * A_STAGE_BYTES;
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sB + stages * b_bytes);
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * MAX_STAGES + 4);
+  __shared__ int s_last;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = CG == 2 ? cluster_rank() : 0;
+  const int unit = blockIdx.x / CG, units = gridDim.x / CG;
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + MAX_STAGES),
+                 tfull0 = smem_u32(bars + 2 * MAX_STAGES), tempty0 = smem_u32(bars + 2 * MAX_STAGES + 2);
+  const uint32_t ncols = bn <= 128 ? (bn <= 64 ? 128u : 256u) : 512u;  // two accumulators
+  const uint32_t acc_stride = ncols / 2;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull0 + 8 * a, 1);
+      mbar_init(tempty0 + 8 * a, 4 * CG);  // one arrival per epilogue warp of each CTA
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == 1) {
+    if (CG == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(ncols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(ncols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+  }
+  tc_fence_before();
+  if (CG == 2) cluster_sync_all();
+  else __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int per_m = p.splits * p.n_tiles;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint32_t full_l = CG == 2 ? map_to_rank(full0, 0) : full0;  // completion counted by the leader
+      int it = 0;
+      bool waited = false;
+      for (int tile = unit; tile < p.tiles; tile += units) {
+        const int mt = tile / per_m, rem = tile % per_m, split = rem / p.n_tiles, nt = rem % p.n_tiles;
+        const int kb0 = split * p.kb_per_split;
+        const int nkb = min(p.kb_total, kb0 + p.kb_per_split) - kb0;
+        const int arow = mt * BM * CG + (int)rank * BM, brow = nt * bn + (int)rank * b_rows;
+        for (int i = 0; i < nkb; ++i, ++it) {
+          const int s = it % stages;
+          const uint32_t ph = (it / stages) & 1;
+          mbar_wait(empty0 + 8 * s, ph ^ 1);
+          if (rank == 0) mbar_expect_tx(full0 + 8 * s, CG * (A_STAGE_BYTES + b_bytes));
+          const int kc = (kb0 + i) * BK;
+          if (CG == 2) {
+            tma_load_2d_pair(&tmA, full_l + 8 * s, smem_u32(sA + s * A_STAGE_BYTES), kc, arow);
+            if (!waited) { pdl_wait(); waited = true; }  // activations come from the previous kernel
+            tma_load_2d_pair(&tmB, full_l + 8 * s, smem_u32(sB + s * b_bytes), kc, brow);
+          } else {
+            tma_load_2d(&tmA, full0 + 8 * s, smem_u32(sA + s * A_STAGE_BYTES), kc, arow);
+            if (!waited) { pdl_wait(); waited = true; }
+            tma_load_2d(&tmB, full0 + 8 * s, smem_u32(sB + s * b_bytes), kc, brow);
+          }
+        }
+      }
+      if (!waited) pdl_wait();
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      // kind::f16, bf16 x bf16 -> f32, K-major A/B, N = bn, M = 128 * CG
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(bn >> 3) << 17) |
+                             ((uint32_t)((BM * CG) >> 4) << 24);
+      int it = 0, lt = 0;
+      for (int tile = unit; tile < p.tiles; tile += units, ++lt) {
+        const int rem = tile % per_m, split = rem / p.n_tiles;
+        const int kb0 = split * p.kb_per_split;
+        const int nkb = min(p.kb_total, kb0 + p.kb_per_split) - kb0;
+        const int acc = lt & 1;
+        mbar_wait(tempty0 + 8 * acc, ((lt >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)acc * acc_stride;
+        for (int i = 0; i < nkb; ++i, ++it) {
+          const int s = it % stages;
+          const uint32_t ph = (it / stages) & 1;
+          mbar_wait(full0 + 8 * s, ph);
+          tc_fence_after();
+          const uint32_t a = smem_u32(sA + s * A_STAGE_BYTES), b = smem_u32(sB + s * b_bytes);
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            if (CG == 2)
+              mma_bf16_pair(d, make_sdesc(a + kk * 32), make_sdesc(b + kk * 32), idesc, (i | kk) != 0 ? 1u : 0u);
+            else
+              mma_bf16(d, make_sdesc(a + kk * 32), make_sdesc(b + kk * 32), idesc, (i | kk) != 0 ? 1u : 0u);
+          }
+          if (CG == 2) mma_commit_pair(empty0 + 8 * s);
+          else mma_commit(empty0 + 8 * s);
+        }
+        if (CG == 2) mma_commit_pair(tfull0 + 8 * acc);
+        else mma_commit(tfull0 + 8 * acc);
+      }
+    }
+    __syncwarp();
+  } else {
+    pdl_wait();  // the epilogue reads bias/residual/gates and writes outputs
+    const int q = warp & 3;
+    const bool split_out = p.splits > 1;
+    const uint32_t tempty_l = CG == 2 ? map_to_rank(tempty0, 0) : tempty0;
+    int lt = 0;
+    for (int tile = unit; tile < p.tiles; tile += units, ++lt) {
+      const int mt = tile / per_m, rem = tile % per_m, split = rem / p.n_tiles, nt = rem % p.n_tiles;
+      const int acc = lt & 1;
+      mbar_wait(tfull0 + 8 * acc, (lt >> 1) & 1);
+      tc_fence_after();
+      const int f = mt * BM * CG + (int)rank * BM + q * 32 + lane;
+      const int n0 = nt * bn;
+      const uint32_t trow = tmem + (uint32_t)acc * acc_stride + ((uint32_t)(q * 32) << 16);
+      epi_tile(p, trow, bn, n0, f, split, split_out);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (CG == 2) mbar_arrive_cluster(tempty_l + 8 * acc);
+        else mbar_arrive_local(tempty0 + 8 * acc);
+      }
+      if (split_out && p.epi.mode != EPI_PARTIALS)
+        splitk_fixup(p, (mt * p.n_tiles + nt) * CG + (int)rank, n0, bn, f, s_last);
+    }
+  }
+  if (threadIdx.x == 0) pdl_trigger();
+  tc_fence_before();
+  if (CG == 2) cluster_sync_all();
+  else __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    if (CG == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols) : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols) : "memory");
   }
 }
 
@@ -427,9 +389,64 @@ CUtensorMap make_map(const void *ptr, int rows, int k, int box_rows) {
   return map;
 }
 
+constexpr int WIDE_SMEM = 220 * 1024;
+
+static int wide_stages(int bn, int cg) {
+  return std::min(MAX_STAGES, (WIDE_SMEM - 2048) / (A_STAGE_BYTES + bn / cg * BK * 2));
+}
+
+// Cost model (SM cycles) of the persistent wide kernel.  Per k-block a CTA
+// needs max(MMA, operand ingest): MMA = 128 x bn x 64 MACs at 4096 MAC/cycle/SM;
+// ingest = (16 KB of weights + bn/CG token rows of 128 B) at ~33 B/cycle/SM
+// (measured: the 2-CTA GEMM at T=800 streams 32-35 B/cycle/SM whether 80 or
+// 148 SMs are active).  Split-K pays a partial-sum round trip and a fix-up.
+static double wide_cost(int n_out, int kb_total, int t, int sms, int cg, int bn, int splits) {
+  const int m_tiles = (n_out + BM * cg - 1) / (BM * cg), n_tiles = (t + bn - 1) / bn;
+  const int tiles = m_tiles * n_tiles * splits, units = sms / cg;
+  const int waves = (tiles + units - 1) / units;
+  const int kbs = (kb_total + splits - 1) / splits;
+  const double mma = 2.0 * bn, bytes = A_STAGE_BYTES + (double)bn / cg * BK * 2;
+  const double per_tile = kbs * std::max(mma, bytes / 33.0) + 600.0;
+  double c = 3000.0 + waves * per_tile + 60.0 * bn;
+  if (splits > 1) c += 2.0 * bn * 128 * 4 * splits / 33.0 + 1500.0;
+  return c;
+}
+
+static bool wide_plan(Plan &p, int n_out, int k, int t, int sms) {
+  const Knobs &kn = knobs();
+  if (kn.wide == 0) return false;
+  double best = 1e30;
+  for (int cg = 1; cg <= 2; ++cg) {
+    if (kn.wide > 0 && cg != kn.wide) continue;
+    for (int bn = 32; bn <= MAX_BN; bn += 16) {
+      if (kn.wide_bn && bn != kn.wide_bn) continue;
+      for (int splits = 1; splits <= 4; ++splits) {
+        if (kn.wide_splits && splits != kn.wide_splits) continue;
+        if (splits > 1 && p.kb_total / splits < 4) continue;
+        const double c = wide_cost(n_out, p.kb_total, t, sms, cg, bn, splits);
+        if (c < best * 0.999) {
+          best = c;
+          p.cg = cg;
+          p.bn = bn;
+          p.splits = splits;
+        }
+      }
+    }
+  }
+  if (best >= 1e30) return false;
+  p.m_tiles = (n_out + BM * p.cg - 1) / (BM * p.cg);
+  p.n_tiles = (t + p.bn - 1) / p.bn;
+  const int per_split = (p.kb_total + p.splits - 1) / p.splits;
+  p.splits = (p.kb_total + per_split - 1) / per_split;
+  p.stages = wide_stages(p.bn, p.cg);
+  return true;
+}
+
 Plan make_plan(int n_out, int k, int t, int sms, int force_splits) {
   Plan p{};
   p.kb_total = (k + BK - 1) / BK;
+  if (t > 64 && force_splits <= 0 && wide_plan(p, n_out, k, t, sms)) return p;
+  p.cg = 0;
   p.m_tiles = (n_out + BM - 1) / BM;
   p.n_tiles = (t + MAX_BN - 1) / MAX_BN;
   // wide token dims (prefill): narrower token tiles until the grid fills the SMs
@@ -455,6 +472,69 @@ static size_t smem_bytes(const Plan &p) {
   return 1024 + (size_t)p.stages * (A_STAGE_BYTES + p.bn * BK * 2) + (2 * MAX_STAGES + 1) * 8 + 16;
 }
 
+static size_t wide_smem_bytes(const Plan &p) {
+  return 1024 + (size_t)p.stages * (A_STAGE_BYTES + p.bn / p.cg * BK * 2) + (2 * MAX_STAGES + 4) * 8 + 16;
+}
+
+static void launch_wide(const void *w, const void *x, int n_out, int k, int t, const EpiParams &epi,
+                        const Plan &plan, float *ws, int *counters, cudaStream_t st) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    OXY_CUDA(cudaFuncSetAttribute(gemm_wide_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
+    OXY_CUDA(cudaFuncSetAttribute(gemm_wide_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
+    attr_set = true;
+  }
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    OXY_CUDA(cudaGetDevice(&dev));
+    OXY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const int cg = plan.cg;
+  CUtensorMap ma = make_map(w, n_out, k, BM);
+  CUtensorMap mb = make_map(x, t, k, plan.bn / cg);
+  WParams wp;
+  wp.n_out = n_out;
+  wp.k = k;
+  wp.t = t;
+  wp.bn = plan.bn;
+  wp.stages = plan.stages;
+  wp.kb_total = plan.kb_total;
+  wp.m_tiles = plan.m_tiles;
+  wp.n_tiles = plan.n_tiles;
+  wp.splits = plan.splits;
+  wp.kb_per_split = (plan.kb_total + plan.splits - 1) / plan.splits;
+  wp.tiles = plan.m_tiles * plan.n_tiles * plan.splits;
+  wp.epi = epi;
+  wp.ws = ws;
+  wp.counters = counters;
+  const int units = std::min(wp.tiles, sms / cg);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(units * cg);
+  cfg.blockDim = dim3(192);
+  cfg.dynamicSmemBytes = wide_smem_bytes(plan);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (knobs().pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (cg == 2) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = 2;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  if (cg == 2) OXY_CUDA(cudaLaunchKernelEx(&cfg, gemm_wide_kernel<2>, ma, mb, wp));
+  else OXY_CUDA(cudaLaunchKernelEx(&cfg, gemm_wide_kernel<1>, ma, mb, wp));
+  __atomic_fetch_add(&g_launches, 1ull, __ATOMIC_RELAXED);
+}
+
 void launch(const void *w, const void *x, int n_out, int k, int t, const EpiParams &epi,
             const Plan &plan, float *ws, int *counters, cudaStream_t st) {
   static bool attr_set = false;
@@ -465,7 +545,11 @@ void launch(const void *w, const void *x, int n_out, int k, int t, const EpiPara
   }
   if (t <= 0) return;
   if (plan.splits > 1 && (!ws || !counters)) fail(OXY_EINVAL, "split-K GEMM needs a workspace");
-  if (plan.splits > 1 && plan.m_tiles * plan.n_tiles > MAX_TILES) fail(OXY_EINVAL, "too many split-K tiles");
+  if (plan.splits > 1 && plan.m_tiles * plan.n_tiles * 2 > MAX_TILES) fail(OXY_EINVAL, "too many split-K tiles");
+  if (plan.cg > 0) {
+    launch_wide(w, x, n_out, k, t, epi, plan, ws, counters, st);
+    return;
+  }
   CUtensorMap ma = make_map(w, n_out, k, BM);
   CUtensorMap mb = make_map(x, t, k, plan.bn);
   KParams kp;

@@ -79,6 +79,7 @@ constexpr int MAX_TILES = 1 << 16;  // split-K tile counters
 
 struct Plan {
   int bn, n_tiles, m_tiles, splits, stages, kb_total;
+  int cg;  // 0: one-tile-per-CTA kernel (skinny); 1 / 2: persistent wide kernel, 1-CTA / CTA-pair tiles
 };
 
 // Host: build a plan for (N_out, K, T) on `sms` SMs.
