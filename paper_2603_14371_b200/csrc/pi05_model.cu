@@ -23,6 +23,7 @@
 
 #include "cuda_util.cuh"
 #include "gemm_sm100.cuh"
+#include "megakernel.cuh"
 #include "pi05_kernels.cuh"
 
 
@@ -307,6 +308,17 @@ struct Model {
 
   int *gemm_counters = nullptr;
   int *dec_counters = nullptr;  // per decode row, for the self-merging attention
+  // persistent layer-program path (megakernel.cu) for the denoise loop: OXY_MK=1
+  // enables it (off by default: slower than the CUDA-graph path, profiles/r01_megakernel.md)
+  bool use_mk = [] {
+    const char *e = getenv("OXY_MK");
+    return e && atoi(e) != 0;
+  }();
+  int mk_grid = [] {
+    const char *e = getenv("OXY_MK_GRID");
+    return e ? atoi(e) : 0;
+  }();
+  std::map<std::string, mk::Program> mk_progs;
 
   // ---- execution lanes.  The members above (stream, events, arena, graph
   // cache, split-K counters) and the per-call scratch describe the ACTIVE lane.
@@ -777,6 +789,20 @@ struct Model {
       groups[i].nkb = H;
     }
     AttnPlan ap = shape_attention(groups, HEAD_DIM);
+    if (use_mk) {
+      const char *e = getenv("OXY_MK_ATTN_TILES");  // key tiles per split item
+      const int per = std::max(1, e ? atoi(e) : 2);
+      ap.splits = std::max(1, (ap.max_tiles + per - 1) / per);
+      if (ap.splits > 1) {
+        attn_ws_need = std::max(attn_ws_need, (size_t)ap.splits * ap.rows * 256);
+        attn_ml_need = std::max(attn_ml_need, (size_t)ap.splits * ap.rows * 2);
+      }
+      for (auto nk : {std::pair<int, int>{We, AP}, {QKV, We}, {We, QDIM}, {2 * c.expert_mlp, We}, {We, c.expert_mlp},
+                      {A, We}}) {
+        const int sp = mk::gemm_splits(nk.first, nk.second, T, sms);
+        if (sp > 1) ws_need = std::max(ws_need, (size_t)sp * T * nk.first);
+      }
+    }
     reserve_common();
     // ---- plan pass 2
     float *a = act.as<float>(0), *X = xe.as<float>(0), *vel_d = vel.as<float>(0);
@@ -804,6 +830,17 @@ struct Model {
       g.ldkv = HEAD_DIM;
     }
     ap.groups = arena_put(groups.data(), groups.size());
+    mk::Program *pg = nullptr;
+    if (use_mk) {
+      pg = &mk_progs[key];
+      if (pg->gen != g_devbuf_reallocs) {
+        build_denoise_program(*pg, n, S, T, d_pos, ap, a, X, vel_d, ab, Y, Qb, Ob, Kd, Vd, Hm, modp);
+        pg->gen = g_devbuf_reallocs;
+        pg->grid = mk_grid;
+        pg->profile = getenv("OXY_MK_PROFILE") != nullptr;
+        pg->upload(mst);
+      }
+    }
     enter(caller);
     OXY_CUDA(cudaEventRecord(alt.t0, mst));
     arena_upload();
@@ -813,6 +850,10 @@ struct Model {
                                  cudaMemcpyDeviceToDevice, mst));
       OXY_CUDA(cudaMemsetAsync(vel_d, 0, (size_t)T * AP * sizeof(float), mst));
       f32_to_bf16(a, ab, (int64_t)T * AP, mst);
+      if (pg) {
+        pg->launch(mst);
+        return;
+      }
       const float dt = -1.f / (float)S;
       for (int s = 0; s < S; ++s) {
         const float *ms = modp + (size_t)s * n_mod;
@@ -834,11 +875,103 @@ struct Model {
       }
     };
     run_body(key, true, body);
+    if (pg && pg->profile) mk_report(*pg);
     OXY_CUDA(cudaMemcpy2DAsync(actions_out_d, A * sizeof(float), a, AP * sizeof(float), A * sizeof(float), T,
                                cudaMemcpyDeviceToDevice, mst));
     OXY_CUDA(cudaEventRecord(alt.t1, mst));
     if (join) leave(caller);
     else OXY_CUDA(cudaEventRecord(ev_out, mst));
+  }
+
+  // OXY_MK_PROFILE: per-phase-type time of the last program run (CTA 0's view of the barriers)
+  void mk_report(mk::Program &pg) {
+    OXY_CUDA(cudaStreamSynchronize(mst));
+    const size_t n = pg.phases.size();
+    const int G = pg.grid > 0 ? pg.grid : sms;
+    std::vector<unsigned long long> t(n * (1 + G));
+    OXY_CUDA(cudaMemcpy(t.data(), pg.d_times, t.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    // release[i] = CTA 0 leaving barrier i; arrive[i][c] = CTA c arriving at barrier i
+    // work(i) = last arrival at barrier i - release of barrier i-1; sync(i) = release[i] - last arrival
+    double work[8] = {0}, sync[8] = {0}, cnt[8] = {0};
+    std::map<std::string, std::pair<double, int>> gem;
+    for (size_t i = 1; i + 1 < n; ++i) {
+      unsigned long long last = 0;
+      for (int c = 0; c < G; ++c) last = std::max(last, t[n + i * G + c]);
+      const double w = ((double)last - (double)t[i - 1]) * 1e-3, sy = ((double)t[i] - (double)last) * 1e-3;
+      const int ty = pg.phases[i].type;
+      work[ty] += w;
+      sync[ty] += sy;
+      cnt[ty] += 1;
+      if (ty == mk::PH_GEMM) {
+        const auto &g = pg.phases[i].g;
+        auto &e = gem[std::to_string(g.n_out) + "x" + std::to_string(g.k) + " s" + std::to_string(g.splits)];
+        e.first += w;
+        e.second += 1;
+      }
+    }
+    const char *names[] = {"gemm", "reduce_epi", "res_norm", "attn", "attn_merge", "euler"};
+    std::fprintf(stderr, "mk profile: %zu phases, %.1f us total (work = slowest CTA, sync = barrier after it)\n", n,
+                 (t[n - 1] - t[0]) * 1e-3);
+    for (int ty = 0; ty < 6; ++ty)
+      if (cnt[ty])
+        std::fprintf(stderr, "  %-11s n=%5.0f work=%6.2f us sync=%5.2f us (mean)\n", names[ty], cnt[ty],
+                     work[ty] / cnt[ty], sync[ty] / cnt[ty]);
+    for (auto &kv : gem)
+      std::fprintf(stderr, "    gemm %-16s n=%4d work=%6.2f us\n", kv.first.c_str(), kv.second.second,
+                   kv.second.first / kv.second.second);
+  }
+
+  // The whole S-step denoise as one persistent layer program (megakernel.cu):
+  // the same math as the multi-kernel body below, phase for phase.
+  void build_denoise_program(mk::Program &pg, int n, int S, int T, const int *d_pos, const AttnPlan &ap, float *a,
+                             float *X, float *vel_d, bf16 *ab, bf16 *Y, bf16 *Qb, bf16 *Ob, bf16 *Kd, bf16 *Vd,
+                             bf16 *Hm, const float *modp) {
+    (void)n;
+    const int We = c.expert_width, A = c.action_dim, AP = apad(), EM = c.expert_mlp;
+    const float eps = 1e-6f, dt = -1.f / (float)S;
+    float *mws = ws.as<float>(0);
+    float *awo = nullptr, *aml = nullptr;
+    if (ap.splits > 1) {
+      awo = attn_ws.as<float>((size_t)ap.splits * ap.rows * 256);
+      aml = attn_ml.as<float>((size_t)ap.splits * ap.rows * 2);
+    }
+    pg.clear();
+    auto epi = [](int mode, void *out, int ldo, const float *bias = nullptr, const float *gate = nullptr) {
+      return EpiParams{mode, out, ldo, bias, nullptr, 0, gate, {}};
+    };
+    const int max_nq = c.H * Q_HEADS;
+    for (int s = 0; s < S; ++s) {
+      const float *ms = modp + (size_t)s * n_mod;
+      EpiParams ei = epi(gemm::EPI_F32, X, We, e_in_b);
+      int sp = pg.gemm(e_in, ab, We, AP, T, ei, mws, sms);
+      if (sp > 1) pg.reduce_epi(mws, sp, T, We, ei);
+      pg.res_norm(nullptr, 0, T, We, nullptr, X, We, Y, We, nullptr, ms, ms + We, eps);
+      const float *mf = ms + (size_t)c.depth * 6 * We;
+      for (int l = 0; l < c.depth; ++l) {
+        const ExpertW &w = E[l];
+        const float *m = ms + (size_t)l * 6 * We;
+        const float *mn = l + 1 < c.depth ? m + 6 * We : mf;
+        EpiParams er{gemm::EPI_QKV_ROPE, nullptr, 0, nullptr, nullptr, 0, nullptr,
+                     gemm::QkvRope{rope_inv, d_pos, nullptr, Qb, Kd, Vd}};
+        sp = pg.gemm(w.wqkv, Y, QKV, We, T, er, mws, sms, 1);  // whole K: RoPE epilogue in place
+        if (sp > 1) pg.reduce_epi(mws, sp, T, QKV, er);
+        pg.attention(ap.groups, ap.n, ap.q_tiles, max_nq, ap.splits, ap.rows, kpool(l), vpool(l), 1.f / 16.f, awo,
+                     aml);
+        sp = pg.gemm(w.wo, Ob, We, QDIM, T, epi(gemm::EPI_ADD_GATED_F32, X, We, nullptr, m + 2 * We), mws, sms);
+        if (sp > 1) pg.res_norm(mws, sp, T, We, m + 2 * We, X, We, Y, We, nullptr, m + 3 * We, m + 4 * We, eps);
+        else pg.res_norm(nullptr, 0, T, We, nullptr, X, We, Y, We, nullptr, m + 3 * We, m + 4 * We, eps);
+        EpiParams eg = epi(gemm::EPI_GEGLU_BF16, Hm, EM);
+        sp = pg.gemm(w.wgu, Y, 2 * EM, We, T, eg, mws, sms, 1);  // whole K: GeGLU epilogue in place
+        if (sp > 1) pg.reduce_epi(mws, sp, T, 2 * EM, eg);
+        sp = pg.gemm(w.wd, Hm, We, EM, T, epi(gemm::EPI_ADD_GATED_F32, X, We, nullptr, m + 5 * We), mws, sms);
+        if (sp > 1) pg.res_norm(mws, sp, T, We, m + 5 * We, X, We, Y, We, nullptr, mn, mn + We, eps);
+        else pg.res_norm(nullptr, 0, T, We, nullptr, X, We, Y, We, nullptr, mn, mn + We, eps);
+      }
+      EpiParams eo = epi(gemm::EPI_F32, vel_d, AP, e_out_b);
+      sp = pg.gemm(e_out, Y, A, We, T, eo, mws, sms);
+      if (sp > 1) pg.reduce_epi(mws, sp, T, A, eo);
+      pg.euler(a, vel_d, ab, T * AP, dt);
+    }
   }
 
   // ------------------------------------------------------------ decode
