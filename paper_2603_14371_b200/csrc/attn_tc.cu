@@ -1,0 +1,349 @@
+// tcgen05 flash attention for head dim 256 (prefix-LM prefill over the paged
+// pool; action-expert suffix over [paged prefix || dense suffix]).
+//
+// CTA = one 128-row query tile x one key split; 6 warps:
+//   warp 0     TMA producer: the Q tile once (4 boxes of 128 rows x 64 dims),
+//              then K and V tiles of 64 keys (one pool block: 4 boxes each)
+//              into a 2-slot ring; paged tiles by block id, dense by row;
+//   warp 1     MMA issuer (one thread): S = Q K^T (M 128, N 64, K 256) into one
+//              of two TMEM S buffers, then O += P V (M 128, N 256, K 64; V read
+//              MN-major straight from its TMA layout) into the TMEM O tile;
+//   warps 2-5  softmax: thread = query row (TMEM lane), 64 scores per tile in
+//              registers, online softmax in the log2 domain with a lazy
+//              reference max (O and l are rescaled only when the row max grows
+//              by more than 2^8), P written bf16 to smem in the 128B-swizzled
+//              K-major layout the PV MMA reads; final O / l to bf16 rows, or
+//              fp32 partials + (m, l) for the split merge (fa_merge).
+// Invariant relied on: pool slots past a sequence's length hold finite values
+// (the pool is zeroed at creation and only ever written with finite K/V), so
+// masked keys contribute p = 0 exactly.
+#include <cmath>
+
+#include "cuda_util.cuh"
+#include "gemm_device.cuh"
+#include "pi05_kernels.cuh"
+
+namespace oxy {
+namespace pi05 {
+
+using namespace gemm;
+
+namespace tc {
+constexpr int TQ = 128, TK = 64, HD = 256;
+constexpr int Q_BOX = TQ * 128;          // 16 KB: 128 rows x 64 dims
+constexpr int KV_BOX = TK * 128;         // 8 KB: 64 keys x 64 dims
+constexpr int Q_BYTES = 4 * Q_BOX;       // 64 KB
+constexpr int KV_BYTES = 4 * KV_BOX;     // 32 KB (K or V tile)
+constexpr int P_BYTES = TQ * 128;        // 16 KB: 128 rows x 64 keys bf16
+constexpr int OFF_K = Q_BYTES, OFF_V = OFF_K + 2 * KV_BYTES, OFF_P = OFF_V + 2 * KV_BYTES;
+constexpr int OFF_BAR = OFF_P + P_BYTES;  // 208 KB
+// barriers: q_full, kv_full[2], kv_empty[2], s_full[2], s_empty[2], p_full, o_done
+constexpr int N_BARS = 11;
+constexpr size_t SMEM = 1024 + OFF_BAR + N_BARS * 8 + 16;
+constexpr uint32_t TMEM_COLS = 512;  // O: 0..255, S buffers: 256.., 320..
+constexpr float LAZY = 8.f;          // rescale when the row max grows by > 2^8
+}  // namespace tc
+
+// MN-major, 128B-swizzled operand (V as the B operand: dims contiguous):
+// 8-key atoms of 1024 B (SBO), 64-dim groups one TMA box apart (LBO).
+__device__ __forceinline__ uint64_t make_sdesc_mn(uint32_t saddr, uint32_t lbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+struct TcAttnArgs {
+  const AttnGroup *groups;
+  int q_tiles, splits, ws_rows;
+  const bf16 *q_base, *kd_base;  // row offsets of the groups' q / dense k,v pointers
+  float scale_log2;
+  float *ws_o, *ws_ml;
+};
+
+__global__ void __launch_bounds__(192, 1)
+    flash_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kpmap,
+                    const __grid_constant__ CUtensorMap vpmap, const __grid_constant__ CUtensorMap kdmap,
+                    const __grid_constant__ CUtensorMap vdmap, TcAttnArgs a) {
+  using namespace tc;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                            ~static_cast<uintptr_t>(1023));
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sm + OFF_BAR);
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + N_BARS);
+  const uint32_t b_q = smem_u32(bars), b_kvf = b_q + 8, b_kve = b_q + 24, b_sf = b_q + 40, b_se = b_q + 56,
+                 b_pf = b_q + 72, b_od = b_q + 80;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  const AttnGroup g = a.groups[blockIdx.x / a.q_tiles];
+  const int qt = blockIdx.x % a.q_tiles, q0 = qt * TQ;
+  if (q0 >= g.nq) return;  // uniform per CTA, before any barrier or TMEM use
+  const int split = blockIdx.y;
+  const int ta = (g.nka + TK - 1) / TK, tb = (g.nkb + TK - 1) / TK, tiles = ta + tb;
+  const int per = (tiles + a.splits - 1) / a.splits;
+  const int t0 = min(tiles, split * per), t1 = min(tiles, t0 + per), n = t1 - t0;
+
+  if (threadIdx.x == 0) {
+    mbar_init(b_q, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(b_kvf + 8 * s, 1);
+      mbar_init(b_kve + 8 * s, 1);
+      mbar_init(b_sf + 8 * s, 1);
+      mbar_init(b_se + 8 * s, 4);
+    }
+    mbar_init(b_pf, 4);
+    mbar_init(b_od, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&qmap)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&kpmap)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&vpmap)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+
+  if (warp == 0) {
+    if (lane == 0 && n > 0) {
+      const int qrow = (int)((g.q - a.q_base) / HD) + q0;
+      mbar_expect_tx(b_q, Q_BYTES);
+      for (int b = 0; b < 4; ++b) tma_load_2d(&qmap, b_q, smem_u32(sm + b * Q_BOX), b * 64, qrow);
+      const int drow0 = g.kb ? (int)((g.kb - a.kd_base) / HD) : 0;
+      for (int i = 0; i < n; ++i) {
+        const int j = t0 + i, s = i & 1;
+        mbar_wait(b_kve + 8 * s, ((i >> 1) & 1) ^ 1);
+        mbar_expect_tx(b_kvf + 8 * s, 2 * KV_BYTES);
+        const bool paged = j < ta;
+        const int row = paged ? g.bt[j] * TK : drow0 + (j - ta) * TK;
+        const CUtensorMap *km = paged ? &kpmap : &kdmap, *vm = paged ? &vpmap : &vdmap;
+        for (int b = 0; b < 4; ++b) {
+          tma_load_2d(km, b_kvf + 8 * s, smem_u32(sm + OFF_K + s * KV_BYTES + b * KV_BOX), b * 64, row);
+          tma_load_2d(vm, b_kvf + 8 * s, smem_u32(sm + OFF_V + s * KV_BYTES + b * KV_BOX), b * 64, row);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && n > 0) {
+      // kind::f16, bf16 in, f32 accumulate; S: K-major A and B, N = 64; O: B (V) MN-major, N = 256
+      const uint32_t idesc_s = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TK >> 3) << 17) |
+                               ((uint32_t)(TQ >> 4) << 24);
+      const uint32_t idesc_o = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(HD >> 3) << 17) |
+                               ((uint32_t)(TQ >> 4) << 24);
+      const uint32_t q_s = smem_u32(sm), p_s = smem_u32(sm + OFF_P);
+      mbar_wait(b_q, 0);
+      auto issue_pv = [&](int i) {
+        mbar_wait(b_pf, i & 1);
+        tc_fence_after();
+        const uint32_t v_s = smem_u32(sm + OFF_V + (i & 1) * KV_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < TK / 16; ++kk)
+          mma_bf16(tmem, make_sdesc(p_s + kk * 32), make_sdesc_mn(v_s + kk * 2048, KV_BOX), idesc_o,
+                   (i | kk) != 0 ? 1u : 0u);
+        mma_commit(b_kve + 8 * (i & 1));
+        mma_commit(b_od);
+      };
+      for (int i = 0; i < n; ++i) {
+        const int s = i & 1;
+        mbar_wait(b_kvf + 8 * s, (i >> 1) & 1);
+        mbar_wait(b_se + 8 * s, ((i >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t k_s = smem_u32(sm + OFF_K + s * KV_BYTES);
+        const uint32_t d_s = tmem + 256 + s * TK;
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk)
+          mma_bf16(d_s, make_sdesc(q_s + (kk >> 2) * Q_BOX + (kk & 3) * 32),
+                   make_sdesc(k_s + (kk >> 2) * KV_BOX + (kk & 3) * 32), idesc_s, kk != 0 ? 1u : 0u);
+        mma_commit(b_sf + 8 * s);
+        if (i > 0) issue_pv(i - 1);
+      }
+      issue_pv(n - 1);
+    }
+    __syncwarp();
+  } else {
+    // softmax / epilogue: thread = query row
+    const int quad = warp & 3, row = quad * 32 + lane;
+    const uint32_t lanes = (uint32_t)(quad * 32) << 16;
+    const int r = q0 + row;
+    float m_ref = -INFINITY, l = 0.f;
+    uint8_t *prow = sm + OFF_P + row * 128;
+    for (int i = 0; i < n; ++i) {
+      const int j = t0 + i, s = i & 1;
+      const int nvalid = j < ta ? min(TK, g.nka - j * TK) : min(TK, g.nkb - (j - ta) * TK);
+      mbar_wait(b_sf + 8 * s, (i >> 1) & 1);
+      tc_fence_after();
+      float sc[TK];
+      {
+        uint32_t v[4][16];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_ld16_nowait(tmem + 256 + s * TK + lanes + c * 16, v[c]);
+        tmem_ld_wait();
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int e = 0; e < 16; ++e) sc[c * 16 + e] = __uint_as_float(v[c][e]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_local(b_se + 8 * s);  // S buffer may be overwritten
+      float mx = -INFINITY;
+#pragma unroll
+      for (int e = 0; e < TK; ++e) {
+        sc[e] = e < nvalid ? sc[e] * a.scale_log2 : -INFINITY;
+        mx = fmaxf(mx, sc[e]);
+      }
+      float corr = 1.f;
+      if (mx > m_ref + LAZY || (m_ref == -INFINITY && mx > -INFINITY)) {
+        corr = m_ref == -INFINITY ? 0.f : exp2f(m_ref - mx);
+        m_ref = mx;
+      }
+      float rs = 0.f;
+      uint32_t pk[TK / 2];
+#pragma unroll
+      for (int e = 0; e < TK; e += 2) {
+        const float p0 = m_ref == -INFINITY ? 0.f : exp2f(sc[e] - m_ref);
+        const float p1 = m_ref == -INFINITY ? 0.f : exp2f(sc[e + 1] - m_ref);
+        rs += p0 + p1;
+        __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
+        pk[e / 2] = *reinterpret_cast<uint32_t *>(&h);
+      }
+      l = l * corr + rs;
+      // PV(i-1) must be complete before O is rescaled and before P is overwritten
+      if (i > 0) {
+        mbar_wait(b_od, (i - 1) & 1);
+        tc_fence_after();
+        if (corr != 1.f) {
+          for (int c = 0; c < HD; c += 16) {
+            uint32_t v[16];
+            tmem_ld16_nowait(tmem + lanes + c, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) * corr);
+            tmem_st16(tmem + lanes + c, v);
+          }
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
+      }
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch)  // 128B swizzle: chunk ch of row r lives at ch ^ (r & 7)
+        *reinterpret_cast<uint4 *>(prow + ((ch ^ (row & 7)) << 4)) =
+            make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_local(b_pf);
+    }
+    // epilogue
+    if (n > 0) {
+      mbar_wait(b_od, (n - 1) & 1);
+      tc_fence_after();
+    }
+    const bool ok = r < g.nq;
+    if (a.splits == 1) {
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      bf16 *orow = g.o + (size_t)r * g.ldo;
+      for (int c = 0; c < HD; c += 16) {
+        uint32_t v[16];
+        if (n > 0) {
+          tmem_ld16_nowait(tmem + lanes + c, v);
+          tmem_ld_wait();
+        } else {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) v[e] = 0u;
+        }
+        uint32_t o[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          __nv_bfloat162 h =
+              __floats2bfloat162_rn(__uint_as_float(v[2 * e]) * inv, __uint_as_float(v[2 * e + 1]) * inv);
+          o[e] = *reinterpret_cast<uint32_t *>(&h);
+        }
+        if (ok) {
+          *reinterpret_cast<uint4 *>(orow + c) = make_uint4(o[0], o[1], o[2], o[3]);
+          *reinterpret_cast<uint4 *>(orow + c + 8) = make_uint4(o[4], o[5], o[6], o[7]);
+        }
+      }
+    } else {
+      const size_t wr = (size_t)split * a.ws_rows + g.wrow0 + r;
+      float *orow = a.ws_o + wr * HD;
+      for (int c = 0; c < HD; c += 16) {
+        uint32_t v[16];
+        if (n > 0) {
+          tmem_ld16_nowait(tmem + lanes + c, v);
+          tmem_ld_wait();
+        } else {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) v[e] = 0u;
+        }
+        if (ok)
+#pragma unroll
+          for (int e = 0; e < 16; e += 4)
+            *reinterpret_cast<float4 *>(orow + c + e) =
+                make_float4(__uint_as_float(v[e]), __uint_as_float(v[e + 1]), __uint_as_float(v[e + 2]),
+                            __uint_as_float(v[e + 3]));
+      }
+      if (ok) {
+        a.ws_ml[wr * 2] = m_ref;
+        a.ws_ml[wr * 2 + 1] = l;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
+  }
+}
+
+void flash_attention_tc(const AttnGroup *groups_d, int n_groups, int q_tiles, int splits, const bf16 *q_base,
+                        int q_rows, const CUtensorMap &kpool_map, const CUtensorMap &vpool_map, const bf16 *kd_base,
+                        const bf16 *vd_base, int kd_rows, float scale, float *ws_o, float *ws_ml, int ws_rows,
+                        cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    OXY_CUDA(cudaFuncSetAttribute(flash_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::SMEM));
+    attr = true;
+  }
+  if (n_groups <= 0 || q_tiles <= 0) return;
+  const CUtensorMap qm = gemm::make_map(q_base, q_rows, tc::HD, tc::TQ);
+  // dense suffix K/V (or the pool maps again when there is none)
+  const CUtensorMap kdm = kd_base ? gemm::make_map(kd_base, kd_rows, tc::HD, tc::TK) : kpool_map;
+  const CUtensorMap vdm = vd_base ? gemm::make_map(vd_base, kd_rows, tc::HD, tc::TK) : vpool_map;
+  if (kd_base && vd_base - kd_base != 0 && (vd_base - kd_base) % tc::HD != 0)
+    fail(OXY_EINVAL, "dense K/V buffers must be row-aligned");
+  TcAttnArgs a{groups_d, q_tiles, splits, ws_rows, q_base, kd_base, scale * 1.4426950408889634f, ws_o, ws_ml};
+  launch_pdl(flash_tc_kernel, dim3(n_groups * q_tiles, splits), dim3(192), tc::SMEM, st, qm, kpool_map, vpool_map,
+             kdm, vdm, a);
+}
+
+}  // namespace pi05
+}  // namespace oxy

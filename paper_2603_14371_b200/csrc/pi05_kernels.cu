@@ -377,6 +377,12 @@ static void flash_launch(const AttnGroup *groups_d, int n_groups, int max_q_tile
   }
 }
 
+void flash_merge(const AttnGroup *groups_d, int n_groups, int max_rows, int splits, const float *ws_o,
+                 const float *ws_ml, int ws_rows, cudaStream_t st) {
+  if (splits <= 1 || n_groups <= 0) return;
+  launch_pdl(fa_merge_kernel<256>, dim3(max_rows, n_groups), dim3(128), 0, st, groups_d, splits, ws_o, ws_ml, ws_rows);
+}
+
 void flash_attention(const AttnGroup *groups_d, int n_groups, int max_q_tiles, int head_dim,
                      const bf16 *kpool, const bf16 *vpool, float scale, int splits, int max_key_tiles,
                      float *ws_o, float *ws_ml, int ws_rows, cudaStream_t st) {

@@ -76,6 +76,18 @@ void flash_attention(const AttnGroup *groups_d, int n_groups, int max_q_tiles, i
                      const bf16 *kpool, const bf16 *vpool, float scale, int splits,
                      int max_key_tiles, float *ws_o, float *ws_ml, int ws_rows, cudaStream_t st);
 
+// tcgen05 flash attention, head dim 256 (attn_tc.cu): groups' q rows are rows of
+// q_base viewed as [q_rows, 256]; paged keys through kpool/vpool maps (box 64x64),
+// dense keys g.kb/g.vb rows of kd_base/vd_base [kd_rows, 256] (null: none).
+// q_tiles = ceil(max nq / 128); splits > 1 writes ws (merge with flash_merge).
+void flash_attention_tc(const AttnGroup *groups_d, int n_groups, int q_tiles, int splits, const bf16 *q_base,
+                        int q_rows, const CUtensorMap &kpool_map, const CUtensorMap &vpool_map, const bf16 *kd_base,
+                        const bf16 *vd_base, int kd_rows, float scale, float *ws_o, float *ws_ml, int ws_rows,
+                        cudaStream_t st);
+// split-order merge of head-dim-256 partials (ws rows as in flash_attention)
+void flash_merge(const AttnGroup *groups_d, int n_groups, int max_rows, int splits, const float *ws_o,
+                 const float *ws_ml, int ws_rows, cudaStream_t st);
+
 // Paged decode attention: rows x 8 q-heads vs 1 KV head, keys [0, pos[r]].
 // q [rows, 8*256] bf16 -> out [rows, 8*256] bf16.  ws: rows*max_blocks*8*(256+2) floats.
 void decode_attention(const bf16 *q, bf16 *out, const bf16 *kpool, const bf16 *vpool,

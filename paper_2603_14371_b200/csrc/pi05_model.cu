@@ -551,6 +551,45 @@ struct Model {
     flash_attention(p.groups, p.n, p.q_tiles, p.hd, kp, vp, 1.f / std::sqrt((float)p.hd), p.splits, p.max_tiles,
                     wo, wml, p.rows, mst);
   }
+  // tcgen05 attention (attn_tc.cu) for head dim 256: OXY_ATTN_TC=0 falls back to the mma.sync kernel
+  bool use_attn_tc = [] {
+    const char *e = getenv("OXY_ATTN_TC");
+    return !e || atoi(e) != 0;
+  }();
+  AttnPlan shape_attention_tc(std::vector<AttnGroup> &groups) {
+    AttnPlan p;
+    p.n = (int)groups.size();
+    p.hd = HEAD_DIM;
+    int max_nq = 0;
+    for (auto &g : groups) {
+      g.wrow0 = p.rows;
+      p.rows += g.nq;
+      max_nq = std::max(max_nq, g.nq);
+      p.max_tiles = std::max(p.max_tiles, (g.nka + 63) / 64 + (g.nkb + 63) / 64);
+    }
+    p.q_tiles = (max_nq + 127) / 128;
+    const int ctas = p.n * p.q_tiles;
+    p.splits = std::max(1, std::min(p.max_tiles, sms / std::max(1, ctas)));
+    if (const char *e = getenv("OXY_ATTN_TC_SPLITS")) p.splits = std::max(1, std::min(p.max_tiles, atoi(e)));
+    if (p.splits > 1) {
+      attn_ws_need = std::max(attn_ws_need, (size_t)p.splits * p.rows * 256);
+      attn_ml_need = std::max(attn_ml_need, (size_t)p.splits * p.rows * 2);
+    }
+    return p;
+  }
+  void attend_tc(const AttnPlan &p, int layer, const bf16 *q_base, int q_rows, const bf16 *kd, const bf16 *vd,
+                 int kd_rows) {
+    if (!p.n) return;
+    float *wo = nullptr, *wml = nullptr;
+    if (p.splits > 1) {
+      wo = attn_ws.as<float>((size_t)p.splits * p.rows * 256);
+      wml = attn_ml.as<float>((size_t)p.splits * p.rows * 2);
+    }
+    flash_attention_tc(p.groups, p.n, p.q_tiles, p.splits, q_base, q_rows, kv_maps[2 * layer], kv_maps[2 * layer + 1],
+                       kd, vd, kd_rows, 1.f / 16.f, wo, wml, p.rows, mst);
+    if (p.splits > 1) flash_merge(p.groups, p.n, p.q_tiles * 128, p.splits, wo, wml, p.rows, mst);
+  }
+
   void reserve_common() {
     if (ws_need) ws.as<float>(ws_need);
     if (attn_ws_need) attn_ws.as<float>(attn_ws_need);
@@ -603,7 +642,7 @@ struct Model {
       g_llm[i].nq = P[i] * Q_HEADS;
       g_llm[i].nka = P[i];
     }
-    AttnPlan a_llm = shape_attention(g_llm, HEAD_DIM), a_vit;
+    AttnPlan a_llm = use_attn_tc ? shape_attention_tc(g_llm) : shape_attention(g_llm, HEAD_DIM), a_vit;
     if (Tv) {
       patches.as<bf16>((size_t)Tv * PATCH_K);
       vit_h.as<float>((size_t)Tv * Dv);
@@ -704,7 +743,8 @@ struct Model {
         rmsnorm(X, W, Y, W, w.ln1, nullptr, nullptr, T, W, 1e-6f, mst);
         gemm_qkv(w.wqkv, Y, W, T, d_pos, d_slot, Qb, kpool(l), vpool(l));
         if (l == c.depth - 1) break;  // the last block's output is not cached
-        attend(a_llm, kpool(l), vpool(l));
+        if (use_attn_tc) attend_tc(a_llm, l, Qb, T * Q_HEADS, nullptr, nullptr, 0);
+        else attend(a_llm, kpool(l), vpool(l));
         gemm(w.wo, Ob, W, QDIM, T, gemm::EPI_ADD_F32, X, W);
         rmsnorm(X, W, Y, W, w.ln2, nullptr, nullptr, T, W, 1e-6f, mst);
         gemm(w.wgu, Y, 2 * c.mlp, W, T, gemm::EPI_GEGLU_BF16, Hm, c.mlp);
@@ -788,7 +828,7 @@ struct Model {
       groups[i].nka = P[i];
       groups[i].nkb = H;
     }
-    AttnPlan ap = shape_attention(groups, HEAD_DIM);
+    AttnPlan ap = (use_attn_tc && !use_mk) ? shape_attention_tc(groups) : shape_attention(groups, HEAD_DIM);
     if (use_mk) {
       const char *e = getenv("OXY_MK_ATTN_TILES");  // key tiles per split item
       const int per = std::max(1, e ? atoi(e) : 2);
@@ -865,7 +905,8 @@ struct Model {
           const float *m = ms + (size_t)l * 6 * We;
           const float *mn = l + 1 < c.depth ? m + 6 * We : mf;  // the norm that follows this layer
           gemm_qkv(w.wqkv, Y, We, T, d_pos, nullptr, Qb, Kd, Vd);
-          attend(ap, kpool(l), vpool(l));
+          if (use_attn_tc) attend_tc(ap, l, Qb, T * Q_HEADS, Kd, Vd, T);
+          else attend(ap, kpool(l), vpool(l));
           gemm_res_norm(w.wo, Ob, We, QDIM, T, m + 2 * We, X, Y, nullptr, m + 3 * We, m + 4 * We);
           gemm(w.wgu, Y, 2 * c.expert_mlp, We, T, gemm::EPI_GEGLU_BF16, Hm, c.expert_mlp);
           gemm_res_norm(w.wd, Hm, We, c.expert_mlp, T, m + 5 * We, X, Y, nullptr, mn, mn + We);
