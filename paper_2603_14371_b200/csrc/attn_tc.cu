@@ -75,6 +75,29 @@ __device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t (&v)[1
 }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+#ifdef OXY_WATCHDOG
+// debug builds: a wait that exceeds ~2 s reports who waits on what, then traps
+__device__ __forceinline__ void wd_wait(uint32_t bar, uint32_t parity, int tag) {
+  const long long t0 = clock64();
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\tselp.u32 %0, 1, 0, P1;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (!ok && clock64() - t0 > 4000000000ll) {
+      printf("flash_tc hang: cta (%d,%d) thread %d tag %d parity %u\n", blockIdx.x, blockIdx.y, threadIdx.x, tag,
+             parity);
+      asm volatile("trap;");
+    }
+  }
+}
+#define MBW(bar, par, tag) wd_wait(bar, par, tag)
+#else
+#define MBW(bar, par, tag) mbar_wait(bar, par)
+#endif
+
 struct TcAttnArgs {
   const AttnGroup *groups;
   int q_tiles, splits, ws_rows;
@@ -140,7 +163,7 @@ __global__ void __launch_bounds__(192, 1)
       const int drow0 = g.kb ? (int)((g.kb - a.kd_base) / HD) : 0;
       for (int i = 0; i < n; ++i) {
         const int j = t0 + i, s = i & 1;
-        mbar_wait(b_kve + 8 * s, ((i >> 1) & 1) ^ 1);
+        MBW(b_kve + 8 * s, ((i >> 1) & 1) ^ 1, 1);
         mbar_expect_tx(b_kvf + 8 * s, 2 * KV_BYTES);
         const bool paged = j < ta;
         const int row = paged ? g.bt[j] * TK : drow0 + (j - ta) * TK;
@@ -159,9 +182,9 @@ __global__ void __launch_bounds__(192, 1)
       const uint32_t idesc_o = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(HD >> 3) << 17) |
                                ((uint32_t)(TQ >> 4) << 24);
       const uint32_t q_s = smem_u32(sm), p_s = smem_u32(sm + OFF_P);
-      mbar_wait(b_q, 0);
+      MBW(b_q, 0, 2);
       auto issue_pv = [&](int i) {
-        mbar_wait(b_pf, i & 1);
+        MBW(b_pf, i & 1, 3);
         tc_fence_after();
         const uint32_t v_s = smem_u32(sm + OFF_V + (i & 1) * KV_BYTES);
 #pragma unroll
@@ -173,8 +196,8 @@ __global__ void __launch_bounds__(192, 1)
       };
       for (int i = 0; i < n; ++i) {
         const int s = i & 1;
-        mbar_wait(b_kvf + 8 * s, (i >> 1) & 1);
-        mbar_wait(b_se + 8 * s, ((i >> 1) & 1) ^ 1);
+        MBW(b_kvf + 8 * s, (i >> 1) & 1, 4);
+        MBW(b_se + 8 * s, ((i >> 1) & 1) ^ 1, 5);
         tc_fence_after();
         const uint32_t k_s = smem_u32(sm + OFF_K + s * KV_BYTES);
         const uint32_t d_s = tmem + 256 + s * TK;
@@ -198,7 +221,7 @@ __global__ void __launch_bounds__(192, 1)
     for (int i = 0; i < n; ++i) {
       const int j = t0 + i, s = i & 1;
       const int nvalid = j < ta ? min(TK, g.nka - j * TK) : min(TK, g.nkb - (j - ta) * TK);
-      mbar_wait(b_sf + 8 * s, (i >> 1) & 1);
+      MBW(b_sf + 8 * s, (i >> 1) & 1, 6);
       tc_fence_after();
       float sc[TK];
       {
@@ -238,9 +261,11 @@ __global__ void __launch_bounds__(192, 1)
       l = l * corr + rs;
       // PV(i-1) must be complete before O is rescaled and before P is overwritten
       if (i > 0) {
-        mbar_wait(b_od, (i - 1) & 1);
+        MBW(b_od, (i - 1) & 1, 7);
         tc_fence_after();
-        if (corr != 1.f) {
+        // tcgen05.ld/st are warp-collective: rescale the warp's 32 rows together
+        // whenever any of them needs it (rows that do not multiply by 1)
+        if (__any_sync(0xffffffffu, corr != 1.f)) {
           for (int c = 0; c < HD; c += 16) {
             uint32_t v[16];
             tmem_ld16_nowait(tmem + lanes + c, v);
@@ -263,7 +288,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     // epilogue
     if (n > 0) {
-      mbar_wait(b_od, (n - 1) & 1);
+      MBW(b_od, (n - 1) & 1, 8);
       tc_fence_after();
     }
     const bool ok = r < g.nq;
