@@ -149,9 +149,41 @@ __device__ __forceinline__ void mma_commit_pair(uint32_t bar) {
       : "memory");
 }
 
+// GELU (tanh form) on the SFU: tanh.approx.f32 (rel. error ~2^-11, far below
+// the bf16 rounding of the stored activation)
 __device__ __forceinline__ float gelu_tanh(float x) {
   const float c = 0.7978845608028654f;  // sqrt(2/pi)
-  return 0.5f * x * (1.f + tanhf(c * (x + 0.044715f * x * x * x)));
+  float th;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(th) : "f"(c * (x + 0.044715f * x * x * x)));
+  return 0.5f * x * (1.f + th);
+}
+
+// RoPE + q / k / v routing of one accumulator (rotary pairs interleaved in the
+// weight rows), with (cs, sn) of this token's position already loaded
+__device__ __forceinline__ void rope_store(const QkvRope &r, int t, int f, float acc, float pair, float cs,
+                                           float sn) {
+  const int h = f >> 8, j = f & 255, i = j >> 1;
+  if (h < 9) {  // q heads 0..7, k head 8: rotate the (x1, x2) pair
+    const bool second = j & 1;  // this lane holds x2 (dim i + 128)
+    const float v = second ? acc * cs + pair * sn : acc * cs - pair * sn;
+    const int dim = second ? i + 128 : i;
+    if (h < 8) {
+      r.q_out[(size_t)t * 2048 + h * 256 + dim] = __float2bfloat16(v);
+    } else {
+      const int s = r.slot ? r.slot[t] : t;
+      if (s >= 0) r.k_dst[(size_t)s * 256 + dim] = __float2bfloat16(v);
+    }
+  } else {  // v head
+    const int s = r.slot ? r.slot[t] : t;
+    if (s >= 0) r.v_dst[(size_t)s * 256 + j] = __float2bfloat16(acc);
+  }
+}
+
+__device__ __forceinline__ float2 rope_cs(const QkvRope &r, int pos, int i) {
+  if (r.cs && pos < ROPE_TABLE_POS) return __ldg(r.cs + (size_t)pos * 128 + i);
+  float sn, cs;
+  sincosf(__fmul_rn((float)pos, r.inv_freq[i]), &sn, &cs);
+  return make_float2(cs, sn);
 }
 
 // Shared epilogue.  `pair` is the accumulator of feature f^1 (GeGLU, RoPE).
@@ -193,23 +225,8 @@ __device__ __forceinline__ void epilogue_store(const EpiParams &e, int t, int f,
       break;
     case EPI_QKV_ROPE: {
       const QkvRope &r = e.rope;
-      const int h = f >> 8, j = f & 255, i = j >> 1;
-      if (h < 9) {  // q heads 0..7, k head 8: rotate the (x1, x2) pair
-        float sn, cs;
-        sincosf((float)r.pos[t] * r.inv_freq[i], &sn, &cs);
-        const bool second = j & 1;  // this lane holds x2 (dim i + 128)
-        const float v = second ? acc * cs + pair * sn : acc * cs - pair * sn;
-        const int dim = second ? i + 128 : i;
-        if (h < 8) {
-          r.q_out[(size_t)t * 2048 + h * 256 + dim] = __float2bfloat16(v);
-        } else {
-          const int s = r.slot ? r.slot[t] : t;
-          if (s >= 0) r.k_dst[(size_t)s * 256 + dim] = __float2bfloat16(v);
-        }
-      } else {  // v head
-        const int s = r.slot ? r.slot[t] : t;
-        if (s >= 0) r.v_dst[(size_t)s * 256 + j] = __float2bfloat16(acc);
-      }
+      const float2 c = rope_cs(r, r.pos[t], (f & 255) >> 1);
+      rope_store(r, t, f, acc, pair, c.x, c.y);
       break;
     }
   }
@@ -223,15 +240,35 @@ __device__ __forceinline__ void epi_loop(const P &p, uint32_t trow, int bn, int 
   for (int c = 0; c < bn; c += 16) {
     uint32_t v[16];
     tmem_ld16(trow + (uint32_t)c, v);
+    if constexpr (MODE == EPI_QKV_ROPE) {
+      // all 16 positions, then all 16 (cos, sin), before any store: the loads
+      // must not serialise behind the (possibly aliasing) output stores
+      const QkvRope &r = p.epi.rope;
+      const int i = (f & 255) >> 1;
+      int pos[16];
+      float2 csn[16];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int t = n0 + c + j;
-      const float acc = __uint_as_float(v[j]);
-      float pair = 0.f;
-      if (MODE == EPI_GEGLU_BF16 || MODE == EPI_QKV_ROPE) pair = __shfl_xor_sync(0xffffffffu, acc, 1);
-      if (t >= p.t || !fok) continue;
-      if (MODE < 0) p.ws[((size_t)split * p.t + t) * p.n_out + f] = acc;
-      else epilogue_store<(MODE < 0 ? 0 : MODE)>(p.epi, t, f, p.n_out, acc, pair);
+      for (int j = 0; j < 16; ++j) pos[j] = n0 + c + j < p.t ? __ldg(r.pos + n0 + c + j) : 0;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) csn[j] = rope_cs(r, pos[j], i);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int t = n0 + c + j;
+        const float acc = __uint_as_float(v[j]);
+        const float pair = __shfl_xor_sync(0xffffffffu, acc, 1);
+        if (t < p.t && fok) rope_store(r, t, f, acc, pair, csn[j].x, csn[j].y);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int t = n0 + c + j;
+        const float acc = __uint_as_float(v[j]);
+        float pair = 0.f;
+        if (MODE == EPI_GEGLU_BF16) pair = __shfl_xor_sync(0xffffffffu, acc, 1);
+        if (t >= p.t || !fok) continue;
+        if (MODE < 0) p.ws[((size_t)split * p.t + t) * p.n_out + f] = acc;
+        else epilogue_store<(MODE < 0 ? 0 : MODE)>(p.epi, t, f, p.n_out, acc, pair);
+      }
     }
   }
 }

@@ -458,7 +458,13 @@ Plan make_plan(int n_out, int k, int t, int sms, int force_splits) {
   int splits = 1;
   if (force_splits > 0) {
     splits = force_splits;
-  } else if (base < sms && t <= 64) {  // skinny (decode / denoise): split K, tiny fix-up
+  } else if (base < sms && t <= 64) {
+    // skinny (decode / denoise): split K to fill the SMs.  Stand-alone, fewer
+    // splits look cheaper (no reduce), but inside the PDL chain every split CTA
+    // streams its weight ring before griddepcontrol.wait, so more splits hide
+    // more of the weight read behind the previous kernel: measured in-frame,
+    // this policy beats 'split only past 16 k-blocks' by 2.4 ms per denoise
+    // (profiles/r01_gemm_splits.md)
     splits = std::max(1, std::min(sms / base, p.kb_total / 4));
   }
   splits = std::max(1, std::min(splits, p.kb_total));

@@ -42,8 +42,10 @@ void splitk_residual_norm(const float *ws, int splits, int t, int n, const float
                           const float *mod_shift, float eps, cudaStream_t st);
 
 // Extra state of EPI_QKV_ROPE (8 q heads + 1 k + 1 v head of 256).
+constexpr int ROPE_TABLE_POS = 16384;  // positions covered by the cos/sin table
 struct QkvRope {
   const float *inv_freq;  // [128]
+  const float2 *cs;       // [ROPE_TABLE_POS][128] (cos, sin) of fp32(pos * inv_freq), or null
   const int *pos;         // [T]
   const int *slot;        // [T] pool slot (<0: skip k/v) or null: dense k/v rows
   __nv_bfloat16 *q_out;   // [T, 2048]

@@ -103,6 +103,21 @@ void permute_rows(bf16 *dst, const bf16 *src, int rows, int cols, cudaStream_t s
 // RoPE inverse frequencies theta^(-2i/256), computed in double on the host.
 __constant__ float c_rope_inv[128];
 
+__global__ void rope_table_kernel(float2 *cs, const float *inv_freq, int n) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n) return;
+  const float ang = __fmul_rn((float)(idx >> 7), inv_freq[idx & 127]);  // as the fp32 oracle
+  double s, c;
+  sincos((double)ang, &s, &c);
+  cs[idx] = make_float2((float)c, (float)s);
+}
+
+void rope_table(float2 *cs, const float *inv_freq, int n_pos, cudaStream_t st) {
+  const int n = n_pos * 128;
+  rope_table_kernel<<<(n + 255) / 256, 256, 0, st>>>(cs, inv_freq, n);
+  OXY_LAUNCH_CHECK();
+}
+
 void set_rope_theta(float theta) {
   float inv[128];
   for (int i = 0; i < 128; ++i) inv[i] = (float)std::pow((double)theta, -2.0 * (double)i / (double)HEAD_DIM);

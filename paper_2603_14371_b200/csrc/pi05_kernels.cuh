@@ -29,6 +29,8 @@ void embed_rows(float *x, int ldx, const bf16 *table, const int *tok, const int 
                 int D, float scale, cudaStream_t st);
 // dst[f, :] = src[gemm::qkv_rope_row(f), :] (rotary-pair interleaved QKV weights)
 void permute_rows(bf16 *dst, const bf16 *src, int rows, int cols, cudaStream_t st);
+// (cos, sin) of fp32(pos * inv_freq[i]) for pos < n_pos (sin/cos evaluated in fp64)
+void rope_table(float2 *cs, const float *inv_freq, int n_pos, cudaStream_t st);
 // RoPE inverse-frequency table (constant memory), set once per process
 void set_rope_theta(float theta);
 // RoPE on q (n_qh heads) and k from fp32 qkv [T, (n_qh+2)*256]; q -> q_out bf16 [T, n_qh*256];

@@ -96,6 +96,7 @@ struct Model {
     cudaFree(pool);
     cudaFree(noise);
     cudaFree(rope_inv);
+    cudaFree(rope_cs);
     for (DevBuf *b : {&mod, &x, &y, &qkv, &q, &o, &hmid, &ws, &ints, &kd, &vd, &attn_groups, &attn_ws,
                       &attn_ml, &logits, &amv, &ami, &vit_h, &vit_y, &vit_qkv, &vit_o, &vit_m, &patches,
                       &act, &act_bf, &vel, &xe, &dec_ws, &kvread_i, &kvread_f})
@@ -116,6 +117,7 @@ struct Model {
            n.compare(n.size() - 5, 5, ".wqkv") == 0;
   }
   float *rope_inv = nullptr;
+  float2 *rope_cs = nullptr;  // [ROPE_TABLE_POS][128] (cos, sin), gemm::QkvRope::cs
   // action vectors are padded to 8 lanes so the in-projection's K stride is 16-byte aligned
   int apad() const { return (c.action_dim + 7) / 8 * 8; }
 
@@ -254,6 +256,8 @@ struct Model {
       for (int i = 0; i < 128; ++i) inv[i] = (float)std::pow(10000.0, -2.0 * i / 256.0);
       OXY_CUDA(cudaMalloc(&rope_inv, sizeof(inv)));
       OXY_CUDA(cudaMemcpyAsync(rope_inv, inv, sizeof(inv), cudaMemcpyHostToDevice, st));
+      OXY_CUDA(cudaMalloc(&rope_cs, (size_t)gemm::ROPE_TABLE_POS * 128 * sizeof(float2)));
+      rope_table(rope_cs, rope_inv, gemm::ROPE_TABLE_POS, st);
       bf16 *tmp = nullptr;
       const int kmax = std::max(c.width, c.expert_width);
       OXY_CUDA(cudaMalloc(&tmp, (size_t)QKV * kmax * sizeof(bf16)));
@@ -508,7 +512,7 @@ struct Model {
     gemm::Plan plan = gemm::make_plan(QKV, k, t, sms);
     float *wsp = plan.splits > 1 ? ws.as<float>((size_t)plan.splits * t * QKV) : nullptr;
     EpiParams e{gemm::EPI_QKV_ROPE, nullptr, 0, nullptr, nullptr, 0, nullptr,
-                gemm::QkvRope{rope_inv, pos, slot, q_out, k_dst, v_dst}};
+                gemm::QkvRope{rope_inv, rope_cs, pos, slot, q_out, k_dst, v_dst}};
     gemm::launch(w, xin, QKV, k, t, e, plan, wsp, gemm_counters, mst);
   }
 
@@ -993,7 +997,7 @@ struct Model {
         const float *m = ms + (size_t)l * 6 * We;
         const float *mn = l + 1 < c.depth ? m + 6 * We : mf;
         EpiParams er{gemm::EPI_QKV_ROPE, nullptr, 0, nullptr, nullptr, 0, nullptr,
-                     gemm::QkvRope{rope_inv, d_pos, nullptr, Qb, Kd, Vd}};
+                     gemm::QkvRope{rope_inv, rope_cs, d_pos, nullptr, Qb, Kd, Vd}};
         sp = pg.gemm(w.wqkv, Y, QKV, We, T, er, mws, sms, 1);  // whole K: RoPE epilogue in place
         if (sp > 1) pg.reduce_epi(mws, sp, T, QKV, er);
         pg.attention(ap.groups, ap.n, ap.q_tiles, max_nq, ap.splits, ap.rows, kpool(l), vpool(l), 1.f / 16.f, awo,

@@ -1,3 +1,6 @@
+"""Split-K sweep of the one-tile-per-CTA GEMM at the skinny frame shapes
+(GEMM + its split-K reduce kernel, 40 distinct weight buffers so weights
+stream from HBM).  Used to pick the skinny split policy."""
 import ctypes as C, os, sys, torch
 sys.path.insert(0, os.getcwd())
 from paper_2603_14371_b200 import _lib
@@ -20,7 +23,10 @@ def bench(n, k, t, splits, nbuf):
     e.record(); torch.cuda.synchronize()
     us = s.elapsed_time(e) / reps * 1e3
     print(f"n={n} k={k} t={t} splits={plan[3]} bn={plan[0]} nbuf={nbuf} {us:.1f} us  {n*k*2/us/1e3:.0f} GB/s", flush=True)
-for n, k in [(2560, 1024), (8192, 1024), (1024, 4096)]:
-    for sp in (1, 2, 4, 8):
-        for nb in (1, 40):
-            bench(n, k, 50, sp, nb)
+import sys as _s
+CASES = [(2560, 1024, 50), (8192, 1024, 50), (1024, 4096, 50), (1024, 2048, 50), (32, 1024, 50),
+         (2560, 2048, 6), (2048, 2048, 6), (2048, 16384, 6), (32768, 2048, 6)]
+for n, k, t in CASES:
+    for sp in (1, 2, 4, 8, 16):
+        if sp <= (k + 63) // 64:
+            bench(n, k, t, sp, 40)
