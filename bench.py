@@ -215,6 +215,16 @@ def timed(ws, backend, frames, warmup, k):
 
 # ----------------------------------------------------------------- kernel rooflines
 
+def ncu_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the roofline
+    kernels, from one committed `ncu --set full` capture (tools/profile_all.sh)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
 def kernel_rooflines(backend, m_decode):
     """CUDA-event timings of single kernels at the frame's shapes."""
     import ctypes as C
@@ -224,6 +234,10 @@ def kernel_rooflines(backend, m_decode):
     cfg = backend.config
     st = torch.cuda.current_stream()
     out = {}
+    tr = ncu_traffic()
+
+    def traffic(key):
+        return tr[key]["traffic_bytes"] if key in tr else None
 
     def time_launches(fn, n=20, warm=3):
         for _ in range(warm):
@@ -256,8 +270,8 @@ def kernel_rooflines(backend, m_decode):
     sec = time_launches(fn)
     byts = n * kk * 2 + t * kk * 2 + t * n * 4
     out["gemm_lm_head"] = {"bound": "hbm", "achieved": byts / sec / 1e9, "peak": hbm, "unit": "GB/s",
-                           "frac": byts / sec / 1e9 / hbm, "traffic": None,
-                           "shape": f"{n}x{kk} bf16 weights, T={t}", "us": sec * 1e6,
+                           "frac": byts / sec / 1e9 / hbm, "traffic": traffic("lm_head"),
+                           "algorithmic_bytes": byts, "shape": f"{n}x{kk} bf16 weights, T={t}", "us": sec * 1e6,
                            "peak_kind": kind}
     del w, x, o, keep
     # 2. prefill FFN gate/up GEMM (tensor-bound): [2*mlp, width] x [800 tokens]
@@ -270,7 +284,7 @@ def kernel_rooflines(backend, m_decode):
     flops = 2.0 * n * kk * t
     out["gemm_prefill_ffn"] = {"bound": "tensor", "achieved": flops / sec / 1e12, "peak": tf_burst,
                                "unit": "TFLOP/s", "frac": flops / sec / 1e12 / tf_burst,
-                               "traffic": None, "shape": f"{n}x{kk} x T={t}", "us": sec * 1e6,
+                               "traffic": traffic("prefill_gu"), "shape": f"{n}x{kk} x T={t}", "us": sec * 1e6,
                                "peak_kind": kind + " burst"}
     del w, x, o, keep
     # 3. paged decode attention: 64 rows x 1024-position contexts (MQA 8q/1kv, hd 256)
@@ -291,8 +305,8 @@ def kernel_rooflines(backend, m_decode):
     sec = time_launches(lambda: _lib.call("oxy_paged_decode_attention", *args))
     byts = rows * ctx * 256 * 2 * 2 + rows * 2048 * 2 * 2
     out["decode_attention"] = {"bound": "hbm", "achieved": byts / sec / 1e9, "peak": hbm,
-                               "unit": "GB/s", "frac": byts / sec / 1e9 / hbm, "traffic": None,
-                               "shape": f"{rows} rows x {ctx} ctx, 8q/1kv hd256 (incl. merge)",
+                               "unit": "GB/s", "frac": byts / sec / 1e9 / hbm, "traffic": traffic("decode_attn"),
+                               "algorithmic_bytes": byts, "shape": f"{rows} rows x {ctx} ctx, 8q/1kv hd256 (incl. merge)",
                                "us": sec * 1e6, "peak_kind": kind}
     return out
 

@@ -34,7 +34,7 @@ struct Knobs {
   // early PDL (weight prefetch + trigger) for skinny / wide GEMMs: -1 = default policy
   int early_skinny = 1, early_wide = 0;
   // persistent wide kernel for T > 64: -1 auto (cost model), 0 off, 1 / 2 force CTA group
-  int wide = 0, wide_bn = 0, wide_splits = 0;  // off: measured slower in-frame (profiles/r01_gemm_wide.md)
+  int wide = 0, wide_bn = 0, wide_splits = 0;  // 0: off, -1: gate/up-sized shapes only (profiles/r01_gemm_wide.md)
   Knobs() {
     if (const char *s = getenv("OXY_GEMM_WIDE")) wide = atoi(s);
     if (const char *s = getenv("OXY_GEMM_WIDE_BN")) wide_bn = atoi(s);
@@ -414,7 +414,6 @@ static double wide_cost(int n_out, int kb_total, int t, int sms, int cg, int bn,
 
 static bool wide_plan(Plan &p, int n_out, int k, int t, int sms) {
   const Knobs &kn = knobs();
-  if (kn.wide == 0) return false;
   double best = 1e30;
   for (int cg = 1; cg <= 2; ++cg) {
     if (kn.wide > 0 && cg != kn.wide) continue;
@@ -445,7 +444,11 @@ static bool wide_plan(Plan &p, int n_out, int k, int t, int sms) {
 Plan make_plan(int n_out, int k, int t, int sms, int force_splits) {
   Plan p{};
   p.kb_total = (k + BK - 1) / BK;
-  if (t > 64 && force_splits <= 0 && wide_plan(p, n_out, k, t, sms)) return p;
+  // persistent 2-CTA kernel: measured faster in-frame only for the wide gate/up
+  // projections (1010-1037 vs 843 TF/s at 32768x2048, T = 800); OXY_GEMM_WIDE
+  // overrides (0 off, 1 / 2 force the CTA group for every T > 64 GEMM)
+  const bool wide_ok = knobs().wide > 0 || (knobs().wide < 0 && n_out >= 16384 && t >= 256);
+  if (t > 64 && force_splits <= 0 && wide_ok && wide_plan(p, n_out, k, t, sms)) return p;
   p.cg = 0;
   p.m_tiles = (n_out + BM - 1) / BM;
   p.n_tiles = (t + MAX_BN - 1) / MAX_BN;
