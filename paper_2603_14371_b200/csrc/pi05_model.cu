@@ -360,10 +360,10 @@ struct Model {
     ~LaneSwap() { m.swap_lane(m.alt); }
   };
 
-  void init_lane() {
+  void init_lane(int priority) {
     OXY_CUDA(cudaMalloc(&gemm_counters, gemm::MAX_TILES * sizeof(int)));
     OXY_CUDA(cudaMemset(gemm_counters, 0, gemm::MAX_TILES * sizeof(int)));
-    OXY_CUDA(cudaStreamCreateWithFlags(&mst, cudaStreamNonBlocking));
+    OXY_CUDA(cudaStreamCreateWithPriority(&mst, cudaStreamNonBlocking, priority));
     OXY_CUDA(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
     OXY_CUDA(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
     arena_cap = 8u << 20;
@@ -382,10 +382,17 @@ struct Model {
   void init_exec() {
     OXY_CUDA(cudaMalloc(&dec_counters, MAX_DECODE_ROWS * sizeof(int)));
     OXY_CUDA(cudaMemset(dec_counters, 0, MAX_DECODE_ROWS * sizeof(int)));
-    init_lane();
+    // The action-expert lane gets the highest stream priority: its denoise is a
+    // latency-bound chain of small kernels, the concurrent language decode is
+    // bandwidth-bound and fills whatever SMs the chain leaves (OXY_LANE_PRIO=0: equal)
+    int lo = 0, hi = 0;
+    OXY_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    const char *e = getenv("OXY_LANE_PRIO");
+    const bool prio = !e || atoi(e) != 0;
+    init_lane(lo);
     {
       LaneSwap g(*this);
-      init_lane();
+      init_lane(prio ? hi : lo);
     }
     OXY_CUDA(cudaEventCreate(&alt.t0));
     OXY_CUDA(cudaEventCreate(&alt.t1));
