@@ -235,9 +235,9 @@ __device__ __forceinline__ void epilogue_store(const EpiParams &e, int t, int f,
 // Epilogue over this thread's output feature f and the tile's BN token columns
 // (TMEM lane = f).  MODE < 0 writes split-K partials.
 template <int MODE, typename P>
-__device__ __forceinline__ void epi_loop(const P &p, uint32_t trow, int bn, int n0, int f, int split) {
+__device__ __forceinline__ void epi_loop(const P &p, uint32_t trow, int c_begin, int c_end, int n0, int f, int split) {
   const bool fok = f < p.n_out;
-  for (int c = 0; c < bn; c += 16) {
+  for (int c = c_begin; c < c_end; c += 16) {
     uint32_t v[16];
     tmem_ld16(trow + (uint32_t)c, v);
     if constexpr (MODE == EPI_QKV_ROPE) {
@@ -273,61 +273,68 @@ __device__ __forceinline__ void epi_loop(const P &p, uint32_t trow, int bn, int 
   }
 }
 
-// the mode switch sits outside the column loop: one tight loop per epilogue
+// the mode switch sits outside the column loop: one tight loop per epilogue.
+// Columns [c_begin, c_end) of the tile (multiples of 16).
 template <typename P>
-__device__ __forceinline__ void epi_tile(const P &p, uint32_t trow, int bn, int n0, int f, int split, bool split_out) {
+__device__ __forceinline__ void epi_tile(const P &p, uint32_t trow, int c_begin, int c_end, int n0, int f, int split,
+                                         bool split_out) {
   switch (split_out ? -1 : p.epi.mode) {
-    case -1: epi_loop<-1>(p, trow, bn, n0, f, split); break;
-    case EPI_F32: epi_loop<EPI_F32>(p, trow, bn, n0, f, split); break;
-    case EPI_BF16: epi_loop<EPI_BF16>(p, trow, bn, n0, f, split); break;
-    case EPI_ADD_F32: epi_loop<EPI_ADD_F32>(p, trow, bn, n0, f, split); break;
-    case EPI_GEGLU_BF16: epi_loop<EPI_GEGLU_BF16>(p, trow, bn, n0, f, split); break;
-    case EPI_GELU_BF16: epi_loop<EPI_GELU_BF16>(p, trow, bn, n0, f, split); break;
-    case EPI_ADD_BF16: epi_loop<EPI_ADD_BF16>(p, trow, bn, n0, f, split); break;
-    case EPI_ADD_GATED_F32: epi_loop<EPI_ADD_GATED_F32>(p, trow, bn, n0, f, split); break;
-    case EPI_SWISH_BF16: epi_loop<EPI_SWISH_BF16>(p, trow, bn, n0, f, split); break;
-    case EPI_QKV_ROPE: epi_loop<EPI_QKV_ROPE>(p, trow, bn, n0, f, split); break;
+    case -1: epi_loop<-1>(p, trow, c_begin, c_end, n0, f, split); break;
+    case EPI_F32: epi_loop<EPI_F32>(p, trow, c_begin, c_end, n0, f, split); break;
+    case EPI_BF16: epi_loop<EPI_BF16>(p, trow, c_begin, c_end, n0, f, split); break;
+    case EPI_ADD_F32: epi_loop<EPI_ADD_F32>(p, trow, c_begin, c_end, n0, f, split); break;
+    case EPI_GEGLU_BF16: epi_loop<EPI_GEGLU_BF16>(p, trow, c_begin, c_end, n0, f, split); break;
+    case EPI_GELU_BF16: epi_loop<EPI_GELU_BF16>(p, trow, c_begin, c_end, n0, f, split); break;
+    case EPI_ADD_BF16: epi_loop<EPI_ADD_BF16>(p, trow, c_begin, c_end, n0, f, split); break;
+    case EPI_ADD_GATED_F32: epi_loop<EPI_ADD_GATED_F32>(p, trow, c_begin, c_end, n0, f, split); break;
+    case EPI_SWISH_BF16: epi_loop<EPI_SWISH_BF16>(p, trow, c_begin, c_end, n0, f, split); break;
+    case EPI_QKV_ROPE: epi_loop<EPI_QKV_ROPE>(p, trow, c_begin, c_end, n0, f, split); break;
   }
 }
 
-// Deterministic split-K fix-up, run by the 4 epilogue warps (named barrier 1)
-// after they wrote this CTA's partials: the last CTA of the tile to arrive sums
-// the partials in split order 0..S-1 and applies the epilogue.
+// Deterministic split-K fix-up, run by the epilogue warps (named barrier 1 over
+// bar_threads threads; `leader` does the tile-counter atomic) after they wrote
+// this CTA's partials: the last CTA of the tile to arrive sums the partials in
+// split order 0..S-1 (columns [c_begin, c_end) of feature f per thread) and
+// applies the epilogue.  16 columns x up to 4 splits of loads are in flight.
 template <typename P>
-__device__ __forceinline__ void splitk_fixup(const P &p, int tile, int n0, int bn, int f, int &s_last) {
+__device__ __forceinline__ void splitk_fixup(const P &p, int tile, int n0, int c_begin, int c_end, int f, int &s_last,
+                                             int bar_threads, int leader) {
   __threadfence();
-  asm volatile("bar.sync 1, 128;" ::: "memory");
-  if (threadIdx.x == 64) s_last = atomicAdd(p.counters + tile, 1) == p.splits - 1;
-  asm volatile("bar.sync 1, 128;" ::: "memory");
+  asm volatile("bar.sync 1, %0;" ::"r"(bar_threads) : "memory");
+  if ((int)threadIdx.x == leader) s_last = atomicAdd(p.counters + tile, 1) == p.splits - 1;
+  asm volatile("bar.sync 1, %0;" ::"r"(bar_threads) : "memory");
   if (s_last) {
     __threadfence();
-    const int ncols = min(bn, p.t - n0);
+    const int ce = min(c_end, p.t - n0);
     const bool fok = f < p.n_out;
-    for (int c0 = 0; c0 < ncols; c0 += 4) {
-      float acc[4] = {0.f, 0.f, 0.f, 0.f};
-      for (int s0 = 0; s0 < p.splits; s0 += 8) {
-        float v[8][4];  // 32 independent L2 loads in flight per thread
+    for (int c0 = c_begin; c0 < ce; c0 += 16) {
+      float acc[16];
 #pragma unroll
-        for (int s = 0; s < 8; ++s)
+      for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+      for (int s0 = 0; s0 < p.splits; s0 += 4) {
+        float v[4][16];
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
-            v[s][j] = (fok && s0 + s < p.splits && c0 + j < ncols)
+        for (int s = 0; s < 4; ++s)
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            v[s][j] = (fok && s0 + s < p.splits && c0 + j < ce)
                           ? __ldcg(p.ws + ((size_t)(s0 + s) * p.t + n0 + c0 + j) * p.n_out + f)
                           : 0.f;
 #pragma unroll
-        for (int s = 0; s < 8; ++s)
+        for (int s = 0; s < 4; ++s)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) acc[j] += v[s][j];  // split order 0..S-1
+          for (int j = 0; j < 16; ++j) acc[j] += v[s][j];  // split order 0..S-1
       }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < 16; ++j) {
         const float pair = __shfl_xor_sync(0xffffffffu, acc[j], 1);
-        if (fok && c0 + j < ncols) epilogue_store(p.epi, n0 + c0 + j, f, p.n_out, acc[j], pair);
+        if (fok && c0 + j < ce) epilogue_store(p.epi, n0 + c0 + j, f, p.n_out, acc[j], pair);
       }
     }
-    if (threadIdx.x == 64) p.counters[tile] = 0;
+    if ((int)threadIdx.x == leader) p.counters[tile] = 0;
   }
-  asm volatile("bar.sync 1, 128;" ::: "memory");  // s_last is reused by the next tile
+  asm volatile("bar.sync 1, %0;" ::"r"(bar_threads) : "memory");  // s_last is reused by the next tile
 }
 
 }  // namespace gemm

@@ -34,7 +34,7 @@ struct Knobs {
   // early PDL (weight prefetch + trigger) for skinny / wide GEMMs: -1 = default policy
   int early_skinny = 1, early_wide = 0;
   // persistent wide kernel for T > 64: -1 auto (cost model), 0 off, 1 / 2 force CTA group
-  int wide = 0, wide_bn = 0, wide_splits = 0;  // 0: off, -1: gate/up-sized shapes only (profiles/r01_gemm_wide.md)
+  int wide = -1, wide_bn = 0, wide_splits = 0;  // -1 auto (see make_plan), 0 off, 1 / 2 force
   Knobs() {
     if (const char *s = getenv("OXY_GEMM_WIDE")) wide = atoi(s);
     if (const char *s = getenv("OXY_GEMM_WIDE_BN")) wide_bn = atoi(s);
@@ -166,8 +166,8 @@ __global__ void __launch_bounds__(192, 2)
     const int f = m0 + q * 32 + lane;
     const bool split_out = p.splits > 1;
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
-    epi_tile(p, trow, bn, n0, f, split, split_out);
-    if (split_out && p.fixup) splitk_fixup(p, blockIdx.y * gridDim.x + blockIdx.x, n0, bn, f, s_last);
+    epi_tile(p, trow, 0, bn, n0, f, split, split_out);
+    if (split_out && p.fixup) splitk_fixup(p, blockIdx.y * gridDim.x + blockIdx.x, n0, 0, bn, f, s_last, 128, 64);
   }
   tc_fence_before();
   __syncthreads();
@@ -195,8 +195,10 @@ struct WParams {
   int *counters;  // one per (tile, CTA of the pair); self-resetting
 };
 
+constexpr int WIDE_THREADS = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue (2 per TMEM lane quadrant)
+
 template <int CG>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(WIDE_THREADS, 1)
     gemm_wide_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, WParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -225,7 +227,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull0 + 8 * a, 1);
-      mbar_init(tempty0 + 8 * a, 4 * CG);  // one arrival per epilogue warp of each CTA
+      mbar_init(tempty0 + 8 * a, 8 * CG);  // one arrival per epilogue warp of each CTA
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
@@ -317,7 +319,10 @@ __global__ void __launch_bounds__(192, 1)
     __syncwarp();
   } else {
     pdl_wait();  // the epilogue reads bias/residual/gates and writes outputs
-    const int q = warp & 3;
+    // two warps per TMEM lane quadrant, each taking half of the tile's 16-column chunks
+    const int q = warp & 3, half = (warp - 2) >> 2;
+    const int chunks = bn / 16, c_mid = ((chunks + 1) / 2) * 16;
+    const int cb = half ? c_mid : 0, ce = half ? bn : c_mid;
     const bool split_out = p.splits > 1;
     const uint32_t tempty_l = CG == 2 ? map_to_rank(tempty0, 0) : tempty0;
     int lt = 0;
@@ -329,7 +334,7 @@ __global__ void __launch_bounds__(192, 1)
       const int f = mt * BM * CG + (int)rank * BM + q * 32 + lane;
       const int n0 = nt * bn;
       const uint32_t trow = tmem + (uint32_t)acc * acc_stride + ((uint32_t)(q * 32) << 16);
-      epi_tile(p, trow, bn, n0, f, split, split_out);
+      epi_tile(p, trow, cb, ce, n0, f, split, split_out);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -337,7 +342,7 @@ __global__ void __launch_bounds__(192, 1)
         else mbar_arrive_local(tempty0 + 8 * acc);
       }
       if (split_out && p.epi.mode != EPI_PARTIALS)
-        splitk_fixup(p, (mt * p.n_tiles + nt) * CG + (int)rank, n0, bn, f, s_last);
+        splitk_fixup(p, (mt * p.n_tiles + nt) * CG + (int)rank, n0, cb, ce, f, s_last, WIDE_THREADS - 64, 64);
     }
   }
   if (threadIdx.x == 0) pdl_trigger();
@@ -444,10 +449,12 @@ static bool wide_plan(Plan &p, int n_out, int k, int t, int sms) {
 Plan make_plan(int n_out, int k, int t, int sms, int force_splits) {
   Plan p{};
   p.kb_total = (k + BK - 1) / BK;
-  // persistent 2-CTA kernel: measured faster in-frame only for the wide gate/up
-  // projections (1010-1037 vs 843 TF/s at 32768x2048, T = 800); OXY_GEMM_WIDE
-  // overrides (0 off, 1 / 2 force the CTA group for every T > 64 GEMM)
-  const bool wide_ok = knobs().wide > 0 || (knobs().wide < 0 && n_out >= 16384 && t >= 256);
+  // persistent 2-CTA kernel: in-frame it wins for the gate/up projections from
+  // T = 256 and for every projection once T >= 2048 (multi-stream prefill);
+  // at 1-stream T = 800 the narrower shapes stay on the one-tile-per-CTA kernel
+  // (profiles/r01_gemm_wide.md).  OXY_GEMM_WIDE: -1 auto, 0 off, 1 / 2 force.
+  const bool wide_ok =
+      knobs().wide > 0 || (knobs().wide < 0 && ((n_out >= 16384 && t >= 256) || t >= 2048));
   if (t > 64 && force_splits <= 0 && wide_ok && wide_plan(p, n_out, k, t, sms)) return p;
   p.cg = 0;
   p.m_tiles = (n_out + BM - 1) / BM;
@@ -520,7 +527,7 @@ static void launch_wide(const void *w, const void *x, int n_out, int k, int t, c
   const int units = std::min(wp.tiles, sms / cg);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(units * cg);
-  cfg.blockDim = dim3(192);
+  cfg.blockDim = dim3(WIDE_THREADS);
   cfg.dynamicSmemBytes = wide_smem_bytes(plan);
   cfg.stream = st;
   cudaLaunchAttribute attr[2];

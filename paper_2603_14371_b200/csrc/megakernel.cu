@@ -126,7 +126,7 @@ __device__ __forceinline__ void gemm_phase(const GemmPh &g, int items, uint8_t *
       tc_fence_after();
       const int f = mt * BM + q * 32 + lane;
       const uint32_t trow = tmem + (uint32_t)acc * MK_MAX_BN + ((uint32_t)(q * 32) << 16);
-      epi_tile(g, trow, bn, nt * bn, f, split, g.splits > 1);
+      epi_tile(g, trow, 0, bn, nt * bn, f, split, g.splits > 1);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_local(tempty0 + 8 * acc);
