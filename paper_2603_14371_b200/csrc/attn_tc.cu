@@ -102,6 +102,7 @@ struct TcAttnArgs {
   const AttnGroup *groups;
   int q_tiles, splits, ws_rows;
   const bf16 *q_base, *kd_base;  // row offsets of the groups' q / dense k,v pointers
+  int kv_ready;  // 1: the paged K/V were not written by the previous kernel (prefetch before the PDL wait)
   float scale_log2;
   float *ws_o, *ws_ml;
 };
@@ -109,7 +110,8 @@ struct TcAttnArgs {
 __global__ void __launch_bounds__(192, 1)
     flash_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kpmap,
                     const __grid_constant__ CUtensorMap vpmap, const __grid_constant__ CUtensorMap kdmap,
-                    const __grid_constant__ CUtensorMap vdmap, TcAttnArgs a) {
+                    const __grid_constant__ CUtensorMap vdmap, const __grid_constant__ CUtensorMap wsmap,
+                    TcAttnArgs a) {
   using namespace tc;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -153,15 +155,14 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  pdl_wait();
+  // let the next kernel (split merge / o-projection) be scheduled now: it waits
+  // in griddepcontrol.wait for our outputs and meanwhile streams its weights
+  if (threadIdx.x == 0) pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0 && n > 0) {
-      const int qrow = (int)((g.q - a.q_base) / HD) + q0;
-      mbar_expect_tx(b_q, Q_BYTES);
-      for (int b = 0; b < 4; ++b) tma_load_2d(&qmap, b_q, smem_u32(sm + b * Q_BOX), b * 64, qrow);
       const int drow0 = g.kb ? (int)((g.kb - a.kd_base) / HD) : 0;
-      for (int i = 0; i < n; ++i) {
+      auto issue = [&](int i) {
         const int j = t0 + i, s = i & 1;
         MBW(b_kve + 8 * s, ((i >> 1) & 1) ^ 1, 1);
         mbar_expect_tx(b_kvf + 8 * s, 2 * KV_BYTES);
@@ -172,7 +173,17 @@ __global__ void __launch_bounds__(192, 1)
           tma_load_2d(km, b_kvf + 8 * s, smem_u32(sm + OFF_K + s * KV_BYTES + b * KV_BOX), b * 64, row);
           tma_load_2d(vm, b_kvf + 8 * s, smem_u32(sm + OFF_V + s * KV_BYTES + b * KV_BOX), b * 64, row);
         }
-      }
+      };
+      int i = 0;
+      // paged prefix K/V written long before this kernel (the expert suffix case):
+      // fill the ring while the previous kernel drains
+      if (a.kv_ready)
+        for (; i < n && i < 2 && t0 + i < ta; ++i) issue(i);
+      pdl_wait();  // Q (and dense K/V) come from the previous kernel
+      const int qrow = (int)((g.q - a.q_base) / HD) + q0;
+      mbar_expect_tx(b_q, Q_BYTES);
+      for (int b = 0; b < 4; ++b) tma_load_2d(&qmap, b_q, smem_u32(sm + b * Q_BOX), b * 64, qrow);
+      for (; i < n; ++i) issue(i);
     }
   } else if (warp == 1) {
     if (lane == 0 && n > 0) {
@@ -213,6 +224,7 @@ __global__ void __launch_bounds__(192, 1)
     __syncwarp();
   } else {
     // softmax / epilogue: thread = query row
+    pdl_wait();  // outputs / workspace may still be read by earlier kernels
     const int quad = warp & 3, row = quad * 32 + lane;
     const uint32_t lanes = (uint32_t)(quad * 32) << 16;
     const int r = q0 + row;
@@ -317,27 +329,44 @@ __global__ void __launch_bounds__(192, 1)
         }
       }
     } else {
-      const size_t wr = (size_t)split * a.ws_rows + g.wrow0 + r;
-      float *orow = a.ws_o + wr * HD;
-      for (int c = 0; c < HD; c += 16) {
-        uint32_t v[16];
+      // fp32 partials through TMA stores: rows staged in smem as 8 boxes of
+      // 128 rows x 32 floats in the 128B-swizzled box layout (conflict-free: the
+      // 8 rows of an smem phase hit 8 different 16-byte slots), then one thread
+      // stores the whole 128-row tile.  Workspace rows are padded per group to
+      // multiples of 128, so rows past nq land in that group's padding.
+      uint8_t *stage = sm;  // Q + K slots: free once the last PV retired
+      for (int b = 0; b < HD / 32; ++b) {
+        uint32_t v[32];
         if (n > 0) {
-          tmem_ld16_nowait(tmem + lanes + c, v);
+          tmem_ld16_nowait(tmem + lanes + b * 32, *reinterpret_cast<uint32_t(*)[16]>(v));
+          tmem_ld16_nowait(tmem + lanes + b * 32 + 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16));
           tmem_ld_wait();
         } else {
 #pragma unroll
-          for (int e = 0; e < 16; ++e) v[e] = 0u;
+          for (int e = 0; e < 32; ++e) v[e] = 0u;
         }
-        if (ok)
+        uint8_t *rowp = stage + b * (TQ * 128) + row * 128;
 #pragma unroll
-          for (int e = 0; e < 16; e += 4)
-            *reinterpret_cast<float4 *>(orow + c + e) =
-                make_float4(__uint_as_float(v[e]), __uint_as_float(v[e + 1]), __uint_as_float(v[e + 2]),
-                            __uint_as_float(v[e + 3]));
+        for (int ch = 0; ch < 8; ++ch)
+          *reinterpret_cast<uint4 *>(rowp + ((ch ^ (row & 7)) << 4)) =
+              make_uint4(v[4 * ch], v[4 * ch + 1], v[4 * ch + 2], v[4 * ch + 3]);
       }
       if (ok) {
+        const size_t wr = (size_t)split * a.ws_rows + g.wrow0 + r;
         a.ws_ml[wr * 2] = m_ref;
         a.ws_ml[wr * 2 + 1] = l;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("bar.sync 3, 128;" ::: "memory");
+      if (threadIdx.x == 64) {
+        const int row0 = split * a.ws_rows + g.wrow0 + q0;
+        for (int b = 0; b < HD / 32; ++b)
+          asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                           reinterpret_cast<uint64_t>(&wsmap)),
+                       "r"(b * 32), "r"(row0), "r"(smem_u32(stage + b * (TQ * 128)))
+                       : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
       }
     }
   }
@@ -352,7 +381,7 @@ __global__ void __launch_bounds__(192, 1)
 void flash_attention_tc(const AttnGroup *groups_d, int n_groups, int q_tiles, int splits, const bf16 *q_base,
                         int q_rows, const CUtensorMap &kpool_map, const CUtensorMap &vpool_map, const bf16 *kd_base,
                         const bf16 *vd_base, int kd_rows, float scale, float *ws_o, float *ws_ml, int ws_rows,
-                        cudaStream_t st) {
+                        bool kv_ready, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     OXY_CUDA(cudaFuncSetAttribute(flash_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::SMEM));
@@ -365,9 +394,13 @@ void flash_attention_tc(const AttnGroup *groups_d, int n_groups, int q_tiles, in
   const CUtensorMap vdm = vd_base ? gemm::make_map(vd_base, kd_rows, tc::HD, tc::TK) : vpool_map;
   if (kd_base && vd_base - kd_base != 0 && (vd_base - kd_base) % tc::HD != 0)
     fail(OXY_EINVAL, "dense K/V buffers must be row-aligned");
-  TcAttnArgs a{groups_d, q_tiles, splits, ws_rows, q_base, kd_base, scale * 1.4426950408889634f, ws_o, ws_ml};
+  if (splits > 1 && ws_rows % tc::TQ != 0) fail(OXY_EINVAL, "attention workspace rows must be padded to 128");
+  // fp32 partial rows [splits * ws_rows, 256], box 32 x 128 (128-byte rows), 128B swizzle
+  const CUtensorMap wsm = splits > 1 ? gemm::make_map_f32(ws_o, splits * ws_rows, tc::HD, 32, tc::TQ) : qm;
+  TcAttnArgs a{groups_d, q_tiles, splits, ws_rows, q_base, kd_base, kv_ready ? 1 : 0, scale * 1.4426950408889634f,
+               ws_o, ws_ml};
   launch_pdl(flash_tc_kernel, dim3(n_groups * q_tiles, splits), dim3(192), tc::SMEM, st, qm, kpool_map, vpool_map,
-             kdm, vdm, a);
+             kdm, vdm, wsm, a);
 }
 
 }  // namespace pi05

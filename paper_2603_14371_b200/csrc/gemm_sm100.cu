@@ -259,6 +259,7 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
       int it = 0;
       bool waited = false;
       for (int tile = unit; tile < p.tiles; tile += units) {
+        if (tile + units >= p.tiles) pdl_trigger();  // last tile: let the next kernel get scheduled
         const int mt = tile / per_m, rem = tile % per_m, split = rem / p.n_tiles, nt = rem % p.n_tiles;
         const int kb0 = split * p.kb_per_split;
         const int nkb = min(p.kb_total, kb0 + p.kb_per_split) - kb0;
@@ -345,7 +346,6 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
         splitk_fixup(p, (mt * p.n_tiles + nt) * CG + (int)rank, n0, cb, ce, f, s_last, WIDE_THREADS - 64, 64);
     }
   }
-  if (threadIdx.x == 0) pdl_trigger();
   tc_fence_before();
   if (CG == 2) cluster_sync_all();
   else __syncthreads();
@@ -444,6 +444,21 @@ static bool wide_plan(Plan &p, int n_out, int k, int t, int sms) {
   p.splits = (p.kb_total + per_split - 1) / per_split;
   p.stages = wide_stages(p.bn, p.cg);
   return true;
+}
+
+// rows x cols fp32 row-major, box (box_cols x box_rows), 128-byte swizzle (box_cols * 4 == 128)
+CUtensorMap make_map_f32(const void *ptr, int rows, int cols, int box_cols, int box_rows) {
+  if ((cols * 4) % 16 != 0 || reinterpret_cast<uintptr_t>(ptr) % 16 != 0) fail(OXY_EINVAL, "fp32 map alignment");
+  CUtensorMap map;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void *>(ptr), dims, strides, box,
+                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(OXY_ECUDA, "cuTensorMapEncodeTiled (f32) failed (%d)", (int)r);
+  return map;
 }
 
 Plan make_plan(int n_out, int k, int t, int sms, int force_splits) {

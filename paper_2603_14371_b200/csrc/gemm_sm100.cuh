@@ -92,6 +92,8 @@ void launch(const void *w, const void *x, int n_out, int k, int t, const EpiPara
             const Plan &plan, float *ws, int *counters, cudaStream_t st);
 // 2-D TMA map over a row-major bf16 [rows, k] matrix, box (64 cols x box_rows), 128-byte swizzle
 CUtensorMap make_map(const void *ptr, int rows, int k, int box_rows);
+// 2-D TMA map over a row-major fp32 [rows, cols] matrix, box (box_cols x box_rows), 128-byte swizzle
+CUtensorMap make_map_f32(const void *ptr, int rows, int cols, int box_cols, int box_rows);
 // self-resetting split-K tile counters for launches made through the C ABI
 int *counters_for_abi();
 

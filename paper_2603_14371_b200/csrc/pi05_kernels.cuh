@@ -82,10 +82,12 @@ void flash_attention(const AttnGroup *groups_d, int n_groups, int max_q_tiles, i
 // q_base viewed as [q_rows, 256]; paged keys through kpool/vpool maps (box 64x64),
 // dense keys g.kb/g.vb rows of kd_base/vd_base [kd_rows, 256] (null: none).
 // q_tiles = ceil(max nq / 128); splits > 1 writes ws (merge with flash_merge).
+// kv_ready: the paged K/V were not written by the previous kernel on the stream
+// (the expert suffix over an earlier prefill), so they are prefetched before the PDL wait.
 void flash_attention_tc(const AttnGroup *groups_d, int n_groups, int q_tiles, int splits, const bf16 *q_base,
                         int q_rows, const CUtensorMap &kpool_map, const CUtensorMap &vpool_map, const bf16 *kd_base,
                         const bf16 *vd_base, int kd_rows, float scale, float *ws_o, float *ws_ml, int ws_rows,
-                        cudaStream_t st);
+                        bool kv_ready, cudaStream_t st);
 // split-order merge of head-dim-256 partials (ws rows as in flash_attention)
 void flash_merge(const AttnGroup *groups_d, int n_groups, int max_rows, int splits, const float *ws_o,
                  const float *ws_ml, int ws_rows, cudaStream_t st);

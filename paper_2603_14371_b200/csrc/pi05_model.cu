@@ -323,6 +323,12 @@ struct Model {
     return e ? atoi(e) : 0;
   }();
   std::map<std::string, mk::Program> mk_progs;
+  // profiling only: OXY_DBG_SKIP bitmask drops kernels from the denoise chain
+  // (results are garbage; used to measure each kernel's marginal cost in-graph)
+  int dbg_skip = [] {
+    const char *e = getenv("OXY_DBG_SKIP");
+    return e ? atoi(e) : 0;
+  }();
 
   // ---- execution lanes.  The members above (stream, events, arena, graph
   // cache, split-K counters) and the per-call scratch describe the ACTIVE lane.
@@ -505,8 +511,9 @@ struct Model {
       float *wsp = ws.as<float>((size_t)plan.splits * t * n_out);
       EpiParams e{gemm::EPI_PARTIALS, nullptr, 0, nullptr, nullptr, 0, nullptr, {}};
       gemm::launch(w, xin, n_out, k, t, e, plan, wsp, gemm_counters, mst);
-      gemm::splitk_residual_norm(wsp, plan.splits, t, n_out, gate, X, n_out, Y, n_out, norm_w, mod_scale,
-                                 mod_shift, 1e-6f, mst);
+      if (!(dbg_skip & 128))
+        gemm::splitk_residual_norm(wsp, plan.splits, t, n_out, gate, X, n_out, Y, n_out, norm_w, mod_scale,
+                                   mod_shift, 1e-6f, mst);
       return;
     }
     gemm(w, xin, n_out, k, t, gate ? gemm::EPI_ADD_GATED_F32 : gemm::EPI_ADD_F32, X, n_out, nullptr, gate);
@@ -572,9 +579,9 @@ struct Model {
     p.n = (int)groups.size();
     p.hd = HEAD_DIM;
     int max_nq = 0;
-    for (auto &g : groups) {
+    for (auto &g : groups) {  // workspace rows padded to whole 128-row tiles (TMA-stored partials)
       g.wrow0 = p.rows;
-      p.rows += g.nq;
+      p.rows += (g.nq + 127) / 128 * 128;
       max_nq = std::max(max_nq, g.nq);
       p.max_tiles = std::max(p.max_tiles, (g.nka + 63) / 64 + (g.nkb + 63) / 64);
     }
@@ -589,7 +596,7 @@ struct Model {
     return p;
   }
   void attend_tc(const AttnPlan &p, int layer, const bf16 *q_base, int q_rows, const bf16 *kd, const bf16 *vd,
-                 int kd_rows) {
+                 int kd_rows, bool kv_ready) {
     if (!p.n) return;
     float *wo = nullptr, *wml = nullptr;
     if (p.splits > 1) {
@@ -597,8 +604,8 @@ struct Model {
       wml = attn_ml.as<float>((size_t)p.splits * p.rows * 2);
     }
     flash_attention_tc(p.groups, p.n, p.q_tiles, p.splits, q_base, q_rows, kv_maps[2 * layer], kv_maps[2 * layer + 1],
-                       kd, vd, kd_rows, 1.f / 16.f, wo, wml, p.rows, mst);
-    if (p.splits > 1) flash_merge(p.groups, p.n, p.q_tiles * 128, p.splits, wo, wml, p.rows, mst);
+                       kd, vd, kd_rows, 1.f / 16.f, wo, wml, p.rows, kv_ready, mst);
+    if (p.splits > 1 && !(dbg_skip & 4)) flash_merge(p.groups, p.n, p.q_tiles * 128, p.splits, wo, wml, p.rows, mst);
   }
 
   void reserve_common() {
@@ -754,7 +761,7 @@ struct Model {
         rmsnorm(X, W, Y, W, w.ln1, nullptr, nullptr, T, W, 1e-6f, mst);
         gemm_qkv(w.wqkv, Y, W, T, d_pos, d_slot, Qb, kpool(l), vpool(l));
         if (l == c.depth - 1) break;  // the last block's output is not cached
-        if (use_attn_tc) attend_tc(a_llm, l, Qb, T * Q_HEADS, nullptr, nullptr, 0);
+        if (use_attn_tc) attend_tc(a_llm, l, Qb, T * Q_HEADS, nullptr, nullptr, 0, false);
         else attend(a_llm, kpool(l), vpool(l));
         gemm(w.wo, Ob, W, QDIM, T, gemm::EPI_ADD_F32, X, W);
         rmsnorm(X, W, Y, W, w.ln2, nullptr, nullptr, T, W, 1e-6f, mst);
@@ -915,12 +922,15 @@ struct Model {
           const ExpertW &w = E[l];
           const float *m = ms + (size_t)l * 6 * We;
           const float *mn = l + 1 < c.depth ? m + 6 * We : mf;  // the norm that follows this layer
-          gemm_qkv(w.wqkv, Y, We, T, d_pos, nullptr, Qb, Kd, Vd);
-          if (use_attn_tc) attend_tc(ap, l, Qb, T * Q_HEADS, Kd, Vd, T);
-          else attend(ap, kpool(l), vpool(l));
-          gemm_res_norm(w.wo, Ob, We, QDIM, T, m + 2 * We, X, Y, nullptr, m + 3 * We, m + 4 * We);
-          gemm(w.wgu, Y, 2 * c.expert_mlp, We, T, gemm::EPI_GEGLU_BF16, Hm, c.expert_mlp);
-          gemm_res_norm(w.wd, Hm, We, c.expert_mlp, T, m + 5 * We, X, Y, nullptr, mn, mn + We);
+          if (!(dbg_skip & 1)) gemm_qkv(w.wqkv, Y, We, T, d_pos, nullptr, Qb, Kd, Vd);
+          if (!(dbg_skip & 2)) {
+            if (use_attn_tc) attend_tc(ap, l, Qb, T * Q_HEADS, Kd, Vd, T, true);
+            else attend(ap, kpool(l), vpool(l));
+          }
+          if (!(dbg_skip & 8)) gemm_res_norm(w.wo, Ob, We, QDIM, T, m + 2 * We, X, Y, nullptr, m + 3 * We, m + 4 * We);
+          if (!(dbg_skip & 16)) gemm(w.wgu, Y, 2 * c.expert_mlp, We, T, gemm::EPI_GEGLU_BF16, Hm, c.expert_mlp);
+          if (!(dbg_skip & 32))
+            gemm_res_norm(w.wd, Hm, We, c.expert_mlp, T, m + 5 * We, X, Y, nullptr, mn, mn + We);
         }
         gemm(e_out, Y, A, We, T, gemm::EPI_F32, vel_d, AP, e_out_b);
         euler_step(a, vel_d, ab, (int64_t)T * AP, dt, mst);
