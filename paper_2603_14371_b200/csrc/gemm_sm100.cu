@@ -616,57 +616,73 @@ void launch(const void *w, const void *x, int n_out, int k, int t, const EpiPara
   }
 }
 
-// one 1024-thread CTA per token row (memory-level parallelism for the skinny
-// decode/denoise rows); thread owns features tid, tid+1024 (coalesced)
-constexpr int RN_THREADS = 1024, RN_MAXV = 2;  // n <= 2048
-__global__ void __launch_bounds__(RN_THREADS)
+// One CTA per token row, one thread per 4 consecutive features (n / 4 threads):
+// every load of the row — all split partials, the residual, gate and norm
+// weights — is issued before any arithmetic, so the kernel costs one L2 round
+// trip plus the block reduction.  Split order 0..S-1 per element.
+constexpr int RN_CHUNK = 16;  // split partials in flight per thread
+__global__ void __launch_bounds__(512)
     splitk_residual_norm_kernel(const float *ws, int splits, int t_rows, int n, const float *gate, float *x,
                                 int ldx, __nv_bfloat16 *y, int ldy, const float *w, const float *ms,
                                 const float *mb, float eps) {
   pdl_trigger();
+  const int t = blockIdx.x, f = threadIdx.x * 4;
+  // weights do not depend on the previous kernel: fetch them before the wait
+  float4 wv = make_float4(0.f, 0.f, 0.f, 0.f), sv = wv, bv = wv, gv = make_float4(1.f, 1.f, 1.f, 1.f);
+  if (w) wv = __ldg(reinterpret_cast<const float4 *>(w + f));
+  else {
+    sv = __ldg(reinterpret_cast<const float4 *>(ms + f));
+    bv = __ldg(reinterpret_cast<const float4 *>(mb + f));
+  }
+  if (gate) gv = __ldg(reinterpret_cast<const float4 *>(gate + f));
   pdl_wait();
   __shared__ float red[32];
-  const int t = blockIdx.x;
-  float v[RN_MAXV] = {0.f, 0.f};
-#pragma unroll 8
-  for (int s = 0; s < splits; ++s) {  // split order 0..S-1 per element
-    const float *row = ws + ((size_t)s * t_rows + t) * n;
+  float4 xv = *reinterpret_cast<const float4 *>(x + (size_t)t * ldx + f);
+  float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int s0 = 0; s0 < splits; s0 += RN_CHUNK) {
+    float4 p[RN_CHUNK];
 #pragma unroll
-    for (int i = 0; i < RN_MAXV; ++i) {
-      const int f = threadIdx.x + i * RN_THREADS;
-      if (f < n) v[i] += row[f];
-    }
-  }
-  float ss = 0.f;
+    for (int s = 0; s < RN_CHUNK; ++s)
+      if (s0 + s < splits) p[s] = __ldcg(reinterpret_cast<const float4 *>(ws + ((size_t)(s0 + s) * t_rows + t) * n + f));
 #pragma unroll
-  for (int i = 0; i < RN_MAXV; ++i) {
-    const int f = threadIdx.x + i * RN_THREADS;
-    if (f < n) {
-      float xv = x[(size_t)t * ldx + f];
-      xv += gate ? gate[f] * v[i] : v[i];
-      x[(size_t)t * ldx + f] = xv;
-      v[i] = xv;
-      ss += xv * xv;
-    }
+    for (int s = 0; s < RN_CHUNK; ++s)
+      if (s0 + s < splits) {
+        a.x += p[s].x;
+        a.y += p[s].y;
+        a.z += p[s].z;
+        a.w += p[s].w;
+      }
   }
+  xv.x += gv.x * a.x;
+  xv.y += gv.y * a.y;
+  xv.z += gv.z * a.z;
+  xv.w += gv.w * a.w;
+  *reinterpret_cast<float4 *>(x + (size_t)t * ldx + f) = xv;
+  float ss = xv.x * xv.x + xv.y * xv.y + xv.z * xv.z + xv.w * xv.w;
   ss = block_sum(ss, red);
   const float inv = rsqrtf(ss / (float)n + eps);
-#pragma unroll
-  for (int i = 0; i < RN_MAXV; ++i) {
-    const int f = threadIdx.x + i * RN_THREADS;
-    if (f < n) {
-      const float o = w ? v[i] * inv * (1.f + w[f]) : v[i] * inv * (1.f + ms[f]) + mb[f];
-      y[(size_t)t * ldy + f] = __float2bfloat16(o);
-    }
+  float o0, o1, o2, o3;
+  if (w) {
+    o0 = xv.x * inv * (1.f + wv.x), o1 = xv.y * inv * (1.f + wv.y);
+    o2 = xv.z * inv * (1.f + wv.z), o3 = xv.w * inv * (1.f + wv.w);
+  } else {
+    o0 = xv.x * inv * (1.f + sv.x) + bv.x, o1 = xv.y * inv * (1.f + sv.y) + bv.y;
+    o2 = xv.z * inv * (1.f + sv.z) + bv.z, o3 = xv.w * inv * (1.f + sv.w) + bv.w;
   }
+  __nv_bfloat162 h0 = __floats2bfloat162_rn(o0, o1), h1 = __floats2bfloat162_rn(o2, o3);
+  uint2 out;
+  out.x = *reinterpret_cast<uint32_t *>(&h0);
+  out.y = *reinterpret_cast<uint32_t *>(&h1);
+  *reinterpret_cast<uint2 *>(y + (size_t)t * ldy + f) = out;
 }
 
 void splitk_residual_norm(const float *ws, int splits, int t, int n, const float *gate, float *x, int ldx,
                           __nv_bfloat16 *y, int ldy, const float *w, const float *mod_scale,
                           const float *mod_shift, float eps, cudaStream_t st) {
   if (t <= 0) return;
-  if (n > RN_THREADS * RN_MAXV) fail(OXY_EINVAL, "fused residual norm supports rows of at most 2048");
-  launch_pdl(splitk_residual_norm_kernel, dim3(t), dim3(RN_THREADS), 0, st, ws, splits, t, n, gate, x, ldx, y, ldy, w,
+  if (n % 128 != 0 || n > 2048) fail(OXY_EINVAL, "fused residual norm: rows of 128..2048 features (multiple of 128)");
+  if (ldx % 4 != 0 || ldy % 4 != 0) fail(OXY_EINVAL, "fused residual norm: row strides must be multiples of 4");
+  launch_pdl(splitk_residual_norm_kernel, dim3(t), dim3(n / 4), 0, st, ws, splits, t, n, gate, x, ldx, y, ldy, w,
              mod_scale, mod_shift, eps);
 }
 
