@@ -633,7 +633,10 @@ __global__ void __launch_bounds__(128, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&vmap)) : "memory");
   }
   __syncthreads();
-  pdl_wait();
+  // pos / active / block table come from earlier steps (argmax update, host
+  // plan), not from the kernel right before us (the QKV projection): read them
+  // and prefetch every pool block but the one holding this step's position
+  // before the PDL wait
   const int r = blockIdx.x, chunk = blockIdx.y;
   if (active && !active[r]) return;
   const int n_keys = pos[r] + 1;
@@ -654,8 +657,12 @@ __global__ void __launch_bounds__(128, 1)
       d3_tma(&vmap, bar, vb + j * D3_SUB, 64 * j, row0);
     }
   };
+  int pre = 0;  // blocks issued before the wait: all but the block holding pos[r]
   if (threadIdx.x == 0)
-    for (int i = 0; i < min(nblk, D3_STAGES); ++i) issue(i);
+    for (; pre < min(nblk, D3_STAGES) && b0 + pre < nb - 1; ++pre) issue(pre);
+  pdl_wait();
+  if (threadIdx.x == 0)
+    for (int i = pre; i < min(nblk, D3_STAGES); ++i) issue(i);
   // Q: the 8 heads as MMA rows 0..7 (rows 8..15 zero)
   const bf16 *qr = q + (size_t)r * Q_HEADS * HEAD_DIM;
   for (int i = threadIdx.x; i < 16 * 32; i += 128) {

@@ -1102,14 +1102,15 @@ struct Model {
         for (int l = 0; l < c.depth; ++l) {
           const LayerW &w = L[l];
           const float *next_norm = l + 1 < c.depth ? L[l + 1].ln1 : final_norm;
-          gemm_qkv(w.wqkv, Y, W, rows, d_pos, d_slot, Qb, kpool(l), vpool(l));
-          decode_attention_v3(kv_maps[2 * l], kv_maps[2 * l + 1], Qb, Ob, d_bt, maxb, d_pos, d_active, rows, maxb,
-                              scale, dws, sms, mst);
-          gemm_res_norm(w.wo, Ob, W, QDIM, rows, nullptr, X, Y, w.ln2, nullptr, nullptr);
-          gemm(w.wgu, Y, 2 * c.mlp, W, rows, gemm::EPI_GEGLU_BF16, Hm, c.mlp);
-          gemm_res_norm(w.wd, Hm, W, c.mlp, rows, nullptr, X, Y, next_norm, nullptr, nullptr);
+          if (!(dbg_skip & 256)) gemm_qkv(w.wqkv, Y, W, rows, d_pos, d_slot, Qb, kpool(l), vpool(l));
+          if (!(dbg_skip & 512))
+            decode_attention_v3(kv_maps[2 * l], kv_maps[2 * l + 1], Qb, Ob, d_bt, maxb, d_pos, d_active, rows, maxb,
+                                scale, dws, sms, mst);
+          if (!(dbg_skip & 2048)) gemm_res_norm(w.wo, Ob, W, QDIM, rows, nullptr, X, Y, w.ln2, nullptr, nullptr);
+          if (!(dbg_skip & 4096)) gemm(w.wgu, Y, 2 * c.mlp, W, rows, gemm::EPI_GEGLU_BF16, Hm, c.mlp);
+          if (!(dbg_skip & 8192)) gemm_res_norm(w.wd, Hm, W, c.mlp, rows, nullptr, X, Y, next_norm, nullptr, nullptr);
         }
-        gemm(lm_head, Y, c.vocab, W, rows, gemm::EPI_F32, LG, c.vocab);
+        if (!(dbg_skip & 16384)) gemm(lm_head, Y, c.vocab, W, rows, gemm::EPI_F32, LG, c.vocab);
         if (logits_h)
           OXY_CUDA(cudaMemcpyAsync(logits_h + (size_t)s * rows * c.vocab, LG, (size_t)rows * c.vocab * sizeof(float),
                                    cudaMemcpyDeviceToHost, mst));
