@@ -198,3 +198,24 @@ def test_metrics_hand_values():
     assert rep.token_throughput == pytest.approx(20.0)
     with pytest.raises(ValueError, match="degenerate"):
         summarize(SimResult((tr(0, 0),), {}), cfg, include_warmup=True)
+
+
+def test_cost_calibration_recovers_constants_and_trends():
+    """calibrate.fit_cost_params inverts the cost model exactly on model-generated
+    samples, and with B200-like constants the reference's sweep trends hold
+    (tests/test_acceptance.py:145-200 shapes)."""
+    from paper_2603_14371_b200.backend import CostModelParams
+    from paper_2603_14371_b200.calibrate import closed_form_speedup, fit_cost_params
+    true = CostModelParams(11, 870, 1300, 12, 1.0)
+    pre = [(p, true.c_prefill_per_token * p) for p in (32, 288, 544, 800)]
+    den = [(s, s * true.c_denoise_per_step) for s in (1, 5, 10)]
+    dec = [(5, m, 5 * (true.c_decode_base + true.c_decode_per_request * m)) for m in (1, 2, 4, 8, 16)]
+    assert fit_cost_params(pre, den, dec) == true
+    # closed form of tests/test_acceptance.py:129-133 with the reference's constants
+    ref = CostModelParams()
+    assert abs(closed_form_speedup(ref, 12, 4, 800, 10) - 142000 / 74800) < 1e-12
+    # unified beats isolated more as N grows, less as k grows
+    s_n = [closed_form_speedup(true, n, 5, 800, 10) for n in (5, 10, 20, 30, 40)]
+    s_k = [closed_form_speedup(true, 30, k, 800, 10) for k in (1, 2, 5, 10, 15, 30)]
+    assert all(b > a for a, b in zip(s_n, s_n[1:]))
+    assert all(b <= a for a, b in zip(s_k, s_k[1:]))
