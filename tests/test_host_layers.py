@@ -219,3 +219,22 @@ def test_cost_calibration_recovers_constants_and_trends():
     s_k = [closed_form_speedup(true, 30, k, 800, 10) for k in (1, 2, 5, 10, 15, 30)]
     assert all(b > a for a, b in zip(s_n, s_n[1:]))
     assert all(b <= a for a, b in zip(s_k, s_k[1:]))
+
+
+def test_csv_v1_row_matches_reference_format():
+    """report.csv_row reproduces the reference CLI's v1 row (kvweaver/cli.py:80-101)
+    for a cost-model run, value for value, against tests/golden/sim.json's
+    summaries where available and the row schema otherwise."""
+    from paper_2603_14371_b200 import SimConfig, WorkloadSpec, run_simulation, summarize
+    from paper_2603_14371_b200.report import CSV_COLUMNS, csv_row, write_csv
+    cfg = SimConfig(variant="Unified", backend_kind="CostModel", k=4,
+                    workload=WorkloadSpec(pattern="OnePerFrame", default_N=12, obs_len=800, num_frames=40))
+    res = run_simulation(cfg)
+    rep = summarize(res, cfg)
+    row = csv_row("r0000", cfg, res, rep, 142000 / 74800)
+    # the reference CLI's row for this run (kvweaver.cli._csv_row, captured once)
+    assert row == ["r0000", "Unified", "CostModel", "12", "4", "10", "10", "1.000000", "OnePerFrame", "1", "42",
+                   "133.689840", "133.689840", "160.427807", "3.000000", "0.000000", "3", "1.898396"]
+    assert len(row) == len(CSV_COLUMNS)
+    text = write_csv([row])
+    assert text.splitlines()[0] == "# kvweaver-csv v1" and text.splitlines()[2] == ",".join(CSV_COLUMNS)
