@@ -847,11 +847,12 @@ struct Model {
       groups[i].nkb = H;
     }
     AttnPlan ap = (use_attn_tc && !use_mk) ? shape_attention_tc(groups) : shape_attention(groups, HEAD_DIM);
-    if (use_attn_tc && !use_mk) {
-      // the expert suffix: key tiles per split (OXY_ATTN_TC_DN_TILES); each split
-      // CTA prefetches its first two pool tiles before the PDL wait
-      const char *e = getenv("OXY_ATTN_TC_DN_TILES");
-      const int per = std::max(1, e ? atoi(e) : 1);
+    const char *dn_tiles = getenv("OXY_ATTN_TC_DN_TILES");
+    if (use_attn_tc && !use_mk && dn_tiles) {
+      // A/B knob: key tiles per split of the expert suffix (the default plan fills
+      // the SMs: one tile per split at 1 stream, measured best; fewer splits as
+      // streams add query tiles)
+      const int per = std::max(1, atoi(dn_tiles));
       ap.splits = std::max(1, (ap.max_tiles + per - 1) / per);
       if (ap.splits > 1) {
         attn_ws_need = std::max(attn_ws_need, (size_t)ap.splits * ap.rows * 256);
