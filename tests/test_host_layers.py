@@ -238,3 +238,23 @@ def test_csv_v1_row_matches_reference_format():
     assert len(row) == len(CSV_COLUMNS)
     text = write_csv([row])
     assert text.splitlines()[0] == "# kvweaver-csv v1" and text.splitlines()[2] == ",".join(CSV_COLUMNS)
+
+
+def test_extra_language_tasks_share_the_arrival():
+    """Arrival.extra_tasks: one prefill, several language
+    requests on the same prefix handle — batched together in the frame's decode."""
+    from paper_2603_14371_b200 import (Arrival, KvManager, Observation, make_backend, BackendConfig,
+                                       CostModelParams)
+    from paper_2603_14371_b200.scheduler import run_frame_unified
+    be = make_backend("CostModel", BackendConfig(), CostModelParams())
+    mgr = KvManager()
+    arr = [Arrival(0, Observation((1, 2, 3), 0), 4, extra_tasks=(6, 2))]
+    res = run_frame_unified(0, arr, mgr, be, 2, 30.0)
+    assert res.trace.batch_size_m == 3 and res.trace.prefill_count == 1
+    states = [mgr.retrieve(r) for r in mgr.active_ids()]  # the 2-token task finished this frame
+    assert sorted(s.max_len for s in states) == [4, 6] and all(len(s.tokens) == 2 for s in states)
+    assert len(res.finished) == 1 and len(res.finished[0][1]) == 2
+    assert len(res.actions) == 1  # one action chunk per observation
+    import pytest
+    with pytest.raises(ValueError):
+        Arrival(0, Observation((1,), 0), 4, extra_tasks=(0,))

@@ -210,3 +210,34 @@ def test_overlapped_frames_match_stage_serial(pattern):
     for tr in runs[True].traces:
         if tr.arrival_count:
             assert 0 < tr.total_us <= sum(tr.latency_components) + 2000, tr
+
+
+def test_extra_tasks_share_prefix_blocks_with_copy_on_write():
+    """Two language tasks on one observation (Arrival.extra_tasks): one prefill,
+    the prefix blocks refcounted by both requests, the shared tail block copied
+    on the first decoded token, and each task's tokens equal to a solo decode
+    of the same prefix (batch-invariant kernels)."""
+    from paper_2603_14371_b200 import Arrival, KvManager
+    from paper_2603_14371_b200.pi05 import TINY, Pi05Backend
+    from paper_2603_14371_b200.scheduler import run_frame_unified
+    be = Pi05Backend(TINY, num_blocks=64)
+    obs = _obs(1, tuple(range(20, 50)))  # 286 positions: 4 full blocks + a partially filled tail
+    free0 = be.allocator.num_free
+    mgr = KvManager()
+    res = run_frame_unified(0, [Arrival(0, obs, 6, extra_tasks=(6,))], mgr, be, 3, 30.0)
+    assert res.trace.prefill_count == 1 and res.trace.batch_size_m == 2
+    a, b = (mgr.retrieve(r) for r in mgr.active_ids())
+    assert a.tokens == b.tokens and len(a.tokens) == 3
+    assert a.kv.blocks[-1] != b.kv.blocks[-1]  # the tail block was copied on write ...
+    assert a.kv.blocks[:-1] == b.kv.blocks[:-1]  # ... the full prefix blocks are shared
+    nb = be.allocator.blocks_for(286 + 3)
+    assert free0 - be.allocator.num_free == nb + 1  # one prefix + one copied tail, not two prefixes
+    solo_kv = be.prefill(obs)
+    solo = be.batched_language_decode(BatchedState((solo_kv,), ((),), (False,), (0,), (6,), (0,)), 3)
+    assert solo.token_buffers[0] == a.tokens
+    del solo, solo_kv, a, b
+    for r in list(mgr.active_ids()):
+        mgr.remove(r)
+    import gc
+    gc.collect()
+    assert be.allocator.num_free == free0

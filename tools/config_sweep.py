@@ -10,7 +10,10 @@
 Prints one JSON line per point.  Timing: CUDA events around the steady frames
 (after warm-up), clocks not sampled (bench.py does that for the headline).
 
-    python tools/config_sweep.py multitask|variants|streams|all
+  tasks      SURVEY.md §8f rank 4: 1 / 2 / 3 language tasks (memory, narration, ...)
+             on each observation's shared prefix (Arrival.extra_tasks)
+
+    python tools/config_sweep.py multitask|tasks|variants|streams|all
 """
 import json
 import os
@@ -55,11 +58,15 @@ def run(backend, frames, warm, k, variant="Unified"):
     return ms, traces
 
 
-def point(name, backend, cfg, streams, budget, k, steps, warm, variant="Unified"):
+def point(name, backend, cfg, streams, budget, k, steps, warm, variant="Unified", extra_tasks=0):
     frames = bench.build_frames(cfg, streams, warm + steps, budget, device=True)
+    if extra_tasks:  # memory + narration style: more language tasks on each observation's prefix
+        import dataclasses
+        frames = [[dataclasses.replace(a, extra_tasks=(budget,) * extra_tasks) for a in f] for f in frames]
     ms, traces = run(backend, frames, warm, k, variant)
     toks = sum(t.tokens_emitted for t in traces)
     line = {"sweep": name, "variant": variant, "streams_per_gpu": streams, "budget_N": budget, "k": k,
+            "language_tasks_per_observation": 1 + extra_tasks,
             "frame_ms": round(ms, 3), "action_hz_per_stream_H50": round(H * 1e3 / ms, 1),
             "action_hz_per_stream_H10": round(10 * 1e3 / ms, 1),
             "action_hz_aggregate_H50": round(H * streams * 1e3 / ms, 1),
@@ -77,6 +84,12 @@ def main():
         for budget, k in ((16, 1), (16, 5), (30, 1), (30, 5), (30, 10), (60, 5), (60, 10)):
             warm = max(4, -(-budget // k) + 2)
             point("multitask", be, cfg, 1, budget, k, 10, warm)
+        del be
+        torch.cuda.empty_cache()
+    if what in ("tasks", "all"):  # several language tasks share one prefix
+        be = Pi05Backend(cfg, num_blocks=1024)
+        for extra in (0, 1, 2):
+            point("tasks", be, cfg, 1, 30, 5, 8, 10, extra_tasks=extra)
         del be
         torch.cuda.empty_cache()
     if what in ("variants", "all"):
