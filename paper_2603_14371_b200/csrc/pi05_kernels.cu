@@ -12,64 +12,74 @@ namespace pi05 {
 
 // ============================================================ elementwise
 
+// Row norms: one CTA per row, one thread per 4 features (D / 4 threads), the
+// row held in registers (one load per element, all in flight), the scale /
+// shift weights fetched before the PDL wait.
 __global__ void rmsnorm_kernel(const float *x, int ldx, bf16 *y, int ldy, const float *w,
                                const float *ms, const float *mb, int D, float eps) {
   pdl_trigger();
+  const int j = threadIdx.x * 4;
+  const bool act = j < D;  // the block is rounded up to whole warps
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 sv = z, bv = z;
+  if (act) {
+    if (w) sv = __ldg(reinterpret_cast<const float4 *>(w + j));
+    else {
+      sv = __ldg(reinterpret_cast<const float4 *>(ms + j));
+      bv = __ldg(reinterpret_cast<const float4 *>(mb + j));
+    }
+  }
   pdl_wait();
   __shared__ float red[32];
-  const float *xr = x + (size_t)blockIdx.x * ldx;
-  bf16 *yr = y + (size_t)blockIdx.x * ldy;
-  float ss = 0.f;
-  for (int j = threadIdx.x * 4; j < D; j += blockDim.x * 4) {
-    float4 v = *reinterpret_cast<const float4 *>(xr + j);
-    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
-  }
-  ss = block_sum(ss, red);
+  const float4 v = act ? *reinterpret_cast<const float4 *>(x + (size_t)blockIdx.x * ldx + j) : z;
+  const float ss = block_sum(v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w, red);
   const float inv = rsqrtf(ss / (float)D + eps);
-  for (int j = threadIdx.x * 4; j < D; j += blockDim.x * 4) {
-    float4 v = *reinterpret_cast<const float4 *>(xr + j);
-    float o[4] = {v.x * inv, v.y * inv, v.z * inv, v.w * inv};
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      if (w) o[e] *= 1.f + w[j + e];
-      else o[e] = o[e] * (1.f + ms[j + e]) + mb[j + e];
-    }
-    __nv_bfloat162 a = __floats2bfloat162_rn(o[0], o[1]), b = __floats2bfloat162_rn(o[2], o[3]);
-    *reinterpret_cast<__nv_bfloat162 *>(yr + j) = a;
-    *reinterpret_cast<__nv_bfloat162 *>(yr + j + 2) = b;
-  }
+  // (1 + w) for RMSNorm, (1 + scale) and + shift for adaRMS
+  const float o0 = v.x * inv * (1.f + sv.x) + bv.x, o1 = v.y * inv * (1.f + sv.y) + bv.y;
+  const float o2 = v.z * inv * (1.f + sv.z) + bv.z, o3 = v.w * inv * (1.f + sv.w) + bv.w;
+  __nv_bfloat162 h0 = __floats2bfloat162_rn(o0, o1), h1 = __floats2bfloat162_rn(o2, o3);
+  uint2 out;
+  out.x = *reinterpret_cast<uint32_t *>(&h0);
+  out.y = *reinterpret_cast<uint32_t *>(&h1);
+  if (act) *reinterpret_cast<uint2 *>(y + (size_t)blockIdx.x * ldy + j) = out;
 }
 
 void rmsnorm(const float *x, int ldx, bf16 *y, int ldy, const float *w, const float *ms,
              const float *mb, int rows, int D, float eps, cudaStream_t st) {
   if (rows <= 0) return;
-  launch_pdl(rmsnorm_kernel, dim3(rows), dim3(256), 0, st, x, ldx, y, ldy, w, ms, mb, D, eps);
+  if (D % 4 != 0 || D > 4096 || ldx % 4 != 0 || ldy % 4 != 0) fail(OXY_EINVAL, "rmsnorm: D %% 4 == 0, D <= 4096");
+  launch_pdl(rmsnorm_kernel, dim3(rows), dim3((D / 4 + 31) / 32 * 32), 0, st, x, ldx, y, ldy, w, ms, mb, D, eps);
 }
 
 __global__ void layernorm_kernel(const float *x, int ldx, bf16 *y, int ldy, const float *w,
                                  const float *b, int D, float eps) {
   pdl_trigger();
+  const int j = threadIdx.x * 4;
+  const bool act = j < D;  // the block is rounded up to whole warps
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  const float4 wv = act ? __ldg(reinterpret_cast<const float4 *>(w + j)) : z;
+  const float4 bv = act ? __ldg(reinterpret_cast<const float4 *>(b + j)) : z;
   pdl_wait();
   __shared__ float red[32];
-  const float *xr = x + (size_t)blockIdx.x * ldx;
-  bf16 *yr = y + (size_t)blockIdx.x * ldy;
-  float s = 0.f;
-  for (int j = threadIdx.x; j < D; j += blockDim.x) s += xr[j];
-  const float mean = block_sum(s, red) / (float)D;
-  float v = 0.f;
-  for (int j = threadIdx.x; j < D; j += blockDim.x) {
-    float d = xr[j] - mean;
-    v += d * d;
-  }
-  const float rstd = rsqrtf(block_sum(v, red) / (float)D + eps);
-  for (int j = threadIdx.x; j < D; j += blockDim.x)
-    yr[j] = __float2bfloat16((xr[j] - mean) * rstd * w[j] + b[j]);
+  const float4 v = act ? *reinterpret_cast<const float4 *>(x + (size_t)blockIdx.x * ldx + j) : z;
+  const float mean = block_sum(v.x + v.y + v.z + v.w, red) / (float)D;
+  const float d0 = act ? v.x - mean : 0.f, d1 = act ? v.y - mean : 0.f, d2 = act ? v.z - mean : 0.f,
+              d3 = act ? v.w - mean : 0.f;
+  __syncthreads();  // red[] is reused
+  const float rstd = rsqrtf(block_sum(d0 * d0 + d1 * d1 + d2 * d2 + d3 * d3, red) / (float)D + eps);
+  __nv_bfloat162 h0 = __floats2bfloat162_rn(d0 * rstd * wv.x + bv.x, d1 * rstd * wv.y + bv.y);
+  __nv_bfloat162 h1 = __floats2bfloat162_rn(d2 * rstd * wv.z + bv.z, d3 * rstd * wv.w + bv.w);
+  uint2 out;
+  out.x = *reinterpret_cast<uint32_t *>(&h0);
+  out.y = *reinterpret_cast<uint32_t *>(&h1);
+  if (act) *reinterpret_cast<uint2 *>(y + (size_t)blockIdx.x * ldy + j) = out;
 }
 
 void layernorm(const float *x, int ldx, bf16 *y, int ldy, const float *w, const float *b, int rows,
                int D, float eps, cudaStream_t st) {
   if (rows <= 0) return;
-  launch_pdl(layernorm_kernel, dim3(rows), dim3(256), 0, st, x, ldx, y, ldy, w, b, D, eps);
+  if (D % 4 != 0 || D > 4096 || ldx % 4 != 0 || ldy % 4 != 0) fail(OXY_EINVAL, "layernorm: D %% 4 == 0, D <= 4096");
+  launch_pdl(layernorm_kernel, dim3(rows), dim3((D / 4 + 31) / 32 * 32), 0, st, x, ldx, y, ldy, w, b, D, eps);
 }
 
 __global__ void embed_kernel(float *x, int ldx, const bf16 *table, const int *tok,
