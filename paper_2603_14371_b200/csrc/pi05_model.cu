@@ -587,8 +587,8 @@ struct Model {
     }
     p.q_tiles = (max_nq + 127) / 128;
     const int ctas = p.n * p.q_tiles;
-    p.splits = std::max(1, std::min(p.max_tiles, sms / std::max(1, ctas)));
-    if (const char *e = getenv("OXY_ATTN_TC_SPLITS")) p.splits = std::max(1, std::min(p.max_tiles, atoi(e)));
+    p.splits = std::max(1, std::min({p.max_tiles, 32, sms / std::max(1, ctas)}));  // merge handles <= 32
+    if (const char *e = getenv("OXY_ATTN_TC_SPLITS")) p.splits = std::max(1, std::min({p.max_tiles, 32, atoi(e)}));
     if (p.splits > 1) {
       attn_ws_need = std::max(attn_ws_need, (size_t)p.splits * p.rows * 256);
       attn_ml_need = std::max(attn_ml_need, (size_t)p.splits * p.rows * 2);
@@ -853,7 +853,7 @@ struct Model {
       // the SMs: one tile per split at 1 stream, measured best; fewer splits as
       // streams add query tiles)
       const int per = std::max(1, atoi(dn_tiles));
-      ap.splits = std::max(1, (ap.max_tiles + per - 1) / per);
+      ap.splits = std::min(32, std::max(1, (ap.max_tiles + per - 1) / per));
       if (ap.splits > 1) {
         attn_ws_need = std::max(attn_ws_need, (size_t)ap.splits * ap.rows * 256);
         attn_ml_need = std::max(attn_ml_need, (size_t)ap.splits * ap.rows * 2);
