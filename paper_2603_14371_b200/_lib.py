@@ -16,7 +16,10 @@ import re
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liboxygen_b200.so")
+# OXY_LIB_VARIANT=<name> loads liboxygen_b200.<name>.so from the same directory
+# (A/B builds of the same sources in one gpurun session); unset: the default build
+_VARIANT = os.environ.get("OXY_LIB_VARIANT")
+LIB_PATH = os.path.join(_HERE, f"liboxygen_b200.{_VARIANT}.so" if _VARIANT else "liboxygen_b200.so")
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "oxygen_b200.h")
 
 _lib = None
