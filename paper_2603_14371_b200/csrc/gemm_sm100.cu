@@ -46,6 +46,10 @@ struct Knobs {
     if (const char *s = getenv("OXY_GEMM_SMEM_KB")) smem_kb = std::max(64, std::min(200, atoi(s)));
   }
 };
+// per-enqueue override of the skinny early-PDL policy (-1: knob); set by the
+// model around one lane's enqueue (host calls are serial)
+int g_early_override = -1;
+
 static const Knobs &knobs() {
   static Knobs k;
   return k;
@@ -637,7 +641,8 @@ void launch(const void *w, const void *x, int n_out, int k, int t, const EpiPara
   kp.ws = ws;
   kp.counters = counters;
   kp.fixup = knobs().fixup;
-  kp.prefetch = kp.trigger = t <= 64 ? knobs().early_skinny : knobs().early_wide;
+  kp.prefetch = kp.trigger = t <= 64 ? (g_early_override >= 0 ? g_early_override : knobs().early_skinny)
+                                     : knobs().early_wide;
   dim3 grid(plan.n_tiles, plan.m_tiles, plan.splits);
   if (knobs().pdl) {
     launch_pdl(gemm_kernel, grid, dim3(192), smem_bytes(plan), st, ma, mb, kp);

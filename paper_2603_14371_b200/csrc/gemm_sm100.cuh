@@ -84,6 +84,10 @@ struct Plan {
   int cg;  // 0: one-tile-per-CTA kernel (skinny); 1 / 2: persistent wide kernel, 1-CTA / CTA-pair tiles
 };
 
+// Skinny-GEMM early PDL (weight prefetch before the wait + early dependent
+// launch) for the launches that follow: -1 = knob default, 0 / 1 = force.
+extern int g_early_override;
+
 // Host: build a plan for (N_out, K, T) on `sms` SMs.
 Plan make_plan(int n_out, int k, int t, int sms, int force_splits = 0);
 

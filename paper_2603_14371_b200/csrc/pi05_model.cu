@@ -1049,8 +1049,18 @@ struct Model {
   }
 
   // ------------------------------------------------------------ decode
+  // A/B: OXY_DECODE_EARLY=0 turns off early PDL for the decode lane's skinny
+  // GEMMs (their waiting CTAs then do not hold SMs the concurrent denoise needs)
+  int decode_early = [] {
+    const char *e = getenv("OXY_DECODE_EARLY");
+    return e ? atoi(e) : -1;
+  }();
   void decode(cudaStream_t caller, int rows, int k, const int *bt_h, int maxb, const int *seq_h, const int *last_h,
               const int *budget_h, const int *cow_h, int *out_tok_h, int *out_cnt_h, float *logits_h) {
+    struct EarlyScope {
+      explicit EarlyScope(int v) { gemm::g_early_override = v; }
+      ~EarlyScope() { gemm::g_early_override = -1; }
+    } early_scope(decode_early);
     const int W = c.width;
     int max_pos = 0;
     for (int r = 0; r < rows; ++r) {
