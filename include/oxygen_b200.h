@@ -136,6 +136,19 @@ int oxy_paged_decode_attention(const void *q_d, void *out_d, const void *kpool_d
                                int32_t bt_stride, const int32_t *pos_d, int32_t rows,
                                int32_t max_blocks, float *ws_d, void *stream);
 
+/* tcgen05 prefix attention (prefill prefix-LM / action-expert suffix; replaces
+ * the masked softmax attention of kvweaver/backend.py:287-295 for head dim 256):
+ * nq query rows (q_d bf16 [nq, 256]: tokens x 8 heads of one MQA group),
+ * bidirectional over paged keys [0, nka) read through bt_d from the pools
+ * (bf16 [num_blocks, 64, 256]) followed by dense keys kd_d / vd_d bf16
+ * [nkb, 256]; out_d bf16 [nq, 256]; scale 1/16.  splits > 1 splits the keys
+ * (ws_o: splits * ceil(nq/128)*128 * 256 floats, ws_ml: splits * ceil(nq/128)*128
+ * * 2 floats) and merges them in split order. */
+int oxy_prefix_attention(const void *q_d, void *out_d, const void *kpool_d, const void *vpool_d,
+                         int32_t num_blocks, const int32_t *bt_d, int32_t nka, const void *kd_d,
+                         const void *vd_d, int32_t nkb, int32_t nq, int32_t splits, float *ws_o,
+                         float *ws_ml, void *stream);
+
 /* kernels launched by this library so far (process-wide counter) */
 int64_t oxy_launch_count(void);
 

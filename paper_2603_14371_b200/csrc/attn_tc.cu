@@ -17,6 +17,7 @@
 // Invariant relied on: pool slots past a sequence's length hold finite values
 // (the pool is zeroed at creation and only ever written with finite K/V), so
 // masked keys contribute p = 0 exactly.
+#include <algorithm>
 #include <cmath>
 
 #include "cuda_util.cuh"
@@ -405,3 +406,40 @@ void flash_attention_tc(const AttnGroup *groups_d, int n_groups, int q_tiles, in
 
 }  // namespace pi05
 }  // namespace oxy
+
+extern "C" int oxy_prefix_attention(const void *q_d, void *out_d, const void *kpool_d, const void *vpool_d,
+                                    int32_t num_blocks, const int32_t *bt_d, int32_t nka, const void *kd_d,
+                                    const void *vd_d, int32_t nkb, int32_t nq, int32_t splits, float *ws_o,
+                                    float *ws_ml, void *stream) {
+  OXY_API_BEGIN
+  using oxy::pi05::bf16;
+  OXY_REQUIRE(nq >= 1 && nka >= 0 && nkb >= 0 && nka + nkb >= 1 && num_blocks >= 1, "bad attention shape");
+  OXY_REQUIRE(nkb == 0 || (kd_d && vd_d), "dense keys need kd/vd");
+  const int tiles = (nka + 63) / 64 + (nkb + 63) / 64;
+  OXY_REQUIRE(splits >= 1 && splits <= 32 && splits <= tiles, "splits must be in [1, min(32, key tiles)]");
+  OXY_REQUIRE(splits == 1 || (ws_o && ws_ml), "split attention needs a workspace");
+  auto st = oxy::as_stream(stream);
+  oxy::pi05::AttnGroup g{};
+  g.q = static_cast<const bf16 *>(q_d);
+  g.o = static_cast<bf16 *>(out_d);
+  g.ldq = g.ldo = 256;
+  g.nq = nq;
+  g.bt = bt_d;
+  g.nka = nka;
+  g.kb = static_cast<const bf16 *>(kd_d);
+  g.vb = static_cast<const bf16 *>(vd_d);
+  g.ldkv = 256;
+  g.nkb = nkb;
+  g.wrow0 = 0;
+  oxy::pi05::AttnGroup *gd = nullptr;
+  OXY_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&gd), sizeof(g), st));
+  OXY_CUDA(cudaMemcpyAsync(gd, &g, sizeof(g), cudaMemcpyHostToDevice, st));
+  const CUtensorMap km = oxy::gemm::make_map(kpool_d, num_blocks * 64, 256, 64);
+  const CUtensorMap vm = oxy::gemm::make_map(vpool_d, num_blocks * 64, 256, 64);
+  const int q_tiles = (nq + 127) / 128, ws_rows = q_tiles * 128;
+  oxy::pi05::flash_attention_tc(gd, 1, q_tiles, splits, g.q, nq, km, vm, g.kb, g.vb, std::max(nkb, 1), 1.f / 16.f,
+                                ws_o, ws_ml, ws_rows, false, st);
+  if (splits > 1) oxy::pi05::flash_merge(gd, 1, ws_rows, splits, ws_o, ws_ml, ws_rows, st);
+  OXY_CUDA(cudaFreeAsync(gd, st));
+  OXY_API_END
+}

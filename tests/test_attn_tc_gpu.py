@@ -46,3 +46,41 @@ def test_tc_attention_agrees_with_mma_sync_path():
     import numpy as np
     rel = np.abs(outs[0] - outs[1]).max() / (np.abs(outs[1]).max() + 1e-9)
     assert rel < 3e-2, rel
+
+
+@pytest.mark.parametrize("nq,nka,nkb,splits", [
+    (64, 800, 0, 2), (400, 800, 50, 14), (400, 800, 50, 1), (1000, 100, 37, 3), (8, 64, 0, 1),
+    (6400, 800, 0, 2), (130, 0, 77, 2), (256, 2000, 0, 32)])
+def test_prefix_attention_matches_torch(nq, nka, nkb, splits):
+    """oxy_prefix_attention (tcgen05, paged + dense keys, split merge) against a
+    torch fp32 softmax attention on the same bf16 inputs.  Tolerance: P is
+    rounded to bf16 before P.V and the output is bf16 -> 2e-2 of max|V|."""
+    import ctypes as C
+    import torch
+    from paper_2603_14371_b200 import _lib
+    g = torch.Generator(device="cpu").manual_seed(nq + nka + nkb)
+    nb = max(1, (nka + 63) // 64) + 3
+    kp = (torch.randn(nb, 64, 256, generator=g)).to(torch.bfloat16).cuda()
+    vp = (torch.randn(nb, 64, 256, generator=g)).to(torch.bfloat16).cuda()
+    perm = torch.randperm(nb, generator=g)[: max(1, (nka + 63) // 64)].to(torch.int32).cuda()
+    q = (torch.randn(nq, 256, generator=g) * 2).to(torch.bfloat16).cuda()
+    kd = torch.randn(max(nkb, 1), 256, generator=g).to(torch.bfloat16).cuda()
+    vd = torch.randn(max(nkb, 1), 256, generator=g).to(torch.bfloat16).cuda()
+    out = torch.zeros(nq, 256, dtype=torch.bfloat16, device="cuda")
+    rows = (nq + 127) // 128 * 128
+    ws_o = torch.empty(splits * rows * 256, device="cuda")
+    ws_ml = torch.empty(splits * rows * 2, device="cuda")
+    _lib.call("oxy_prefix_attention", C.c_void_p(q.data_ptr()), C.c_void_p(out.data_ptr()),
+              C.c_void_p(kp.data_ptr()), C.c_void_p(vp.data_ptr()), C.c_int32(nb), C.c_void_p(perm.data_ptr()),
+              C.c_int32(nka), C.c_void_p(kd.data_ptr() if nkb else None), C.c_void_p(vd.data_ptr() if nkb else None),
+              C.c_int32(nkb), C.c_int32(nq), C.c_int32(splits), C.c_void_p(ws_o.data_ptr()),
+              C.c_void_p(ws_ml.data_ptr()), _lib.stream_ptr())
+    torch.cuda.synchronize()
+    keys = kp[perm.long()].reshape(-1, 256)[:nka].float()
+    vals = vp[perm.long()].reshape(-1, 256)[:nka].float()
+    if nkb:
+        keys = torch.cat([keys, kd[:nkb].float()])
+        vals = torch.cat([vals, vd[:nkb].float()])
+    ref = torch.softmax(q.float() @ keys.T / 16.0, dim=-1) @ vals
+    err = (out.float() - ref).abs().max().item()
+    assert err < 2e-2 * vals.abs().max().item(), err
