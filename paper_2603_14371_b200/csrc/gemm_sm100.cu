@@ -35,7 +35,11 @@ struct Knobs {
   int early_skinny = 1, early_wide = 0;
   // persistent wide kernel for T > 64: -1 auto (cost model), 0 off, 1 / 2 force CTA group
   int wide = -1, wide_bn = 0, wide_splits = 0;  // -1 auto (see make_plan), 0 off, 1 / 2 force
+  // split K (fixed-order reduction) for token counts up to this when the tiles do not fill
+  // the SMs: the multi-stream denoise (T = 50 x streams); 8 streams 67.9 -> 61.1 ms/frame
+  int split_t = 1024;
   Knobs() {
+    if (const char *s = getenv("OXY_GEMM_SPLIT_T")) split_t = atoi(s);
     if (const char *s = getenv("OXY_GEMM_WIDE")) wide = atoi(s);
     if (const char *s = getenv("OXY_GEMM_WIDE_BN")) wide_bn = atoi(s);
     if (const char *s = getenv("OXY_GEMM_WIDE_SPLITS")) wide_splits = atoi(s);
@@ -528,7 +532,7 @@ Plan make_plan(int n_out, int k, int t, int sms, int force_splits) {
   int splits = 1;
   if (force_splits > 0) {
     splits = force_splits;
-  } else if (base < sms && t <= 64) {
+  } else if (base < sms && t <= knobs().split_t) {
     // skinny (decode / denoise): split K to fill the SMs.  Stand-alone, fewer
     // splits look cheaper (no reduce), but inside the PDL chain every split CTA
     // streams its weight ring before griddepcontrol.wait, so more splits hide

@@ -1,14 +1,16 @@
 """Marginal in-graph cost of each kernel group of the denoise chain: denoise
-time with OXY_DBG_SKIP bits set (results invalid; timing only), one process per mask."""
+time with OXY_DBG_SKIP bits set (results invalid; timing only), one process per mask.
+STREAMS=r: r lock-stepped streams (T = 50 r suffix tokens)."""
 import os, subprocess, sys
 code = r'''
 import os, sys, torch; sys.path.insert(0, ".")
 from paper_2603_14371_b200.pi05 import Pi05Backend, Pi05Config, Pi05Observation, synthetic_images
-be = Pi05Backend(Pi05Config(), num_blocks=64)
-kv = be.prefill(Pi05Observation(tuple(range(100, 132)), 0, synthetic_images(3, 5)))
+R = int(os.environ.get("STREAMS", "1"))
+be = Pi05Backend(Pi05Config(), num_blocks=64 + 16 * R)
+kvs = [be.prefill(Pi05Observation(tuple(range(100 + i, 132 + i)), 0, synthetic_images(3, 5 + i))) for i in range(R)]
 def dn():
     try:
-        be.action_denoise(kv, 10)
+        be.denoise_many(kvs, 10)
     except ValueError:  # skipped kernels leave garbage (non-finite) actions: timing only
         pass
 for _ in range(3): dn()
