@@ -241,3 +241,37 @@ def test_extra_tasks_share_prefix_blocks_with_copy_on_write():
     import gc
     gc.collect()
     assert be.allocator.num_free == free0
+
+
+def test_cross_variant_invariance_on_pi05_backend():
+    """The reference's acceptance criterion 3 (tests/test_acceptance.py:81-113) on
+    the pi0.5 backend: Unified, SharedNoBatch and IsolatedSequential produce the
+    same request set, greedy tokens and action chunks (exact equality), because
+    every kernel is batch-invariant and deterministic."""
+    from paper_2603_14371_b200.pi05 import TINY, Pi05Backend
+    from paper_2603_14371_b200.rng import SplitMix64
+    from paper_2603_14371_b200.sim_engine import SimConfig, run_simulation
+    from paper_2603_14371_b200.workload import WorkloadSpec
+    rng = SplitMix64(2026)
+    be = Pi05Backend(TINY, num_blocks=512)
+    compared = 0
+    for i in range(4):
+        pattern = ("OnePerFrame", "Uniform", "Poisson", "MixedLength")[i]
+        wl = WorkloadSpec(pattern=pattern, default_N=2 + rng.below(9), obs_len=2 + rng.below(9),
+                          num_frames=4 + rng.below(5), seed=rng.below(1 << 32), lam=0.25 + rng.uniform(),
+                          r=1 + rng.below(2), short_N=2 + rng.below(5), long_N=8 + rng.below(6),
+                          p_long=rng.uniform())
+        k = 1 + rng.below(6)
+        bc = BackendConfig(vocab=TINY.vocab)
+        runs = {v: run_simulation(SimConfig(variant=v, backend_kind="Pi05", backend_config=bc, workload=wl, k=k),
+                                  backend=be)
+                for v in ("Unified", "SharedNoBatch", "IsolatedSequential")}
+        base = runs["Unified"].transcript
+        for v in ("SharedNoBatch", "IsolatedSequential"):
+            other = runs[v].transcript
+            assert sorted(other) == sorted(base), (i, v)
+            for rid, entry in base.items():
+                assert other[rid].tokens == entry.tokens, (i, v, rid)
+                assert other[rid].action == entry.action, (i, v, rid)
+                compared += 1
+    assert compared > 0
