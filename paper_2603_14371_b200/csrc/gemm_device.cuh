@@ -296,41 +296,70 @@ __device__ __forceinline__ void epi_tile(const P &p, uint32_t trow, int c_begin,
 // bar_threads threads; `leader` does the tile-counter atomic) after they wrote
 // this CTA's partials: the last CTA of the tile to arrive sums the partials in
 // split order 0..S-1 (columns [c_begin, c_end) of feature f per thread) and
-// applies the epilogue.  16 columns x up to 4 splits of loads are in flight.
-template <typename P>
-__device__ __forceinline__ void splitk_fixup(const P &p, int tile, int n0, int c_begin, int c_end, int f, int &s_last,
-                                             int bar_threads, int leader) {
-  __threadfence();
-  asm volatile("bar.sync 1, %0;" ::"r"(bar_threads) : "memory");
-  if ((int)threadIdx.x == leader) s_last = atomicAdd(p.counters + tile, 1) == p.splits - 1;
-  asm volatile("bar.sync 1, %0;" ::"r"(bar_threads) : "memory");
-  if (s_last) {
-    __threadfence();
-    const int ce = min(c_end, p.t - n0);
-    const bool fok = f < p.n_out;
-    for (int c0 = c_begin; c0 < ce; c0 += 16) {
-      float acc[16];
+// applies the epilogue (mode fixed at compile time, as in epi_loop).
+template <int MODE, typename P>
+__device__ __forceinline__ void fixup_sum(const P &p, int n0, int c_begin, int c_end, int f) {
+  const int ce = min(c_end, p.t - n0);
+  const bool fok = f < p.n_out;
+  for (int c0 = c_begin; c0 < ce; c0 += 16) {
+    float acc[16];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) acc[j] = 0.f;
-      for (int s0 = 0; s0 < p.splits; s0 += 4) {
-        float v[4][16];
+    for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+    for (int s = 0; s < p.splits; ++s) {  // split order 0..S-1; 16 loads in flight per split
+      float v[16];
 #pragma unroll
-        for (int s = 0; s < 4; ++s)
+      for (int j = 0; j < 16; ++j)
+        v[j] = (fok && c0 + j < ce) ? __ldcg(p.ws + ((size_t)s * p.t + n0 + c0 + j) * p.n_out + f) : 0.f;
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            v[s][j] = (fok && s0 + s < p.splits && c0 + j < ce)
-                          ? __ldcg(p.ws + ((size_t)(s0 + s) * p.t + n0 + c0 + j) * p.n_out + f)
-                          : 0.f;
+      for (int j = 0; j < 16; ++j) acc[j] += v[j];
+    }
+    if constexpr (MODE == EPI_QKV_ROPE) {
+      const QkvRope &r = p.epi.rope;
+      const int i = (f & 255) >> 1;
 #pragma unroll
-        for (int s = 0; s < 4; ++s)
-#pragma unroll
-          for (int j = 0; j < 16; ++j) acc[j] += v[s][j];  // split order 0..S-1
+      for (int j = 0; j < 16; ++j) {
+        const int t = n0 + c0 + j;
+        const float pair = __shfl_xor_sync(0xffffffffu, acc[j], 1);
+        if (fok && c0 + j < ce) {
+          const float2 c = rope_cs(r, __ldg(r.pos + t), i);
+          rope_store(r, t, f, acc[j], pair, c.x, c.y);
+        }
       }
+    } else {
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const float pair = __shfl_xor_sync(0xffffffffu, acc[j], 1);
-        if (fok && c0 + j < ce) epilogue_store(p.epi, n0 + c0 + j, f, p.n_out, acc[j], pair);
+        if (fok && c0 + j < ce) epilogue_store<MODE>(p.epi, n0 + c0 + j, f, p.n_out, acc[j], pair);
       }
+    }
+  }
+}
+
+template <typename P>
+__device__ __forceinline__ void splitk_fixup(const P &p, int tile, int n0, int c_begin, int c_end, int f, int &s_last,
+                                             int bar_threads, int leader) {
+  // the CTA's partial stores are ordered before the leader's release by bar.sync
+  // (cumulativity); the leader's acquire + bar.sync orders the reads after every
+  // other split's release
+  asm volatile("bar.sync 1, %0;" ::"r"(bar_threads) : "memory");
+  if ((int)threadIdx.x == leader) {
+    int old;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(p.counters + tile) : "memory");
+    s_last = old == p.splits - 1;
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(bar_threads) : "memory");
+  if (s_last) {
+    switch (p.epi.mode) {
+      case EPI_F32: fixup_sum<EPI_F32>(p, n0, c_begin, c_end, f); break;
+      case EPI_BF16: fixup_sum<EPI_BF16>(p, n0, c_begin, c_end, f); break;
+      case EPI_ADD_F32: fixup_sum<EPI_ADD_F32>(p, n0, c_begin, c_end, f); break;
+      case EPI_GEGLU_BF16: fixup_sum<EPI_GEGLU_BF16>(p, n0, c_begin, c_end, f); break;
+      case EPI_GELU_BF16: fixup_sum<EPI_GELU_BF16>(p, n0, c_begin, c_end, f); break;
+      case EPI_ADD_BF16: fixup_sum<EPI_ADD_BF16>(p, n0, c_begin, c_end, f); break;
+      case EPI_ADD_GATED_F32: fixup_sum<EPI_ADD_GATED_F32>(p, n0, c_begin, c_end, f); break;
+      case EPI_SWISH_BF16: fixup_sum<EPI_SWISH_BF16>(p, n0, c_begin, c_end, f); break;
+      case EPI_QKV_ROPE: fixup_sum<EPI_QKV_ROPE>(p, n0, c_begin, c_end, f); break;
+      default: break;
     }
     if ((int)threadIdx.x == leader) p.counters[tile] = 0;
   }
