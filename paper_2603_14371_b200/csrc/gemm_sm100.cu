@@ -35,6 +35,7 @@ struct Knobs {
   int early_skinny = 1, early_wide = 0;
   // persistent wide kernel for T > 64: -1 auto (cost model), 0 off, 1 / 2 force CTA group
   int wide = -1, wide_bn = 0, wide_splits = 0;  // -1 auto (see make_plan), 0 off, 1 / 2 force
+  int wide_cl = 0;  // 0 auto, 1 / 2 force the pairs per cluster
   // split K (fixed-order reduction) for token counts up to this when the tiles do not fill
   // the SMs: the multi-stream denoise (T = 50 x streams); 8 streams 67.9 -> 61.1 ms/frame
   int split_t = 1024;
@@ -43,6 +44,7 @@ struct Knobs {
     if (const char *s = getenv("OXY_GEMM_WIDE")) wide = atoi(s);
     if (const char *s = getenv("OXY_GEMM_WIDE_BN")) wide_bn = atoi(s);
     if (const char *s = getenv("OXY_GEMM_WIDE_SPLITS")) wide_splits = atoi(s);
+    if (const char *s = getenv("OXY_GEMM_WIDE_CL")) wide_cl = atoi(s);
     if (const char *s = getenv("OXY_PDL_EARLY_SKINNY")) early_skinny = atoi(s);
     if (const char *s = getenv("OXY_PDL_EARLY_WIDE")) early_wide = atoi(s);
     if (const char *s = getenv("OXY_SPLITK")) fixup = std::string(s) == "fixup";
@@ -227,6 +229,21 @@ __global__ void __launch_bounds__(192, 2)
   }
 }
 
+__device__ __forceinline__ void tma_load_2d_pair_mc(const CUtensorMap *map, uint32_t bar_leader, uint32_t dst, int c0,
+                                                    int c1, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%4, %5}], [%2], %3;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_leader), "h"(mask), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_mask(uint32_t bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+      "h"(mask)
+      : "memory");
+}
+
 // ------------------------------------------------------------------ wide (prefill) GEMM
 //
 // Persistent, one CTA per SM (or one CTA pair per TPC with CG = 2), static
@@ -246,9 +263,15 @@ struct WParams {
 
 constexpr int WIDE_THREADS = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue (2 per TMEM lane quadrant)
 
-template <int CG>
+// CL = 2 (with CG = 2): a cluster of two CTA pairs works on two adjacent token
+// tiles of one weight tile; each CTA TMA-loads half of its 128 weight rows and
+// multicasts them to the same-rank CTA of the other pair, halving the weight
+// bytes read from L2 (the prefill GEMMs are L2-bandwidth bound at ~10 TB/s).
+// Stage reuse then needs both pairs' MMA commits (empty count = CL).
+template <int CG, int CL = 1>
 __global__ void __launch_bounds__(WIDE_THREADS, 1)
     gemm_wide_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, WParams p) {
+  static_assert(CL == 1 || CG == 2, "A multicast across pairs needs CTA pairs");
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~static_cast<uintptr_t>(1023));
@@ -262,8 +285,10 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
   __shared__ int s_last;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = CG == 2 ? cluster_rank() : 0;
-  const int unit = blockIdx.x / CG, units = gridDim.x / CG;
+  const uint32_t crank = CG == 2 ? cluster_rank() : 0;
+  const uint32_t rank = crank & 1, pp = crank >> 1;  // CTA within its pair, pair within the cluster
+  const int unit = blockIdx.x / (CG * CL), units = gridDim.x / (CG * CL);
+  const int ngr = (p.n_tiles + CL - 1) / CL;  // token-tile groups (one tile per pair)
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + MAX_STAGES),
                  tfull0 = smem_u32(bars + 2 * MAX_STAGES), tempty0 = smem_u32(bars + 2 * MAX_STAGES + 2);
   const uint32_t ncols = bn <= 128 ? (bn <= 64 ? 128u : 256u) : 512u;  // two accumulators
@@ -272,11 +297,11 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(full0 + 8 * s, 1);
-      mbar_init(empty0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, CL);  // one MMA commit per pair reading this stage's multicast A
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull0 + 8 * a, 1);
-      mbar_init(tempty0 + 8 * a, 8 * CG);  // one arrival per epilogue warp of each CTA
+      mbar_init(tempty0 + 8 * a, 8 * CG);  // one arrival per epilogue warp of each CTA of the pair
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
@@ -300,26 +325,35 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int per_m = p.splits * p.n_tiles;
+  const int per_m = p.splits * ngr;
 
   if (warp == 0) {
     if (lane == 0) {
-      const uint32_t full_l = CG == 2 ? map_to_rank(full0, 0) : full0;  // completion counted by the leader
+      // completion is counted on the pair leader's barrier: the cvta address of
+      // a cluster CTA carries its rank in bits 24+, so clearing bit 24 names it
+      const uint32_t full_l = full0 & ~(1u << 24);
+      const uint16_t a_mask = (uint16_t)((1u << rank) | (1u << (2 + rank)));  // same rank in both pairs
       int it = 0;
       bool waited = false;
       for (int tile = unit; tile < p.tiles; tile += units) {
         if (tile + units >= p.tiles) pdl_trigger();  // last tile: let the next kernel get scheduled
-        const int mt = tile / per_m, rem = tile % per_m, split = rem / p.n_tiles, nt = rem % p.n_tiles;
+        const int mt = tile / per_m, rem = tile % per_m, split = rem / ngr, nt = (rem % ngr) * CL + (int)pp;
         const int kb0 = split * p.kb_per_split;
         const int nkb = min(p.kb_total, kb0 + p.kb_per_split) - kb0;
-        const int arow = mt * BM * CG + (int)rank * BM, brow = nt * bn + (int)rank * b_rows;
+        const int arow = mt * BM * CG + (int)rank * BM + (CL == 2 ? (int)pp * (BM / 2) : 0),
+                  brow = nt * bn + (int)rank * b_rows;
         for (int i = 0; i < nkb; ++i, ++it) {
           const int s = it % stages;
           const uint32_t ph = (it / stages) & 1;
           mbar_wait(empty0 + 8 * s, ph ^ 1);
           if (rank == 0) mbar_expect_tx(full0 + 8 * s, CG * (A_STAGE_BYTES + b_bytes));
           const int kc = (kb0 + i) * BK;
-          if (CG == 2) {
+          if (CL == 2) {  // half of this CTA's weight rows, to both pairs
+            tma_load_2d_pair_mc(&tmA, full_l + 8 * s, smem_u32(sA + s * A_STAGE_BYTES + (int)pp * (A_STAGE_BYTES / 2)),
+                                kc, arow, a_mask);
+            if (!waited) { pdl_wait(); waited = true; }
+            tma_load_2d_pair(&tmB, full_l + 8 * s, smem_u32(sB + s * b_bytes), kc, brow);
+          } else if (CG == 2) {
             tma_load_2d_pair(&tmA, full_l + 8 * s, smem_u32(sA + s * A_STAGE_BYTES), kc, arow);
             if (!waited) { pdl_wait(); waited = true; }  // activations come from the previous kernel
             tma_load_2d_pair(&tmB, full_l + 8 * s, smem_u32(sB + s * b_bytes), kc, brow);
@@ -337,9 +371,10 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
       // kind::f16, bf16 x bf16 -> f32, K-major A/B, N = bn, M = 128 * CG
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(bn >> 3) << 17) |
                              ((uint32_t)((BM * CG) >> 4) << 24);
+      const uint16_t all_mask = (uint16_t)((1u << (CG * CL)) - 1), pair_mask = (uint16_t)(3u << (2 * pp));
       int it = 0, lt = 0;
       for (int tile = unit; tile < p.tiles; tile += units, ++lt) {
-        const int rem = tile % per_m, split = rem / p.n_tiles;
+        const int rem = tile % per_m, split = rem / ngr;
         const int kb0 = split * p.kb_per_split;
         const int nkb = min(p.kb_total, kb0 + p.kb_per_split) - kb0;
         const int acc = lt & 1;
@@ -359,10 +394,10 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
             else
               mma_bf16(d, make_sdesc(a + kk * 32), make_sdesc(b + kk * 32), idesc, (i | kk) != 0 ? 1u : 0u);
           }
-          if (CG == 2) mma_commit_pair(empty0 + 8 * s);
+          if (CG == 2) mma_commit_mask(empty0 + 8 * s, all_mask);  // both pairs may refill the stage
           else mma_commit(empty0 + 8 * s);
         }
-        if (CG == 2) mma_commit_pair(tfull0 + 8 * acc);
+        if (CG == 2) mma_commit_mask(tfull0 + 8 * acc, pair_mask);
         else mma_commit(tfull0 + 8 * acc);
       }
     }
@@ -374,10 +409,10 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
     const int chunks = bn / 16, c_mid = ((chunks + 1) / 2) * 16;
     const int cb = half ? c_mid : 0, ce = half ? bn : c_mid;
     const bool split_out = p.splits > 1;
-    const uint32_t tempty_l = CG == 2 ? map_to_rank(tempty0, 0) : tempty0;
+    const uint32_t tempty_l = CG == 2 ? map_to_rank(tempty0, 2 * pp) : tempty0;
     int lt = 0;
     for (int tile = unit; tile < p.tiles; tile += units, ++lt) {
-      const int mt = tile / per_m, rem = tile % per_m, split = rem / p.n_tiles, nt = rem % p.n_tiles;
+      const int mt = tile / per_m, rem = tile % per_m, split = rem / ngr, nt = (rem % ngr) * CL + (int)pp;
       const int acc = lt & 1;
       mbar_wait(tfull0 + 8 * acc, (lt >> 1) & 1);
       tc_fence_after();
@@ -391,7 +426,7 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
         if (CG == 2) mbar_arrive_cluster(tempty_l + 8 * acc);
         else mbar_arrive_local(tempty0 + 8 * acc);
       }
-      if (split_out && p.epi.mode != EPI_PARTIALS)
+      if (split_out && p.epi.mode != EPI_PARTIALS && nt < p.n_tiles)  // (the odd pair of a ragged group idles)
         splitk_fixup(p, (mt * p.n_tiles + nt) * CG + (int)rank, n0, cb, ce, f, s_last, WIDE_THREADS - 64, 64);
     }
   }
@@ -454,15 +489,17 @@ static int wide_stages(int bn, int cg) {
 // ingest = (16 KB of weights + bn/CG token rows of 128 B) at ~33 B/cycle/SM
 // (measured: the 2-CTA GEMM at T=800 streams 32-35 B/cycle/SM whether 80 or
 // 148 SMs are active).  Split-K pays a partial-sum round trip and a fix-up.
-static double wide_cost(int n_out, int kb_total, int t, int sms, int cg, int bn, int splits) {
+static double wide_cost(int n_out, int kb_total, int t, int sms, int cg, int bn, int splits, int cl = 1) {
   const int m_tiles = (n_out + BM * cg - 1) / (BM * cg), n_tiles = (t + bn - 1) / bn;
-  const int tiles = m_tiles * n_tiles * splits, units = sms / cg;
+  const int tiles = m_tiles * ((n_tiles + cl - 1) / cl) * splits, units = sms / (cg * cl);
   const int waves = (tiles + units - 1) / units;
   const int kbs = (kb_total + splits - 1) / splits;
-  const double mma = 2.0 * bn, bytes = A_STAGE_BYTES + (double)bn / cg * BK * 2;
+  // weight bytes per CTA and k-block are read from L2 once per cluster (multicast)
+  const double mma = 2.0 * bn, bytes = A_STAGE_BYTES / cl + (double)bn / cg * BK * 2;
   const double per_tile = kbs * std::max(mma, bytes / 33.0) + 600.0;
   double c = 3000.0 + waves * per_tile + 60.0 * bn;
   if (splits > 1) c += 2.0 * bn * 128 * 4 * splits / 33.0 + 1500.0;
+  if (cl > 1 && n_tiles % cl) c *= 1.0 + 0.5 / n_tiles;  // an idle pair on ragged token groups
   return c;
 }
 
@@ -471,17 +508,24 @@ static bool wide_plan(Plan &p, int n_out, int k, int t, int sms) {
   double best = 1e30;
   for (int cg = 1; cg <= 2; ++cg) {
     if (kn.wide > 0 && cg != kn.wide) continue;
-    for (int bn = 32; bn <= MAX_BN; bn += 16) {
-      if (kn.wide_bn && bn != kn.wide_bn) continue;
-      for (int splits = 1; splits <= 4; ++splits) {
-        if (kn.wide_splits && splits != kn.wide_splits) continue;
-        if (splits > 1 && p.kb_total / splits < 4) continue;
-        const double c = wide_cost(n_out, p.kb_total, t, sms, cg, bn, splits);
-        if (c < best * 0.999) {
-          best = c;
-          p.cg = cg;
-          p.bn = bn;
-          p.splits = splits;
+    for (int cl = 1; cl <= (cg == 2 ? 2 : 1); ++cl) {
+      // two pairs per cluster multicasting the weight tile is correct but measured
+      // slower (gate/up at T = 6400: 1139 vs 651 us), so only when forced
+      if (kn.wide_cl ? cl != kn.wide_cl : cl != 1) continue;
+      for (int bn = 32; bn <= MAX_BN; bn += 16) {
+        if (kn.wide_bn && bn != kn.wide_bn) continue;
+        if (cl == 2 && (t + bn - 1) / bn < 2) continue;
+        for (int splits = 1; splits <= 4; ++splits) {
+          if (kn.wide_splits && splits != kn.wide_splits) continue;
+          if (splits > 1 && p.kb_total / splits < 4) continue;
+          const double c = wide_cost(n_out, p.kb_total, t, sms, cg, bn, splits, cl);
+          if (c < best * 0.999) {
+            best = c;
+            p.cg = cg;
+            p.cl = cl;
+            p.bn = bn;
+            p.splits = splits;
+          }
         }
       }
     }
@@ -517,14 +561,22 @@ Plan make_plan(int n_out, int k, int t, int sms, int force_splits) {
   // T = 256 and for every projection once T >= 2048 (multi-stream prefill);
   // at 1-stream T = 800 the narrower shapes stay on the one-tile-per-CTA kernel
   // (profiles/r01_gemm_wide.md).  OXY_GEMM_WIDE: -1 auto, 0 off, 1 / 2 force.
+  // (K >= 8192 projections at T = 800 — the prefill down projection, 73.7 vs 98 us
+  // stand-alone with split-K 2 — measured slower in the frame: 9.37 vs 9.27 ms prefill)
   const bool wide_ok =
       knobs().wide > 0 || (knobs().wide < 0 && ((n_out >= 16384 && t >= 256) || t >= 2048));
   if (t > 64 && force_splits <= 0 && wide_ok && wide_plan(p, n_out, k, t, sms)) return p;
   p.cg = 0;
+  p.cl = 1;
   p.m_tiles = (n_out + BM - 1) / BM;
   p.n_tiles = (t + MAX_BN - 1) / MAX_BN;
-  // wide token dims (prefill): narrower token tiles until the grid fills the SMs
-  while (t > 64 && p.m_tiles * p.n_tiles < sms && (t + p.n_tiles) / (p.n_tiles + 1) >= 48) ++p.n_tiles;
+  // wide token dims (prefill): narrower token tiles while the grid still fits one
+  // CTA per SM.  Overshooting (e.g. 16 x 10 = 160 CTAs on 148 SMs) doubles 12 SMs
+  // up and makes them, at twice the per-CTA time, the critical path.
+  if (t > 64 && p.m_tiles * p.n_tiles < sms) {
+    const int n_fit = std::min(sms / p.m_tiles, std::max(1, t / 48));
+    p.n_tiles = std::max(p.n_tiles, n_fit);
+  }
   int per = (t + p.n_tiles - 1) / p.n_tiles;
   p.bn = std::max(16, (per + 15) / 16 * 16);
   p.n_tiles = (t + p.bn - 1) / p.bn;
@@ -562,6 +614,7 @@ static void launch_wide(const void *w, const void *x, int n_out, int k, int t, c
   if (!attr_set) {
     OXY_CUDA(cudaFuncSetAttribute(gemm_wide_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
     OXY_CUDA(cudaFuncSetAttribute(gemm_wide_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
+    OXY_CUDA(cudaFuncSetAttribute(gemm_wide_kernel<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
     attr_set = true;
   }
   static int sms = 0;
@@ -570,8 +623,8 @@ static void launch_wide(const void *w, const void *x, int n_out, int k, int t, c
     OXY_CUDA(cudaGetDevice(&dev));
     OXY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
-  const int cg = plan.cg;
-  CUtensorMap ma = make_map(w, n_out, k, BM);
+  const int cg = plan.cg, cl = plan.cl > 0 ? plan.cl : 1;
+  CUtensorMap ma = make_map(w, n_out, k, cl == 2 ? BM / 2 : BM);  // CL = 2: each CTA loads half its rows
   CUtensorMap mb = make_map(x, t, k, plan.bn / cg);
   WParams wp;
   wp.n_out = n_out;
@@ -584,13 +637,13 @@ static void launch_wide(const void *w, const void *x, int n_out, int k, int t, c
   wp.n_tiles = plan.n_tiles;
   wp.splits = plan.splits;
   wp.kb_per_split = (plan.kb_total + plan.splits - 1) / plan.splits;
-  wp.tiles = plan.m_tiles * plan.n_tiles * plan.splits;
+  wp.tiles = plan.m_tiles * ((plan.n_tiles + cl - 1) / cl) * plan.splits;
   wp.epi = epi;
   wp.ws = ws;
   wp.counters = counters;
-  const int units = std::min(wp.tiles, sms / cg);
+  const int units = std::min(wp.tiles, sms / (cg * cl));
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(units * cg);
+  cfg.gridDim = dim3(units * cg * cl);
   cfg.blockDim = dim3(WIDE_THREADS);
   cfg.dynamicSmemBytes = wide_smem_bytes(plan);
   cfg.stream = st;
@@ -603,14 +656,15 @@ static void launch_wide(const void *w, const void *x, int n_out, int k, int t, c
   }
   if (cg == 2) {
     attr[na].id = cudaLaunchAttributeClusterDimension;
-    attr[na].val.clusterDim.x = 2;
+    attr[na].val.clusterDim.x = 2 * cl;
     attr[na].val.clusterDim.y = 1;
     attr[na].val.clusterDim.z = 1;
     ++na;
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  if (cg == 2) OXY_CUDA(cudaLaunchKernelEx(&cfg, gemm_wide_kernel<2>, ma, mb, wp));
+  if (cg == 2 && cl == 2) OXY_CUDA(cudaLaunchKernelEx(&cfg, gemm_wide_kernel<2, 2>, ma, mb, wp));
+  else if (cg == 2) OXY_CUDA(cudaLaunchKernelEx(&cfg, gemm_wide_kernel<2>, ma, mb, wp));
   else OXY_CUDA(cudaLaunchKernelEx(&cfg, gemm_wide_kernel<1>, ma, mb, wp));
   __atomic_fetch_add(&g_launches, 1ull, __ATOMIC_RELAXED);
 }

@@ -82,6 +82,7 @@ constexpr int MAX_TILES = 1 << 16;  // split-K tile counters
 struct Plan {
   int bn, n_tiles, m_tiles, splits, stages, kb_total;
   int cg;  // 0: one-tile-per-CTA kernel (skinny); 1 / 2: persistent wide kernel, 1-CTA / CTA-pair tiles
+  int cl;  // wide kernel: CTA pairs per cluster sharing (multicasting) the weight tile (1 or 2)
 };
 
 // Skinny-GEMM early PDL (weight prefetch before the wait + early dependent
