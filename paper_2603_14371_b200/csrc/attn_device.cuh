@@ -187,8 +187,8 @@ __device__ __forceinline__ void flash_item(const AttnGroup &g, int qt, int split
     for (int nt = 0; nt < 8; ++nt) {
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const float mref = mx[e >> 1];
-        const float p = (mref == -INFINITY) ? 0.f : exp2f(s[nt][e] - mref);
+        const float mref = mx[e >> 1] == -INFINITY ? 0.f : mx[e >> 1];  // fully masked row: scores are -inf
+        const float p = exp2_approx(s[nt][e] - mref);
         s[nt][e] = p;
         rs[e >> 1] += p;
       }

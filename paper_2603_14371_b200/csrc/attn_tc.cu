@@ -13,12 +13,20 @@
 //              reference max (O and l are rescaled only when the row max grows
 //              by more than 2^8), P written bf16 to smem in the 128B-swizzled
 //              K-major layout the PV MMA reads; final O / l to bf16 rows, or
-//              fp32 partials + (m, l) for the split merge (fa_merge).
+//              fp32 partials + (m, l) for the split merge.
+// Split merge, two ways: (a) cluster merge — the splits of a query tile are one
+// thread-block cluster (<= 16 CTAs); each keeps its fp32 partial and (m, l) in
+// its own smem, and after a cluster barrier CTA k merges rows
+// [128k/splits, 128(k+1)/splits) of the tile by reading every peer's rows over
+// DSMEM, in split order, and writes the bf16 output (no workspace round trip,
+// no merge launch); (b) fp32 partials TMA-stored to a workspace, merged by
+// fa_merge (splits > 16, or OXY_ATTN_CMERGE=0).
 // Invariant relied on: pool slots past a sequence's length hold finite values
 // (the pool is zeroed at creation and only ever written with finite K/V), so
 // masked keys contribute p = 0 exactly.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "cuda_util.cuh"
 #include "gemm_device.cuh"
@@ -43,6 +51,7 @@ constexpr int N_BARS = 11;
 constexpr size_t SMEM = 1024 + OFF_BAR + N_BARS * 8 + 16;
 constexpr uint32_t TMEM_COLS = 512;  // O: 0..255, S buffers: 256.., 320..
 constexpr float LAZY = 8.f;          // rescale when the row max grows by > 2^8
+constexpr int MAX_CLUSTER = 16;      // cluster merge: splits per cluster (non-portable above 8)
 }  // namespace tc
 
 // MN-major, 128B-swizzled operand (V as the B operand: dims contiguous):
@@ -99,11 +108,42 @@ __device__ __forceinline__ void wd_wait(uint32_t bar, uint32_t parity, int tag) 
 #define MBW(bar, par, tag) mbar_wait(bar, par)
 #endif
 
+#ifdef OXY_ATTN_PROF
+// timing builds: %globaltimer at pipeline events of query tile 0, splits < 32
+// (the last launch wins), read back by oxy_debug_attn_prof()
+__device__ unsigned long long g_attn_prof[32][24];
+#define APROF(ev)                                                                  \
+  do {                                                                             \
+    if (blockIdx.x == 0 && blockIdx.y < 32) {                                      \
+      unsigned long long t_;                                                       \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                       \
+      g_attn_prof[blockIdx.y][ev] = t_;                                            \
+    }                                                                              \
+  } while (0)
+// stamp taken after `dep` is computed (the timer read takes it as an operand)
+#define APROF_DEP(ev, dep)                                                         \
+  do {                                                                             \
+    if (blockIdx.x == 0 && blockIdx.y < 32) {                                      \
+      unsigned long long t_;                                                       \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_) : "f"(dep));           \
+      g_attn_prof[blockIdx.y][ev] = t_;                                            \
+    }                                                                              \
+  } while (0)
+#else
+#define APROF_DEP(ev, dep) \
+  do {                     \
+  } while (0)
+#define APROF(ev) \
+  do {            \
+  } while (0)
+#endif
+
 struct TcAttnArgs {
   const AttnGroup *groups;
   int q_tiles, splits, ws_rows;
   const bf16 *q_base, *kd_base;  // row offsets of the groups' q / dense k,v pointers
   int kv_ready;  // 1: the paged K/V were not written by the previous kernel (prefetch before the PDL wait)
+  int cmerge;    // 1: launched as clusters of `splits` CTAs along y, merge over DSMEM
   float scale_log2;
   float *ws_o, *ws_ml;
 };
@@ -122,6 +162,7 @@ __global__ void __launch_bounds__(192, 1)
   const uint32_t b_q = smem_u32(bars), b_kvf = b_q + 8, b_kve = b_q + 24, b_sf = b_q + 40, b_se = b_q + 56,
                  b_pf = b_q + 72, b_od = b_q + 80;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) APROF(0);
 
   const AttnGroup g = a.groups[blockIdx.x / a.q_tiles];
   const int qt = blockIdx.x % a.q_tiles, q0 = qt * TQ;
@@ -158,7 +199,10 @@ __global__ void __launch_bounds__(192, 1)
   const uint32_t tmem = *tmem_slot;
   // let the next kernel (split merge / o-projection) be scheduled now: it waits
   // in griddepcontrol.wait for our outputs and meanwhile streams its weights
-  if (threadIdx.x == 0) pdl_trigger();
+  if (threadIdx.x == 0) {
+    pdl_trigger();
+    APROF(1);
+  }
 
   if (warp == 0) {
     if (lane == 0 && n > 0) {
@@ -181,6 +225,7 @@ __global__ void __launch_bounds__(192, 1)
       if (a.kv_ready)
         for (; i < n && i < 2 && t0 + i < ta; ++i) issue(i);
       pdl_wait();  // Q (and dense K/V) come from the previous kernel
+      APROF(2);
       const int qrow = (int)((g.q - a.q_base) / HD) + q0;
       mbar_expect_tx(b_q, Q_BYTES);
       for (int b = 0; b < 4; ++b) tma_load_2d(&qmap, b_q, smem_u32(sm + b * Q_BOX), b * 64, qrow);
@@ -195,6 +240,7 @@ __global__ void __launch_bounds__(192, 1)
                                ((uint32_t)(TQ >> 4) << 24);
       const uint32_t q_s = smem_u32(sm), p_s = smem_u32(sm + OFF_P);
       MBW(b_q, 0, 2);
+      APROF(3);
       auto issue_pv = [&](int i) {
         MBW(b_pf, i & 1, 3);
         tc_fence_after();
@@ -226,6 +272,7 @@ __global__ void __launch_bounds__(192, 1)
   } else {
     // softmax / epilogue: thread = query row
     pdl_wait();  // outputs / workspace may still be read by earlier kernels
+    if (threadIdx.x == 64) APROF(4);
     const int quad = warp & 3, row = quad * 32 + lane;
     const uint32_t lanes = (uint32_t)(quad * 32) << 16;
     const int r = q0 + row;
@@ -236,6 +283,7 @@ __global__ void __launch_bounds__(192, 1)
       const int nvalid = j < ta ? min(TK, g.nka - j * TK) : min(TK, g.nkb - (j - ta) * TK);
       MBW(b_sf + 8 * s, (i >> 1) & 1, 6);
       tc_fence_after();
+      if (threadIdx.x == 64 && i < 2) APROF(i == 0 ? 5 : 16);
       float sc[TK];
       {
         uint32_t v[4][16];
@@ -247,6 +295,7 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
           for (int e = 0; e < 16; ++e) sc[c * 16 + e] = __uint_as_float(v[c][e]);
       }
+      if (threadIdx.x == 64 && i == 0) APROF_DEP(19, sc[63]);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_local(b_se + 8 * s);  // S buffer may be overwritten
@@ -256,6 +305,7 @@ __global__ void __launch_bounds__(192, 1)
         sc[e] = e < nvalid ? sc[e] * a.scale_log2 : -INFINITY;
         mx = fmaxf(mx, sc[e]);
       }
+      if (threadIdx.x == 64 && i < 2) APROF_DEP(i == 0 ? 14 : 17, mx);
       float corr = 1.f;
       if (mx > m_ref + LAZY || (m_ref == -INFINITY && mx > -INFINITY)) {
         corr = m_ref == -INFINITY ? 0.f : exp2f(m_ref - mx);
@@ -263,15 +313,17 @@ __global__ void __launch_bounds__(192, 1)
       }
       float rs = 0.f;
       uint32_t pk[TK / 2];
+      const float mref = m_ref == -INFINITY ? 0.f : m_ref;  // fully masked so far: every score is -inf
 #pragma unroll
       for (int e = 0; e < TK; e += 2) {
-        const float p0 = m_ref == -INFINITY ? 0.f : exp2f(sc[e] - m_ref);
-        const float p1 = m_ref == -INFINITY ? 0.f : exp2f(sc[e + 1] - m_ref);
+        const float p0 = exp2_approx(sc[e] - mref);
+        const float p1 = exp2_approx(sc[e + 1] - mref);
         rs += p0 + p1;
         __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
         pk[e / 2] = *reinterpret_cast<uint32_t *>(&h);
       }
       l = l * corr + rs;
+      if (threadIdx.x == 64 && i < 2) APROF_DEP(i == 0 ? 15 : 18, l);
       // PV(i-1) must be complete before O is rescaled and before P is overwritten
       if (i > 0) {
         MBW(b_od, (i - 1) & 1, 7);
@@ -298,12 +350,14 @@ __global__ void __launch_bounds__(192, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_local(b_pf);
+      if (threadIdx.x == 64) APROF(6);
     }
     // epilogue
     if (n > 0) {
       MBW(b_od, (n - 1) & 1, 8);
       tc_fence_after();
     }
+    if (threadIdx.x == 64) APROF(7);
     const bool ok = r < g.nq;
     if (a.splits == 1) {
       const float inv = l > 0.f ? 1.f / l : 0.f;
@@ -352,14 +406,19 @@ __global__ void __launch_bounds__(192, 1)
           *reinterpret_cast<uint4 *>(rowp + ((ch ^ (row & 7)) << 4)) =
               make_uint4(v[4 * ch], v[4 * ch + 1], v[4 * ch + 2], v[4 * ch + 3]);
       }
-      if (ok) {
-        const size_t wr = (size_t)split * a.ws_rows + g.wrow0 + r;
-        a.ws_ml[wr * 2] = m_ref;
-        a.ws_ml[wr * 2 + 1] = l;
+      if (a.cmerge) {  // (m, l) next to the partial; peers read both after the cluster barrier
+        reinterpret_cast<float2 *>(sm + OFF_P)[row] = make_float2(m_ref, l);
+      } else {
+        if (ok) {
+          const size_t wr = (size_t)split * a.ws_rows + g.wrow0 + r;
+          a.ws_ml[wr * 2] = m_ref;
+          a.ws_ml[wr * 2 + 1] = l;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("bar.sync 3, 128;" ::: "memory");
-      if (threadIdx.x == 64) {
+      if (threadIdx.x == 64) APROF(8);
+      if (threadIdx.x == 64 && !a.cmerge) {
         const int row0 = split * a.ws_rows + g.wrow0 + q0;
         for (int b = 0; b < HD / 32; ++b)
           asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
@@ -367,27 +426,105 @@ __global__ void __launch_bounds__(192, 1)
                        "r"(b * 32), "r"(row0), "r"(smem_u32(stage + b * (TQ * 128)))
                        : "memory");
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        // smem may be released once the copies have READ it; the global writes
+        // complete before the grid does (what the merge waits for)
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        APROF(9);
       }
     }
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) APROF(10);
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
   }
+  if (a.cmerge) {
+    cluster_sync_all();  // every split's partial and (m, l) are staged
+    if (threadIdx.x == 0) APROF(11);
+    const int cs = a.splits;
+    const int rb = split * TQ / cs, re = min((split + 1) * TQ / cs, g.nq - q0);
+    const int nr = max(0, re - rb);
+    float *wgt = reinterpret_cast<float *>(sm + OFF_V);  // [nr][16]: split weight / L per row
+    const uint32_t ml_s = smem_u32(sm + OFF_P), st_s = smem_u32(sm);
+    for (int i = threadIdx.x; i < nr; i += blockDim.x) {
+      const int row = rb + i;
+      float m[16], lv[16], M = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j < cs) {
+          asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];"
+                       : "=f"(m[j]), "=f"(lv[j])
+                       : "r"(map_to_rank(ml_s + row * 8, j))
+                       : "memory");
+          M = fmaxf(M, m[j]);
+        }
+      float L = 0.f;
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j < cs) {
+          m[j] = m[j] == -INFINITY ? 0.f : exp2f(m[j] - M);
+          L += lv[j] * m[j];
+        }
+      const float inv = L > 0.f ? 1.f / L : 0.f;
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j < cs) wgt[i * 16 + j] = m[j] * inv;
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < nr * (HD / 4); idx += blockDim.x) {
+      const int i = idx / (HD / 4), c4 = idx % (HD / 4), row = rb + i;
+      // float4 c4 of the row: box c4/8 (32 floats), 16-byte chunk (c4%8) ^ (row%8)
+      const uint32_t off = (c4 >> 3) * (TQ * 128) + row * 128 + (((c4 & 7) ^ (row & 7)) << 4);
+      float4 v[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j < cs)
+          asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                       : "=f"(v[j].x), "=f"(v[j].y), "=f"(v[j].z), "=f"(v[j].w)
+                       : "r"(map_to_rank(st_s + off, j))
+                       : "memory");
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j < cs) {  // split order
+          const float w = wgt[i * 16 + j];
+          acc.x += w * v[j].x;
+          acc.y += w * v[j].y;
+          acc.z += w * v[j].z;
+          acc.w += w * v[j].w;
+        }
+      __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x, acc.y), hi = __floats2bfloat162_rn(acc.z, acc.w);
+      *reinterpret_cast<uint2 *>(g.o + (size_t)(q0 + row) * g.ldo + c4 * 4) =
+          make_uint2(*reinterpret_cast<uint32_t *>(&lo), *reinterpret_cast<uint32_t *>(&hi));
+    }
+    if (threadIdx.x == 0) APROF(12);
+    cluster_sync_all();  // peers may still be reading this CTA's smem
+    if (threadIdx.x == 0) APROF(13);
+  }
+}
+
+int attn_cluster_merge_max() {
+  static const int v = [] {
+    const char *e = getenv("OXY_ATTN_CMERGE");
+    return std::min(tc::MAX_CLUSTER, e ? atoi(e) : tc::MAX_CLUSTER);
+  }();
+  return v;
 }
 
 void flash_attention_tc(const AttnGroup *groups_d, int n_groups, int q_tiles, int splits, const bf16 *q_base,
                         int q_rows, const CUtensorMap &kpool_map, const CUtensorMap &vpool_map, const bf16 *kd_base,
                         const bf16 *vd_base, int kd_rows, float scale, float *ws_o, float *ws_ml, int ws_rows,
-                        bool kv_ready, cudaStream_t st) {
+                        bool kv_ready, bool cmerge, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     OXY_CUDA(cudaFuncSetAttribute(flash_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::SMEM));
+    OXY_CUDA(cudaFuncSetAttribute(flash_tc_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     attr = true;
   }
+  cmerge = cmerge && splits > 1;
+  if (cmerge && splits > tc::MAX_CLUSTER) fail(OXY_EINVAL, "cluster merge needs splits <= %d", tc::MAX_CLUSTER);
   if (n_groups <= 0 || q_tiles <= 0) return;
   const CUtensorMap qm = gemm::make_map(q_base, q_rows, tc::HD, tc::TQ);
   // dense suffix K/V (or the pool maps again when there is none)
@@ -395,13 +532,13 @@ void flash_attention_tc(const AttnGroup *groups_d, int n_groups, int q_tiles, in
   const CUtensorMap vdm = vd_base ? gemm::make_map(vd_base, kd_rows, tc::HD, tc::TK) : vpool_map;
   if (kd_base && vd_base - kd_base != 0 && (vd_base - kd_base) % tc::HD != 0)
     fail(OXY_EINVAL, "dense K/V buffers must be row-aligned");
-  if (splits > 1 && ws_rows % tc::TQ != 0) fail(OXY_EINVAL, "attention workspace rows must be padded to 128");
+  if (splits > 1 && !cmerge && ws_rows % tc::TQ != 0) fail(OXY_EINVAL, "attention workspace rows must be padded to 128");
   // fp32 partial rows [splits * ws_rows, 256], box 32 x 128 (128-byte rows), 128B swizzle
-  const CUtensorMap wsm = splits > 1 ? gemm::make_map_f32(ws_o, splits * ws_rows, tc::HD, 32, tc::TQ) : qm;
-  TcAttnArgs a{groups_d, q_tiles, splits, ws_rows, q_base, kd_base, kv_ready ? 1 : 0, scale * 1.4426950408889634f,
-               ws_o, ws_ml};
-  launch_pdl(flash_tc_kernel, dim3(n_groups * q_tiles, splits), dim3(192), tc::SMEM, st, qm, kpool_map, vpool_map,
-             kdm, vdm, wsm, a);
+  const CUtensorMap wsm = splits > 1 && !cmerge ? gemm::make_map_f32(ws_o, splits * ws_rows, tc::HD, 32, tc::TQ) : qm;
+  TcAttnArgs a{groups_d, q_tiles, splits, ws_rows, q_base, kd_base, kv_ready ? 1 : 0, cmerge ? 1 : 0,
+               scale * 1.4426950408889634f, ws_o, ws_ml};
+  launch_pdl_cluster(flash_tc_kernel, dim3(n_groups * q_tiles, splits), dim3(192), tc::SMEM, st,
+                     dim3(1, cmerge ? splits : 1, 1), qm, kpool_map, vpool_map, kdm, vdm, wsm, a);
 }
 
 }  // namespace pi05
@@ -417,7 +554,8 @@ extern "C" int oxy_prefix_attention(const void *q_d, void *out_d, const void *kp
   OXY_REQUIRE(nkb == 0 || (kd_d && vd_d), "dense keys need kd/vd");
   const int tiles = (nka + 63) / 64 + (nkb + 63) / 64;
   OXY_REQUIRE(splits >= 1 && splits <= 32 && splits <= tiles, "splits must be in [1, min(32, key tiles)]");
-  OXY_REQUIRE(splits == 1 || (ws_o && ws_ml), "split attention needs a workspace");
+  const bool cm = splits > 1 && splits <= oxy::pi05::attn_cluster_merge_max();
+  OXY_REQUIRE(splits == 1 || cm || (ws_o && ws_ml), "split attention needs a workspace");
   auto st = oxy::as_stream(stream);
   oxy::pi05::AttnGroup g{};
   g.q = static_cast<const bf16 *>(q_d);
@@ -438,8 +576,14 @@ extern "C" int oxy_prefix_attention(const void *q_d, void *out_d, const void *kp
   const CUtensorMap vm = oxy::gemm::make_map(vpool_d, num_blocks * 64, 256, 64);
   const int q_tiles = (nq + 127) / 128, ws_rows = q_tiles * 128;
   oxy::pi05::flash_attention_tc(gd, 1, q_tiles, splits, g.q, nq, km, vm, g.kb, g.vb, std::max(nkb, 1), 1.f / 16.f,
-                                ws_o, ws_ml, ws_rows, false, st);
-  if (splits > 1) oxy::pi05::flash_merge(gd, 1, ws_rows, splits, ws_o, ws_ml, ws_rows, st);
+                                ws_o, ws_ml, ws_rows, false, cm, st);
+  if (splits > 1 && !cm) oxy::pi05::flash_merge(gd, 1, ws_rows, splits, ws_o, ws_ml, ws_rows, st);
   OXY_CUDA(cudaFreeAsync(gd, st));
   OXY_API_END
 }
+
+#ifdef OXY_ATTN_PROF
+extern "C" int oxy_debug_attn_prof(unsigned long long *out) {
+  return cudaMemcpyFromSymbol(out, oxy::pi05::g_attn_prof, sizeof(oxy::pi05::g_attn_prof)) == cudaSuccess ? 0 : -1;
+}
+#endif

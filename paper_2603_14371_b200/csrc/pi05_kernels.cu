@@ -110,9 +110,6 @@ void permute_rows(bf16 *dst, const bf16 *src, int rows, int cols, cudaStream_t s
   OXY_LAUNCH_CHECK();
 }
 
-// RoPE inverse frequencies theta^(-2i/256), computed in double on the host.
-__constant__ float c_rope_inv[128];
-
 __global__ void rope_table_kernel(float2 *cs, const float *inv_freq, int n) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= n) return;
@@ -126,56 +123,6 @@ void rope_table(float2 *cs, const float *inv_freq, int n_pos, cudaStream_t st) {
   const int n = n_pos * 128;
   rope_table_kernel<<<(n + 255) / 256, 256, 0, st>>>(cs, inv_freq, n);
   OXY_LAUNCH_CHECK();
-}
-
-void set_rope_theta(float theta) {
-  float inv[128];
-  for (int i = 0; i < 128; ++i) inv[i] = (float)std::pow((double)theta, -2.0 * (double)i / (double)HEAD_DIM);
-  OXY_CUDA(cudaMemcpyToSymbol(c_rope_inv, inv, sizeof(inv)));
-}
-
-// One CTA per token; thread i < 128 owns rotary pair (i, i+128) of every head.
-__global__ void rope_split_kernel(const float *__restrict__ qkv, int n_qh, const int *pos, const int *slot,
-                                  const int *active, bf16 *__restrict__ q_out, bf16 *kpool, bf16 *vpool,
-                                  bf16 *k_dense, bf16 *v_dense, float theta) {
-  pdl_trigger();
-  pdl_wait();
-  const int t = blockIdx.x;
-  if (active && !active[t]) return;
-  const int ld = (n_qh + 2) * HEAD_DIM;
-  const float *row = qkv + (size_t)t * ld;
-  const int i = threadIdx.x;  // 0..127
-  const float inv = c_rope_inv[i];
-  float sn, cs;
-  sincosf((float)pos[t] * inv, &sn, &cs);
-  const int s = slot ? slot[t] : -1;
-  bf16 *kdst = s >= 0 ? kpool + (size_t)s * HEAD_DIM : (k_dense ? k_dense + (size_t)t * HEAD_DIM : nullptr);
-  bf16 *vdst = s >= 0 ? vpool + (size_t)s * HEAD_DIM : (v_dense ? v_dense + (size_t)t * HEAD_DIM : nullptr);
-  float x1[Q_HEADS + 2], x2[Q_HEADS + 2];  // all loads first (n_qh == Q_HEADS)
-#pragma unroll
-  for (int h = 0; h < Q_HEADS + 2; ++h) {
-    x1[h] = __ldg(row + h * HEAD_DIM + i);
-    x2[h] = __ldg(row + h * HEAD_DIM + i + 128);
-  }
-#pragma unroll
-  for (int h = 0; h <= Q_HEADS; ++h) {
-    bf16 *dst = h < Q_HEADS ? q_out + (size_t)t * Q_HEADS * HEAD_DIM + h * HEAD_DIM : kdst;
-    if (dst) {
-      dst[i] = __float2bfloat16(x1[h] * cs - x2[h] * sn);
-      dst[i + 128] = __float2bfloat16(x2[h] * cs + x1[h] * sn);
-    }
-  }
-  if (vdst) {
-    vdst[i] = __float2bfloat16(x1[Q_HEADS + 1]);
-    vdst[i + 128] = __float2bfloat16(x2[Q_HEADS + 1]);
-  }
-}
-
-void rope_split(const float *qkv, int T, int n_qh, const int *pos, const int *slot,
-                const int *active, bf16 *q_out, bf16 *kpool, bf16 *vpool, bf16 *k_dense,
-                bf16 *v_dense, float theta, cudaStream_t st) {
-  if (T <= 0) return;
-  launch_pdl(rope_split_kernel, dim3(T), dim3(128), 0, st, qkv, n_qh, pos, slot, active, q_out, kpool, vpool, k_dense, v_dense, theta);
 }
 
 __global__ void patchify_kernel(const uint8_t *img, bf16 *patches, int kpad) {
@@ -430,166 +377,6 @@ void flash_attention(const AttnGroup *groups_d, int n_groups, int max_q_tiles, i
 
 constexpr int DA_PART = Q_HEADS * (HEAD_DIM + 2);
 
-__global__ void decode_merge_kernel(const float *ws, bf16 *out, const int *pos, const int *active,
-                                    int max_blocks) {
-  pdl_trigger();
-  pdl_wait();
-  const int r = blockIdx.x, h = blockIdx.y, d = threadIdx.x;
-  if (active && !active[r]) return;
-  const int nb = (pos[r] + 1 + KV_BLOCK - 1) / KV_BLOCK;
-  const float *base = ws + (size_t)r * max_blocks * DA_PART + h * (HEAD_DIM + 2);
-  float M = -INFINITY;
-  for (int b = 0; b < nb; ++b) M = fmaxf(M, base[(size_t)b * DA_PART + HEAD_DIM]);
-  float L = 0.f, acc = 0.f;
-  for (int b = 0; b < nb; ++b) {
-    const float *p = base + (size_t)b * DA_PART;
-    const float w = exp2f(p[HEAD_DIM] - M);
-    L += p[HEAD_DIM + 1] * w;
-    acc += p[d] * w;
-  }
-  out[(size_t)r * Q_HEADS * HEAD_DIM + h * HEAD_DIM + d] = __float2bfloat16(acc / L);
-}
-
-// CTA = (row, 64-key block), 4 warps.  The
-// block's K and V (2 x 32 KB, one pool block per layer) are staged in smem
-// with 16-byte cp.async; the 8 query heads are the 16-row MMA A tile (rows
-// 8..15 zero); warp w owns keys 16w..16w+15: S = Q K^T (16 MMAs x 2), online
-// softmax in registers, O = P V (32 MMAs), then the 4 warps' (m, l, O) are
-// merged in smem into one partial per block.  HBM-bound: 64 KB per CTA.
-constexpr int DM_LDS = HEAD_DIM + 8;
-constexpr size_t DM_SMEM = (size_t)(16 + 2 * KV_BLOCK) * DM_LDS * sizeof(bf16);
-
-__global__ void __launch_bounds__(128)
-    decode_attn_mma_kernel(const bf16 *q, const bf16 *kpool, const bf16 *vpool, const int *bt, int bt_stride,
-                           const int *pos, const int *active, int max_blocks, float scale_log2, float *ws) {
-  pdl_trigger();
-  pdl_wait();
-  extern __shared__ __align__(16) unsigned char dm_smem[];
-  bf16 *sQ = reinterpret_cast<bf16 *>(dm_smem);
-  bf16 *sK = sQ + 16 * DM_LDS;
-  bf16 *sV = sK + KV_BLOCK * DM_LDS;
-  const int r = blockIdx.x, blk = blockIdx.y;
-  if (active && !active[r]) return;
-  const int n_keys = pos[r] + 1;
-  const int k0 = blk * KV_BLOCK;
-  if (k0 >= n_keys) return;
-  const int nvalid = min(KV_BLOCK, n_keys - k0);
-  const int b = bt[(size_t)r * bt_stride + blk];
-  const bf16 *kb = kpool + (size_t)b * KV_BLOCK * HEAD_DIM;
-  const bf16 *vb = vpool + (size_t)b * KV_BLOCK * HEAD_DIM;
-  const bf16 *qr = q + (size_t)r * Q_HEADS * HEAD_DIM;
-  for (int i = threadIdx.x; i < KV_BLOCK * 32; i += 128) {
-    const int row = i >> 5, ch = i & 31;
-    if (row < nvalid) {
-      cp_async16(smem_addr(sK + row * DM_LDS + ch * 8), kb + (size_t)row * HEAD_DIM + ch * 8);
-      cp_async16(smem_addr(sV + row * DM_LDS + ch * 8), vb + (size_t)row * HEAD_DIM + ch * 8);
-    } else {
-      *reinterpret_cast<int4 *>(sK + row * DM_LDS + ch * 8) = make_int4(0, 0, 0, 0);
-      *reinterpret_cast<int4 *>(sV + row * DM_LDS + ch * 8) = make_int4(0, 0, 0, 0);
-    }
-  }
-  for (int i = threadIdx.x; i < 16 * 32; i += 128) {
-    const int row = i >> 5, ch = i & 31;
-    if (row < Q_HEADS) cp_async16(smem_addr(sQ + row * DM_LDS + ch * 8), qr + (size_t)row * HEAD_DIM + ch * 8);
-    else *reinterpret_cast<int4 *>(sQ + row * DM_LDS + ch * 8) = make_int4(0, 0, 0, 0);
-  }
-  cp_commit();
-  cp_wait<0>();
-  __syncthreads();
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-  const uint32_t qa = smem_addr(sQ + (lane & 15) * DM_LDS + (lane >> 4) * 8);
-  const int kkey = warp * 16 + (lane & 7) + ((lane >> 4) << 3);
-  const uint32_t ka = smem_addr(sK + kkey * DM_LDS + ((lane >> 3) & 1) * 8);
-#pragma unroll
-  for (int kk = 0; kk < HEAD_DIM / 16; ++kk) {
-    uint32_t a0, a1, a2, a3, b0, b1, b2, b3;
-    ldsm_x4(qa + kk * 32, a0, a1, a2, a3);
-    ldsm_x4(ka + kk * 32, b0, b1, b2, b3);
-    mma16816(s[0], a0, a1, a2, a3, b0, b1);
-    mma16816(s[1], a0, a1, a2, a3, b2, b3);
-  }
-  // softmax over this warp's 16 keys for query row g = lane >> 2 (heads; rows 8..15 pad)
-  float mx = -INFINITY;
-#pragma unroll
-  for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int key = warp * 16 + nt * 8 + (lane & 3) * 2 + (e & 1);
-      float v = s[nt][e] * scale_log2;
-      if (key >= nvalid) v = -INFINITY;
-      s[nt][e] = v;
-      if (e < 2) mx = fmaxf(mx, v);
-    }
-  mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-  mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-  float l = 0.f;
-#pragma unroll
-  for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const float p = (e < 2 && mx != -INFINITY) ? exp2f(s[nt][e] - mx) : 0.f;
-      s[nt][e] = p;
-      l += p;
-    }
-  l += __shfl_xor_sync(0xffffffffu, l, 1);
-  l += __shfl_xor_sync(0xffffffffu, l, 2);
-  const uint32_t pa0 = pack_bf16(s[0][0], s[0][1]), pa1 = pack_bf16(s[0][2], s[0][3]);
-  const uint32_t pa2 = pack_bf16(s[1][0], s[1][1]), pa3 = pack_bf16(s[1][2], s[1][3]);
-  float o[32][4];
-#pragma unroll
-  for (int i = 0; i < 32; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
-  const uint32_t va = smem_addr(sV + (warp * 16 + (lane & 15)) * DM_LDS + (lane >> 4) * 8);
-#pragma unroll
-  for (int np = 0; np < 16; ++np) {
-    uint32_t b0, b1, b2, b3;
-    ldsm_x4_t(va + np * 32, b0, b1, b2, b3);
-    mma16816(o[2 * np], pa0, pa1, pa2, pa3, b0, b1);
-    mma16816(o[2 * np + 1], pa0, pa1, pa2, pa3, b2, b3);
-  }
-  __syncthreads();  // K/V smem is reused for the cross-warp merge
-  float *sO = reinterpret_cast<float *>(sK);                  // [4][8][256]
-  float *sM = reinterpret_cast<float *>(sQ);                  // [4][8] m, then [4][8] l
-  const int g = lane >> 2;
-#pragma unroll
-  for (int nt = 0; nt < 32; ++nt) {
-    const int c = nt * 8 + (lane & 3) * 2;
-    sO[(warp * 8 + g) * HEAD_DIM + c] = o[nt][0];
-    sO[(warp * 8 + g) * HEAD_DIM + c + 1] = o[nt][1];
-  }
-  if ((lane & 3) == 0) {
-    sM[warp * 8 + g] = mx;
-    sM[32 + warp * 8 + g] = l;
-  }
-  __syncthreads();
-  float *part = ws + ((size_t)r * max_blocks + blk) * DA_PART;
-  for (int i = threadIdx.x; i < Q_HEADS * HEAD_DIM; i += 128) {
-    const int h = i / HEAD_DIM, d = i % HEAD_DIM;
-    float M = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) M = fmaxf(M, sM[w * 8 + h]);
-    float acc = 0.f;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      const float mw = sM[w * 8 + h];
-      if (mw != -INFINITY) acc += sO[(w * 8 + h) * HEAD_DIM + d] * exp2f(mw - M);
-    }
-    part[h * (HEAD_DIM + 2) + d] = acc;
-    if (d == 0) {
-      float L = 0.f;
-#pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        const float mw = sM[w * 8 + h];
-        if (mw != -INFINITY) L += sM[32 + w * 8 + h] * exp2f(mw - M);
-      }
-      part[h * (HEAD_DIM + 2) + HEAD_DIM] = M;
-      part[h * (HEAD_DIM + 2) + HEAD_DIM + 1] = L;
-    }
-  }
-}
-
-// ---- v3 (used): TMA-fed, chunked, pipelined ----------------------------------
 // CTA = (row, chunk of `cb` pool blocks), 4 warps, 1 CTA/SM.  One thread
 // streams each block's K and V (2 x 32 KB) with 8 TMA tensor copies (64-column
 // sub-tiles, 128-byte swizzle) into a 3-stage mbarrier ring, so the SM keeps up
@@ -724,11 +511,12 @@ __global__ void __launch_bounds__(128, 1)
     mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
     const float corr = (mx == -INFINITY) ? 1.f : exp2f(m_run - mx);
     float ls = 0.f;
+    const float mxs = mx == -INFINITY ? 0.f : mx;  // all keys masked: every score is -inf
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const float p = mx == -INFINITY ? 0.f : exp2f(sc[nt][e] - mx);
+        const float p = exp2_approx(sc[nt][e] - mxs);
         sc[nt][e] = p;
         ls += p;
       }
@@ -861,259 +649,6 @@ void decode_attention_v3(const CUtensorMap &kmap, const CUtensorMap &vmap, const
                max_chunks);
 }
 
-// ---- v2: chunked, pipelined, self-merging (superseded by v3) ----------------
-// CTA = (row, chunk of up to `cb` pool blocks).  Blocks stream through a
-// 2-stage cp.async ring of unpadded, XOR-swizzled 32 KB K and V tiles (16-byte
-// chunk c of key row r lives at c ^ (r & 7): conflict-free ldmatrix).  Warp w
-// owns keys 16w..16w+15 of every block and keeps a running (m, l, O) across
-// the chunk; the 4 warps merge once at the end.  A row's chunks are merged by
-// the last-arriving CTA in chunk order (deterministic, no extra launch).
-constexpr int DV_ROW = HEAD_DIM * 2;                 // 512 B per key row
-constexpr int DV_TILE = KV_BLOCK * DV_ROW;           // 32 KB
-constexpr size_t DV_SMEM = 16 * DV_ROW + 2 * 2 * DV_TILE + 64;
-
-__device__ __forceinline__ uint32_t swz(uint32_t base, int row, int chunk) {
-  return base + row * DV_ROW + ((chunk ^ (row & 7)) << 4);
-}
-
-__global__ void __launch_bounds__(128, 1)
-    decode_attn_v2_kernel(const bf16 *q, const bf16 *kpool, const bf16 *vpool, const int *bt, int bt_stride,
-                          const int *pos, const int *active, int cb, int max_chunks, float scale_log2,
-                          float *ws, int *counters, bf16 *out) {
-  pdl_trigger();
-  pdl_wait();
-  extern __shared__ __align__(128) unsigned char dv_smem[];
-  const uint32_t sQ = smem_addr(dv_smem);
-  const uint32_t sKV = sQ + 16 * DV_ROW;  // stage s: K at sKV + s*2*DV_TILE, V after it
-  __shared__ int s_last;
-  const int r = blockIdx.x, chunk = blockIdx.y;
-  if (active && !active[r]) return;
-  const int n_keys = pos[r] + 1;
-  const int nb = (n_keys + KV_BLOCK - 1) / KV_BLOCK;
-  const int n_chunks = (nb + cb - 1) / cb;
-  if (chunk >= n_chunks) return;
-  const int b0 = chunk * cb, b1 = min(nb, b0 + cb);
-  const int *btr = bt + (size_t)r * bt_stride;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  auto load_block = [&](int b, int stage) {
-    const int blk = btr[b];
-    const int nvalid = min(KV_BLOCK, n_keys - b * KV_BLOCK);
-    const bf16 *kb = kpool + (size_t)blk * KV_BLOCK * HEAD_DIM;
-    const bf16 *vb = vpool + (size_t)blk * KV_BLOCK * HEAD_DIM;
-    const uint32_t kbase = sKV + stage * 2 * DV_TILE, vbase = kbase + DV_TILE;
-    for (int i = threadIdx.x; i < KV_BLOCK * 32; i += 128) {
-      const int row = i >> 5, ch = i & 31;
-      if (row < nvalid) {
-        cp_async16(swz(kbase, row, ch), kb + (size_t)row * HEAD_DIM + ch * 8);
-        cp_async16(swz(vbase, row, ch), vb + (size_t)row * HEAD_DIM + ch * 8);
-      } else {  // zero rows: masked scores, and V must not hold NaN garbage
-        asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(swz(kbase, row, ch)), "r"(0));
-        asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(swz(vbase, row, ch)), "r"(0));
-      }
-    }
-  };
-  // group 0: Q (8 heads, rows 8..15 zero) + first block; group 1: second block
-  const bf16 *qr = q + (size_t)r * Q_HEADS * HEAD_DIM;
-  for (int i = threadIdx.x; i < 16 * 32; i += 128) {
-    const int row = i >> 5, ch = i & 31;
-    if (row < Q_HEADS) cp_async16(swz(sQ, row, ch), qr + (size_t)row * HEAD_DIM + ch * 8);
-    else asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(swz(sQ, row, ch)), "r"(0));
-  }
-  load_block(b0, 0);
-  cp_commit();
-  if (b0 + 1 < b1) load_block(b0 + 1, 1);
-  cp_commit();
-
-  float o[32][4];
-#pragma unroll
-  for (int i = 0; i < 32; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
-  float m_run = -INFINITY, l_run = 0.f;  // query row g = lane >> 2 (rows 8..15 are padding)
-  for (int b = b0; b < b1; ++b) {
-    const int stage = (b - b0) & 1;
-    cp_wait<1>();
-    __syncthreads();
-    const uint32_t kbase = sKV + stage * 2 * DV_TILE, vbase = kbase + DV_TILE;
-    float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-    const int krow = warp * 16 + (lane & 7) + ((lane >> 4) << 3);
-#pragma unroll
-    for (int kk = 0; kk < HEAD_DIM / 16; ++kk) {
-      uint32_t a0, a1, a2, a3, k0, k1, k2, k3;
-      ldsm_x4(swz(sQ, lane & 15, kk * 2 + (lane >> 4)), a0, a1, a2, a3);
-      ldsm_x4(swz(kbase, krow, kk * 2 + ((lane >> 3) & 1)), k0, k1, k2, k3);
-      mma16816(s[0], a0, a1, a2, a3, k0, k1);
-      mma16816(s[1], a0, a1, a2, a3, k2, k3);
-    }
-    float mx = m_run;
-#pragma unroll
-    for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int key = b * KV_BLOCK + warp * 16 + nt * 8 + (lane & 3) * 2 + (e & 1);
-        float v = s[nt][e] * scale_log2;
-        if (key >= n_keys) v = -INFINITY;
-        s[nt][e] = v;
-        if (e < 2) mx = fmaxf(mx, v);
-      }
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-    const float corr = (mx == -INFINITY) ? 1.f : exp2f(m_run - mx);
-    float ls = 0.f;
-#pragma unroll
-    for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float p = (e < 2 && mx != -INFINITY) ? exp2f(s[nt][e] - mx) : 0.f;
-        s[nt][e] = p;
-        ls += p;
-      }
-    ls += __shfl_xor_sync(0xffffffffu, ls, 1);
-    ls += __shfl_xor_sync(0xffffffffu, ls, 2);
-    l_run = l_run * corr + ls;
-    m_run = mx;
-#pragma unroll
-    for (int nt = 0; nt < 32; ++nt) {
-      o[nt][0] *= corr;
-      o[nt][1] *= corr;
-    }
-    const uint32_t pa0 = pack_bf16(s[0][0], s[0][1]), pa1 = pack_bf16(s[0][2], s[0][3]);
-    const uint32_t pa2 = pack_bf16(s[1][0], s[1][1]), pa3 = pack_bf16(s[1][2], s[1][3]);
-    const int vrow = warp * 16 + (lane & 15);
-#pragma unroll
-    for (int np = 0; np < 16; ++np) {
-      uint32_t v0, v1, v2, v3;
-      ldsm_x4_t(swz(vbase, vrow, np * 2 + (lane >> 4)), v0, v1, v2, v3);
-      mma16816(o[2 * np], pa0, pa1, pa2, pa3, v0, v1);
-      mma16816(o[2 * np + 1], pa0, pa1, pa2, pa3, v2, v3);
-    }
-    __syncthreads();  // everyone is done with this stage
-    if (b + 2 < b1) load_block(b + 2, stage);
-    cp_commit();
-  }
-  cp_wait<0>();
-  // ---- merge the 4 warps (stage buffers reused) -> chunk partial (m, l, O[8][256])
-  float *sO = reinterpret_cast<float *>(dv_smem + 16 * DV_ROW);   // [4][8][256]
-  float *sM = sO + 4 * 8 * HEAD_DIM;                               // [4][8] m, [4][8] l
-  const int g = lane >> 2;
-#pragma unroll
-  for (int nt = 0; nt < 32; ++nt) {
-    const int c = nt * 8 + (lane & 3) * 2;
-    *reinterpret_cast<float2 *>(sO + (warp * 8 + g) * HEAD_DIM + c) = make_float2(o[nt][0], o[nt][1]);
-  }
-  if ((lane & 3) == 0) {
-    sM[warp * 8 + g] = m_run;
-    sM[32 + warp * 8 + g] = l_run;
-  }
-  __syncthreads();
-  float pm[Q_HEADS], pl[Q_HEADS];
-#pragma unroll
-  for (int h = 0; h < Q_HEADS; ++h) {
-    float M = -INFINITY, L = 0.f;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) M = fmaxf(M, sM[w * 8 + h]);
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      const float mw = sM[w * 8 + h];
-      if (mw != -INFINITY) L += sM[32 + w * 8 + h] * exp2f(mw - M);
-    }
-    pm[h] = M;
-    pl[h] = L;
-  }
-  // thread owns 16 of the 8 x 256 outputs: (h, d) = (i / 256, i % 256) for i = tid + 128 j
-  float po[16];
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    const int i = threadIdx.x + 128 * j, h = i >> 8, d = i & 255;
-    float acc = 0.f;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      const float mw = sM[w * 8 + h];
-      if (mw != -INFINITY) acc += sO[(w * 8 + h) * HEAD_DIM + d] * exp2f(mw - pm[h]);
-    }
-    po[j] = acc;
-  }
-  bf16 *orow = out + (size_t)r * Q_HEADS * HEAD_DIM;
-  if (n_chunks == 1) {
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int i = threadIdx.x + 128 * j;
-      orow[i] = __float2bfloat16(po[j] / pl[i >> 8]);
-    }
-    return;
-  }
-  float *part = ws + ((size_t)r * max_chunks + chunk) * DA_PART;
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    const int i = threadIdx.x + 128 * j;
-    part[(i >> 8) * (HEAD_DIM + 2) + (i & 255)] = po[j];
-  }
-  if (threadIdx.x < Q_HEADS) {
-    part[threadIdx.x * (HEAD_DIM + 2) + HEAD_DIM] = pm[threadIdx.x];
-    part[threadIdx.x * (HEAD_DIM + 2) + HEAD_DIM + 1] = pl[threadIdx.x];
-  }
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(counters + r, 1) == n_chunks - 1;
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  const float *base = ws + (size_t)r * max_chunks * DA_PART;
-#pragma unroll 1
-  for (int j = 0; j < 16; ++j) {
-    const int i = threadIdx.x + 128 * j, h = i >> 8, d = i & 255;
-    float M = -INFINITY;
-    for (int c = 0; c < n_chunks; ++c) M = fmaxf(M, __ldcg(base + (size_t)c * DA_PART + h * (HEAD_DIM + 2) + HEAD_DIM));
-    float L = 0.f, acc = 0.f;
-#pragma unroll 4
-    for (int c = 0; c < n_chunks; ++c) {
-      const float *p = base + (size_t)c * DA_PART + h * (HEAD_DIM + 2);
-      const float w = exp2f(__ldcg(p + HEAD_DIM) - M);
-      L += __ldcg(p + HEAD_DIM + 1) * w;
-      acc += __ldcg(p + d) * w;
-    }
-    orow[i] = __float2bfloat16(acc / L);
-  }
-  if (threadIdx.x == 0) counters[r] = 0;
-}
-
-int decode_chunk_blocks(int rows, int max_blocks, int sms) {
-  // enough CTAs for ~2 per SM, at least 2 blocks per CTA so the ring pipelines
-  int cb = std::max(1, (rows * max_blocks + 2 * sms - 1) / (2 * sms));
-  return std::min(cb, max_blocks);
-}
-
-void decode_attention_v2(const bf16 *q, bf16 *out, const bf16 *kpool, const bf16 *vpool, const int *bt,
-                         int bt_stride, const int *pos, const int *active, int rows, int max_blocks, float scale,
-                         float *ws, int *counters, int sms, cudaStream_t st) {
-  if (rows <= 0) return;
-  static bool attr = false;
-  if (!attr) {
-    OXY_CUDA(cudaFuncSetAttribute(decode_attn_v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)DV_SMEM));
-    attr = true;
-  }
-  const int cb = decode_chunk_blocks(rows, max_blocks, sms);
-  const int max_chunks = (max_blocks + cb - 1) / cb;
-  launch_pdl(decode_attn_v2_kernel, dim3(rows, max_chunks), dim3(128), DV_SMEM, st, q, kpool, vpool, bt,
-             bt_stride, pos, active, cb, max_chunks, scale * 1.4426950408889634f, ws, counters, out);
-}
-
-void decode_attention(const bf16 *q, bf16 *out, const bf16 *kpool, const bf16 *vpool, const int *bt,
-                      int bt_stride, const int *pos, const int *active, int rows, int max_blocks,
-                      float scale, float *ws, cudaStream_t st) {
-  if (rows <= 0) return;
-  static bool attr = false;
-  if (!attr) {
-    OXY_CUDA(cudaFuncSetAttribute(decode_attn_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)DM_SMEM));
-    attr = true;
-  }
-  const float sl2 = scale * 1.4426950408889634f;
-  launch_pdl(decode_attn_mma_kernel, dim3(rows, max_blocks), dim3(128), DM_SMEM, st, q, kpool, vpool, bt,
-             bt_stride, pos, active, max_blocks, sl2, ws);
-  launch_pdl(decode_merge_kernel, dim3(rows, Q_HEADS), dim3(HEAD_DIM), 0, st, ws, out, pos, active, max_blocks);
-}
-
 // ============================================================ argmax
 
 constexpr int AM_CHUNKS = 64;
@@ -1152,7 +687,7 @@ __global__ void argmax_partial_kernel(const float *logits, int V, const int *act
 
 __global__ void argmax_final_kernel(int rows, const float *pv, const int *pi, int step, int k, int eos,
                                     int *active, int *tok, int *pos, int *count, const int *budget,
-                                    int *out_tokens, int *plain_out) {
+                                    int *out_tokens) {
   pdl_trigger();
   pdl_wait();
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1162,7 +697,6 @@ __global__ void argmax_final_kernel(int rows, const float *pv, const int *pi, in
   int bi = 0x7fffffff;
   for (int c = 0; c < AM_CHUNKS; ++c) better(bv, bi, pv[r * AM_CHUNKS + c], pi[r * AM_CHUNKS + c]);
   if (bi == 0x7fffffff) bi = 0;
-  if (plain_out) { plain_out[r] = bi; return; }
   out_tokens[(size_t)r * k + step] = bi;
   tok[r] = bi;
   pos[r] += 1;
@@ -1174,13 +708,7 @@ void argmax_update(const float *logits, int rows, int V, int step, int k, int eo
                    int *pos, int *count, const int *budget, int *out_tokens, float *pv, int *pi,
                    cudaStream_t st) {
   launch_pdl(argmax_partial_kernel, dim3(rows, AM_CHUNKS), dim3(256), 0, st, logits, V, active, pv, pi);
-  launch_pdl(argmax_final_kernel, dim3((rows + 63) / 64), dim3(64), 0, st, rows, pv, pi, step, k, eos, active, tok, pos, count, budget, out_tokens, nullptr);
-}
-
-void argmax_rows(const float *logits, int rows, int V, int *out, float *pv, int *pi, cudaStream_t st) {
-  argmax_partial_kernel<<<dim3(rows, AM_CHUNKS), 256, 0, st>>>(logits, V, nullptr, pv, pi);
-  OXY_LAUNCH_CHECK();
-  launch_pdl(argmax_final_kernel, dim3((rows + 63) / 64), dim3(64), 0, st, rows, pv, pi, 0, 1, -1, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, out);
+  launch_pdl(argmax_final_kernel, dim3((rows + 63) / 64), dim3(64), 0, st, rows, pv, pi, step, k, eos, active, tok, pos, count, budget, out_tokens);
 }
 
 }  // namespace pi05

@@ -31,13 +31,6 @@ void embed_rows(float *x, int ldx, const bf16 *table, const int *tok, const int 
 void permute_rows(bf16 *dst, const bf16 *src, int rows, int cols, cudaStream_t st);
 // (cos, sin) of fp32(pos * inv_freq[i]) for pos < n_pos (sin/cos evaluated in fp64)
 void rope_table(float2 *cs, const float *inv_freq, int n_pos, cudaStream_t st);
-// RoPE inverse-frequency table (constant memory), set once per process
-void set_rope_theta(float theta);
-// RoPE on q (n_qh heads) and k from fp32 qkv [T, (n_qh+2)*256]; q -> q_out bf16 [T, n_qh*256];
-// k, v -> pool rows at slot[t] (layer base pointers) or dense rows (k_dense/v_dense, ld 256).
-void rope_split(const float *qkv, int T, int n_qh, const int *pos, const int *slot,
-                const int *active, bf16 *q_out, bf16 *kpool, bf16 *vpool, bf16 *k_dense,
-                bf16 *v_dense, float theta, cudaStream_t st);
 // images uint8 [n, 224, 224, 3] -> patches bf16 [n*256, kpad] (x/127.5 - 1, (dy,dx,c) order)
 void patchify(const uint8_t *img, int n, bf16 *patches, int kpad, cudaStream_t st);
 // dst[i*ld + j] = src[(i % period) * ld_src + j] (broadcast of per-image tables)
@@ -87,39 +80,28 @@ void flash_attention(const AttnGroup *groups_d, int n_groups, int max_q_tiles, i
 void flash_attention_tc(const AttnGroup *groups_d, int n_groups, int q_tiles, int splits, const bf16 *q_base,
                         int q_rows, const CUtensorMap &kpool_map, const CUtensorMap &vpool_map, const bf16 *kd_base,
                         const bf16 *vd_base, int kd_rows, float scale, float *ws_o, float *ws_ml, int ws_rows,
-                        bool kv_ready, cudaStream_t st);
+                        bool kv_ready, bool cmerge, cudaStream_t st);
+// largest split count merged inside the attention kernel over DSMEM (clusters of
+// `splits` CTAs); larger counts use the workspace + flash_merge.  OXY_ATTN_CMERGE:
+// the cap (default 16; 0 or 1 = always the workspace merge)
+int attn_cluster_merge_max();
 // split-order merge of head-dim-256 partials (ws rows as in flash_attention)
 void flash_merge(const AttnGroup *groups_d, int n_groups, int max_rows, int splits, const float *ws_o,
                  const float *ws_ml, int ws_rows, cudaStream_t st);
 
-// Paged decode attention: rows x 8 q-heads vs 1 KV head, keys [0, pos[r]].
-// q [rows, 8*256] bf16 -> out [rows, 8*256] bf16.  ws: rows*max_blocks*8*(256+2) floats.
-void decode_attention(const bf16 *q, bf16 *out, const bf16 *kpool, const bf16 *vpool,
-                      const int *bt, int bt_stride, const int *pos, const int *active, int rows,
-                      int max_blocks, float scale, float *ws, cudaStream_t st);
-
-// v3 (used): TMA-fed 3-stage ring over chunks of pool blocks + ordered chunk merge.
+// Paged decode attention: rows x 8 q-heads vs 1 KV head, keys [0, pos[r]].  TMA-fed
+// 3-stage ring over chunks of pool blocks + ordered chunk merge.
 // kmap/vmap: 2-D tensor maps over one layer's K / V pool viewed as [num_blocks*64, 256]
 // (box 64 x 64, 128-byte swizzle; gemm::make_map).  ws: rows*max_blocks*8*(256+2) floats.
 void decode_attention_v3(const CUtensorMap &kmap, const CUtensorMap &vmap, const bf16 *q, bf16 *out, const int *bt,
                          int bt_stride, const int *pos, const int *active, int rows, int max_blocks, float scale,
                          float *ws, int sms, cudaStream_t st);
 int decode_chunk_blocks3(int rows, int max_blocks, int sms);
-// v2 (superseded): chunked + pipelined, last-arriving chunk merges (counters: one per row,
-// zero-initialised, self-resetting).  ws: rows*max_blocks*8*(256+2) floats.
-void decode_attention_v2(const bf16 *q, bf16 *out, const bf16 *kpool, const bf16 *vpool, const int *bt,
-                         int bt_stride, const int *pos, const int *active, int rows, int max_blocks, float scale,
-                         float *ws, int *counters, int sms, cudaStream_t st);
-int decode_chunk_blocks(int rows, int max_blocks, int sms);
 
 // Greedy token + continuous-batching state update over logits [rows, V].
 // part: rows * 64 (val, idx) scratch.
 void argmax_update(const float *logits, int rows, int V, int step, int k, int eos, int *active,
                    int *tok, int *pos, int *count, const int *budget, int *out_tokens,
                    float *part_val, int *part_idx, cudaStream_t st);
-// plain argmax per row (prefill-free greedy checks)
-void argmax_rows(const float *logits, int rows, int V, int *out, float *part_val, int *part_idx,
-                 cudaStream_t st);
-
 }  // namespace pi05
 }  // namespace oxy

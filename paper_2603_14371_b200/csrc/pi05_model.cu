@@ -16,6 +16,7 @@
 // splitmix64 counter draws, U(+-sqrt(3/fan_in)) for matrices.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <string>
@@ -250,7 +251,6 @@ struct Model {
     OXY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     declare();
     materialise(st);
-    set_rope_theta(10000.f);
     {  // device RoPE table for the fused QKV epilogue, and the rotary-pair row order
       float inv[128];
       for (int i = 0; i < 128; ++i) inv[i] = (float)std::pow(10000.0, -2.0 * i / 256.0);
@@ -486,17 +486,35 @@ struct Model {
     OXY_CUDA(cudaGraphLaunch(g.exec, mst));
   }
 
+  // SMs the GEMM / attention split policies may fill.  A/B knob OXY_LANE_SMS=dn,dec
+  // caps the action-expert denoise and the language decode separately (0 = all),
+  // so two concurrent chains can be sized to share the SMs instead of each
+  // splitting for the whole GPU.
+  int plan_sms = 0;
+  int psms() const { return plan_sms > 0 ? std::min(plan_sms, sms) : sms; }
+  std::pair<int, int> lane_sms = [] {
+    std::pair<int, int> v{0, 0};
+    if (const char *e = getenv("OXY_LANE_SMS")) sscanf(e, "%d,%d", &v.first, &v.second);
+    return v;
+  }();
+  struct PlanSms {
+    Model &m;
+    int prev;
+    PlanSms(Model &mm, int v) : m(mm), prev(mm.plan_sms) { m.plan_sms = v; }
+    ~PlanSms() { m.plan_sms = prev; }
+  };
+
   // split-K workspace is reserved by plan_gemm(); gemm() only fetches it
   size_t ws_need = 0;
   void plan_gemm(int n_out, int k, int t) {
     if (t <= 0) return;
-    gemm::Plan p = gemm::make_plan(n_out, k, t, sms);
+    gemm::Plan p = gemm::make_plan(n_out, k, t, psms());
     if (p.splits > 1) ws_need = std::max(ws_need, (size_t)p.splits * t * n_out);
   }
   void gemm(const bf16 *w, const bf16 *xin, int n_out, int k, int t, int mode, void *out, int ldo,
             const float *bias = nullptr, const float *gate = nullptr) {
     if (t <= 0) return;
-    gemm::Plan plan = gemm::make_plan(n_out, k, t, sms);
+    gemm::Plan plan = gemm::make_plan(n_out, k, t, psms());
     float *wsp = plan.splits > 1 ? ws.as<float>((size_t)plan.splits * t * n_out) : nullptr;
     EpiParams e{mode, out, ldo, bias, nullptr, 0, gate, {}};
     gemm::launch(w, xin, n_out, k, t, e, plan, wsp, gemm_counters, mst);
@@ -506,7 +524,7 @@ struct Model {
   void gemm_res_norm(const bf16 *w, const bf16 *xin, int n_out, int k, int t, const float *gate, float *X, bf16 *Y,
                      const float *norm_w, const float *mod_scale, const float *mod_shift) {
     if (t <= 0) return;
-    gemm::Plan plan = gemm::make_plan(n_out, k, t, sms);
+    gemm::Plan plan = gemm::make_plan(n_out, k, t, psms());
     if (plan.splits > 1 && n_out <= 2048) {
       float *wsp = ws.as<float>((size_t)plan.splits * t * n_out);
       EpiParams e{gemm::EPI_PARTIALS, nullptr, 0, nullptr, nullptr, 0, nullptr, {}};
@@ -523,7 +541,7 @@ struct Model {
   void gemm_qkv(const bf16 *w, const bf16 *xin, int k, int t, const int *pos, const int *slot, bf16 *q_out,
                 bf16 *k_dst, bf16 *v_dst) {
     if (t <= 0) return;
-    gemm::Plan plan = gemm::make_plan(QKV, k, t, sms);
+    gemm::Plan plan = gemm::make_plan(QKV, k, t, psms());
     float *wsp = plan.splits > 1 ? ws.as<float>((size_t)plan.splits * t * QKV) : nullptr;
     EpiParams e{gemm::EPI_QKV_ROPE, nullptr, 0, nullptr, nullptr, 0, nullptr,
                 gemm::QkvRope{rope_inv, rope_cs, pos, slot, q_out, k_dst, v_dst}};
@@ -587,7 +605,7 @@ struct Model {
     }
     p.q_tiles = (max_nq + 127) / 128;
     const int ctas = p.n * p.q_tiles;
-    p.splits = std::max(1, std::min({p.max_tiles, 32, sms / std::max(1, ctas)}));  // merge handles <= 32
+    p.splits = std::max(1, std::min({p.max_tiles, 32, psms() / std::max(1, ctas)}));  // merge handles <= 32
     if (const char *e = getenv("OXY_ATTN_TC_SPLITS")) p.splits = std::max(1, std::min({p.max_tiles, 32, atoi(e)}));
     if (p.splits > 1) {
       attn_ws_need = std::max(attn_ws_need, (size_t)p.splits * p.rows * 256);
@@ -603,9 +621,10 @@ struct Model {
       wo = attn_ws.as<float>((size_t)p.splits * p.rows * 256);
       wml = attn_ml.as<float>((size_t)p.splits * p.rows * 2);
     }
+    const bool cm = p.splits > 1 && p.splits <= attn_cluster_merge_max();
     flash_attention_tc(p.groups, p.n, p.q_tiles, p.splits, q_base, q_rows, kv_maps[2 * layer], kv_maps[2 * layer + 1],
-                       kd, vd, kd_rows, 1.f / 16.f, wo, wml, p.rows, kv_ready, mst);
-    if (p.splits > 1 && !(dbg_skip & 4)) flash_merge(p.groups, p.n, p.q_tiles * 128, p.splits, wo, wml, p.rows, mst);
+                       kd, vd, kd_rows, 1.f / 16.f, wo, wml, p.rows, kv_ready, cm, mst);
+    if (p.splits > 1 && !cm && !(dbg_skip & 4)) flash_merge(p.groups, p.n, p.q_tiles * 128, p.splits, wo, wml, p.rows, mst);
   }
 
   void reserve_common() {
@@ -813,6 +832,7 @@ struct Model {
                bool join = true) {
     OXY_REQUIRE(S >= 1, "denoise step count must be >= 1, got %d", S);
     LaneSwap lane(*this);
+    PlanSms plan_scope(*this, lane_sms.first);
     const int We = c.expert_width, H = c.H, A = c.action_dim, T = n * H, AP = apad();
     ensure_mod(S);
     std::string key = "denoise/" + std::to_string(S);
@@ -1061,6 +1081,7 @@ struct Model {
       explicit EarlyScope(int v) { gemm::g_early_override = v; }
       ~EarlyScope() { gemm::g_early_override = -1; }
     } early_scope(decode_early);
+    PlanSms plan_scope(*this, lane_sms.second);
     const int W = c.width;
     int max_pos = 0;
     for (int r = 0; r < rows; ++r) {
@@ -1116,7 +1137,7 @@ struct Model {
           if (!(dbg_skip & 256)) gemm_qkv(w.wqkv, Y, W, rows, d_pos, d_slot, Qb, kpool(l), vpool(l));
           if (!(dbg_skip & 512))
             decode_attention_v3(kv_maps[2 * l], kv_maps[2 * l + 1], Qb, Ob, d_bt, maxb, d_pos, d_active, rows, maxb,
-                                scale, dws, sms, mst);
+                                scale, dws, psms(), mst);
           if (!(dbg_skip & 2048)) gemm_res_norm(w.wo, Ob, W, QDIM, rows, nullptr, X, Y, w.ln2, nullptr, nullptr);
           if (!(dbg_skip & 4096)) gemm(w.wgu, Y, 2 * c.mlp, W, rows, gemm::EPI_GEGLU_BF16, Hm, c.mlp);
           if (!(dbg_skip & 8192)) gemm_res_norm(w.wd, Hm, W, c.mlp, rows, nullptr, X, Y, next_norm, nullptr, nullptr);

@@ -15,9 +15,11 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("splits", ["1", "3", "7", "64"])
-def test_attention_splits_match_oracle(splits):
-    env = dict(os.environ, OXY_ATTN_TC="1", OXY_ATTN_TC_SPLITS=splits)
+@pytest.mark.parametrize("splits,cmerge", [("1", "16"), ("3", "16"), ("7", "16"), ("14", "16"), ("7", "0"),
+                                           ("64", "16")])
+def test_attention_splits_match_oracle(splits, cmerge):
+    """cmerge 16: splits <= 16 merge over DSMEM inside the kernel; 0: workspace + fa_merge."""
+    env = dict(os.environ, OXY_ATTN_TC="1", OXY_ATTN_TC_SPLITS=splits, OXY_ATTN_CMERGE=cmerge)
     cmd = [sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider", os.path.join(ROOT, "tests", "test_pi05_gpu.py"),
            "-k", "prefill_kv or action_denoise or decode_logits or batch_invariant or graph_replay"]
     res = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=240)
@@ -50,7 +52,8 @@ def test_tc_attention_agrees_with_mma_sync_path():
 
 @pytest.mark.parametrize("nq,nka,nkb,splits", [
     (64, 800, 0, 2), (400, 800, 50, 14), (400, 800, 50, 1), (1000, 100, 37, 3), (8, 64, 0, 1),
-    (6400, 800, 0, 2), (130, 0, 77, 2), (256, 2000, 0, 32)])
+    (6400, 800, 0, 2), (130, 0, 77, 2), (256, 2000, 0, 32), (400, 800, 50, 12), (400, 800, 300, 16),
+    (400, 1100, 0, 17)])
 def test_prefix_attention_matches_torch(nq, nka, nkb, splits):
     """oxy_prefix_attention (tcgen05, paged + dense keys, split merge) against a
     torch fp32 softmax attention on the same bf16 inputs.  Tolerance: P is
@@ -67,7 +70,7 @@ def test_prefix_attention_matches_torch(nq, nka, nkb, splits):
     kd = torch.randn(max(nkb, 1), 256, generator=g).to(torch.bfloat16).cuda()
     vd = torch.randn(max(nkb, 1), 256, generator=g).to(torch.bfloat16).cuda()
     out = torch.zeros(nq, 256, dtype=torch.bfloat16, device="cuda")
-    rows = (nq + 127) // 128 * 128
+    rows = (nq + 127) // 128 * 128  # (splits <= 16 merge in-kernel and leave the workspace untouched)
     ws_o = torch.empty(splits * rows * 256, device="cuda")
     ws_ml = torch.empty(splits * rows * 2, device="cuda")
     _lib.call("oxy_prefix_attention", C.c_void_p(q.data_ptr()), C.c_void_p(out.data_ptr()),
@@ -84,3 +87,12 @@ def test_prefix_attention_matches_torch(nq, nka, nkb, splits):
     ref = torch.softmax(q.float() @ keys.T / 16.0, dim=-1) @ vals
     err = (out.float() - ref).abs().max().item()
     assert err < 2e-2 * vals.abs().max().item(), err
+
+
+def test_prefix_attention_workspace_merge():
+    """The same direct shapes with the in-kernel cluster merge off (workspace + fa_merge)."""
+    env = dict(os.environ, OXY_ATTN_CMERGE="0")
+    cmd = [sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider", os.path.abspath(__file__),
+           "-k", "test_prefix_attention_matches_torch"]
+    res = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=300)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-2000:]
