@@ -142,8 +142,10 @@ int oxy_paged_decode_attention(const void *q_d, void *out_d, const void *kpool_d
  * bidirectional over paged keys [0, nka) read through bt_d from the pools
  * (bf16 [num_blocks, 64, 256]) followed by dense keys kd_d / vd_d bf16
  * [nkb, 256]; out_d bf16 [nq, 256]; scale 1/16.  splits > 1 splits the keys
- * (ws_o: splits * ceil(nq/128)*128 * 256 floats, ws_ml: splits * ceil(nq/128)*128
- * * 2 floats) and merges them in split order. */
+ * and merges them in split order: splits <= 16 inside the kernel over
+ * distributed shared memory (ws_o / ws_ml unused, may be NULL), larger counts
+ * through the workspace (ws_o: at least splits * ceil(nq/128)*128 * 256 bf16,
+ * i.e. half that many floats; ws_ml: splits * ceil(nq/128)*128 * 2 floats). */
 int oxy_prefix_attention(const void *q_d, void *out_d, const void *kpool_d, const void *vpool_d,
                          int32_t num_blocks, const int32_t *bt_d, int32_t nka, const void *kd_d,
                          const void *vd_d, int32_t nkb, int32_t nq, int32_t splits, float *ws_o,

@@ -13,13 +13,13 @@
 //              reference max (O and l are rescaled only when the row max grows
 //              by more than 2^8), P written bf16 to smem in the 128B-swizzled
 //              K-major layout the PV MMA reads; final O / l to bf16 rows, or
-//              fp32 partials + (m, l) for the split merge.
+//              bf16 partials (unnormalised O) + fp32 (m, l) for the split merge.
 // Split merge, two ways: (a) cluster merge — the splits of a query tile are one
 // thread-block cluster (<= 16 CTAs); each keeps its fp32 partial and (m, l) in
 // its own smem, and after a cluster barrier CTA k merges rows
 // [128k/splits, 128(k+1)/splits) of the tile by reading every peer's rows over
 // DSMEM, in split order, and writes the bf16 output (no workspace round trip,
-// no merge launch); (b) fp32 partials TMA-stored to a workspace, merged by
+// no merge launch); (b) bf16 partials TMA-stored to a workspace, merged by
 // fa_merge (splits > 16, or OXY_ATTN_CMERGE=0).
 // Invariant relied on: pool slots past a sequence's length hold finite values
 // (the pool is zeroed at creation and only ever written with finite K/V), so
@@ -284,46 +284,27 @@ __global__ void __launch_bounds__(192, 1)
       MBW(b_sf + 8 * s, (i >> 1) & 1, 6);
       tc_fence_after();
       if (threadIdx.x == 64 && i < 2) APROF(i == 0 ? 5 : 16);
-      float sc[TK];
-      {
-        uint32_t v[4][16];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) tmem_ld16_nowait(tmem + 256 + s * TK + lanes + c * 16, v[c]);
+      // Rolled 16-score chunks re-read from TMEM: this code runs once or a few
+      // times per CTA, so it is instruction-fetch bound when cold; a fully
+      // unrolled 64-score body measured 2-3x slower on its first pass.
+      const uint32_t s_t = tmem + 256 + s * TK + lanes;
+      float mx = -INFINITY;
+#pragma unroll 1
+      for (int c = 0; c < TK / 16; ++c) {
+        uint32_t v[16];
+        tmem_ld16_nowait(s_t + c * 16, v);
         tmem_ld_wait();
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-#pragma unroll
-          for (int e = 0; e < 16; ++e) sc[c * 16 + e] = __uint_as_float(v[c][e]);
+        for (int e = 0; e < 16; ++e)
+          if (c * 16 + e < nvalid) mx = fmaxf(mx, __uint_as_float(v[e]));
       }
-      if (threadIdx.x == 64 && i == 0) APROF_DEP(19, sc[63]);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_local(b_se + 8 * s);  // S buffer may be overwritten
-      float mx = -INFINITY;
-#pragma unroll
-      for (int e = 0; e < TK; ++e) {
-        sc[e] = e < nvalid ? sc[e] * a.scale_log2 : -INFINITY;
-        mx = fmaxf(mx, sc[e]);
-      }
+      mx *= a.scale_log2;  // scale > 0: max commutes with it
       if (threadIdx.x == 64 && i < 2) APROF_DEP(i == 0 ? 14 : 17, mx);
       float corr = 1.f;
       if (mx > m_ref + LAZY || (m_ref == -INFINITY && mx > -INFINITY)) {
         corr = m_ref == -INFINITY ? 0.f : exp2f(m_ref - mx);
         m_ref = mx;
       }
-      float rs = 0.f;
-      uint32_t pk[TK / 2];
-      const float mref = m_ref == -INFINITY ? 0.f : m_ref;  // fully masked so far: every score is -inf
-#pragma unroll
-      for (int e = 0; e < TK; e += 2) {
-        const float p0 = exp2_approx(sc[e] - mref);
-        const float p1 = exp2_approx(sc[e + 1] - mref);
-        rs += p0 + p1;
-        __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
-        pk[e / 2] = *reinterpret_cast<uint32_t *>(&h);
-      }
-      l = l * corr + rs;
-      if (threadIdx.x == 64 && i < 2) APROF_DEP(i == 0 ? 15 : 18, l);
       // PV(i-1) must be complete before O is rescaled and before P is overwritten
       if (i > 0) {
         MBW(b_od, (i - 1) & 1, 7);
@@ -331,6 +312,7 @@ __global__ void __launch_bounds__(192, 1)
         // tcgen05.ld/st are warp-collective: rescale the warp's 32 rows together
         // whenever any of them needs it (rows that do not multiply by 1)
         if (__any_sync(0xffffffffu, corr != 1.f)) {
+#pragma unroll 1
           for (int c = 0; c < HD; c += 16) {
             uint32_t v[16];
             tmem_ld16_nowait(tmem + lanes + c, v);
@@ -342,10 +324,32 @@ __global__ void __launch_bounds__(192, 1)
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
       }
+      const float mref = m_ref == -INFINITY ? 0.f : m_ref;  // fully masked so far: every score is -inf
+      float rs = 0.f;
+#pragma unroll 1
+      for (int c = 0; c < TK / 16; ++c) {
+        uint32_t v[16];
+        tmem_ld16_nowait(s_t + c * 16, v);
+        tmem_ld_wait();
+        uint32_t pk[8];
 #pragma unroll
-      for (int ch = 0; ch < 8; ++ch)  // 128B swizzle: chunk ch of row r lives at ch ^ (r & 7)
-        *reinterpret_cast<uint4 *>(prow + ((ch ^ (row & 7)) << 4)) =
-            make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
+        for (int e = 0; e < 16; e += 2) {
+          const float x0 = c * 16 + e < nvalid ? __uint_as_float(v[e]) * a.scale_log2 : -INFINITY;
+          const float x1 = c * 16 + e + 1 < nvalid ? __uint_as_float(v[e + 1]) * a.scale_log2 : -INFINITY;
+          const float p0 = exp2_approx(x0 - mref), p1 = exp2_approx(x1 - mref);
+          rs += p0 + p1;
+          __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
+          pk[e / 2] = *reinterpret_cast<uint32_t *>(&h);
+        }
+        // 128B swizzle: 16-byte chunk ch of row r lives at ch ^ (r & 7)
+        *reinterpret_cast<uint4 *>(prow + (((2 * c) ^ (row & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        *reinterpret_cast<uint4 *>(prow + (((2 * c + 1) ^ (row & 7)) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      }
+      l = l * corr + rs;
+      if (threadIdx.x == 64 && i < 2) APROF_DEP(i == 0 ? 15 : 18, l);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_local(b_se + 8 * s);  // S buffer may be overwritten
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       tc_fence_before();
       __syncwarp();
@@ -362,6 +366,7 @@ __global__ void __launch_bounds__(192, 1)
     if (a.splits == 1) {
       const float inv = l > 0.f ? 1.f / l : 0.f;
       bf16 *orow = g.o + (size_t)r * g.ldo;
+#pragma unroll 1
       for (int c = 0; c < HD; c += 16) {
         uint32_t v[16];
         if (n > 0) {
@@ -384,27 +389,39 @@ __global__ void __launch_bounds__(192, 1)
         }
       }
     } else {
-      // fp32 partials through TMA stores: rows staged in smem as 8 boxes of
-      // 128 rows x 32 floats in the 128B-swizzled box layout (conflict-free: the
+      // bf16 partials through TMA stores: rows staged in smem as 4 boxes of
+      // 128 rows x 64 bf16 in the 128B-swizzled box layout (conflict-free: the
       // 8 rows of an smem phase hit 8 different 16-byte slots), then one thread
       // stores the whole 128-row tile.  Workspace rows are padded per group to
       // multiples of 128, so rows past nq land in that group's padding.
-      uint8_t *stage = sm;  // Q + K slots: free once the last PV retired
-      for (int b = 0; b < HD / 32; ++b) {
-        uint32_t v[32];
-        if (n > 0) {
-          tmem_ld16_nowait(tmem + lanes + b * 32, *reinterpret_cast<uint32_t(*)[16]>(v));
-          tmem_ld16_nowait(tmem + lanes + b * 32 + 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16));
-          tmem_ld_wait();
-        } else {
+      uint8_t *stage = sm;  // Q slot: free once the last PV retired
+#pragma unroll 1
+      for (int b = 0; b < HD / 64; ++b) {  // partials in bf16 (unnormalised O; m, l stay fp32)
 #pragma unroll
-          for (int e = 0; e < 32; ++e) v[e] = 0u;
+        for (int hh = 0; hh < 2; ++hh) {
+          uint32_t v[32];
+          if (n > 0) {
+            tmem_ld16_nowait(tmem + lanes + b * 64 + hh * 32, *reinterpret_cast<uint32_t(*)[16]>(v));
+            tmem_ld16_nowait(tmem + lanes + b * 64 + hh * 32 + 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16));
+            tmem_ld_wait();
+          } else {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) v[e] = 0u;
+          }
+          uint32_t pk[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1]));
+            pk[e] = *reinterpret_cast<uint32_t *>(&h);
+          }
+          uint8_t *rowp = stage + b * (TQ * 128) + row * 128;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int ch = hh * 4 + q;
+            *reinterpret_cast<uint4 *>(rowp + ((ch ^ (row & 7)) << 4)) =
+                make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+          }
         }
-        uint8_t *rowp = stage + b * (TQ * 128) + row * 128;
-#pragma unroll
-        for (int ch = 0; ch < 8; ++ch)
-          *reinterpret_cast<uint4 *>(rowp + ((ch ^ (row & 7)) << 4)) =
-              make_uint4(v[4 * ch], v[4 * ch + 1], v[4 * ch + 2], v[4 * ch + 3]);
       }
       if (a.cmerge) {  // (m, l) next to the partial; peers read both after the cluster barrier
         reinterpret_cast<float2 *>(sm + OFF_P)[row] = make_float2(m_ref, l);
@@ -420,10 +437,10 @@ __global__ void __launch_bounds__(192, 1)
       if (threadIdx.x == 64) APROF(8);
       if (threadIdx.x == 64 && !a.cmerge) {
         const int row0 = split * a.ws_rows + g.wrow0 + q0;
-        for (int b = 0; b < HD / 32; ++b)
+        for (int b = 0; b < HD / 64; ++b)
           asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
                            reinterpret_cast<uint64_t>(&wsmap)),
-                       "r"(b * 32), "r"(row0), "r"(smem_u32(stage + b * (TQ * 128)))
+                       "r"(b * 64), "r"(row0), "r"(smem_u32(stage + b * (TQ * 128)))
                        : "memory");
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         // smem may be released once the copies have READ it; the global writes
@@ -473,31 +490,38 @@ __global__ void __launch_bounds__(192, 1)
         if (j < cs) wgt[i * 16 + j] = m[j] * inv;
     }
     __syncthreads();
-    for (int idx = threadIdx.x; idx < nr * (HD / 4); idx += blockDim.x) {
-      const int i = idx / (HD / 4), c4 = idx % (HD / 4), row = rb + i;
-      // float4 c4 of the row: box c4/8 (32 floats), 16-byte chunk (c4%8) ^ (row%8)
-      const uint32_t off = (c4 >> 3) * (TQ * 128) + row * 128 + (((c4 & 7) ^ (row & 7)) << 4);
-      float4 v[16];
+    for (int idx = threadIdx.x; idx < nr * (HD / 8); idx += blockDim.x) {
+      const int i = idx / (HD / 8), c8 = idx % (HD / 8), row = rb + i;
+      // 8 bf16 c8 of the row: box c8/8 (64 columns), 16-byte chunk (c8%8) ^ (row%8)
+      const uint32_t off = (c8 >> 3) * (TQ * 128) + row * 128 + (((c8 & 7) ^ (row & 7)) << 4);
+      uint4 v[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j)
         if (j < cs)
-          asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
-                       : "=f"(v[j].x), "=f"(v[j].y), "=f"(v[j].z), "=f"(v[j].w)
+          asm volatile("ld.shared::cluster.v4.u32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(v[j].x), "=r"(v[j].y), "=r"(v[j].z), "=r"(v[j].w)
                        : "r"(map_to_rank(st_s + off, j))
                        : "memory");
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int j = 0; j < 16; ++j)
         if (j < cs) {  // split order
           const float w = wgt[i * 16 + j];
-          acc.x += w * v[j].x;
-          acc.y += w * v[j].y;
-          acc.z += w * v[j].z;
-          acc.w += w * v[j].w;
+          const uint32_t u[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&u[e]));
+            acc[2 * e] += w * f.x;
+            acc[2 * e + 1] += w * f.y;
+          }
         }
-      __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x, acc.y), hi = __floats2bfloat162_rn(acc.z, acc.w);
-      *reinterpret_cast<uint2 *>(g.o + (size_t)(q0 + row) * g.ldo + c4 * 4) =
-          make_uint2(*reinterpret_cast<uint32_t *>(&lo), *reinterpret_cast<uint32_t *>(&hi));
+      uint32_t o[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        __nv_bfloat162 h = __floats2bfloat162_rn(acc[2 * e], acc[2 * e + 1]);
+        o[e] = *reinterpret_cast<uint32_t *>(&h);
+      }
+      *reinterpret_cast<uint4 *>(g.o + (size_t)(q0 + row) * g.ldo + c8 * 8) = make_uint4(o[0], o[1], o[2], o[3]);
     }
     if (threadIdx.x == 0) APROF(12);
     cluster_sync_all();  // peers may still be reading this CTA's smem
@@ -533,8 +557,10 @@ void flash_attention_tc(const AttnGroup *groups_d, int n_groups, int q_tiles, in
   if (kd_base && vd_base - kd_base != 0 && (vd_base - kd_base) % tc::HD != 0)
     fail(OXY_EINVAL, "dense K/V buffers must be row-aligned");
   if (splits > 1 && !cmerge && ws_rows % tc::TQ != 0) fail(OXY_EINVAL, "attention workspace rows must be padded to 128");
-  // fp32 partial rows [splits * ws_rows, 256], box 32 x 128 (128-byte rows), 128B swizzle
-  const CUtensorMap wsm = splits > 1 && !cmerge ? gemm::make_map_f32(ws_o, splits * ws_rows, tc::HD, 32, tc::TQ) : qm;
+  // bf16 partial rows [splits * ws_rows, 256], box 64 x 128 (128-byte rows), 128B swizzle
+  const CUtensorMap wsm =
+      splits > 1 && !cmerge ? gemm::make_map(reinterpret_cast<const bf16 *>(ws_o), splits * ws_rows, tc::HD, tc::TQ)
+                            : qm;
   TcAttnArgs a{groups_d, q_tiles, splits, ws_rows, q_base, kd_base, kv_ready ? 1 : 0, cmerge ? 1 : 0,
                scale * 1.4426950408889634f, ws_o, ws_ml};
   launch_pdl_cluster(flash_tc_kernel, dim3(n_groups * q_tiles, splits), dim3(192), tc::SMEM, st,
@@ -577,7 +603,8 @@ extern "C" int oxy_prefix_attention(const void *q_d, void *out_d, const void *kp
   const int q_tiles = (nq + 127) / 128, ws_rows = q_tiles * 128;
   oxy::pi05::flash_attention_tc(gd, 1, q_tiles, splits, g.q, nq, km, vm, g.kb, g.vb, std::max(nkb, 1), 1.f / 16.f,
                                 ws_o, ws_ml, ws_rows, false, cm, st);
-  if (splits > 1 && !cm) oxy::pi05::flash_merge(gd, 1, ws_rows, splits, ws_o, ws_ml, ws_rows, st);
+  if (splits > 1 && !cm)
+    oxy::pi05::flash_merge(gd, 1, ws_rows, splits, reinterpret_cast<const bf16 *>(ws_o), ws_ml, ws_rows, st);
   OXY_CUDA(cudaFreeAsync(gd, st));
   OXY_API_END
 }

@@ -293,8 +293,14 @@ __global__ void __launch_bounds__(128)
 // A variant with every thread loading all (m, l) and O pairs up front measured
 // slower in the denoise chain (9.0 vs 8.8 ms per denoise).  CTA = one query
 // row, thread = one column pair; split loads unrolled for memory parallelism.
-template <int HD>
-__global__ void fa_merge_kernel(const AttnGroup *groups, int splits, const float *ws_o, const float *ws_ml,
+__device__ __forceinline__ float2 ld_pair(const float *p) { return *reinterpret_cast<const float2 *>(p); }
+__device__ __forceinline__ float2 ld_pair(const bf16 *p) {
+  return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(p));
+}
+
+// PT: partial element type (fp32 from the mma.sync kernel, bf16 from the tcgen05 one)
+template <int HD, typename PT>
+__global__ void fa_merge_kernel(const AttnGroup *groups, int splits, const PT *ws_o, const float *ws_ml,
                                 int ws_rows) {
   pdl_trigger();
   pdl_wait();
@@ -319,12 +325,12 @@ __global__ void fa_merge_kernel(const AttnGroup *groups, int splits, const float
   __syncthreads();
   const int c = threadIdx.x * 2;
   if (c >= HD) return;
-  const float *o = ws_o + row0 * C::HDP + c;
+  const PT *o = ws_o + row0 * C::HDP + c;
   const size_t ostride = (size_t)ws_rows * C::HDP;
   float a0 = 0.f, a1 = 0.f;
 #pragma unroll 8
   for (int s = 0; s < splits; ++s) {  // split order; independent loads
-    const float2 v = *reinterpret_cast<const float2 *>(o + s * ostride);
+    const float2 v = ld_pair(o + s * ostride);
     a0 += v.x * wsh[s];
     a1 += v.y * wsh[s];
   }
@@ -349,15 +355,15 @@ static void flash_launch(const AttnGroup *groups_d, int n_groups, int max_q_tile
   dim3 grid(n_groups * max_q_tiles, splits);
   launch_pdl(flash_attn_kernel<HD>, dim3(grid), dim3(128), C::SMEM, st, groups_d, max_q_tiles, kpool, vpool, scale_log2, splits, ws_o, ws_ml, ws_rows);
   if (splits > 1) {
-    launch_pdl(fa_merge_kernel<HD>, dim3(max_q_tiles * FA_BQ, n_groups), dim3((HD / 2 + 31) / 32 * 32), 0, st,
+    launch_pdl(fa_merge_kernel<HD, float>, dim3(max_q_tiles * FA_BQ, n_groups), dim3((HD / 2 + 31) / 32 * 32), 0, st,
                groups_d, splits, ws_o, ws_ml, ws_rows);
   }
 }
 
-void flash_merge(const AttnGroup *groups_d, int n_groups, int max_rows, int splits, const float *ws_o,
+void flash_merge(const AttnGroup *groups_d, int n_groups, int max_rows, int splits, const bf16 *ws_o,
                  const float *ws_ml, int ws_rows, cudaStream_t st) {
   if (splits <= 1 || n_groups <= 0) return;
-  launch_pdl(fa_merge_kernel<256>, dim3(max_rows, n_groups), dim3(128), 0, st, groups_d, splits, ws_o, ws_ml, ws_rows);
+  launch_pdl(fa_merge_kernel<256, bf16>, dim3(max_rows, n_groups), dim3(128), 0, st, groups_d, splits, ws_o, ws_ml, ws_rows);
 }
 
 void flash_attention(const AttnGroup *groups_d, int n_groups, int max_q_tiles, int head_dim,

@@ -85,8 +85,8 @@ void flash_attention_tc(const AttnGroup *groups_d, int n_groups, int q_tiles, in
 // `splits` CTAs); larger counts use the workspace + flash_merge.  OXY_ATTN_CMERGE:
 // the cap (default 16; 0 or 1 = always the workspace merge)
 int attn_cluster_merge_max();
-// split-order merge of head-dim-256 partials (ws rows as in flash_attention)
-void flash_merge(const AttnGroup *groups_d, int n_groups, int max_rows, int splits, const float *ws_o,
+// split-order merge of the tcgen05 kernel's bf16 head-dim-256 partials (ws rows as in flash_attention)
+void flash_merge(const AttnGroup *groups_d, int n_groups, int max_rows, int splits, const bf16 *ws_o,
                  const float *ws_ml, int ws_rows, cudaStream_t st);
 
 // Paged decode attention: rows x 8 q-heads vs 1 KV head, keys [0, pos[r]].  TMA-fed

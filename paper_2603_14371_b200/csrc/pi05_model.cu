@@ -624,7 +624,8 @@ struct Model {
     const bool cm = p.splits > 1 && p.splits <= attn_cluster_merge_max();
     flash_attention_tc(p.groups, p.n, p.q_tiles, p.splits, q_base, q_rows, kv_maps[2 * layer], kv_maps[2 * layer + 1],
                        kd, vd, kd_rows, 1.f / 16.f, wo, wml, p.rows, kv_ready, cm, mst);
-    if (p.splits > 1 && !cm && !(dbg_skip & 4)) flash_merge(p.groups, p.n, p.q_tiles * 128, p.splits, wo, wml, p.rows, mst);
+    if (p.splits > 1 && !cm && !(dbg_skip & 4))
+      flash_merge(p.groups, p.n, p.q_tiles * 128, p.splits, reinterpret_cast<const bf16 *>(wo), wml, p.rows, mst);
   }
 
   void reserve_common() {
