@@ -179,6 +179,21 @@ __device__ __forceinline__ void rope_store(const QkvRope &r, int t, int f, float
   }
 }
 
+// rope_store with the k / v destination slot already loaded (s < 0: dropped)
+__device__ __forceinline__ void rope_store_slot(const QkvRope &r, int t, int s, int f, float acc, float pair,
+                                                float cs, float sn) {
+  const int h = f >> 8, j = f & 255, i = j >> 1;
+  if (h < 9) {
+    const bool second = j & 1;
+    const float v = second ? acc * cs + pair * sn : acc * cs - pair * sn;
+    const int dim = second ? i + 128 : i;
+    if (h < 8) r.q_out[(size_t)t * 2048 + h * 256 + dim] = __float2bfloat16(v);
+    else if (s >= 0) r.k_dst[(size_t)s * 256 + dim] = __float2bfloat16(v);
+  } else if (s >= 0) {
+    r.v_dst[(size_t)s * 256 + j] = __float2bfloat16(acc);
+  }
+}
+
 __device__ __forceinline__ float2 rope_cs(const QkvRope &r, int pos, int i) {
   if (r.cs && pos < ROPE_TABLE_POS) return __ldg(r.cs + (size_t)pos * 128 + i);
   float sn, cs;
@@ -233,41 +248,113 @@ __device__ __forceinline__ void epilogue_store(const EpiParams &e, int t, int f,
 }
 
 // Epilogue over this thread's output feature f and the tile's BN token columns
-// (TMEM lane = f).  MODE < 0 writes split-K partials.
+// (TMEM lane = f).  MODE < 0 writes split-K partials.  Per 16-token chunk every
+// load (per-feature bias / gate once, the chunk's residual or RoPE operands)
+// is issued before any store, and stores are predicated, not branched: the
+// compiler cannot prove the outputs do not alias the operands, so a
+// load-after-store per token serialised the epilogue on L2 latency, and one
+// divergent region per token cost ~1 us per 16-token chunk (tools/gemm_prof.py).
 template <int MODE, typename P>
 __device__ __forceinline__ void epi_loop(const P &p, uint32_t trow, int c_begin, int c_end, int n0, int f, int split) {
   const bool fok = f < p.n_out;
-  for (int c = c_begin; c < c_end; c += 16) {
-    uint32_t v[16];
-    tmem_ld16(trow + (uint32_t)c, v);
-    if constexpr (MODE == EPI_QKV_ROPE) {
-      // all 16 positions, then all 16 (cos, sin), before any store: the loads
-      // must not serialise behind the (possibly aliasing) output stores
-      const QkvRope &r = p.epi.rope;
-      const int i = (f & 255) >> 1;
-      int pos[16];
-      float2 csn[16];
+  const EpiParams &e = p.epi;
+  if constexpr (MODE == EPI_QKV_ROPE) {
+    const QkvRope &r = e.rope;
+    const int i = (f & 255) >> 1;
+    const bool kv = (f >> 8) >= 8;  // k / v head rows: routed through the slot table
+    for (int c = c_begin; c < c_end; c += 16) {
+      uint32_t v[16];
+      tmem_ld16(trow + (uint32_t)c, v);
+      const int t0 = n0 + c;
+      const int nv = fok ? max(0, min(16, p.t - t0)) : 0;
+      int pos[16], sl[16];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) pos[j] = n0 + c + j < p.t ? __ldg(r.pos + n0 + c + j) : 0;
+      for (int j = 0; j < 16; ++j) {
+        pos[j] = j < nv ? __ldg(r.pos + t0 + j) : 0;
+        sl[j] = kv && j < nv ? (r.slot ? r.slot[t0 + j] : t0 + j) : -1;
+      }
+      float2 csn[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) csn[j] = rope_cs(r, pos[j], i);
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
-        const int t = n0 + c + j;
         const float acc = __uint_as_float(v[j]);
         const float pair = __shfl_xor_sync(0xffffffffu, acc, 1);
-        if (t < p.t && fok) rope_store(r, t, f, acc, pair, csn[j].x, csn[j].y);
+        if (j < nv) rope_store_slot(r, t0 + j, sl[j], f, acc, pair, csn[j].x, csn[j].y);
       }
-    } else {
+    }
+  } else {
+    const float bias = (MODE >= 0 && e.bias && fok) ? __ldg(e.bias + f) : 0.f;
+    const float bias_up = (MODE == EPI_GEGLU_BF16 && e.bias && fok) ? __ldg(e.bias + (f | 1)) : 0.f;
+    const float gate = (MODE == EPI_ADD_GATED_F32 && fok) ? __ldg(e.gate + f) : 0.f;
+    for (int c = c_begin; c < c_end; c += 16) {
+      uint32_t v[16];
+      tmem_ld16(trow + (uint32_t)c, v);
+      const int t0 = n0 + c;
+      const int nv = fok ? max(0, min(16, p.t - t0)) : 0;
+      if constexpr (MODE < 0) {
+        float *dst = p.ws + ((size_t)split * p.t + t0) * p.n_out + f;
+        const size_t ld = p.n_out;
+        if (nv == 16) {  // full chunk: straight-line stores
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int t = n0 + c + j;
-        const float acc = __uint_as_float(v[j]);
-        float pair = 0.f;
-        if (MODE == EPI_GEGLU_BF16) pair = __shfl_xor_sync(0xffffffffu, acc, 1);
-        if (t >= p.t || !fok) continue;
-        if (MODE < 0) p.ws[((size_t)split * p.t + t) * p.n_out + f] = acc;
-        else epilogue_store<(MODE < 0 ? 0 : MODE)>(p.epi, t, f, p.n_out, acc, pair);
+          for (int j = 0; j < 16; ++j) dst[j * ld] = __uint_as_float(v[j]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (j < nv) dst[j * ld] = __uint_as_float(v[j]);
+        }
+      } else if constexpr (MODE == EPI_ADD_F32 || MODE == EPI_ADD_GATED_F32 || MODE == EPI_ADD_BF16) {
+        const float *src = MODE == EPI_ADD_BF16 ? e.res + (size_t)t0 * e.ldr + f
+                                                : static_cast<const float *>(e.out) + (size_t)t0 * e.ldo + f;
+        const int lds = MODE == EPI_ADD_BF16 ? e.ldr : e.ldo;
+        float old[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) old[j] = j < nv ? src[(size_t)j * lds] : 0.f;
+        auto put = [&](int j) {
+          const float acc = __uint_as_float(v[j]) + bias;
+          const size_t o = (size_t)(t0 + j) * e.ldo + f;
+          if constexpr (MODE == EPI_ADD_F32) static_cast<float *>(e.out)[o] = old[j] + acc;
+          else if constexpr (MODE == EPI_ADD_GATED_F32) static_cast<float *>(e.out)[o] = old[j] + gate * acc;
+          else static_cast<__nv_bfloat16 *>(e.out)[o] = __float2bfloat16(acc + old[j]);
+        };
+        if (nv == 16) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) put(j);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (j < nv) put(j);
+        }
+      } else {
+        float pair[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          pair[j] = MODE == EPI_GEGLU_BF16 ? __shfl_xor_sync(0xffffffffu, __uint_as_float(v[j]), 1) : 0.f;
+        auto put = [&](int j) {
+          const float acc = __uint_as_float(v[j]) + bias;
+          const size_t o = (size_t)(t0 + j) * e.ldo + f;
+          if constexpr (MODE == EPI_F32) {
+            static_cast<float *>(e.out)[o] = acc;
+          } else if constexpr (MODE == EPI_BF16) {
+            static_cast<__nv_bfloat16 *>(e.out)[o] = __float2bfloat16(acc);
+          } else if constexpr (MODE == EPI_GEGLU_BF16) {
+            if ((f & 1) == 0)
+              static_cast<__nv_bfloat16 *>(e.out)[(size_t)(t0 + j) * e.ldo + (f >> 1)] =
+                  __float2bfloat16(gelu_tanh(acc) * (pair[j] + bias_up));
+          } else if constexpr (MODE == EPI_GELU_BF16) {
+            static_cast<__nv_bfloat16 *>(e.out)[o] = __float2bfloat16(gelu_tanh(acc));
+          } else if constexpr (MODE == EPI_SWISH_BF16) {
+            static_cast<__nv_bfloat16 *>(e.out)[o] = __float2bfloat16(acc / (1.f + __expf(-acc)));
+          }
+        };
+        if (nv == 16) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) put(j);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (j < nv) put(j);
+        }
       }
     }
   }

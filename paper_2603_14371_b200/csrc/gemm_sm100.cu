@@ -120,6 +120,27 @@ __global__ void splitk_reduce_kernel(const float *ws, int splits, int t_rows, in
   if (f + 1 < n_out) epilogue_store(e, t, f + 1, n_out, a1, a0);
 }
 
+#ifdef OXY_GEMM_PROF
+// timing builds: %globaltimer at pipeline events of weight tile 0 / token tile 0
+// of the launches matching (n_out, k) set by oxy_debug_gemm_prof_select, one row
+// per split (the last matching launch wins)
+__device__ unsigned long long g_gemm_prof[32][16];
+__device__ int g_gemm_prof_sel[2];
+#define GPROF(ev)                                                                             \
+  do {                                                                                        \
+    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z < 32 && p.n_out == g_gemm_prof_sel[0] && \
+        p.k == g_gemm_prof_sel[1]) {                                                          \
+      unsigned long long t_;                                                                  \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                  \
+      g_gemm_prof[blockIdx.z][ev] = t_;                                                       \
+    }                                                                                         \
+  } while (0)
+#else
+#define GPROF(ev) \
+  do {            \
+  } while (0)
+#endif
+
 __global__ void __launch_bounds__(192, 2)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 KParams p) {
@@ -143,6 +164,7 @@ __global__ void __launch_bounds__(192, 2)
                  done = smem_u32(bars + 2 * MAX_STAGES);
   uint32_t ncols = 32;
   while (ncols < (uint32_t)bn) ncols <<= 1;
+  if (threadIdx.x == 0) GPROF(0);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
@@ -165,6 +187,7 @@ __global__ void __launch_bounds__(192, 2)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) GPROF(1);
   if (warp == 0) {
     if (lane == 0) {
       // Weights never depend on the previous kernel: stream the first ring of
@@ -174,7 +197,9 @@ __global__ void __launch_bounds__(192, 2)
         mbar_expect_tx(full0 + 8 * i, A_STAGE_BYTES + b_bytes);
         tma_load_2d(&tmA, full0 + 8 * i, smem_u32(sA + i * A_STAGE_BYTES), (kb0 + i) * BK, m0);
       }
+      GPROF(2);
       pdl_wait();
+      GPROF(3);
       for (int i = 0; i < pre; ++i)
         tma_load_2d(&tmB, full0 + 8 * i, smem_u32(sB + i * b_bytes), (kb0 + i) * BK, n0);
       for (int i = pre; i < nkb; ++i) {
@@ -188,6 +213,7 @@ __global__ void __launch_bounds__(192, 2)
       }
       // all operand loads are in flight: let the next kernel start its
       // prologue and weight prefetch while this CTA drains
+      GPROF(4);
       if (p.trigger) pdl_trigger();
     }
   } else if (warp == 1) {
@@ -199,6 +225,7 @@ __global__ void __launch_bounds__(192, 2)
         const uint32_t ph = (i / stages) & 1;
         mbar_wait(full0 + 8 * s, ph);
         tc_fence_after();
+        if (i == 0) GPROF(5);
         const uint32_t a = smem_u32(sA + s * A_STAGE_BYTES), b = smem_u32(sB + s * b_bytes);
 #pragma unroll
         for (int kk = 0; kk < BK / 16; ++kk)
@@ -207,21 +234,35 @@ __global__ void __launch_bounds__(192, 2)
         mma_commit(empty0 + 8 * s);
       }
       mma_commit(done);
+      GPROF(6);
     }
     __syncwarp();
   } else {
-    pdl_wait();  // the epilogue reads bias/residual/gates and writes outputs
-    mbar_wait(done, 0);
-    tc_fence_after();
     const int q = warp & 3;
     const int f = m0 + q * 32 + lane;
     const bool split_out = p.splits > 1;
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
+    pdl_wait();  // the epilogue reads bias/residual/gates and writes outputs
+    if (threadIdx.x == 64) GPROF(7);
+    mbar_wait(done, 0);
+    tc_fence_after();
+    if (threadIdx.x == 64) GPROF(8);
+#ifdef OXY_GEMM_PROF
+    if (bn > 32) {
+      epi_tile(p, trow, 0, 16, n0, f, split, split_out);
+      if (threadIdx.x == 64) GPROF(11);
+      epi_tile(p, trow, 16, 32, n0, f, split, split_out);
+      if (threadIdx.x == 64) GPROF(12);
+      epi_tile(p, trow, 32, bn, n0, f, split, split_out);
+    } else
+#endif
     epi_tile(p, trow, 0, bn, n0, f, split, split_out);
+    if (threadIdx.x == 64) GPROF(9);
     if (split_out && p.fixup) splitk_fixup(p, blockIdx.y * gridDim.x + blockIdx.x, n0, 0, bn, f, s_last, 128, 64);
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) GPROF(10);
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols)
@@ -836,3 +877,13 @@ extern "C" int oxy_gemm_plan(int32_t n_out, int32_t k, int32_t t, int32_t splits
   out6[5] = p.kb_total;
   OXY_API_END
 }
+
+#ifdef OXY_GEMM_PROF
+extern "C" int oxy_debug_gemm_prof_select(int n_out, int k) {
+  const int v[2] = {n_out, k};
+  return cudaMemcpyToSymbol(oxy::gemm::g_gemm_prof_sel, v, sizeof(v)) == cudaSuccess ? 0 : -1;
+}
+extern "C" int oxy_debug_gemm_prof(unsigned long long *out) {
+  return cudaMemcpyFromSymbol(out, oxy::gemm::g_gemm_prof, sizeof(oxy::gemm::g_gemm_prof)) == cudaSuccess ? 0 : -1;
+}
+#endif

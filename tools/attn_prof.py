@@ -1,5 +1,5 @@
 """Per-event timeline of the tcgen05 attention kernel inside the denoise chain
-(needs the timing build: tools/attn_prof_build.sh, OXY_LIB_VARIANT=aprof).
+(needs the timing build: tools/prof_build.sh, OXY_LIB_VARIANT=aprof).
 Prints, for query tile 0 of the LAST attention launch, each split CTA's
 %globaltimer events in us relative to the earliest kernel entry.
   SKIP=<OXY_DBG_SKIP mask> for chain variants (57: attention kernels only)."""
