@@ -273,9 +273,19 @@ __device__ __forceinline__ void epi_loop(const P &p, uint32_t trow, int c_begin,
         pos[j] = j < nv ? __ldg(r.pos + t0 + j) : 0;
         sl[j] = kv && j < nv ? (r.slot ? r.slot[t0 + j] : t0 + j) : -1;
       }
-      float2 csn[16];
+      // one chunk-uniform table test, then 16 independent table loads (a
+      // per-token table-or-sincosf branch serialised them: 14 us per chunk)
+      int pmax = 0;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) csn[j] = rope_cs(r, pos[j], i);
+      for (int j = 0; j < 16; ++j) pmax = max(pmax, pos[j]);
+      float2 csn[16];
+      if (r.cs && pmax < ROPE_TABLE_POS) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) csn[j] = __ldg(r.cs + (size_t)pos[j] * 128 + i);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) csn[j] = rope_cs(r, pos[j], i);
+      }
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const float acc = __uint_as_float(v[j]);

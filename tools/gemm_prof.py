@@ -33,3 +33,12 @@ print(f"n_out {n_out} k {k}\nsplit " + " ".join(f"{e:>12s}" for e in EV))
 for i in rows:
     print(f"{i:5d} " + " ".join(f"{(a[i, j] - t0) / 1e3:12.2f}" if a[i, j] >= t0 else f"{'-':>12s}"
                                 for j in range(len(EV))))
+if hasattr(_lib.lib(), "oxy_debug_gemm_prof2"):
+    try:
+        b2 = (C.c_ulonglong * (32 * 8))()
+        if _lib.lib().oxy_debug_gemm_prof2(b2) == 0:
+            a2 = np.array(b2, dtype=np.int64).reshape(32, 8)
+            for i in rows[:2]:
+                print("epi chunk0 events", [round((a2[i, j] - t0) / 1e3, 2) for j in range(3) if a2[i, j] > 0])
+    except AttributeError:
+        pass
