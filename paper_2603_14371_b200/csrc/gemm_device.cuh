@@ -247,6 +247,67 @@ __device__ __forceinline__ void epilogue_store(const EpiParams &e, int t, int f,
   }
 }
 
+// Staged bf16 store of one 16-token chunk.  Lane l of the warp holds y[j] for
+// feature f0 + l and token j; the warp transposes the chunk through a private
+// smem tile (16 rows x 36 floats: conflict-free row writes and float4 reads)
+// and each lane then writes 16-byte vectors of consecutive output columns of
+// one token, instead of 16 two-byte stores per lane.  KIND 0: column f (32
+// columns from f0); 1: GeGLU, column f/2 from the even lanes (16 columns);
+// 2: RoPE q, dims i0.. from the even lanes and 128 + i0.. from the odd ones.
+// out0 = the chunk's first token row at the warp's first column; ncols =
+// valid columns from there (KIND 0 / 1).  Returns after the warp's stores.
+constexpr int STG_LD = 36;
+template <int KIND>
+__device__ __forceinline__ void stage_store_bf16(float *stg, const float (&y)[16], int nvt, __nv_bfloat16 *out0,
+                                                 size_t ld, int ncols) {
+  const int lane = threadIdx.x & 31;
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 16; ++j) stg[j * STG_LD + lane] = y[j];
+  __syncwarp();
+  const int j = lane >> 1, h = lane & 1;
+  if (j >= nvt) return;
+  const float *row = stg + j * STG_LD;
+  constexpr int N = KIND == 1 ? 8 : 16;
+  float x[16];
+  int col;
+  if constexpr (KIND == 0) {
+    col = 16 * h;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float4 a = *reinterpret_cast<const float4 *>(row + 16 * h + 4 * q);
+      x[4 * q] = a.x;
+      x[4 * q + 1] = a.y;
+      x[4 * q + 2] = a.z;
+      x[4 * q + 3] = a.w;
+    }
+  } else if constexpr (KIND == 1) {
+    col = 8 * h;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = row[2 * (8 * h + k)];
+  } else {
+    col = 128 * h;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) x[k] = row[2 * k + h];
+  }
+  __nv_bfloat16 *dst = out0 + (size_t)j * ld + col;
+  uint32_t w[8];
+#pragma unroll
+  for (int k = 0; k < N / 2; ++k) {
+    __nv_bfloat162 b = __floats2bfloat162_rn(x[2 * k], x[2 * k + 1]);
+    w[k] = *reinterpret_cast<uint32_t *>(&b);
+  }
+  const bool full = KIND == 2 || col + N <= ncols;
+  if (full && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+    *reinterpret_cast<uint4 *>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+    if constexpr (N == 16) *reinterpret_cast<uint4 *>(dst + 8) = make_uint4(w[4], w[5], w[6], w[7]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < N; ++k)
+      if (KIND == 2 || col + k < ncols) dst[k] = __float2bfloat16(x[k]);
+  }
+}
+
 // Epilogue over this thread's output feature f and the tile's BN token columns
 // (TMEM lane = f).  MODE < 0 writes split-K partials.  Per 16-token chunk every
 // load (per-feature bias / gate once, the chunk's residual or RoPE operands)
@@ -255,7 +316,8 @@ __device__ __forceinline__ void epilogue_store(const EpiParams &e, int t, int f,
 // load-after-store per token serialised the epilogue on L2 latency, and one
 // divergent region per token cost ~1 us per 16-token chunk (tools/gemm_prof.py).
 template <int MODE, typename P>
-__device__ __forceinline__ void epi_loop(const P &p, uint32_t trow, int c_begin, int c_end, int n0, int f, int split) {
+__device__ __forceinline__ void epi_loop(const P &p, uint32_t trow, int c_begin, int c_end, int n0, int f, int split,
+                                         float *stg = nullptr) {
   const bool fok = f < p.n_out;
   const EpiParams &e = p.epi;
   if constexpr (MODE == EPI_QKV_ROPE) {
@@ -285,6 +347,20 @@ __device__ __forceinline__ void epi_loop(const P &p, uint32_t trow, int c_begin,
       } else {
 #pragma unroll
         for (int j = 0; j < 16; ++j) csn[j] = rope_cs(r, pos[j], i);
+      }
+      if (stg && !kv) {  // q heads (warp-uniform: a warp's 32 features lie in one head)
+        const int hd = f >> 8, second = f & 1;
+        float y[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float acc = __uint_as_float(v[j]);
+          const float pair = __shfl_xor_sync(0xffffffffu, acc, 1);
+          y[j] = second ? acc * csn[j].x + pair * csn[j].y : acc * csn[j].x - pair * csn[j].y;
+        }
+        const int nvt = max(0, min(16, p.t - t0));
+        const int i0 = ((f - (threadIdx.x & 31)) & 255) >> 1;
+        stage_store_bf16<2>(stg, y, nvt, r.q_out + (size_t)t0 * 2048 + hd * 256 + i0, 2048, 0);
+        continue;
       }
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
@@ -335,6 +411,29 @@ __device__ __forceinline__ void epi_loop(const P &p, uint32_t trow, int c_begin,
           for (int j = 0; j < 16; ++j)
             if (j < nv) put(j);
         }
+      } else if (MODE != EPI_F32 && stg != nullptr && (e.ldo & 7) == 0) {  // bf16 outputs, staged
+        const int f0 = f - (int)(threadIdx.x & 31);
+        float y[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float acc = __uint_as_float(v[j]) + bias;
+          if constexpr (MODE == EPI_GEGLU_BF16) {
+            const float pr = __shfl_xor_sync(0xffffffffu, __uint_as_float(v[j]), 1);
+            y[j] = gelu_tanh(acc) * (pr + bias_up);
+          } else if constexpr (MODE == EPI_GELU_BF16) {
+            y[j] = gelu_tanh(acc);
+          } else if constexpr (MODE == EPI_SWISH_BF16) {
+            y[j] = acc / (1.f + __expf(-acc));
+          } else {
+            y[j] = acc;
+          }
+        }
+        const int nvt = max(0, min(16, p.t - t0));
+        __nv_bfloat16 *o = static_cast<__nv_bfloat16 *>(e.out) + (size_t)t0 * e.ldo;
+        if constexpr (MODE == EPI_GEGLU_BF16)
+          stage_store_bf16<1>(stg, y, nvt, o + (f0 >> 1), e.ldo, (p.n_out - f0) >> 1);
+        else
+          stage_store_bf16<0>(stg, y, nvt, o + f0, e.ldo, p.n_out - f0);
       } else {
         float pair[16];
 #pragma unroll
@@ -374,18 +473,18 @@ __device__ __forceinline__ void epi_loop(const P &p, uint32_t trow, int c_begin,
 // Columns [c_begin, c_end) of the tile (multiples of 16).
 template <typename P>
 __device__ __forceinline__ void epi_tile(const P &p, uint32_t trow, int c_begin, int c_end, int n0, int f, int split,
-                                         bool split_out) {
+                                         bool split_out, float *stg = nullptr) {
   switch (split_out ? -1 : p.epi.mode) {
     case -1: epi_loop<-1>(p, trow, c_begin, c_end, n0, f, split); break;
-    case EPI_F32: epi_loop<EPI_F32>(p, trow, c_begin, c_end, n0, f, split); break;
-    case EPI_BF16: epi_loop<EPI_BF16>(p, trow, c_begin, c_end, n0, f, split); break;
-    case EPI_ADD_F32: epi_loop<EPI_ADD_F32>(p, trow, c_begin, c_end, n0, f, split); break;
-    case EPI_GEGLU_BF16: epi_loop<EPI_GEGLU_BF16>(p, trow, c_begin, c_end, n0, f, split); break;
-    case EPI_GELU_BF16: epi_loop<EPI_GELU_BF16>(p, trow, c_begin, c_end, n0, f, split); break;
-    case EPI_ADD_BF16: epi_loop<EPI_ADD_BF16>(p, trow, c_begin, c_end, n0, f, split); break;
-    case EPI_ADD_GATED_F32: epi_loop<EPI_ADD_GATED_F32>(p, trow, c_begin, c_end, n0, f, split); break;
-    case EPI_SWISH_BF16: epi_loop<EPI_SWISH_BF16>(p, trow, c_begin, c_end, n0, f, split); break;
-    case EPI_QKV_ROPE: epi_loop<EPI_QKV_ROPE>(p, trow, c_begin, c_end, n0, f, split); break;
+    case EPI_F32: epi_loop<EPI_F32>(p, trow, c_begin, c_end, n0, f, split, stg); break;
+    case EPI_BF16: epi_loop<EPI_BF16>(p, trow, c_begin, c_end, n0, f, split, stg); break;
+    case EPI_ADD_F32: epi_loop<EPI_ADD_F32>(p, trow, c_begin, c_end, n0, f, split, stg); break;
+    case EPI_GEGLU_BF16: epi_loop<EPI_GEGLU_BF16>(p, trow, c_begin, c_end, n0, f, split, stg); break;
+    case EPI_GELU_BF16: epi_loop<EPI_GELU_BF16>(p, trow, c_begin, c_end, n0, f, split, stg); break;
+    case EPI_ADD_BF16: epi_loop<EPI_ADD_BF16>(p, trow, c_begin, c_end, n0, f, split, stg); break;
+    case EPI_ADD_GATED_F32: epi_loop<EPI_ADD_GATED_F32>(p, trow, c_begin, c_end, n0, f, split, stg); break;
+    case EPI_SWISH_BF16: epi_loop<EPI_SWISH_BF16>(p, trow, c_begin, c_end, n0, f, split, stg); break;
+    case EPI_QKV_ROPE: epi_loop<EPI_QKV_ROPE>(p, trow, c_begin, c_end, n0, f, split, stg); break;
   }
 }
 

@@ -247,16 +247,18 @@ __global__ void __launch_bounds__(192, 2)
     mbar_wait(done, 0);
     tc_fence_after();
     if (threadIdx.x == 64) GPROF(8);
+    // the operand ring is idle once `done` fired: 4 x 2.3 KB transpose tiles for the bf16 epilogues
+    float *stg = reinterpret_cast<float *>(sA) + q * (16 * STG_LD);
 #ifdef OXY_GEMM_PROF
     if (bn > 32) {
-      epi_tile(p, trow, 0, 16, n0, f, split, split_out);
+      epi_tile(p, trow, 0, 16, n0, f, split, split_out, stg);
       if (threadIdx.x == 64) GPROF(11);
-      epi_tile(p, trow, 16, 32, n0, f, split, split_out);
+      epi_tile(p, trow, 16, 32, n0, f, split, split_out, stg);
       if (threadIdx.x == 64) GPROF(12);
-      epi_tile(p, trow, 32, bn, n0, f, split, split_out);
+      epi_tile(p, trow, 32, bn, n0, f, split, split_out, stg);
     } else
 #endif
-    epi_tile(p, trow, 0, bn, n0, f, split, split_out);
+    epi_tile(p, trow, 0, bn, n0, f, split, split_out, stg);
     if (threadIdx.x == 64) GPROF(9);
     if (split_out && p.fixup) splitk_fixup(p, blockIdx.y * gridDim.x + blockIdx.x, n0, 0, bn, f, s_last, 128, 64);
   }
