@@ -36,6 +36,7 @@ struct Knobs {
   // persistent wide kernel for T > 64: -1 auto (cost model), 0 off, 1 / 2 force CTA group
   int wide = -1, wide_bn = 0, wide_splits = 0;  // -1 auto (see make_plan), 0 off, 1 / 2 force
   int wide_cl = 0;  // 0 auto, 1 / 2 force the pairs per cluster
+  int wide_min_k = 0;  // > 0: also take the wide kernel for K >= this at T >= 256 (A/B knob)
   // split K (fixed-order reduction) for token counts up to this when the tiles do not fill
   // the SMs: the multi-stream denoise (T = 50 x streams); 8 streams 67.9 -> 61.1 ms/frame
   int split_t = 1024;
@@ -45,6 +46,7 @@ struct Knobs {
     if (const char *s = getenv("OXY_GEMM_WIDE_BN")) wide_bn = atoi(s);
     if (const char *s = getenv("OXY_GEMM_WIDE_SPLITS")) wide_splits = atoi(s);
     if (const char *s = getenv("OXY_GEMM_WIDE_CL")) wide_cl = atoi(s);
+    if (const char *s = getenv("OXY_GEMM_WIDE_MIN_K")) wide_min_k = atoi(s);
     if (const char *s = getenv("OXY_PDL_EARLY_SKINNY")) early_skinny = atoi(s);
     if (const char *s = getenv("OXY_PDL_EARLY_WIDE")) early_wide = atoi(s);
     if (const char *s = getenv("OXY_SPLITK")) fixup = std::string(s) == "fixup";
@@ -607,7 +609,8 @@ Plan make_plan(int n_out, int k, int t, int sms, int force_splits) {
   // (K >= 8192 projections at T = 800 — the prefill down projection, 73.7 vs 98 us
   // stand-alone with split-K 2 — measured slower in the frame: 9.37 vs 9.27 ms prefill)
   const bool wide_ok =
-      knobs().wide > 0 || (knobs().wide < 0 && ((n_out >= 16384 && t >= 256) || t >= 2048));
+      knobs().wide > 0 || (knobs().wide < 0 && ((n_out >= 16384 && t >= 256) || t >= 2048 ||
+                                                (knobs().wide_min_k > 0 && k >= knobs().wide_min_k && t >= 256)));
   if (t > 64 && force_splits <= 0 && wide_ok && wide_plan(p, n_out, k, t, sms)) return p;
   p.cg = 0;
   p.cl = 1;

@@ -93,3 +93,31 @@ def test_split_k_is_deterministic_and_close_to_single():
     c, _ = run(w, x, 0, splits=1)
     assert (a == b).all()
     assert (a - c).abs().max().item() < 1e-3
+
+
+@pytest.mark.parametrize("n,k,t,pad", [(4304, 256, 37, 0), (200, 136, 33, 0), (512, 128, 50, 3), (96, 64, 17, 1)])
+def test_bf16_epilogues_ragged(n, k, t, pad):
+    """bf16 outputs go through the per-warp smem transpose and 16-byte stores:
+    ragged features (n % 32), ragged tokens (t % 16) and a row stride that is not
+    a multiple of 8 (pad > 0: the scalar fall-back) against torch fp32."""
+    import torch
+    w = rand((n, k), 7, 0.05)
+    x = rand((t, k), 8)
+    bias = torch.linspace(-1, 1, n, device="cuda")
+    acc = x.float() @ w.float().T
+    out = torch.zeros(t, n + pad, dtype=torch.bfloat16, device="cuda")
+    run(w, x, 1, out=out, splits=1)
+    torch.testing.assert_close(out[:, :n].float(), acc, rtol=1e-2, atol=2e-2)
+    assert (out[:, n:] == 0).all()
+    out = torch.zeros(t, n + pad, dtype=torch.bfloat16, device="cuda")
+    run(w, x, 4, out=out, bias=bias, splits=1)
+    h = acc + bias
+    torch.testing.assert_close(out[:, :n].float(), 0.5 * h * (1 + torch.tanh(
+        0.7978845608028654 * (h + 0.044715 * h ** 3))), rtol=2e-2, atol=2e-2)
+    if n % 2 == 0:
+        out = torch.zeros(t, n // 2 + pad, dtype=torch.bfloat16, device="cuda")
+        run(w, x, 3, out=out, splits=1)
+        g, u = acc[:, 0::2], acc[:, 1::2]
+        gelu = 0.5 * g * (1 + torch.tanh(0.7978845608028654 * (g + 0.044715 * g ** 3)))
+        torch.testing.assert_close(out[:, :n // 2].float(), gelu * u, rtol=2e-2, atol=2e-2)
+        assert (out[:, n // 2:] == 0).all()
