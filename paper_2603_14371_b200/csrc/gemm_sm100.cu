@@ -37,6 +37,7 @@ struct Knobs {
   int wide = -1, wide_bn = 0, wide_splits = 0;  // -1 auto (see make_plan), 0 off, 1 / 2 force
   int wide_cl = 0;  // 0 auto, 1 / 2 force the pairs per cluster
   int wide_min_k = 0;  // > 0: also take the wide kernel for K >= this at T >= 256 (A/B knob)
+  int split_slots = 1;  // skinny split-K fills split_slots CTAs per SM (A/B knob)
   // split K (fixed-order reduction) for token counts up to this when the tiles do not fill
   // the SMs: the multi-stream denoise (T = 50 x streams); 8 streams 67.9 -> 61.1 ms/frame
   int split_t = 1024;
@@ -47,6 +48,7 @@ struct Knobs {
     if (const char *s = getenv("OXY_GEMM_WIDE_SPLITS")) wide_splits = atoi(s);
     if (const char *s = getenv("OXY_GEMM_WIDE_CL")) wide_cl = atoi(s);
     if (const char *s = getenv("OXY_GEMM_WIDE_MIN_K")) wide_min_k = atoi(s);
+    if (const char *s = getenv("OXY_GEMM_SPLIT_SLOTS")) split_slots = std::max(1, atoi(s));
     if (const char *s = getenv("OXY_PDL_EARLY_SKINNY")) early_skinny = atoi(s);
     if (const char *s = getenv("OXY_PDL_EARLY_WIDE")) early_wide = atoi(s);
     if (const char *s = getenv("OXY_SPLITK")) fixup = std::string(s) == "fixup";
@@ -57,6 +59,8 @@ struct Knobs {
 // per-enqueue override of the skinny early-PDL policy (-1: knob); set by the
 // model around one lane's enqueue (host calls are serial)
 int g_early_override = -1;
+// per-enqueue override of the split-K slot target (0: knob), same discipline
+int g_split_slots_override = 0;
 
 static const Knobs &knobs() {
   static Knobs k;
@@ -634,7 +638,8 @@ Plan make_plan(int n_out, int k, int t, int sms, int force_splits) {
     // more of the weight read behind the previous kernel: measured in-frame,
     // this policy beats 'split only past 16 k-blocks' by 2.4 ms per denoise
     // (profiles/r01_gemm_splits.md)
-    splits = std::max(1, std::min(sms / base, p.kb_total / 4));
+    const int slots = g_split_slots_override > 0 ? g_split_slots_override : knobs().split_slots;
+    splits = std::max(1, std::min(slots * sms / base, p.kb_total / 4));
   }
   splits = std::max(1, std::min(splits, p.kb_total));
   const int per_split = (p.kb_total + splits - 1) / splits;
