@@ -38,6 +38,7 @@ struct Knobs {
   int wide_cl = 0;  // 0 auto, 1 / 2 force the pairs per cluster
   int wide_min_k = 0;  // > 0: also take the wide kernel for K >= this at T >= 256 (A/B knob)
   int split_slots = 1;  // skinny split-K fills split_slots CTAs per SM (A/B knob)
+  int bigk_min = 0, bigk_bn = 0, bigk_splits = 0;  // OXY_GEMM_BIGK=kmin,bn,splits (A/B knob)
   // split K (fixed-order reduction) for token counts up to this when the tiles do not fill
   // the SMs: the multi-stream denoise (T = 50 x streams); 8 streams 67.9 -> 61.1 ms/frame
   int split_t = 1024;
@@ -49,6 +50,7 @@ struct Knobs {
     if (const char *s = getenv("OXY_GEMM_WIDE_CL")) wide_cl = atoi(s);
     if (const char *s = getenv("OXY_GEMM_WIDE_MIN_K")) wide_min_k = atoi(s);
     if (const char *s = getenv("OXY_GEMM_SPLIT_SLOTS")) split_slots = std::max(1, atoi(s));
+    if (const char *s = getenv("OXY_GEMM_BIGK")) sscanf(s, "%d,%d,%d", &bigk_min, &bigk_bn, &bigk_splits);
     if (const char *s = getenv("OXY_PDL_EARLY_SKINNY")) early_skinny = atoi(s);
     if (const char *s = getenv("OXY_PDL_EARLY_WIDE")) early_wide = atoi(s);
     if (const char *s = getenv("OXY_SPLITK")) fixup = std::string(s) == "fixup";
@@ -61,6 +63,8 @@ struct Knobs {
 int g_early_override = -1;
 // per-enqueue override of the split-K slot target (0: knob), same discipline
 int g_split_slots_override = 0;
+// per-enqueue deep-K token tiling {k_min, bn, splits} (k_min 0: off), same discipline
+int g_deepk[3] = {0, 0, 0};
 
 static const Knobs &knobs() {
   static Knobs k;
@@ -626,6 +630,13 @@ Plan make_plan(int n_out, int k, int t, int sms, int force_splits) {
   while (t > 64 && p.m_tiles * p.n_tiles < sms && (t + p.n_tiles) / (p.n_tiles + 1) >= 48) ++p.n_tiles;
   int per = (t + p.n_tiles - 1) / p.n_tiles;
   p.bn = std::max(16, (per + 15) / 16 * 16);
+  // deep-K projections at prefill token counts: wider token tiles (half the weight
+  // re-reads through L2) and split-K 2 to keep both CTA slots per SM busy
+  const int *dk = knobs().bigk_min > 0 ? &knobs().bigk_min : g_deepk;
+  if (dk[0] > 0 && k >= dk[0] && t >= 256 && force_splits <= 0) {
+    if (dk[1] > 0) p.bn = std::min(MAX_BN, dk[1]);
+    if (dk[2] > 0) force_splits = dk[2];
+  }
   p.n_tiles = (t + p.bn - 1) / p.bn;
   const int base = p.m_tiles * p.n_tiles;
   int splits = 1;

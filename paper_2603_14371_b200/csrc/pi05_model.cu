@@ -644,10 +644,19 @@ struct Model {
     // prefill projections whose tiles just miss two waves (e.g. the ViT 1152-wide ones,
     // 144 tiles) split K to fill both CTA slots per SM: 7.49 -> 7.32 ms prefill; the
     // denoise / decode chains keep one slot (OXY_PREFILL_SPLIT_SLOTS, 0 = knob default)
+    // and K >= 2048 projections (Gemma qkv / o / down, ViT fc2) take 128-token tiles with
+    // split-K 2: half the weight re-reads through L2, both CTA slots busy, and the o / down
+    // residual + RMSNorm fused into the split reduce: 7.3 -> 6.45 ms prefill (OXY_PREFILL_DEEPK=0: off)
     struct SlotScope {
-      explicit SlotScope(int v) { gemm::g_split_slots_override = v; }
-      ~SlotScope() { gemm::g_split_slots_override = 0; }
-    } slot_scope(prefill_split_slots);
+      SlotScope(int v, bool deepk) {
+        gemm::g_split_slots_override = v;
+        if (deepk) gemm::g_deepk[0] = 2048, gemm::g_deepk[1] = 128, gemm::g_deepk[2] = 2;
+      }
+      ~SlotScope() {
+        gemm::g_split_slots_override = 0;
+        gemm::g_deepk[0] = gemm::g_deepk[1] = gemm::g_deepk[2] = 0;
+      }
+    } slot_scope(prefill_split_slots, prefill_deepk);
     const int W = c.width, Dv = c.vit_width, nh = c.vit_heads, hd = nh ? Dv / nh : 72;
     std::vector<int> P(n_obs), off(n_obs), boff(n_obs);
     int T = 0, nb = 0, n_images = 0, n_tok = 0;
@@ -1079,6 +1088,10 @@ struct Model {
   // ------------------------------------------------------------ decode
   // A/B: OXY_DECODE_EARLY=0 turns off early PDL for the decode lane's skinny
   // GEMMs (their waiting CTAs then do not hold SMs the concurrent denoise needs)
+  bool prefill_deepk = [] {
+    const char *e = getenv("OXY_PREFILL_DEEPK");
+    return !e || atoi(e) != 0;
+  }();
   int prefill_split_slots = [] {
     const char *e = getenv("OXY_PREFILL_SPLIT_SLOTS");
     return e ? atoi(e) : 2;
