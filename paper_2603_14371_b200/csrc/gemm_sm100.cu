@@ -63,8 +63,9 @@ struct Knobs {
 int g_early_override = -1;
 // per-enqueue override of the split-K slot target (0: knob), same discipline
 int g_split_slots_override = 0;
-// per-enqueue deep-K token tiling {k_min, bn, splits} (k_min 0: off), same discipline
-int g_deepk[3] = {0, 0, 0};
+// per-enqueue token tiling by K band {k_min, bn, splits} x 2 (first matching band; k_min 0:
+// off), same discipline
+int g_deepk[6] = {0, 0, 0, 0, 0, 0};
 
 static const Knobs &knobs() {
   static Knobs k;
@@ -633,6 +634,7 @@ Plan make_plan(int n_out, int k, int t, int sms, int force_splits) {
   // deep-K projections at prefill token counts: wider token tiles (half the weight
   // re-reads through L2) and split-K 2 to keep both CTA slots per SM busy
   const int *dk = knobs().bigk_min > 0 ? &knobs().bigk_min : g_deepk;
+  if (knobs().bigk_min <= 0 && dk[0] > 0 && k < dk[0] && dk[3] > 0) dk += 3;  // second band
   if (dk[0] > 0 && k >= dk[0] && t >= 256 && force_splits <= 0) {
     if (dk[1] > 0) p.bn = std::min(MAX_BN, dk[1]);
     if (dk[2] > 0) force_splits = dk[2];

@@ -89,7 +89,7 @@ struct Plan {
 // launch) for the launches that follow: -1 = knob default, 0 / 1 = force.
 extern int g_early_override;
 extern int g_split_slots_override;
-extern int g_deepk[3];
+extern int g_deepk[6];
 
 // Host: build a plan for (N_out, K, T) on `sms` SMs.
 Plan make_plan(int n_out, int k, int t, int sms, int force_splits = 0);
