@@ -798,17 +798,18 @@ struct Model {
             gemm(vproj, yv + (size_t)img0 * 256 * Dv, W, Dv, n_img[i] * 256, gemm::EPI_F32,
                  X + (size_t)off[i] * W, W, vproj_b);
       }
+      // residual projections go through gemm_res_norm: with the prefill's split-K
+      // plans the split reduce, the residual add and the next RMSNorm are one kernel
+      rmsnorm(X, W, Y, W, L[0].ln1, nullptr, nullptr, T, W, 1e-6f, mst);
       for (int l = 0; l < c.depth; ++l) {
         const LayerW &w = L[l];
-        rmsnorm(X, W, Y, W, w.ln1, nullptr, nullptr, T, W, 1e-6f, mst);
         gemm_qkv(w.wqkv, Y, W, T, d_pos, d_slot, Qb, kpool(l), vpool(l));
         if (l == c.depth - 1) break;  // the last block's output is not cached
         if (use_attn_tc) attend_tc(a_llm, l, Qb, T * Q_HEADS, nullptr, nullptr, 0, false);
         else attend(a_llm, kpool(l), vpool(l));
-        gemm(w.wo, Ob, W, QDIM, T, gemm::EPI_ADD_F32, X, W);
-        rmsnorm(X, W, Y, W, w.ln2, nullptr, nullptr, T, W, 1e-6f, mst);
+        gemm_res_norm(w.wo, Ob, W, QDIM, T, nullptr, X, Y, w.ln2, nullptr, nullptr);
         gemm(w.wgu, Y, 2 * c.mlp, W, T, gemm::EPI_GEGLU_BF16, Hm, c.mlp);
-        gemm(w.wd, Hm, W, c.mlp, T, gemm::EPI_ADD_F32, X, W);
+        gemm_res_norm(w.wd, Hm, W, c.mlp, T, nullptr, X, Y, L[l + 1].ln1, nullptr, nullptr);
       }
     };
     run_body(key, true, body);
