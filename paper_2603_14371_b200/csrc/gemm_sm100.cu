@@ -32,7 +32,9 @@ struct KParams {
 struct Knobs {
   int fixup = 0, pdl = 1, smem_kb = 100;  // 2 CTAs per SM (measured best)
   // early PDL (weight prefetch + trigger) for skinny / wide GEMMs: -1 = default policy
-  int early_skinny = 1, early_wide = 0;
+  // (T > 64 on the one-tile-per-CTA kernel: neutral at 1 stream, 0 to -1.3 ms per
+  // 8-stream frame and 0 to -1 ms at 16 across same-session A/Bs)
+  int early_skinny = 1, early_wide = 1;
   // persistent wide kernel for T > 64: -1 auto (cost model), 0 off, 1 / 2 force CTA group
   int wide = -1, wide_bn = 0, wide_splits = 0;  // -1 auto (see make_plan), 0 off, 1 / 2 force
   int wide_cl = 0;  // 0 auto, 1 / 2 force the pairs per cluster
