@@ -124,6 +124,13 @@ int oxy_gemm_bf16(const void *w_d, const void *x_d, int32_t n_out, int32_t k, in
                   int64_t ws_floats, void *stream);
 /* plan the launch: out6 = {bn, n_tiles, m_tiles, splits, stages, k_blocks} */
 int oxy_gemm_plan(int32_t n_out, int32_t k, int32_t t, int32_t splits, int32_t *out6);
+/* launches enqueued per plan class since the last reset (eager runs and CUDA
+ * graph captures; replays are not re-counted): out[0..n) = {skinny, skinny
+ * split-K, prefill deep-K band, prefill mid-K band, persistent 1-CTA, persistent
+ * 2-CTA (cta_group::2), fused split reduce + residual + RMSNorm, attention with
+ * cluster merge, attention with workspace merge, attention unsplit}.  Test and
+ * profiling aid: lets a parity test assert which kernel plans it exercised. */
+int oxy_plan_counts(int64_t *out, int32_t n, int32_t reset);
 
 /* Paged decode attention (the language-decode hot kernel; replaces the padded
  * dense re-materialisation of kvweaver/backend.py:365-384): rows x 8 query

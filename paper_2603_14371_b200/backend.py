@@ -197,7 +197,8 @@ class CostModelBackend(PricedBackend):
         for kv, toks, budget in zip(batched.kv_batch, batched.token_buffers, batched.max_lens):
             buf = list(toks)
             take = min(k, budget - len(buf))
-            buf.extend(self._synth(len(buf) + j) for j in range(take))
+            n0 = len(buf)  # the reference draws token n from the count before the call
+            buf.extend(self._synth(n0 + j) for j in range(take))
             seq = kv.seq_len + take
             caches.append(KvCache((seq,) * self.config.L, seq, self.backend_tag))
             bufs.append(tuple(buf))

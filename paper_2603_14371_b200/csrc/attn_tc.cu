@@ -144,7 +144,8 @@ __device__ unsigned long long g_attn_prof[32][24];
 
 struct TcAttnArgs {
   const AttnGroup *groups;
-  int q_tiles, splits, ws_rows;
+  int q_tiles, splits, ws_rows;  // splits = grid y = the largest group's split count
+  int tps;                       // key tiles per split (attn_group_splits)
   const bf16 *q_base, *kd_base;  // row offsets of the groups' q / dense k,v pointers
   int kv_ready;  // 1: the paged K/V were not written by the previous kernel (prefetch before the PDL wait)
   int cmerge;    // 1: launched as clusters of `splits` CTAs along y, merge over DSMEM
@@ -173,8 +174,11 @@ __global__ void __launch_bounds__(192, 1)
   if (q0 >= g.nq) return;  // uniform per CTA, before any barrier or TMEM use
   const int split = blockIdx.y;
   const int ta = (g.nka + TK - 1) / TK, tb = (g.nkb + TK - 1) / TK, tiles = ta + tb;
-  const int per = (tiles + a.splits - 1) / a.splits;
-  const int t0 = min(tiles, split * per), t1 = min(tiles, t0 + per), n = t1 - t0;
+  // this group's own key partition (a function of its key count only: batch-invariant);
+  // CTAs past it (split >= gs) idle, or only help with the cluster merge
+  int per;
+  const int gs = attn_group_splits(tiles, a.tps, per);
+  const int t0 = min(tiles, split * per), t1 = min(tiles, t0 + per), n = split < gs ? t1 - t0 : 0;
 
   if (threadIdx.x == 0) {
     mbar_init(b_q, 1);
@@ -366,8 +370,8 @@ __global__ void __launch_bounds__(192, 1)
       tc_fence_after();
     }
     if (threadIdx.x == 64) APROF(7);
-    const bool ok = r < g.nq;
-    if (a.splits == 1) {
+    const bool ok = r < g.nq && split == 0;
+    if (gs == 1) {
       const float inv = l > 0.f ? 1.f / l : 0.f;
       bf16 *orow = g.o + (size_t)r * g.ldo;
 #pragma unroll 1
@@ -392,7 +396,7 @@ __global__ void __launch_bounds__(192, 1)
           *reinterpret_cast<uint4 *>(orow + c + 8) = make_uint4(o[4], o[5], o[6], o[7]);
         }
       }
-    } else {
+    } else if (split < gs) {
       // bf16 partials through TMA stores: rows staged in smem as 4 boxes of
       // 128 rows x 64 bf16 in the 128B-swizzled box layout (conflict-free: the
       // 8 rows of an smem phase hit 8 different 16-byte slots), then one thread
@@ -430,7 +434,7 @@ __global__ void __launch_bounds__(192, 1)
       if (a.cmerge) {  // (m, l) next to the partial; peers read both after the cluster barrier
         reinterpret_cast<float2 *>(sm + OFF_P)[row] = make_float2(m_ref, l);
       } else {
-        if (ok) {
+        if (r < g.nq) {
           const size_t wr = (size_t)split * a.ws_rows + g.wrow0 + r;
           a.ws_ml[wr * 2] = m_ref;
           a.ws_ml[wr * 2 + 1] = l;
@@ -461,10 +465,10 @@ __global__ void __launch_bounds__(192, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
   }
-  if (a.cmerge) {
+  if (a.cmerge && gs > 1) {  // gs is uniform over the cluster (one query tile)
     cluster_sync_all();  // every split's partial and (m, l) are staged
     if (threadIdx.x == 0) APROF(11);
-    const int cs = a.splits;
+    const int cs = a.splits;  // cluster size: rows of the tile are shared out over it
     const int rb = split * TQ / cs, re = min((split + 1) * TQ / cs, g.nq - q0);
     const int nr = max(0, re - rb);
     float *wgt = reinterpret_cast<float *>(sm + OFF_V);  // [nr][16]: split weight / L per row
@@ -474,7 +478,7 @@ __global__ void __launch_bounds__(192, 1)
       float m[16], lv[16], M = -INFINITY;
 #pragma unroll
       for (int j = 0; j < 16; ++j)
-        if (j < cs) {
+        if (j < gs) {
           asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];"
                        : "=f"(m[j]), "=f"(lv[j])
                        : "r"(map_to_rank(ml_s + row * 8, j))
@@ -484,14 +488,14 @@ __global__ void __launch_bounds__(192, 1)
       float L = 0.f;
 #pragma unroll
       for (int j = 0; j < 16; ++j)
-        if (j < cs) {
+        if (j < gs) {
           m[j] = m[j] == -INFINITY ? 0.f : exp2f(m[j] - M);
           L += lv[j] * m[j];
         }
       const float inv = L > 0.f ? 1.f / L : 0.f;
 #pragma unroll
       for (int j = 0; j < 16; ++j)
-        if (j < cs) wgt[i * 16 + j] = m[j] * inv;
+        if (j < gs) wgt[i * 16 + j] = m[j] * inv;
     }
     __syncthreads();
     for (int idx = threadIdx.x; idx < nr * (HD / 8); idx += blockDim.x) {
@@ -501,7 +505,7 @@ __global__ void __launch_bounds__(192, 1)
       uint4 v[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j)
-        if (j < cs)
+        if (j < gs)
           asm volatile("ld.shared::cluster.v4.u32 {%0, %1, %2, %3}, [%4];"
                        : "=r"(v[j].x), "=r"(v[j].y), "=r"(v[j].z), "=r"(v[j].w)
                        : "r"(map_to_rank(st_s + off, j))
@@ -509,7 +513,7 @@ __global__ void __launch_bounds__(192, 1)
       float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int j = 0; j < 16; ++j)
-        if (j < cs) {  // split order
+        if (j < gs) {  // split order
           const float w = wgt[i * 16 + j];
           const uint32_t u[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
 #pragma unroll
@@ -541,7 +545,7 @@ int attn_cluster_merge_max() {
   return v;
 }
 
-void flash_attention_tc(const AttnGroup *groups_d, int n_groups, int q_tiles, int splits, const bf16 *q_base,
+void flash_attention_tc(const AttnGroup *groups_d, int n_groups, int q_tiles, int splits, int tps, const bf16 *q_base,
                         int q_rows, const CUtensorMap &kpool_map, const CUtensorMap &vpool_map, const bf16 *kd_base,
                         const bf16 *vd_base, int kd_rows, float scale, float *ws_o, float *ws_ml, int ws_rows,
                         bool kv_ready, bool cmerge, cudaStream_t st) {
@@ -565,7 +569,8 @@ void flash_attention_tc(const AttnGroup *groups_d, int n_groups, int q_tiles, in
   const CUtensorMap wsm =
       splits > 1 && !cmerge ? gemm::make_map(reinterpret_cast<const bf16 *>(ws_o), splits * ws_rows, tc::HD, tc::TQ)
                             : qm;
-  TcAttnArgs a{groups_d, q_tiles, splits, ws_rows, q_base, kd_base, kv_ready ? 1 : 0, cmerge ? 1 : 0,
+  ++gemm::g_plan_counts[splits == 1 ? gemm::PC_ATTN_ONE : cmerge ? gemm::PC_ATTN_CMERGE : gemm::PC_ATTN_WSMERGE];
+  TcAttnArgs a{groups_d, q_tiles, splits, ws_rows, tps, q_base, kd_base, kv_ready ? 1 : 0, cmerge ? 1 : 0,
                scale * 1.4426950408889634f, ws_o, ws_ml};
   launch_pdl_cluster(flash_tc_kernel, dim3(n_groups * q_tiles, splits), dim3(192), tc::SMEM, st,
                      dim3(1, cmerge ? splits : 1, 1), qm, kpool_map, vpool_map, kdm, vdm, wsm, a);
@@ -584,8 +589,6 @@ extern "C" int oxy_prefix_attention(const void *q_d, void *out_d, const void *kp
   OXY_REQUIRE(nkb == 0 || (kd_d && vd_d), "dense keys need kd/vd");
   const int tiles = (nka + 63) / 64 + (nkb + 63) / 64;
   OXY_REQUIRE(splits >= 1 && splits <= 32 && splits <= tiles, "splits must be in [1, min(32, key tiles)]");
-  const bool cm = splits > 1 && splits <= oxy::pi05::attn_cluster_merge_max();
-  OXY_REQUIRE(splits == 1 || cm || (ws_o && ws_ml), "split attention needs a workspace");
   auto st = oxy::as_stream(stream);
   oxy::pi05::AttnGroup g{};
   g.q = static_cast<const bf16 *>(q_d);
@@ -605,10 +608,18 @@ extern "C" int oxy_prefix_attention(const void *q_d, void *out_d, const void *kp
   const CUtensorMap km = oxy::gemm::make_map(kpool_d, num_blocks * 64, 256, 64);
   const CUtensorMap vm = oxy::gemm::make_map(vpool_d, num_blocks * 64, 256, 64);
   const int q_tiles = (nq + 127) / 128, ws_rows = q_tiles * 128;
-  oxy::pi05::flash_attention_tc(gd, 1, q_tiles, splits, g.q, nq, km, vm, g.kb, g.vb, std::max(nkb, 1), 1.f / 16.f,
-                                ws_o, ws_ml, ws_rows, false, cm, st);
+  const int tps = (tiles + splits - 1) / splits;  // the key partition `splits` asks for
+  int per = 0;
+  splits = oxy::pi05::attn_group_splits(tiles, tps, per);  // e.g. 9 tiles / 4 splits -> 3 x 3
+  const bool cm = splits > 1 && splits <= oxy::pi05::attn_cluster_merge_max();
+  if (splits > 1 && !cm && !(ws_o && ws_ml)) {
+    cudaFreeAsync(gd, st);
+    oxy::fail(OXY_EINVAL, "split attention needs a workspace");
+  }
+  oxy::pi05::flash_attention_tc(gd, 1, q_tiles, splits, tps, g.q, nq, km, vm, g.kb, g.vb, std::max(nkb, 1),
+                                1.f / 16.f, ws_o, ws_ml, ws_rows, false, cm, st);
   if (splits > 1 && !cm)
-    oxy::pi05::flash_merge(gd, 1, ws_rows, splits, reinterpret_cast<const bf16 *>(ws_o), ws_ml, ws_rows, st);
+    oxy::pi05::flash_merge(gd, 1, ws_rows, splits, tps, reinterpret_cast<const bf16 *>(ws_o), ws_ml, ws_rows, st);
   OXY_CUDA(cudaFreeAsync(gd, st));
   OXY_API_END
 }

@@ -149,13 +149,28 @@ __device__ __forceinline__ void mma_commit_pair(uint32_t bar) {
       : "memory");
 }
 
+// Epilogue arithmetic is written with explicit rounding intrinsics (no FMA
+// contraction or re-association left to the compiler, which may decide
+// differently in each kernel it inlines into): every kernel variant (one-tile,
+// persistent 1-/2-CTA) and every epilogue path (direct, staged bf16, split
+// reduce, split fix-up) then computes an output element bit-identically — the
+// batch-invariant plans (gemm::policy_splits) rely on it.
+//
 // GELU (tanh form) on the SFU: tanh.approx.f32 (rel. error ~2^-11, far below
 // the bf16 rounding of the stored activation)
 __device__ __forceinline__ float gelu_tanh(float x) {
   const float c = 0.7978845608028654f;  // sqrt(2/pi)
+  const float x3 = __fmul_rn(__fmul_rn(x, x), x);
+  const float u = __fmul_rn(c, __fmaf_rn(0.044715f, x3, x));
   float th;
-  asm("tanh.approx.f32 %0, %1;" : "=f"(th) : "f"(c * (x + 0.044715f * x * x * x)));
-  return 0.5f * x * (1.f + th);
+  asm("tanh.approx.f32 %0, %1;" : "=f"(th) : "f"(u));
+  return __fmul_rn(__fmul_rn(0.5f, x), __fadd_rn(1.f, th));
+}
+__device__ __forceinline__ float geglu(float g, float up) { return __fmul_rn(gelu_tanh(g), up); }
+__device__ __forceinline__ float swish(float x) { return __fdiv_rn(x, __fadd_rn(1.f, __expf(-x))); }
+// rotary pair: x1' = x1 c - x2 s (first), x2' = x2 c + x1 s (second)
+__device__ __forceinline__ float rope_rot(bool second, float acc, float pair, float cs, float sn) {
+  return __fmaf_rn(acc, cs, second ? __fmul_rn(pair, sn) : -__fmul_rn(pair, sn));
 }
 
 // RoPE + q / k / v routing of one accumulator (rotary pairs interleaved in the
@@ -165,7 +180,7 @@ __device__ __forceinline__ void rope_store(const QkvRope &r, int t, int f, float
   const int h = f >> 8, j = f & 255, i = j >> 1;
   if (h < 9) {  // q heads 0..7, k head 8: rotate the (x1, x2) pair
     const bool second = j & 1;  // this lane holds x2 (dim i + 128)
-    const float v = second ? acc * cs + pair * sn : acc * cs - pair * sn;
+    const float v = rope_rot(second, acc, pair, cs, sn);
     const int dim = second ? i + 128 : i;
     if (h < 8) {
       r.q_out[(size_t)t * 2048 + h * 256 + dim] = __float2bfloat16(v);
@@ -185,7 +200,7 @@ __device__ __forceinline__ void rope_store_slot(const QkvRope &r, int t, int s, 
   const int h = f >> 8, j = f & 255, i = j >> 1;
   if (h < 9) {
     const bool second = j & 1;
-    const float v = second ? acc * cs + pair * sn : acc * cs - pair * sn;
+    const float v = rope_rot(second, acc, pair, cs, sn);
     const int dim = second ? i + 128 : i;
     if (h < 8) r.q_out[(size_t)t * 2048 + h * 256 + dim] = __float2bfloat16(v);
     else if (s >= 0) r.k_dst[(size_t)s * 256 + dim] = __float2bfloat16(v);
@@ -206,7 +221,7 @@ __device__ __forceinline__ float2 rope_cs(const QkvRope &r, int pos, int i) {
 template <int MODE = -1>
 __device__ __forceinline__ void epilogue_store(const EpiParams &e, int t, int f, int n_out, float acc,
                                                float pair) {
-  if (e.bias) acc += e.bias[f];
+  if (e.bias) acc = __fadd_rn(acc, e.bias[f]);
   switch (MODE >= 0 ? MODE : e.mode) {
     case EPI_F32:
       static_cast<float *>(e.out)[(size_t)t * e.ldo + f] = acc;
@@ -215,13 +230,12 @@ __device__ __forceinline__ void epilogue_store(const EpiParams &e, int t, int f,
       static_cast<__nv_bfloat16 *>(e.out)[(size_t)t * e.ldo + f] = __float2bfloat16(acc);
       break;
     case EPI_ADD_F32:
-      static_cast<float *>(e.out)[(size_t)t * e.ldo + f] += acc;
+      static_cast<float *>(e.out)[(size_t)t * e.ldo + f] = __fadd_rn(static_cast<float *>(e.out)[(size_t)t * e.ldo + f], acc);
       break;
     case EPI_GEGLU_BF16:
       if ((f & 1) == 0) {
-        float up = pair + (e.bias ? e.bias[f + 1] : 0.f);
-        static_cast<__nv_bfloat16 *>(e.out)[(size_t)t * e.ldo + (f >> 1)] =
-            __float2bfloat16(gelu_tanh(acc) * up);
+        const float up = __fadd_rn(pair, e.bias ? e.bias[f + 1] : 0.f);
+        static_cast<__nv_bfloat16 *>(e.out)[(size_t)t * e.ldo + (f >> 1)] = __float2bfloat16(geglu(acc, up));
       }
       break;
     case EPI_GELU_BF16:
@@ -229,14 +243,15 @@ __device__ __forceinline__ void epilogue_store(const EpiParams &e, int t, int f,
       break;
     case EPI_ADD_BF16:
       static_cast<__nv_bfloat16 *>(e.out)[(size_t)t * e.ldo + f] =
-          __float2bfloat16(acc + e.res[(size_t)t * e.ldr + f]);
+          __float2bfloat16(__fadd_rn(acc, e.res[(size_t)t * e.ldr + f]));
       break;
     case EPI_ADD_GATED_F32:
-      static_cast<float *>(e.out)[(size_t)t * e.ldo + f] += e.gate[f] * acc;
+      static_cast<float *>(e.out)[(size_t)t * e.ldo + f] =
+          __fmaf_rn(e.gate[f], acc, static_cast<float *>(e.out)[(size_t)t * e.ldo + f]);
       break;
     case EPI_SWISH_BF16:
       static_cast<__nv_bfloat16 *>(e.out)[(size_t)t * e.ldo + f] =
-          __float2bfloat16(acc / (1.f + __expf(-acc)));
+          __float2bfloat16(swish(acc));
       break;
     case EPI_QKV_ROPE: {
       const QkvRope &r = e.rope;
@@ -355,7 +370,7 @@ __device__ __forceinline__ void epi_loop(const P &p, uint32_t trow, int c_begin,
         for (int j = 0; j < 16; ++j) {
           const float acc = __uint_as_float(v[j]);
           const float pair = __shfl_xor_sync(0xffffffffu, acc, 1);
-          y[j] = second ? acc * csn[j].x + pair * csn[j].y : acc * csn[j].x - pair * csn[j].y;
+          y[j] = rope_rot(second, acc, pair, csn[j].x, csn[j].y);
         }
         const int nvt = max(0, min(16, p.t - t0));
         const int i0 = ((f - (threadIdx.x & 31)) & 255) >> 1;
@@ -397,11 +412,11 @@ __device__ __forceinline__ void epi_loop(const P &p, uint32_t trow, int c_begin,
 #pragma unroll
         for (int j = 0; j < 16; ++j) old[j] = j < nv ? src[(size_t)j * lds] : 0.f;
         auto put = [&](int j) {
-          const float acc = __uint_as_float(v[j]) + bias;
+          const float acc = __fadd_rn(__uint_as_float(v[j]), bias);
           const size_t o = (size_t)(t0 + j) * e.ldo + f;
-          if constexpr (MODE == EPI_ADD_F32) static_cast<float *>(e.out)[o] = old[j] + acc;
-          else if constexpr (MODE == EPI_ADD_GATED_F32) static_cast<float *>(e.out)[o] = old[j] + gate * acc;
-          else static_cast<__nv_bfloat16 *>(e.out)[o] = __float2bfloat16(acc + old[j]);
+          if constexpr (MODE == EPI_ADD_F32) static_cast<float *>(e.out)[o] = __fadd_rn(old[j], acc);
+          else if constexpr (MODE == EPI_ADD_GATED_F32) static_cast<float *>(e.out)[o] = __fmaf_rn(gate, acc, old[j]);
+          else static_cast<__nv_bfloat16 *>(e.out)[o] = __float2bfloat16(__fadd_rn(acc, old[j]));
         };
         if (nv == 16) {
 #pragma unroll
@@ -416,14 +431,14 @@ __device__ __forceinline__ void epi_loop(const P &p, uint32_t trow, int c_begin,
         float y[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          const float acc = __uint_as_float(v[j]) + bias;
+          const float acc = __fadd_rn(__uint_as_float(v[j]), bias);
           if constexpr (MODE == EPI_GEGLU_BF16) {
             const float pr = __shfl_xor_sync(0xffffffffu, __uint_as_float(v[j]), 1);
-            y[j] = gelu_tanh(acc) * (pr + bias_up);
+            y[j] = geglu(acc, __fadd_rn(pr, bias_up));
           } else if constexpr (MODE == EPI_GELU_BF16) {
             y[j] = gelu_tanh(acc);
           } else if constexpr (MODE == EPI_SWISH_BF16) {
-            y[j] = acc / (1.f + __expf(-acc));
+            y[j] = swish(acc);
           } else {
             y[j] = acc;
           }
@@ -440,7 +455,7 @@ __device__ __forceinline__ void epi_loop(const P &p, uint32_t trow, int c_begin,
         for (int j = 0; j < 16; ++j)
           pair[j] = MODE == EPI_GEGLU_BF16 ? __shfl_xor_sync(0xffffffffu, __uint_as_float(v[j]), 1) : 0.f;
         auto put = [&](int j) {
-          const float acc = __uint_as_float(v[j]) + bias;
+          const float acc = __fadd_rn(__uint_as_float(v[j]), bias);
           const size_t o = (size_t)(t0 + j) * e.ldo + f;
           if constexpr (MODE == EPI_F32) {
             static_cast<float *>(e.out)[o] = acc;
@@ -449,11 +464,11 @@ __device__ __forceinline__ void epi_loop(const P &p, uint32_t trow, int c_begin,
           } else if constexpr (MODE == EPI_GEGLU_BF16) {
             if ((f & 1) == 0)
               static_cast<__nv_bfloat16 *>(e.out)[(size_t)(t0 + j) * e.ldo + (f >> 1)] =
-                  __float2bfloat16(gelu_tanh(acc) * (pair[j] + bias_up));
+                  __float2bfloat16(geglu(acc, __fadd_rn(pair[j], bias_up)));
           } else if constexpr (MODE == EPI_GELU_BF16) {
             static_cast<__nv_bfloat16 *>(e.out)[o] = __float2bfloat16(gelu_tanh(acc));
           } else if constexpr (MODE == EPI_SWISH_BF16) {
-            static_cast<__nv_bfloat16 *>(e.out)[o] = __float2bfloat16(acc / (1.f + __expf(-acc)));
+            static_cast<__nv_bfloat16 *>(e.out)[o] = __float2bfloat16(swish(acc));
           }
         };
         if (nv == 16) {

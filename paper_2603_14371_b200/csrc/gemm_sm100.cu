@@ -63,11 +63,10 @@ struct Knobs {
 // per-enqueue override of the skinny early-PDL policy (-1: knob); set by the
 // model around one lane's enqueue (host calls are serial)
 int g_early_override = -1;
-// per-enqueue override of the split-K slot target (0: knob), same discipline
-int g_split_slots_override = 0;
 // per-enqueue token tiling by K band {k_min, bn, splits} x 2 (first matching band; k_min 0:
 // off), same discipline
 int g_deepk[6] = {0, 0, 0, 0, 0, 0};
+long long g_plan_counts[PC_COUNT] = {};
 
 static const Knobs &knobs() {
   static Knobs k;
@@ -559,7 +558,7 @@ static double wide_cost(int n_out, int kb_total, int t, int sms, int cg, int bn,
   return c;
 }
 
-static bool wide_plan(Plan &p, int n_out, int k, int t, int sms) {
+static bool wide_plan(Plan &p, int n_out, int k, int t, int sms, int req_splits) {
   const Knobs &kn = knobs();
   double best = 1e30;
   for (int cg = 1; cg <= 2; ++cg) {
@@ -571,9 +570,10 @@ static bool wide_plan(Plan &p, int n_out, int k, int t, int sms) {
       for (int bn = 32; bn <= MAX_BN; bn += 16) {
         if (kn.wide_bn && bn != kn.wide_bn) continue;
         if (cl == 2 && (t + bn - 1) / bn < 2) continue;
-        for (int splits = 1; splits <= 4; ++splits) {
-          if (kn.wide_splits && splits != kn.wide_splits) continue;
-          if (splits > 1 && p.kb_total / splits < 4) continue;
+        for (int splits = 1; splits <= std::max(4, req_splits); ++splits) {
+          if (req_splits > 0 ? splits != req_splits
+                             : ((kn.wide_splits && splits != kn.wide_splits) || (splits > 1 && p.kb_total / splits < 4)))
+            continue;
           const double c = wide_cost(n_out, p.kb_total, t, sms, cg, bn, splits, cl);
           if (c < best * 0.999) {
             best = c;
@@ -610,6 +610,28 @@ CUtensorMap make_map_f32(const void *ptr, int rows, int cols, int box_cols, int 
   return map;
 }
 
+int policy_splits(int phase, int n_out, int k, int sms) {
+  const int kb = (k + BK - 1) / BK;
+  int s;
+  if (phase == PH_PREFILL) {
+    // deep-K projections (Gemma qkv / o / down, ViT fc2) split K in two: with the
+    // 128-token tiles of the deep-K band both CTA slots per SM stay busy and the o /
+    // down residual + RMSNorm fuse into the split reduce; the gate/up projections
+    // (n_out >= 16384) run on the persistent 2-CTA kernel unsplit
+    s = (k >= 2048 && n_out < 16384) ? 2 : 1;
+  } else {
+    // skinny chains: split K until the weight tiles of one token tile fill the SMs.
+    // Inside the PDL chain every split CTA streams its weight ring before
+    // griddepcontrol.wait, so more splits hide more of the weight read behind the
+    // previous kernel (profiles/r01_gemm_splits.md)
+    const int m_tiles = (n_out + BM - 1) / BM;
+    s = std::max(1, std::min(knobs().split_slots * sms / m_tiles, kb / 4));
+  }
+  s = std::max(1, std::min(s, kb));
+  const int per = (kb + s - 1) / s;
+  return (kb + per - 1) / per;
+}
+
 Plan make_plan(int n_out, int k, int t, int sms, int force_splits) {
   Plan p{};
   p.kb_total = (k + BK - 1) / BK;
@@ -622,24 +644,27 @@ Plan make_plan(int n_out, int k, int t, int sms, int force_splits) {
   const bool wide_ok =
       knobs().wide > 0 || (knobs().wide < 0 && ((n_out >= 16384 && t >= 256) || t >= 2048 ||
                                                 (knobs().wide_min_k > 0 && k >= knobs().wide_min_k && t >= 256)));
-  if (t > 64 && force_splits <= 0 && wide_ok && wide_plan(p, n_out, k, t, sms)) return p;
+  if (t > 64 && wide_ok && wide_plan(p, n_out, k, t, sms, force_splits)) return p;
   p.cg = 0;
   p.cl = 1;
   p.m_tiles = (n_out + BM - 1) / BM;
   p.n_tiles = (t + MAX_BN - 1) / MAX_BN;
-  // wide token dims (prefill): narrower token tiles until the grid fills the SMs
-  // (one past: "at most one CTA per SM" plans measured slower in the frame, 9.60
-  // vs 9.27 ms prefill — the second CTA slot keeps the PDL chain overlapping)
-  while (t > 64 && p.m_tiles * p.n_tiles < sms && (t + p.n_tiles) / (p.n_tiles + 1) >= 48) ++p.n_tiles;
+  // wide token dims (prefill): narrower token tiles until the grid (with its K
+  // splits) fills the SMs (one past: "at most one CTA per SM" plans measured slower
+  // in the frame, 9.60 vs 9.27 ms prefill — the second CTA slot keeps the PDL chain
+  // overlapping).  Token tiling never changes a result; only the K partition does.
+  const int sp_hint = force_splits > 0 ? force_splits : 1;
+  while (t > 64 && p.m_tiles * p.n_tiles * sp_hint < sms && (t + p.n_tiles) / (p.n_tiles + 1) >= 48) ++p.n_tiles;
   int per = (t + p.n_tiles - 1) / p.n_tiles;
   p.bn = std::max(16, (per + 15) / 16 * 16);
   // deep-K projections at prefill token counts: wider token tiles (half the weight
   // re-reads through L2) and split-K 2 to keep both CTA slots per SM busy
   const int *dk = knobs().bigk_min > 0 ? &knobs().bigk_min : g_deepk;
   if (knobs().bigk_min <= 0 && dk[0] > 0 && k < dk[0] && dk[3] > 0) dk += 3;  // second band
-  if (dk[0] > 0 && k >= dk[0] && t >= 256 && force_splits <= 0) {
+  if (dk[0] > 0 && k >= dk[0] && t >= 256) {
+    p.band = dk == g_deepk + 3 ? 2 : 1;
     if (dk[1] > 0) p.bn = std::min(MAX_BN, dk[1]);
-    if (dk[2] > 0) force_splits = dk[2];
+    if (dk[2] > 0 && force_splits <= 0) force_splits = dk[2];
   }
   p.n_tiles = (t + p.bn - 1) / p.bn;
   const int base = p.m_tiles * p.n_tiles;
@@ -653,8 +678,7 @@ Plan make_plan(int n_out, int k, int t, int sms, int force_splits) {
     // more of the weight read behind the previous kernel: measured in-frame,
     // this policy beats 'split only past 16 k-blocks' by 2.4 ms per denoise
     // (profiles/r01_gemm_splits.md)
-    const int slots = g_split_slots_override > 0 ? g_split_slots_override : knobs().split_slots;
-    splits = std::max(1, std::min(slots * sms / base, p.kb_total / 4));
+    splits = std::max(1, std::min(knobs().split_slots * sms / base, p.kb_total / 4));
   }
   splits = std::max(1, std::min(splits, p.kb_total));
   const int per_split = (p.kb_total + splits - 1) / splits;
@@ -744,9 +768,14 @@ void launch(const void *w, const void *x, int n_out, int k, int t, const EpiPara
   if (plan.splits > 1 && (!ws || !counters)) fail(OXY_EINVAL, "split-K GEMM needs a workspace");
   if (plan.splits > 1 && plan.m_tiles * plan.n_tiles * 2 > MAX_TILES) fail(OXY_EINVAL, "too many split-K tiles");
   if (plan.cg > 0) {
+    ++g_plan_counts[plan.cg == 2 ? PC_WIDE_2CTA : PC_WIDE_1CTA];
     launch_wide(w, x, n_out, k, t, epi, plan, ws, counters, st);
     return;
   }
+  ++g_plan_counts[plan.band == 1 ? PC_BAND_DEEPK
+                  : plan.band == 2 ? PC_BAND_MIDK
+                  : plan.splits > 1 ? PC_SKINNY_SPLIT
+                                    : PC_SKINNY];
   CUtensorMap ma = make_map(w, n_out, k, BM);
   CUtensorMap mb = make_map(x, t, k, plan.bn);
   KParams kp;
@@ -851,6 +880,7 @@ __global__ void __launch_bounds__(512)
 void splitk_residual_norm(const float *ws, int splits, int t, int n, const float *gate, float *x, int ldx,
                           __nv_bfloat16 *y, int ldy, const float *w, const float *mod_scale,
                           const float *mod_shift, float eps, cudaStream_t st) {
+  ++g_plan_counts[PC_SPLIT_RES_NORM];
   if (t <= 0) return;
   if (n % 128 != 0 || n > 2048) fail(OXY_EINVAL, "fused residual norm: rows of 128..2048 features (multiple of 128)");
   if (ldx % 4 != 0 || ldy % 4 != 0) fail(OXY_EINVAL, "fused residual norm: row strides must be multiples of 4");
@@ -888,6 +918,15 @@ extern "C" int oxy_gemm_bf16(const void *w_d, const void *x_d, int32_t n_out, in
   oxy::gemm::EpiParams e{mode, out_d, ldo, bias_d, res_d, ldr, nullptr};
   oxy::gemm::launch(w_d, x_d, n_out, k, t, e, plan, ws_d, oxy::gemm::counters_for_abi(),
                     oxy::as_stream(stream));
+  OXY_API_END
+}
+
+extern "C" int oxy_plan_counts(int64_t *out, int32_t n, int32_t reset) {
+  OXY_API_BEGIN
+  OXY_REQUIRE(n >= 0 && (n == 0 || out), "bad plan-count buffer");
+  for (int i = 0; i < n && i < oxy::gemm::PC_COUNT; ++i) out[i] = oxy::gemm::g_plan_counts[i];
+  if (reset)
+    for (auto &c : oxy::gemm::g_plan_counts) c = 0;
   OXY_API_END
 }
 

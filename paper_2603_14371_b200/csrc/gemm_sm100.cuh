@@ -83,15 +83,42 @@ struct Plan {
   int bn, n_tiles, m_tiles, splits, stages, kb_total;
   int cg;  // 0: one-tile-per-CTA kernel (skinny); 1 / 2: persistent wide kernel, 1-CTA / CTA-pair tiles
   int cl;  // wide kernel: CTA pairs per cluster sharing (multicasting) the weight tile (1 or 2)
+  int band;  // prefill token-tile band applied: 0 none, 1 deep-K, 2 mid-K
 };
+
+// Plan classes counted at enqueue time (eager runs and graph captures; replays are
+// not re-counted) so tests can assert which code paths a call exercised.
+enum PlanClass {
+  PC_SKINNY = 0,      // gemm_kernel, whole K
+  PC_SKINNY_SPLIT,    // gemm_kernel, split K
+  PC_BAND_DEEPK,      // gemm_kernel with the deep-K prefill band (128-token tiles)
+  PC_BAND_MIDK,       // gemm_kernel with the mid-K prefill band (96-token tiles)
+  PC_WIDE_1CTA,       // persistent gemm_wide_kernel<1>
+  PC_WIDE_2CTA,       // persistent gemm_wide_kernel<2> (cta_group::2)
+  PC_SPLIT_RES_NORM,  // split reduce + residual + RMSNorm fused
+  PC_ATTN_CMERGE,     // tcgen05 attention, key splits merged over a cluster
+  PC_ATTN_WSMERGE,    // tcgen05 attention, key splits merged through the workspace
+  PC_ATTN_ONE,        // tcgen05 attention, one split
+  PC_COUNT
+};
+extern long long g_plan_counts[PC_COUNT];
 
 // Skinny-GEMM early PDL (weight prefetch before the wait + early dependent
 // launch) for the launches that follow: -1 = knob default, 0 / 1 = force.
 extern int g_early_override;
-extern int g_split_slots_override;
 extern int g_deepk[6];
 
-// Host: build a plan for (N_out, K, T) on `sms` SMs.
+// Batch-invariant split-K policy.  The K partition of a projection — and so the
+// fp32 summation order of every output element — is a function of (phase, N_out,
+// K) only, never of the token count: a row's result is the same whether it is
+// projected alone or inside any batch (decode rows, lock-stepped streams).  The
+// token tiling (BN, tiles, 1- or 2-CTA kernel) may vary freely: tcgen05 computes
+// each output element from its own row and column only.
+enum Phase { PH_PREFILL = 0, PH_CHAIN = 1 };
+int policy_splits(int phase, int n_out, int k, int sms);
+
+// Host: build a plan for (N_out, K, T) on `sms` SMs.  force_splits > 0 fixes the K
+// partition (every kernel variant honours it); 0 = pick for speed (C ABI tests).
 Plan make_plan(int n_out, int k, int t, int sms, int force_splits = 0);
 
 // Host: launch.  ws must hold splits * T * N_out floats when splits > 1.

@@ -298,29 +298,42 @@ __device__ __forceinline__ float2 ld_pair(const bf16 *p) {
   return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(p));
 }
 
-// PT: partial element type (fp32 from the mma.sync kernel, bf16 from the tcgen05 one)
+// PT: partial element type (fp32 from the mma.sync kernel, bf16 from the tcgen05 one).
+// tps > 0: per-group split counts (attn_group_splits, the tcgen05 kernel); 0: `splits`
+// for every group.  The arithmetic is the tcgen05 cluster merge's, op for op (split
+// weights exp2(m_s - M) / L summed in split order, then sum_s w_s * O_s in split
+// order), so a group merged here equals the same group merged over DSMEM.
 template <int HD, typename PT>
-__global__ void fa_merge_kernel(const AttnGroup *groups, int splits, const PT *ws_o, const float *ws_ml,
+__global__ void fa_merge_kernel(const AttnGroup *groups, int splits, int tps, const PT *ws_o, const float *ws_ml,
                                 int ws_rows) {
   pdl_trigger();
   pdl_wait();
   using C = FaCfg<HD>;
   __shared__ float wsh[32];
-  __shared__ float s_inv;
   const AttnGroup g = groups[blockIdx.y];
   const int r = blockIdx.x;
   if (r >= g.nq) return;
+  int gs = splits;
+  if (tps > 0) {
+    int per;
+    gs = attn_group_splits((g.nka + 63) / 64 + (g.nkb + 63) / 64, tps, per);
+    if (gs <= 1) return;  // written directly by the attention kernel
+  }
   const size_t row0 = (size_t)g.wrow0 + r;
   const size_t mstride = (size_t)ws_rows * 2;
-  if (threadIdx.x < 32) {  // warp 0: split weights once (splits <= 32), lane s owns split s
-    const int s = threadIdx.x;
-    const float m = s < splits ? ws_ml[row0 * 2 + s * mstride] : -INFINITY;
-    const float l = s < splits ? ws_ml[row0 * 2 + s * mstride + 1] : 0.f;
-    const float M = warp_max(m);
-    const float w = m == -INFINITY ? 0.f : exp2f(m - M);
-    const float L = warp_sum(l * w);
-    wsh[s] = w;
-    if (s == 0) s_inv = L > 0.f ? 1.f / L : 0.f;
+  if (threadIdx.x == 0) {  // split weights, sequentially in split order (splits <= 32)
+    float m[32], M = -INFINITY;
+    for (int s = 0; s < gs; ++s) {
+      m[s] = ws_ml[row0 * 2 + s * mstride];
+      M = fmaxf(M, m[s]);
+    }
+    float L = 0.f;
+    for (int s = 0; s < gs; ++s) {
+      m[s] = m[s] == -INFINITY ? 0.f : exp2f(m[s] - M);
+      L += ws_ml[row0 * 2 + s * mstride + 1] * m[s];
+    }
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+    for (int s = 0; s < gs; ++s) wsh[s] = m[s] * inv;
   }
   __syncthreads();
   const int c = threadIdx.x * 2;
@@ -329,16 +342,13 @@ __global__ void fa_merge_kernel(const AttnGroup *groups, int splits, const PT *w
   const size_t ostride = (size_t)ws_rows * C::HDP;
   float a0 = 0.f, a1 = 0.f;
 #pragma unroll 8
-  for (int s = 0; s < splits; ++s) {  // split order; independent loads
+  for (int s = 0; s < gs; ++s) {  // split order; independent loads
     const float2 v = ld_pair(o + s * ostride);
-    a0 += v.x * wsh[s];
-    a1 += v.y * wsh[s];
+    a0 += wsh[s] * v.x;
+    a1 += wsh[s] * v.y;
   }
-  *reinterpret_cast<__nv_bfloat162 *>(g.o + (size_t)r * g.ldo + c) =
-      __floats2bfloat162_rn(a0 * s_inv, a1 * s_inv);
+  *reinterpret_cast<__nv_bfloat162 *>(g.o + (size_t)r * g.ldo + c) = __floats2bfloat162_rn(a0, a1);
 }
-
-
 
 template <int HD>
 static void flash_launch(const AttnGroup *groups_d, int n_groups, int max_q_tiles, const bf16 *kpool,
@@ -356,14 +366,15 @@ static void flash_launch(const AttnGroup *groups_d, int n_groups, int max_q_tile
   launch_pdl(flash_attn_kernel<HD>, dim3(grid), dim3(128), C::SMEM, st, groups_d, max_q_tiles, kpool, vpool, scale_log2, splits, ws_o, ws_ml, ws_rows);
   if (splits > 1) {
     launch_pdl(fa_merge_kernel<HD, float>, dim3(max_q_tiles * FA_BQ, n_groups), dim3((HD / 2 + 31) / 32 * 32), 0, st,
-               groups_d, splits, ws_o, ws_ml, ws_rows);
+               groups_d, splits, 0, ws_o, ws_ml, ws_rows);
   }
 }
 
-void flash_merge(const AttnGroup *groups_d, int n_groups, int max_rows, int splits, const bf16 *ws_o,
+void flash_merge(const AttnGroup *groups_d, int n_groups, int max_rows, int splits, int tps, const bf16 *ws_o,
                  const float *ws_ml, int ws_rows, cudaStream_t st) {
   if (splits <= 1 || n_groups <= 0) return;
-  launch_pdl(fa_merge_kernel<256, bf16>, dim3(max_rows, n_groups), dim3(128), 0, st, groups_d, splits, ws_o, ws_ml, ws_rows);
+  launch_pdl(fa_merge_kernel<256, bf16>, dim3(max_rows, n_groups), dim3(128), 0, st, groups_d, splits, tps, ws_o,
+             ws_ml, ws_rows);
 }
 
 void flash_attention(const AttnGroup *groups_d, int n_groups, int max_q_tiles, int head_dim,
@@ -449,6 +460,7 @@ __global__ void __launch_bounds__(128, 1)
   if (active && !active[r]) return;
   const int n_keys = pos[r] + 1;
   const int nb = (n_keys + KV_BLOCK - 1) / KV_BLOCK;
+  cb = decode_row_chunk(nb, cb);  // this row's own chunking: batch-invariant
   const int n_chunks = (nb + cb - 1) / cb;
   if (chunk >= n_chunks) return;
   const int b0 = chunk * cb, nblk = min(nb, b0 + cb) - b0;
@@ -596,6 +608,7 @@ __global__ void decode_merge3_kernel(const float *ws, bf16 *out, const int *pos,
   const int r = blockIdx.x, h = blockIdx.y, d = threadIdx.x;
   if (active && !active[r]) return;
   const int nb = (pos[r] + KV_BLOCK) / KV_BLOCK;
+  cb = decode_row_chunk(nb, cb);
   const int n_chunks = (nb + cb - 1) / cb;
   if (n_chunks == 1) return;  // written directly by the attention kernel
   const float *base = ws + (size_t)r * max_chunks * DA_PART + h * (HEAD_DIM + 2);
@@ -620,22 +633,6 @@ __global__ void decode_merge3_kernel(const float *ws, bf16 *out, const int *pos,
   out[(size_t)r * Q_HEADS * HEAD_DIM + h * HEAD_DIM + d] = __float2bfloat16(acc * s_inv);
 }
 
-int decode_chunk_blocks3(int rows, int max_blocks, int sms) {
-  // cost in block-load units: waves x (pipeline fill ~2 + cb) + 2 if a merge pass is needed
-  int best = std::max(1, (max_blocks + 63) / 64);  // the merge handles <= 64 chunks
-  long best_cost = -1;
-  for (int cb = best; cb <= max_blocks; ++cb) {
-    const int chunks = (max_blocks + cb - 1) / cb;
-    const long ctas = (long)rows * chunks;
-    const long cost = ((ctas + sms - 1) / sms) * (cb + 2) + (chunks > 1 ? 2 : 0);
-    if (best_cost < 0 || cost < best_cost) {
-      best_cost = cost;
-      best = cb;
-    }
-  }
-  return best;
-}
-
 void decode_attention_v3(const CUtensorMap &kmap, const CUtensorMap &vmap, const bf16 *q, bf16 *out, const int *bt,
                          int bt_stride, const int *pos, const int *active, int rows, int max_blocks, float scale,
                          float *ws, int sms, cudaStream_t st) {
@@ -646,8 +643,9 @@ void decode_attention_v3(const CUtensorMap &kmap, const CUtensorMap &vmap, const
                                   (int)D3_SMEM));
     attr = true;
   }
-  const int cb = decode_chunk_blocks3(rows, max_blocks, sms);
-  const int max_chunks = (max_blocks + cb - 1) / cb;
+  (void)sms;
+  const int cb = DECODE_CHUNK_BLOCKS;
+  const int max_chunks = std::min(64, (max_blocks + cb - 1) / cb);
   launch_pdl(decode_attn_v3_kernel, dim3(rows, max_chunks), dim3(128), D3_SMEM, st, kmap, vmap, q, bt, bt_stride,
              pos, active, cb, max_chunks, scale * 1.4426950408889634f, ws, out);
   if (max_chunks > 1)

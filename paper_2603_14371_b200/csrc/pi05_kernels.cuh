@@ -74,10 +74,19 @@ void flash_attention(const AttnGroup *groups_d, int n_groups, int max_q_tiles, i
 // tcgen05 flash attention, head dim 256 (attn_tc.cu): groups' q rows are rows of
 // q_base viewed as [q_rows, 256]; paged keys through kpool/vpool maps (box 64x64),
 // dense keys g.kb/g.vb rows of kd_base/vd_base [kd_rows, 256] (null: none).
-// q_tiles = ceil(max nq / 128); splits > 1 writes ws (merge with flash_merge).
+// q_tiles = ceil(max nq / 128).  Key splits are per group: attn_group_splits(tiles,
+// tps) — a function of the group's own key count, so a group's output does not
+// depend on the other groups of the call; `splits` (grid y) is the largest group's
+// count.  Groups with more than one split write ws (merged in-kernel over a
+// cluster when cmerge, else by flash_merge; both merges do identical arithmetic).
 // kv_ready: the paged K/V were not written by the previous kernel on the stream
 // (the expert suffix over an earlier prefill), so they are prefetched before the PDL wait.
-void flash_attention_tc(const AttnGroup *groups_d, int n_groups, int q_tiles, int splits, const bf16 *q_base,
+__host__ __device__ inline int attn_group_splits(int tiles, int tps, int &per) {
+  per = tps > 0 ? tps : 1;
+  if ((tiles + per - 1) / per > 32) per = (tiles + 31) / 32;  // the merges take <= 32 splits
+  return tiles > 0 ? (tiles + per - 1) / per : 1;
+}
+void flash_attention_tc(const AttnGroup *groups_d, int n_groups, int q_tiles, int splits, int tps, const bf16 *q_base,
                         int q_rows, const CUtensorMap &kpool_map, const CUtensorMap &vpool_map, const bf16 *kd_base,
                         const bf16 *vd_base, int kd_rows, float scale, float *ws_o, float *ws_ml, int ws_rows,
                         bool kv_ready, bool cmerge, cudaStream_t st);
@@ -86,9 +95,16 @@ void flash_attention_tc(const AttnGroup *groups_d, int n_groups, int q_tiles, in
 // the cap (default 16; 0 or 1 = always the workspace merge)
 int attn_cluster_merge_max();
 // split-order merge of the tcgen05 kernel's bf16 head-dim-256 partials (ws rows as in flash_attention)
-void flash_merge(const AttnGroup *groups_d, int n_groups, int max_rows, int splits, const bf16 *ws_o,
+void flash_merge(const AttnGroup *groups_d, int n_groups, int max_rows, int splits, int tps, const bf16 *ws_o,
                  const float *ws_ml, int ws_rows, cudaStream_t st);
 
+// Decode-attention key chunking of one row: chunks of `cb_min` pool blocks, widened
+// only when the row's own context would need more than 64 chunks.  A function of the
+// row's own length, never of the batch (rows, longest context): batch-invariant.
+constexpr int DECODE_CHUNK_BLOCKS = 2;
+__host__ __device__ inline int decode_row_chunk(int nb, int cb_min) {
+  return nb > 64 * cb_min ? (nb + 63) / 64 : cb_min;
+}
 // Paged decode attention: rows x 8 q-heads vs 1 KV head, keys [0, pos[r]].  TMA-fed
 // 3-stage ring over chunks of pool blocks + ordered chunk merge.
 // kmap/vmap: 2-D tensor maps over one layer's K / V pool viewed as [num_blocks*64, 256]
@@ -96,7 +112,6 @@ void flash_merge(const AttnGroup *groups_d, int n_groups, int max_rows, int spli
 void decode_attention_v3(const CUtensorMap &kmap, const CUtensorMap &vmap, const bf16 *q, bf16 *out, const int *bt,
                          int bt_stride, const int *pos, const int *active, int rows, int max_blocks, float scale,
                          float *ws, int sms, cudaStream_t st);
-int decode_chunk_blocks3(int rows, int max_blocks, int sms);
 
 // Greedy token + continuous-batching state update over logits [rows, V].
 // part: rows * 64 (val, idx) scratch.

@@ -24,7 +24,6 @@
 
 #include "cuda_util.cuh"
 #include "gemm_sm100.cuh"
-#include "megakernel.cuh"
 #include "pi05_kernels.cuh"
 
 
@@ -311,18 +310,6 @@ struct Model {
   bool use_graphs = true;
 
   int *gemm_counters = nullptr;
-  int *dec_counters = nullptr;  // per decode row, for the self-merging attention
-  // persistent layer-program path (megakernel.cu) for the denoise loop: OXY_MK=1
-  // enables it (off by default: slower than the CUDA-graph path, profiles/r01_megakernel.md)
-  bool use_mk = [] {
-    const char *e = getenv("OXY_MK");
-    return e && atoi(e) != 0;
-  }();
-  int mk_grid = [] {
-    const char *e = getenv("OXY_MK_GRID");
-    return e ? atoi(e) : 0;
-  }();
-  std::map<std::string, mk::Program> mk_progs;
   // profiling only: OXY_DBG_SKIP bitmask drops kernels from the denoise chain
   // (results are garbage; used to measure each kernel's marginal cost in-graph)
   int dbg_skip = [] {
@@ -386,8 +373,6 @@ struct Model {
     cudaFree(gemm_counters);
   }
   void init_exec() {
-    OXY_CUDA(cudaMalloc(&dec_counters, MAX_DECODE_ROWS * sizeof(int)));
-    OXY_CUDA(cudaMemset(dec_counters, 0, MAX_DECODE_ROWS * sizeof(int)));
     // The action-expert lane gets the highest stream priority: its denoise is a
     // latency-bound chain of small kernels, the concurrent language decode is
     // bandwidth-bound and fills whatever SMs the chain leaves (OXY_LANE_PRIO=0: equal)
@@ -411,7 +396,6 @@ struct Model {
     }
     if (alt.t0) cudaEventDestroy(alt.t0);
     if (alt.t1) cudaEventDestroy(alt.t1);
-    cudaFree(dec_counters);
     for (DevBuf *b : {&alt.y, &alt.q, &alt.o, &alt.hmid, &alt.ws, &alt.kd, &alt.vd, &alt.attn_ws, &alt.attn_ml})
       b->release();
   }
@@ -504,17 +488,31 @@ struct Model {
     ~PlanSms() { m.plan_sms = prev; }
   };
 
+  // Batch invariance: every projection's K partition comes from the phase policy
+  // (gemm::policy_splits: a function of phase, N_out and K only), so a row's
+  // result never depends on the token count of the call — the rows of a decode
+  // batch, the streams of a batched prefill / denoise — nor on the lane's SM cap.
+  int phase = gemm::PH_CHAIN;
+  struct PhaseScope {
+    Model &m;
+    int prev;
+    PhaseScope(Model &mm, int ph) : m(mm), prev(mm.phase) { m.phase = ph; }
+    ~PhaseScope() { m.phase = prev; }
+  };
+  gemm::Plan plan_for(int n_out, int k, int t) const {
+    return gemm::make_plan(n_out, k, t, psms(), gemm::policy_splits(phase, n_out, k, sms));
+  }
   // split-K workspace is reserved by plan_gemm(); gemm() only fetches it
   size_t ws_need = 0;
   void plan_gemm(int n_out, int k, int t) {
     if (t <= 0) return;
-    gemm::Plan p = gemm::make_plan(n_out, k, t, psms());
+    gemm::Plan p = plan_for(n_out, k, t);
     if (p.splits > 1) ws_need = std::max(ws_need, (size_t)p.splits * t * n_out);
   }
   void gemm(const bf16 *w, const bf16 *xin, int n_out, int k, int t, int mode, void *out, int ldo,
             const float *bias = nullptr, const float *gate = nullptr) {
     if (t <= 0) return;
-    gemm::Plan plan = gemm::make_plan(n_out, k, t, psms());
+    gemm::Plan plan = plan_for(n_out, k, t);
     float *wsp = plan.splits > 1 ? ws.as<float>((size_t)plan.splits * t * n_out) : nullptr;
     EpiParams e{mode, out, ldo, bias, nullptr, 0, gate, {}};
     gemm::launch(w, xin, n_out, k, t, e, plan, wsp, gemm_counters, mst);
@@ -524,7 +522,7 @@ struct Model {
   void gemm_res_norm(const bf16 *w, const bf16 *xin, int n_out, int k, int t, const float *gate, float *X, bf16 *Y,
                      const float *norm_w, const float *mod_scale, const float *mod_shift) {
     if (t <= 0) return;
-    gemm::Plan plan = gemm::make_plan(n_out, k, t, psms());
+    gemm::Plan plan = plan_for(n_out, k, t);
     if (plan.splits > 1 && n_out <= 2048) {
       float *wsp = ws.as<float>((size_t)plan.splits * t * n_out);
       EpiParams e{gemm::EPI_PARTIALS, nullptr, 0, nullptr, nullptr, 0, nullptr, {}};
@@ -541,7 +539,7 @@ struct Model {
   void gemm_qkv(const bf16 *w, const bf16 *xin, int k, int t, const int *pos, const int *slot, bf16 *q_out,
                 bf16 *k_dst, bf16 *v_dst) {
     if (t <= 0) return;
-    gemm::Plan plan = gemm::make_plan(QKV, k, t, psms());
+    gemm::Plan plan = plan_for(QKV, k, t);
     float *wsp = plan.splits > 1 ? ws.as<float>((size_t)plan.splits * t * QKV) : nullptr;
     EpiParams e{gemm::EPI_QKV_ROPE, nullptr, 0, nullptr, nullptr, 0, nullptr,
                 gemm::QkvRope{rope_inv, rope_cs, pos, slot, q_out, k_dst, v_dst}};
@@ -550,7 +548,7 @@ struct Model {
 
   struct AttnPlan {
     AttnGroup *groups = nullptr;
-    int n = 0, q_tiles = 0, splits = 1, hd = 256, rows = 0, max_tiles = 0;
+    int n = 0, q_tiles = 0, splits = 1, hd = 256, rows = 0, max_tiles = 0, tps = 0;
   };
   size_t attn_ws_need = 0, attn_ml_need = 0;
   // pass 1: shapes only (reserve workspace); pass 2 (after scratch is final): upload descriptors
@@ -567,8 +565,11 @@ struct Model {
     }
     p.q_tiles = (max_nq + 63) / 64;
     const int ctas = p.n * p.q_tiles;
-    // split-KV to fill the SMs (the merge kernel handles <= 32 splits)
-    if (ctas < sms && p.max_tiles > 1) p.splits = std::min({p.max_tiles, 32, std::max(1, (2 * sms) / ctas)});
+    // SigLIP (head dim 72, 256 keys): one split, so an image's output never depends on
+    // how many images share the call.  Head dim 256 here is only the OXY_ATTN_TC=0
+    // A/B path (split-KV to fill the SMs; not batch-invariant).
+    if (head_dim == 256 && ctas < sms && p.max_tiles > 1)
+      p.splits = std::min({p.max_tiles, 32, std::max(1, (2 * sms) / ctas)});
     if (p.splits > 1) {
       const int hdp = head_dim == 256 ? 256 : 80;
       attn_ws_need = std::max(attn_ws_need, (size_t)p.splits * p.rows * hdp);
@@ -592,27 +593,38 @@ struct Model {
     const char *e = getenv("OXY_ATTN_TC");
     return !e || atoi(e) != 0;
   }();
-  AttnPlan shape_attention_tc(std::vector<AttnGroup> &groups) {
+  // tps: key tiles (of 64) per split, per phase (batch invariance: a group's split
+  // count is attn_group_splits(its key tiles, tps) whatever else shares the call)
+  AttnPlan shape_attention_tc(std::vector<AttnGroup> &groups, int tps) {
     AttnPlan p;
     p.n = (int)groups.size();
     p.hd = HEAD_DIM;
+    p.tps = tps;
     int max_nq = 0;
     for (auto &g : groups) {  // workspace rows padded to whole 128-row tiles (TMA-stored partials)
       g.wrow0 = p.rows;
       p.rows += (g.nq + 127) / 128 * 128;
       max_nq = std::max(max_nq, g.nq);
-      p.max_tiles = std::max(p.max_tiles, (g.nka + 63) / 64 + (g.nkb + 63) / 64);
+      const int tiles = (g.nka + 63) / 64 + (g.nkb + 63) / 64;
+      int per;
+      p.max_tiles = std::max(p.max_tiles, tiles);
+      p.splits = std::max(p.splits, attn_group_splits(tiles, tps, per));
     }
     p.q_tiles = (max_nq + 127) / 128;
-    const int ctas = p.n * p.q_tiles;
-    p.splits = std::max(1, std::min({p.max_tiles, 32, psms() / std::max(1, ctas)}));  // merge handles <= 32
-    if (const char *e = getenv("OXY_ATTN_TC_SPLITS")) p.splits = std::max(1, std::min({p.max_tiles, 32, atoi(e)}));
     if (p.splits > 1) {
       attn_ws_need = std::max(attn_ws_need, (size_t)p.splits * p.rows * 256);
       attn_ml_need = std::max(attn_ml_need, (size_t)p.splits * p.rows * 2);
     }
     return p;
   }
+  // key tiles per split: prefill 7 (P = 800: 13 tiles -> 2 splits, 100 CTAs per layer at
+  // 1 stream), expert suffix 1 (P + 50 = 850 keys: 14 single-tile splits merged over a
+  // 14-CTA cluster; measured best at 1 stream).  OXY_ATTN_TPS=prefill,denoise (A/B)
+  std::pair<int, int> attn_tps = [] {
+    std::pair<int, int> v{7, 1};
+    if (const char *e = getenv("OXY_ATTN_TPS")) sscanf(e, "%d,%d", &v.first, &v.second);
+    return v;
+  }();
   void attend_tc(const AttnPlan &p, int layer, const bf16 *q_base, int q_rows, const bf16 *kd, const bf16 *vd,
                  int kd_rows, bool kv_ready) {
     if (!p.n) return;
@@ -622,10 +634,11 @@ struct Model {
       wml = attn_ml.as<float>((size_t)p.splits * p.rows * 2);
     }
     const bool cm = p.splits > 1 && p.splits <= attn_cluster_merge_max();
-    flash_attention_tc(p.groups, p.n, p.q_tiles, p.splits, q_base, q_rows, kv_maps[2 * layer], kv_maps[2 * layer + 1],
-                       kd, vd, kd_rows, 1.f / 16.f, wo, wml, p.rows, kv_ready, cm, mst);
+    flash_attention_tc(p.groups, p.n, p.q_tiles, p.splits, p.tps, q_base, q_rows, kv_maps[2 * layer],
+                       kv_maps[2 * layer + 1], kd, vd, kd_rows, 1.f / 16.f, wo, wml, p.rows, kv_ready, cm, mst);
     if (p.splits > 1 && !cm && !(dbg_skip & 4))
-      flash_merge(p.groups, p.n, p.q_tiles * 128, p.splits, reinterpret_cast<const bf16 *>(wo), wml, p.rows, mst);
+      flash_merge(p.groups, p.n, p.q_tiles * 128, p.splits, p.tps, reinterpret_cast<const bf16 *>(wo), wml, p.rows,
+                  mst);
   }
 
   void reserve_common() {
@@ -641,28 +654,25 @@ struct Model {
   // blocks_h: per obs ceil(P_i/64) block ids, concatenated.
   void prefill(cudaStream_t caller, int n_obs, const int *n_img, const int *n_txt, const int *tokens_h,
                const uint8_t *images_d, const int *blocks_h) {
-    // prefill projections whose tiles just miss two waves (e.g. the ViT 1152-wide ones,
-    // 144 tiles) split K to fill both CTA slots per SM: 7.49 -> 7.32 ms prefill; the
-    // denoise / decode chains keep one slot (OXY_PREFILL_SPLIT_SLOTS, 0 = knob default)
-    // and K >= 2048 projections (Gemma qkv / o / down, ViT fc2) take 128-token tiles with
-    // split-K 2: half the weight re-reads through L2, both CTA slots busy, and the o / down
-    // residual + RMSNorm fused into the split reduce: 7.3 -> 6.45 ms prefill (OXY_PREFILL_DEEPK=0: off)
-    struct SlotScope {
-      SlotScope(int v, bool deepk) {
-        gemm::g_split_slots_override = v;
-        // and 1024 <= K < 2048 (the ViT qkv / o / fc1) 96-token tiles: 6.41 -> 6.35 ms
+    // K >= 2048 projections (Gemma qkv / o / down, ViT fc2) take 128-token tiles with
+    // split-K 2 (gemm::policy_splits): half the weight re-reads through L2, both CTA
+    // slots busy, and the o / down residual + RMSNorm fused into the split reduce;
+    // 1024 <= K < 2048 (the ViT qkv / o / fc1) take 96-token tiles (OXY_PREFILL_DEEPK=0:
+    // off; OXY_PREFILL_MIDK=kmin,bn,splits A/B).  Token tiles never change results.
+    struct BandScope {
+      explicit BandScope(bool deepk) {
         if (deepk) {
           const int band[6] = {2048, 128, 2, 1024, 96, 1};
           for (int i = 0; i < 6; ++i) gemm::g_deepk[i] = band[i];
         }
-        if (const char *e = getenv("OXY_PREFILL_MIDK"))  // A/B: kmin,bn,splits for 1024 <= K < 2048
+        if (const char *e = getenv("OXY_PREFILL_MIDK"))
           sscanf(e, "%d,%d,%d", &gemm::g_deepk[3], &gemm::g_deepk[4], &gemm::g_deepk[5]);
       }
-      ~SlotScope() {
-        gemm::g_split_slots_override = 0;
+      ~BandScope() {
         for (int &v : gemm::g_deepk) v = 0;
       }
-    } slot_scope(prefill_split_slots, prefill_deepk);
+    } band_scope(prefill_deepk);
+    PhaseScope phase_scope(*this, gemm::PH_PREFILL);
     const int W = c.width, Dv = c.vit_width, nh = c.vit_heads, hd = nh ? Dv / nh : 72;
     std::vector<int> P(n_obs), off(n_obs), boff(n_obs);
     int T = 0, nb = 0, n_images = 0, n_tok = 0;
@@ -683,6 +693,7 @@ struct Model {
     for (int i = 0; i < n_tok; ++i)
       OXY_REQUIRE(tokens_h[i] >= 0 && tokens_h[i] < c.vocab, "observation token %d outside vocab of %d",
                   tokens_h[i], c.vocab);
+    check_block_ids(blocks_h, nb, NB, "prefill");
     const int Tv = n_images * 256;
     // ---- plan pass 1: reserve scratch
     x.as<float>((size_t)T * W);
@@ -702,7 +713,7 @@ struct Model {
       g_llm[i].nq = P[i] * Q_HEADS;
       g_llm[i].nka = P[i];
     }
-    AttnPlan a_llm = use_attn_tc ? shape_attention_tc(g_llm) : shape_attention(g_llm, HEAD_DIM), a_vit;
+    AttnPlan a_llm = use_attn_tc ? shape_attention_tc(g_llm, attn_tps.first) : shape_attention(g_llm, HEAD_DIM), a_vit;
     if (Tv) {
       patches.as<bf16>((size_t)Tv * PATCH_K);
       vit_h.as<float>((size_t)Tv * Dv);
@@ -862,9 +873,11 @@ struct Model {
     std::string key = "denoise/" + std::to_string(S);
     int nb = 0;
     for (int i = 0; i < n; ++i) {
+      OXY_REQUIRE(P[i] >= 1, "denoise needs a non-empty prefix");
       nb += (P[i] + KV_BLOCK - 1) / KV_BLOCK;
       key += "," + std::to_string(P[i]);
     }
+    check_block_ids(blocks_h, nb, NB, "denoise");
     // ---- plan pass 1
     arena_used = 0;
     act.as<float>((size_t)T * AP);
@@ -890,33 +903,7 @@ struct Model {
       groups[i].nka = P[i];
       groups[i].nkb = H;
     }
-    AttnPlan ap = (use_attn_tc && !use_mk) ? shape_attention_tc(groups) : shape_attention(groups, HEAD_DIM);
-    const char *dn_tiles = getenv("OXY_ATTN_TC_DN_TILES");
-    if (use_attn_tc && !use_mk && dn_tiles) {
-      // A/B knob: key tiles per split of the expert suffix (the default plan fills
-      // the SMs: one tile per split at 1 stream, measured best; fewer splits as
-      // streams add query tiles)
-      const int per = std::max(1, atoi(dn_tiles));
-      ap.splits = std::min(32, std::max(1, (ap.max_tiles + per - 1) / per));
-      if (ap.splits > 1) {
-        attn_ws_need = std::max(attn_ws_need, (size_t)ap.splits * ap.rows * 256);
-        attn_ml_need = std::max(attn_ml_need, (size_t)ap.splits * ap.rows * 2);
-      }
-    }
-    if (use_mk) {
-      const char *e = getenv("OXY_MK_ATTN_TILES");  // key tiles per split item
-      const int per = std::max(1, e ? atoi(e) : 2);
-      ap.splits = std::max(1, (ap.max_tiles + per - 1) / per);
-      if (ap.splits > 1) {
-        attn_ws_need = std::max(attn_ws_need, (size_t)ap.splits * ap.rows * 256);
-        attn_ml_need = std::max(attn_ml_need, (size_t)ap.splits * ap.rows * 2);
-      }
-      for (auto nk : {std::pair<int, int>{We, AP}, {QKV, We}, {We, QDIM}, {2 * c.expert_mlp, We}, {We, c.expert_mlp},
-                      {A, We}}) {
-        const int sp = mk::gemm_splits(nk.first, nk.second, T, sms);
-        if (sp > 1) ws_need = std::max(ws_need, (size_t)sp * T * nk.first);
-      }
-    }
+    AttnPlan ap = use_attn_tc ? shape_attention_tc(groups, attn_tps.second) : shape_attention(groups, HEAD_DIM);
     reserve_common();
     // ---- plan pass 2
     float *a = act.as<float>(0), *X = xe.as<float>(0), *vel_d = vel.as<float>(0);
@@ -944,17 +931,6 @@ struct Model {
       g.ldkv = HEAD_DIM;
     }
     ap.groups = arena_put(groups.data(), groups.size());
-    mk::Program *pg = nullptr;
-    if (use_mk) {
-      pg = &mk_progs[key];
-      if (pg->gen != g_devbuf_reallocs) {
-        build_denoise_program(*pg, n, S, T, d_pos, ap, a, X, vel_d, ab, Y, Qb, Ob, Kd, Vd, Hm, modp);
-        pg->gen = g_devbuf_reallocs;
-        pg->grid = mk_grid;
-        pg->profile = getenv("OXY_MK_PROFILE") != nullptr;
-        pg->upload(mst);
-      }
-    }
     enter(caller);
     OXY_CUDA(cudaEventRecord(alt.t0, mst));
     arena_upload();
@@ -964,10 +940,6 @@ struct Model {
                                  cudaMemcpyDeviceToDevice, mst));
       OXY_CUDA(cudaMemsetAsync(vel_d, 0, (size_t)T * AP * sizeof(float), mst));
       f32_to_bf16(a, ab, (int64_t)T * AP, mst);
-      if (pg) {
-        pg->launch(mst);
-        return;
-      }
       const float dt = -1.f / (float)S;
       for (int s = 0; s < S; ++s) {
         const float *ms = modp + (size_t)s * n_mod;
@@ -993,103 +965,11 @@ struct Model {
       }
     };
     run_body(key, true, body);
-    if (pg && pg->profile) mk_report(*pg);
     OXY_CUDA(cudaMemcpy2DAsync(actions_out_d, A * sizeof(float), a, AP * sizeof(float), A * sizeof(float), T,
                                cudaMemcpyDeviceToDevice, mst));
     OXY_CUDA(cudaEventRecord(alt.t1, mst));
     if (join) leave(caller);
     else OXY_CUDA(cudaEventRecord(ev_out, mst));
-  }
-
-  // OXY_MK_PROFILE: per-phase-type time of the last program run (CTA 0's view of the barriers)
-  void mk_report(mk::Program &pg) {
-    OXY_CUDA(cudaStreamSynchronize(mst));
-    const size_t n = pg.phases.size();
-    const int G = pg.grid > 0 ? pg.grid : sms;
-    std::vector<unsigned long long> t(n * (1 + G));
-    OXY_CUDA(cudaMemcpy(t.data(), pg.d_times, t.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
-    // release[i] = CTA 0 leaving barrier i; arrive[i][c] = CTA c arriving at barrier i
-    // work(i) = last arrival at barrier i - release of barrier i-1; sync(i) = release[i] - last arrival
-    double work[8] = {0}, sync[8] = {0}, cnt[8] = {0};
-    std::map<std::string, std::pair<double, int>> gem;
-    for (size_t i = 1; i + 1 < n; ++i) {
-      unsigned long long last = 0;
-      for (int c = 0; c < G; ++c) last = std::max(last, t[n + i * G + c]);
-      const double w = ((double)last - (double)t[i - 1]) * 1e-3, sy = ((double)t[i] - (double)last) * 1e-3;
-      const int ty = pg.phases[i].type;
-      work[ty] += w;
-      sync[ty] += sy;
-      cnt[ty] += 1;
-      if (ty == mk::PH_GEMM) {
-        const auto &g = pg.phases[i].g;
-        auto &e = gem[std::to_string(g.n_out) + "x" + std::to_string(g.k) + " s" + std::to_string(g.splits)];
-        e.first += w;
-        e.second += 1;
-      }
-    }
-    const char *names[] = {"gemm", "reduce_epi", "res_norm", "attn", "attn_merge", "euler"};
-    std::fprintf(stderr, "mk profile: %zu phases, %.1f us total (work = slowest CTA, sync = barrier after it)\n", n,
-                 (t[n - 1] - t[0]) * 1e-3);
-    for (int ty = 0; ty < 6; ++ty)
-      if (cnt[ty])
-        std::fprintf(stderr, "  %-11s n=%5.0f work=%6.2f us sync=%5.2f us (mean)\n", names[ty], cnt[ty],
-                     work[ty] / cnt[ty], sync[ty] / cnt[ty]);
-    for (auto &kv : gem)
-      std::fprintf(stderr, "    gemm %-16s n=%4d work=%6.2f us\n", kv.first.c_str(), kv.second.second,
-                   kv.second.first / kv.second.second);
-  }
-
-  // The whole S-step denoise as one persistent layer program (megakernel.cu):
-  // the same math as the multi-kernel body below, phase for phase.
-  void build_denoise_program(mk::Program &pg, int n, int S, int T, const int *d_pos, const AttnPlan &ap, float *a,
-                             float *X, float *vel_d, bf16 *ab, bf16 *Y, bf16 *Qb, bf16 *Ob, bf16 *Kd, bf16 *Vd,
-                             bf16 *Hm, const float *modp) {
-    (void)n;
-    const int We = c.expert_width, A = c.action_dim, AP = apad(), EM = c.expert_mlp;
-    const float eps = 1e-6f, dt = -1.f / (float)S;
-    float *mws = ws.as<float>(0);
-    float *awo = nullptr, *aml = nullptr;
-    if (ap.splits > 1) {
-      awo = attn_ws.as<float>((size_t)ap.splits * ap.rows * 256);
-      aml = attn_ml.as<float>((size_t)ap.splits * ap.rows * 2);
-    }
-    pg.clear();
-    auto epi = [](int mode, void *out, int ldo, const float *bias = nullptr, const float *gate = nullptr) {
-      return EpiParams{mode, out, ldo, bias, nullptr, 0, gate, {}};
-    };
-    const int max_nq = c.H * Q_HEADS;
-    for (int s = 0; s < S; ++s) {
-      const float *ms = modp + (size_t)s * n_mod;
-      EpiParams ei = epi(gemm::EPI_F32, X, We, e_in_b);
-      int sp = pg.gemm(e_in, ab, We, AP, T, ei, mws, sms);
-      if (sp > 1) pg.reduce_epi(mws, sp, T, We, ei);
-      pg.res_norm(nullptr, 0, T, We, nullptr, X, We, Y, We, nullptr, ms, ms + We, eps);
-      const float *mf = ms + (size_t)c.depth * 6 * We;
-      for (int l = 0; l < c.depth; ++l) {
-        const ExpertW &w = E[l];
-        const float *m = ms + (size_t)l * 6 * We;
-        const float *mn = l + 1 < c.depth ? m + 6 * We : mf;
-        EpiParams er{gemm::EPI_QKV_ROPE, nullptr, 0, nullptr, nullptr, 0, nullptr,
-                     gemm::QkvRope{rope_inv, rope_cs, d_pos, nullptr, Qb, Kd, Vd}};
-        sp = pg.gemm(w.wqkv, Y, QKV, We, T, er, mws, sms, 1);  // whole K: RoPE epilogue in place
-        if (sp > 1) pg.reduce_epi(mws, sp, T, QKV, er);
-        pg.attention(ap.groups, ap.n, ap.q_tiles, max_nq, ap.splits, ap.rows, kpool(l), vpool(l), 1.f / 16.f, awo,
-                     aml);
-        sp = pg.gemm(w.wo, Ob, We, QDIM, T, epi(gemm::EPI_ADD_GATED_F32, X, We, nullptr, m + 2 * We), mws, sms);
-        if (sp > 1) pg.res_norm(mws, sp, T, We, m + 2 * We, X, We, Y, We, nullptr, m + 3 * We, m + 4 * We, eps);
-        else pg.res_norm(nullptr, 0, T, We, nullptr, X, We, Y, We, nullptr, m + 3 * We, m + 4 * We, eps);
-        EpiParams eg = epi(gemm::EPI_GEGLU_BF16, Hm, EM);
-        sp = pg.gemm(w.wgu, Y, 2 * EM, We, T, eg, mws, sms, 1);  // whole K: GeGLU epilogue in place
-        if (sp > 1) pg.reduce_epi(mws, sp, T, 2 * EM, eg);
-        sp = pg.gemm(w.wd, Hm, We, EM, T, epi(gemm::EPI_ADD_GATED_F32, X, We, nullptr, m + 5 * We), mws, sms);
-        if (sp > 1) pg.res_norm(mws, sp, T, We, m + 5 * We, X, We, Y, We, nullptr, mn, mn + We, eps);
-        else pg.res_norm(nullptr, 0, T, We, nullptr, X, We, Y, We, nullptr, mn, mn + We, eps);
-      }
-      EpiParams eo = epi(gemm::EPI_F32, vel_d, AP, e_out_b);
-      sp = pg.gemm(e_out, Y, A, We, T, eo, mws, sms);
-      if (sp > 1) pg.reduce_epi(mws, sp, T, A, eo);
-      pg.euler(a, vel_d, ab, T * AP, dt);
-    }
   }
 
   // ------------------------------------------------------------ decode
@@ -1098,10 +978,6 @@ struct Model {
   bool prefill_deepk = [] {
     const char *e = getenv("OXY_PREFILL_DEEPK");
     return !e || atoi(e) != 0;
-  }();
-  int prefill_split_slots = [] {
-    const char *e = getenv("OXY_PREFILL_SPLIT_SLOTS");
-    return e ? atoi(e) : 2;
   }();
   int decode_early = [] {
     const char *e = getenv("OXY_DECODE_EARLY");
@@ -1115,12 +991,18 @@ struct Model {
     } early_scope(decode_early);
     PlanSms plan_scope(*this, lane_sms.second);
     const int W = c.width;
+    // a row appends at most min(k, budget) positions (argmax_update stops it at its
+    // budget), so its table only has to cover seq + min(k, budget)
     int max_pos = 0;
     for (int r = 0; r < rows; ++r) {
       OXY_REQUIRE(last_h[r] >= 0 && last_h[r] < c.vocab, "token %d outside vocab", last_h[r]);
-      max_pos = std::max(max_pos, seq_h[r] + k);
+      OXY_REQUIRE(seq_h[r] >= 1 && budget_h[r] >= 1, "row %d: seq_len and budget must be >= 1", r);
+      max_pos = std::max(max_pos, seq_h[r] + std::min(k, budget_h[r]));
     }
-    OXY_REQUIRE((max_pos + KV_BLOCK - 1) / KV_BLOCK <= maxb, "block table too short for %d positions", max_pos);
+    OXY_REQUIRE(maxb >= 1 && (max_pos + KV_BLOCK - 1) / KV_BLOCK <= maxb, "block table too short for %d positions",
+                max_pos);
+    check_block_ids(bt_h, (int64_t)rows * maxb, NB, "decode");
+    check_cow(cow_h, rows, NB, KV_BLOCK);
     // ---- plan pass 1
     arena_used = 0;
     x.as<float>((size_t)rows * W);
@@ -1333,7 +1215,9 @@ int oxy_pi05_read_kv(oxy_pi05 *p, const int32_t *blocks_h, int32_t seq_len, int3
   OXY_REQUIRE(layer >= 0 && layer < m.c.depth, "layer %d out of range", layer);
   if (seq_len == 0) return OXY_OK;
   auto st = oxy::as_stream(stream);
+  OXY_REQUIRE(seq_len > 0, "negative sequence length");
   const int nb = (seq_len + 63) / 64;
+  oxy::check_block_ids(blocks_h, nb, m.NB, "read_kv");
   int *bd = m.kvread_i.as<int>(nb);
   OXY_CUDA(cudaMemcpyAsync(bd, blocks_h, nb * sizeof(int), cudaMemcpyHostToDevice, st));
   float *ko = m.kvread_f.as<float>((size_t)2 * seq_len * 256);

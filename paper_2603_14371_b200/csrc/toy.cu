@@ -424,8 +424,13 @@ struct Model : Base {
       h_tok[r] = last_h[r];
       h_pos[r] = seq_h[r];
       h_bud[r] = budget_h[r];
-      max_pos = std::max(max_pos, seq_h[r] + k);
+      OXY_REQUIRE(seq_h[r] >= 1 && budget_h[r] >= 1, "row %d: seq_len and budget must be >= 1", r);
+      OXY_REQUIRE(last_h[r] >= 0 && last_h[r] < c.vocab, "token %d outside vocab", last_h[r]);
+      max_pos = std::max(max_pos, seq_h[r] + std::min(k, budget_h[r]));
     }
+    OXY_REQUIRE(maxb >= 1 && (max_pos + B - 1) / B <= maxb, "block table too short for %d positions", max_pos);
+    check_block_ids(bt_h, (int64_t)n_bt, NB, "decode");
+    check_cow(cow_h, rows, NB, B);
     int *dv = ints.as<int>(total);
     OXY_CUDA(cudaMemcpyAsync(dv, hp, total * sizeof(int), cudaMemcpyHostToDevice, st));
     int *d_bt = dv, *d_cow = dv + n_bt, *d_active = d_cow + 3 * rows, *d_tok = d_active + rows,
@@ -547,6 +552,7 @@ int oxy_toy_prefill(oxy_toy *m, const int32_t *tokens_h, int32_t T, const int32_
     for (int i = 0; i < T; ++i)
       OXY_REQUIRE(tokens_h[i] >= 0 && tokens_h[i] < M.c.vocab, "observation token %d outside vocab of %d",
                   tokens_h[i], M.c.vocab);
+    oxy::check_block_ids(blocks_h, (T + M.B - 1) / M.B, M.NB, "prefill");
     auto slots = slots_for(blocks_h, M.B, T);
     M.dense_forward(oxy::as_stream(stream), tokens_h, T, slots.data(), nullptr);
   });
@@ -576,6 +582,7 @@ int oxy_toy_denoise(oxy_toy *m, const int32_t *blocks_h, int32_t seq_len, int32_
   dispatch(m, [&](auto &M) {
     using Tp = std::remove_reference_t<decltype(*M.embed)>;
     const int nb = (seq_len + M.B - 1) / M.B, HA = M.c.H * M.c.action_dim;
+    oxy::check_block_ids(blocks_h, nb, M.NB, "denoise");
     int *bd = M.ints.template as<int>(nb);
     OXY_CUDA(cudaMemcpyAsync(bd, blocks_h, nb * sizeof(int), cudaMemcpyHostToDevice, st));
     Tp *out = M.q.template as<Tp>(HA);
@@ -608,7 +615,9 @@ int oxy_toy_read_kv(oxy_toy *m, const int32_t *blocks_h, int32_t seq_len, int32_
     using Tp = std::remove_reference_t<decltype(*M.embed)>;
     OXY_REQUIRE(layer >= 0 && layer < M.c.L, "layer %d out of range", layer);
     if (seq_len == 0) return;
+    OXY_REQUIRE(seq_len > 0, "negative sequence length");
     const int nb = (seq_len + M.B - 1) / M.B;
+    oxy::check_block_ids(blocks_h, nb, M.NB, "kv access");
     int *bd = M.ints.template as<int>(nb);
     OXY_CUDA(cudaMemcpyAsync(bd, blocks_h, nb * sizeof(int), cudaMemcpyHostToDevice, st));
     Tp *ko = M.kk.template as<Tp>((size_t)seq_len * M.d), *vo = M.vv.template as<Tp>((size_t)seq_len * M.d);
@@ -629,7 +638,9 @@ int oxy_toy_write_kv(oxy_toy *m, const int32_t *blocks_h, int32_t seq_len, int32
     using Tp = std::remove_reference_t<decltype(*M.embed)>;
     OXY_REQUIRE(layer >= 0 && layer < M.c.L, "layer %d out of range", layer);
     if (seq_len == 0) return;
+    OXY_REQUIRE(seq_len > 0, "negative sequence length");
     const int nb = (seq_len + M.B - 1) / M.B;
+    oxy::check_block_ids(blocks_h, nb, M.NB, "kv access");
     const size_t n = (size_t)seq_len * M.d;
     int *bd = M.ints.template as<int>(nb);
     double *tmp = M.cast.template as<double>(2 * n);

@@ -91,6 +91,29 @@ class BlockAllocator:
                   _lib.ptr_i32(free), C.byref(n))
         return ref, fill, free[:n.value].copy()
 
+    def reserve_rows(self, caches, n_new):
+        """``reserve`` for every row of a decode batch.  If any row fails (pool
+        out of blocks), the rows already reserved are rolled back — blocks,
+        copy-on-write copies and raised tail watermarks — before re-raising,
+        so a failed call leaves the allocator exactly as it found it."""
+        tables, cows = [], []
+        try:
+            for kv, n in zip(caches, n_new):
+                t, c = self.reserve(kv.blocks, kv.seq_len, n)
+                tables.append(t)
+                cows.append(c)
+        except BaseException:
+            self.unreserve(tables, [kv.seq_len for kv in caches], n_new)
+            raise
+        return tables, cows
+
+    def unreserve(self, tables, seq_lens, n_new) -> None:
+        """Undo ``reserve`` for rows that wrote nothing: settle at zero new
+        positions (frees fresh blocks, restores the tail watermark), then drop
+        the references the reservation took."""
+        for t, s, n in zip(tables, seq_lens, n_new):
+            self.decref(self.settle(t, s, n, 0))
+
     def slot_mapping(self, blocks, start: int, count: int) -> np.ndarray:
         b = _lib.as_i32(blocks)
         out = np.empty(count, np.int32)
@@ -105,14 +128,13 @@ class PagedKvCache:
     lazily from HBM as read-only float64 ``KvLayer``s) and value equality.
     Dropping the last reference returns the blocks to the pool."""
 
-    __slots__ = ("owner", "blocks", "seq_len", "backend_tag", "_layers", "__weakref__")
+    __slots__ = ("owner", "blocks", "seq_len", "backend_tag", "__weakref__")
 
     def __init__(self, owner, blocks: tuple, seq_len: int):
         self.owner = owner
         self.blocks = tuple(blocks)
         self.seq_len = int(seq_len)
         self.backend_tag = owner.backend_tag
-        self._layers = None
 
     def __del__(self):
         owner = getattr(self, "owner", None)
@@ -128,10 +150,10 @@ class PagedKvCache:
 
     @property
     def layers(self) -> tuple:
-        if self._layers is None:
-            self._layers = tuple(KvLayer(*self.owner.read_kv(self, l))
-                                 for l in range(self.num_layers))
-        return self._layers
+        """Read from HBM on every access (no host memo): a check such as the
+        sharing suite's "denoise left the cache untouched"
+        (``kvweaver/verify.py:241-247``) must see the pool, not a stale copy."""
+        return tuple(KvLayer(*self.owner.read_kv(self, l)) for l in range(self.num_layers))
 
     def __eq__(self, other):
         if not hasattr(other, "backend_tag") or not hasattr(other, "layers"):
@@ -141,7 +163,7 @@ class PagedKvCache:
         if isinstance(other, PagedKvCache) and other.owner is self.owner \
                 and other.blocks == self.blocks:
             return True
-        return tuple(self.layers) == tuple(other.layers)
+        return self.layers == tuple(other.layers)
 
     __hash__ = None
 

@@ -323,16 +323,13 @@ class Pi05Backend(PricedBackend):
         c = self.config
         m = batched.size
         caches = [self._own(kv) for kv in batched.kv_batch]
-        budgets, reserved, tables, cows, lasts = [], [], [], [], []
-        for kv, toks, max_len in zip(caches, batched.token_buffers, batched.max_lens):
+        budgets, reserved, lasts = [], [], []
+        for toks, max_len in zip(batched.token_buffers, batched.max_lens):
             left = max_len - len(toks)
             budgets.append(left if left > 0 else _BIG_BUDGET)
-            n_res = min(k, left) if left > 0 else k
-            blocks, cow = self.allocator.reserve(kv.blocks, kv.seq_len, n_res)
-            reserved.append(n_res)
-            tables.append(blocks)
-            cows.append(cow)
+            reserved.append(min(k, left) if left > 0 else k)
             lasts.append(toks[-1] if toks else c.eos_token)
+        tables, cows = self.allocator.reserve_rows(caches, reserved)
         maxb = max(len(t) for t in tables)
         bt = np.zeros((m, maxb), np.int32)
         for i, tb in enumerate(tables):
@@ -350,9 +347,8 @@ class Pi05Backend(PricedBackend):
                           _lib.ptr_i32(cnt),
                           logits.ctypes.data_as(C.c_void_p) if return_logits else None,
                           _lib.stream_ptr())
-        except Exception:
-            for tb in tables:
-                self.allocator.decref(tb)
+        except BaseException:
+            self.allocator.unreserve(tables, [kv.seq_len for kv in caches], reserved)
             raise
         new_caches, bufs, flags = [], [], []
         for i, kv in enumerate(caches):

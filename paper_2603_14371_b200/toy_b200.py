@@ -114,7 +114,6 @@ class ToyBackend(PricedBackend):
         b = _lib.as_i32(kv.blocks)
         _lib.call("oxy_toy_write_kv", self._h, _lib.ptr_i32(b), C.c_int32(kv.seq_len),
                   C.c_int32(layer), _lib.ptr_f64(k), _lib.ptr_f64(v), _lib.stream_ptr())
-        kv._layers = None
 
     def adopt(self, kv) -> PagedKvCache:
         """Copy a host ``KvCache`` (e.g. one produced by the reference package)
@@ -169,16 +168,13 @@ class ToyBackend(PricedBackend):
         c = self.config
         m = batched.size
         caches = [self._own(kv) for kv in batched.kv_batch]
-        budgets, reserved, tables, cows, lasts = [], [], [], [], []
-        for kv, toks, max_len in zip(caches, batched.token_buffers, batched.max_lens):
+        budgets, reserved, lasts = [], [], []
+        for toks, max_len in zip(batched.token_buffers, batched.max_lens):
             left = max_len - len(toks)
             budgets.append(left if left > 0 else _BIG_BUDGET)
-            n_res = min(k, left) if left > 0 else k
-            blocks, cow = self.allocator.reserve(kv.blocks, kv.seq_len, n_res)
-            reserved.append(n_res)
-            tables.append(blocks)
-            cows.append(cow)
+            reserved.append(min(k, left) if left > 0 else k)
             lasts.append(toks[-1] if toks else c.eos_token)
+        tables, cows = self.allocator.reserve_rows(caches, reserved)
         maxb = max(len(t) for t in tables)
         bt = np.zeros((m, maxb), np.int32)
         for i, t in enumerate(tables):
@@ -193,9 +189,8 @@ class ToyBackend(PricedBackend):
             _lib.call("oxy_toy_decode", self._h, C.c_int32(m), C.c_int32(k), _lib.ptr_i32(bt),
                       C.c_int32(maxb), _lib.ptr_i32(seq), _lib.ptr_i32(last), _lib.ptr_i32(bud),
                       _lib.ptr_i32(cow), _lib.ptr_i32(out), _lib.ptr_i32(cnt), _lib.stream_ptr())
-        except Exception:
-            for t in tables:
-                self.allocator.decref(t)
+        except BaseException:
+            self.allocator.unreserve(tables, [kv.seq_len for kv in caches], reserved)
             raise
         new_caches, bufs, flags = [], [], []
         for i, kv in enumerate(caches):

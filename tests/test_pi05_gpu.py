@@ -66,17 +66,20 @@ def test_decode_logits_and_tokens_match_oracle(tiny):
     kv = be.prefill(obs)
     out, logits = be.batched_language_decode(
         BatchedState((kv,), ((),), (False,), (0,), (6,), (0,)), 6, return_logits=True)
-    toks, _, want_logits = ref.decode(ref.prefill(obs), (), 6)
+    import torch
+    dev_kv = [tuple(torch.tensor(x, dtype=torch.float32) for x in be.read_kv(kv, l))
+              for l in range(be.config.depth)]
+    toks, _, want_logits = ref.decode(dev_kv, (), 6)  # the device prefix: decode numerics alone
     got = out.token_buffers[0]
     n = min(len(got), len(toks))
     for s in range(n):
+        if got[:s] != toks[:s]:
+            break  # diverged on an earlier near-tie: later steps see different inputs
         a, b = logits[s, 0].astype(np.float64), want_logits[s].astype(np.float64)
         cos = a @ b / (np.linalg.norm(a) * np.linalg.norm(b))
-        assert cos > 0.999, (s, cos)
-        if got[:s] != toks[:s]:
-            break
+        assert cos > 0.9999, (s, cos)
         top2 = np.sort(b)[-2:]
-        if top2[1] - top2[0] > 4 * np.max(np.abs(a - b)):
+        if top2[1] - top2[0] > 2 * np.max(np.abs(a - b)):
             assert got[s] == toks[s], (s, got, toks)
 
 
@@ -85,7 +88,6 @@ def test_kv_pool_shared_between_action_and_language(tiny):
     kv = be.prefill(_obs(1, (1, 2, 3)))
     snap = [(l.keys.copy(), l.values.copy()) for l in kv.layers]
     a1 = be.action_denoise(kv, be.config.S)
-    kv._layers = None
     for (k0, v0), layer in zip(snap, kv.layers):
         assert np.array_equal(k0, layer.keys) and np.array_equal(v0, layer.values)
     a2 = be.action_denoise(kv, be.config.S)
@@ -275,3 +277,66 @@ def test_cross_variant_invariance_on_pi05_backend():
                 assert other[rid].action == entry.action, (i, v, rid)
                 compared += 1
     assert compared > 0
+
+
+def test_decode_budget_below_k_across_block_boundary(tiny):
+    """seq + k crosses a 64-slot block, seq + remaining budget does not: the row
+    reserves min(k, budget) positions and the call must accept the shorter table."""
+    be, _ = tiny
+    kv = be.prefill(_obs(0, tuple(range(2, 62))))  # P = 60: one block
+    out = be.batched_language_decode(BatchedState((kv,), ((),), (False,), (0,), (2,), (0,)), 8)
+    n = len(out.token_buffers[0])
+    assert 1 <= n <= 2 and out.kv_batch[0].seq_len == 60 + n
+    assert len(out.kv_batch[0].blocks) == 1
+
+
+def test_abi_rejects_block_ids_outside_the_pool(tiny):
+    """A non-Python host cannot make the pi0.5 entry points touch memory past the
+    pool: every block id is checked against the pool size (OXY_EINVAL)."""
+    import ctypes as C
+    from paper_2603_14371_b200 import _lib
+    be, _ = tiny
+    nb = be.allocator.num_blocks
+    toks = _lib.as_i32([5, 6, 7])
+    for bad in (nb, -1, 1 << 20):
+        blocks = _lib.as_i32([bad])
+        with pytest.raises(ValueError, match="outside pool"):
+            _lib.call("oxy_pi05_prefill", be._h, C.c_int32(1), _lib.ptr_i32(_lib.as_i32([0])),
+                      _lib.ptr_i32(_lib.as_i32([3])), _lib.ptr_i32(toks), None, _lib.ptr_i32(blocks),
+                      _lib.stream_ptr())
+        with pytest.raises(ValueError, match="outside pool"):
+            _lib.call("oxy_pi05_denoise_async", be._h, C.c_int32(1), _lib.ptr_i32(_lib.as_i32([3])),
+                      _lib.ptr_i32(blocks), C.c_int32(2), None, _lib.stream_ptr())
+        out = np.zeros(4, np.int32)
+        with pytest.raises(ValueError, match="outside pool"):
+            _lib.call("oxy_pi05_decode", be._h, C.c_int32(1), C.c_int32(1), _lib.ptr_i32(blocks),
+                      C.c_int32(1), _lib.ptr_i32(_lib.as_i32([3])), _lib.ptr_i32(_lib.as_i32([1])),
+                      _lib.ptr_i32(_lib.as_i32([1])), _lib.ptr_i32(_lib.as_i32([-1, -1, 0])),
+                      _lib.ptr_i32(out), _lib.ptr_i32(out), None, _lib.stream_ptr())
+        with pytest.raises(ValueError, match="outside pool"):
+            _lib.call("oxy_pi05_decode", be._h, C.c_int32(1), C.c_int32(1), _lib.ptr_i32(_lib.as_i32([0])),
+                      C.c_int32(1), _lib.ptr_i32(_lib.as_i32([3])), _lib.ptr_i32(_lib.as_i32([1])),
+                      _lib.ptr_i32(_lib.as_i32([1])), _lib.ptr_i32(_lib.as_i32([0, bad, 3])),
+                      _lib.ptr_i32(out), _lib.ptr_i32(out), None, _lib.stream_ptr())
+        keys = np.zeros((3, 256), np.float32)
+        with pytest.raises(ValueError, match="outside pool"):
+            _lib.call("oxy_pi05_read_kv", be._h, _lib.ptr_i32(blocks), C.c_int32(3), C.c_int32(0),
+                      keys.ctypes.data_as(C.c_void_p), keys.ctypes.data_as(C.c_void_p), _lib.stream_ptr())
+
+
+def test_failed_decode_reservation_leaves_the_pool_unchanged():
+    """Pool exhaustion part-way through a batch's reservations rolls back the rows
+    already reserved (blocks, copy-on-write copies, tail watermarks): the allocator
+    state after the MemoryError equals the state before the call."""
+    from paper_2603_14371_b200.pi05 import TINY, Pi05Backend
+    be = Pi05Backend(TINY, num_blocks=6)
+    a = be.prefill(_obs(0, tuple(range(2, 40))))    # 1 block, tail partially filled
+    b = be.prefill(_obs(0, tuple(range(2, 130))))   # 3 blocks
+    snap = be.allocator.snapshot()
+    # row 0 shares a's tail with row 1 (copy-on-write), row 2 needs more blocks than are left
+    with pytest.raises(MemoryError):
+        be.batched_language_decode(BatchedState((a, a, b), ((),) * 3, (False,) * 3, (0, 1, 2),
+                                                (200,) * 3, (0,) * 3), 150)
+    after = be.allocator.snapshot()
+    for x, y in zip(snap, after):
+        assert np.array_equal(x, y)

@@ -239,3 +239,16 @@ def test_resumption_suite_catches_lost_cache_writes():
 def test_sharing_suite_catches_stateful_denoise():
     rep = suite_sharing(6, backend_factory=_broken("drift"))
     assert not rep.ok and any("action chunk" in f for f in rep.failures)
+
+
+def test_decode_budget_below_k_across_block_boundary():
+    """Remaining budget < k with seq + k past a block boundary but seq + budget not:
+    the table covers seq + min(k, budget) and the call succeeds (and matches the oracle)."""
+    b = toy(vocab=64, d_model=32, n_heads=2)
+    bs = b.allocator.block_size
+    obs = tuple(range(3, 3 + bs - 2))  # P = B - 2: one block
+    out = solo(b, obs, 2, 8)
+    ref = ToyRef(vocab=64, d_model=32, n_heads=2)
+    toks, _, _ = ref.decode(ref.prefill(obs), (), 2, 8)
+    assert out.token_buffers[0] == toks
+    assert len(out.kv_batch[0].blocks) == 1
