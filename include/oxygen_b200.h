@@ -213,6 +213,13 @@ int oxy_pi05_decode(oxy_pi05 *m, int32_t rows, int32_t k, const int32_t *block_t
                     int32_t max_blocks, const int32_t *seq_lens_h, const int32_t *last_tokens_h,
                     const int32_t *budgets_h, const int32_t *cow_h, int32_t *out_tokens_h,
                     int32_t *out_count_h, float *logits_h, void *stream);
+/* no-cache logits of the last of n tokens (replaces kvweaver/backend.py:301-304,
+ * the oracle route of suite_reference, kvweaver/verify.py:152-181): one dense
+ * forward over the whole sequence, positions [0, prefix_len) bidirectional
+ * (prefix-LM), later positions causal; plain fp32 attention, no pool or block
+ * tables.  logits_h: host f32 [vocab]. */
+int oxy_pi05_recompute_logits(oxy_pi05 *m, const int32_t *tokens_h, int32_t n, int32_t prefix_len,
+                              float *logits_h, void *stream);
 int oxy_pi05_read_kv(oxy_pi05 *m, const int32_t *blocks_h, int32_t seq_len, int32_t layer,
                      float *keys_h, float *values_h, void *stream);
 

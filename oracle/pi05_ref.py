@@ -23,7 +23,7 @@ import math
 import numpy as np
 import torch
 
-from paper_2603_14371_b200.rng import counter_uniform
+from oracle.rng_ref import counter_uniform
 
 HD = 256
 NQH = 8

@@ -100,6 +100,7 @@ int oxy_alloc_destroy(oxy_alloc *a) {
 
 int oxy_alloc_seq(oxy_alloc *a, int32_t n_tokens, int32_t *blocks_h) {
   OXY_API_BEGIN
+  OXY_REQUIRE(a != nullptr, "null allocator handle");
   OXY_REQUIRE(n_tokens >= 1, "sequence needs at least one position");
   int32_t nb = a->blocks_for(n_tokens);
   if ((int32_t)a->heap.size() < nb)
@@ -114,6 +115,7 @@ int oxy_alloc_seq(oxy_alloc *a, int32_t n_tokens, int32_t *blocks_h) {
 
 int oxy_alloc_incref(oxy_alloc *a, const int32_t *blocks_h, int32_t n) {
   OXY_API_BEGIN
+  OXY_REQUIRE(a != nullptr, "null allocator handle");
   for (int32_t i = 0; i < n; ++i) a->check_id(blocks_h[i]);
   for (int32_t i = 0; i < n; ++i) a->ref[blocks_h[i]]++;
   OXY_API_END
@@ -121,6 +123,7 @@ int oxy_alloc_incref(oxy_alloc *a, const int32_t *blocks_h, int32_t n) {
 
 int oxy_alloc_decref(oxy_alloc *a, const int32_t *blocks_h, int32_t n) {
   OXY_API_BEGIN
+  OXY_REQUIRE(a != nullptr, "null allocator handle");
   for (int32_t i = 0; i < n; ++i) a->decref(blocks_h[i]);
   OXY_API_END
 }
@@ -128,6 +131,7 @@ int oxy_alloc_decref(oxy_alloc *a, const int32_t *blocks_h, int32_t n) {
 int oxy_alloc_reserve(oxy_alloc *a, const int32_t *blocks_h, int32_t seq_len, int32_t n_new,
                       int32_t *new_blocks_h, int32_t *cow_h) {
   OXY_API_BEGIN
+  OXY_REQUIRE(a != nullptr, "null allocator handle");
   OXY_REQUIRE(seq_len >= 1 && n_new >= 0, "reserve needs seq_len >= 1 and n_new >= 0");
   const int32_t bs = a->bs;
   const int32_t nb_old = a->blocks_for(seq_len);
@@ -174,6 +178,7 @@ int oxy_alloc_reserve(oxy_alloc *a, const int32_t *blocks_h, int32_t seq_len, in
 int oxy_alloc_settle(oxy_alloc *a, const int32_t *blocks_h, int32_t seq_len, int32_t n_reserved,
                      int32_t n_actual, int32_t *n_blocks_out) {
   OXY_API_BEGIN
+  OXY_REQUIRE(a != nullptr, "null allocator handle");
   OXY_REQUIRE(n_actual >= 0 && n_actual <= n_reserved, "settle: n_actual %d outside [0, %d]",
               n_actual, n_reserved);
   const int32_t nb_res = a->blocks_for((int64_t)seq_len + n_reserved);
@@ -191,13 +196,16 @@ int oxy_alloc_settle(oxy_alloc *a, const int32_t *blocks_h, int32_t seq_len, int
 }
 
 int oxy_alloc_num_free(const oxy_alloc *a, int32_t *out) {
+  OXY_API_BEGIN
+  OXY_REQUIRE(a != nullptr && out != nullptr, "null allocator handle");
   *out = (int32_t)a->heap.size();
-  return OXY_OK;
+  OXY_API_END
 }
 
 int oxy_alloc_snapshot(const oxy_alloc *a, int32_t *refcount_h, int32_t *fill_h, int32_t *free_h,
                        int32_t *n_free) {
   OXY_API_BEGIN
+  OXY_REQUIRE(a != nullptr, "null allocator handle");
   std::memcpy(refcount_h, a->ref.data(), sizeof(int32_t) * a->num_blocks);
   std::memcpy(fill_h, a->fill.data(), sizeof(int32_t) * a->num_blocks);
   int32_t n = 0;

@@ -653,6 +653,55 @@ void decode_attention_v3(const CUtensorMap &kmap, const CUtensorMap &vmap, const
                max_chunks);
 }
 
+// ============================================================ no-cache recompute attention
+// The oracle route of suite_reference (kvweaver/verify.py:152-181): plain fp32
+// softmax attention over dense rows with the prefix-LM mask — query t sees keys
+// [0, P) and, past the prefix, [P, t] — deliberately independent of the tiled
+// kernels, the paged pool and the decode path.  CTA = (query, head), thread = dim.
+__global__ void prefix_lm_attention_ref_kernel(const bf16 *q, const bf16 *k, const bf16 *v, bf16 *out, int T, int P,
+                                               float scale) {
+  extern __shared__ float ra_sh[];
+  float *qs = ra_sh, *sc = ra_sh + HEAD_DIM, *red = sc + T;
+  const int t = blockIdx.x, h = blockIdx.y, d = threadIdx.x;
+  qs[d] = __bfloat162float(q[(size_t)t * Q_HEADS * HEAD_DIM + h * HEAD_DIM + d]);
+  __syncthreads();
+  const int nk = t < P ? P : t + 1;
+  float mx = -INFINITY;
+  for (int j = d; j < nk; j += blockDim.x) {
+    const bf16 *kr = k + (size_t)j * HEAD_DIM;
+    float acc = 0.f;
+    for (int e = 0; e < HEAD_DIM; ++e) acc = fmaf(qs[e], __bfloat162float(kr[e]), acc);
+    sc[j] = acc * scale;
+    mx = fmaxf(mx, sc[j]);
+  }
+  const float M = block_max(mx, red);
+  float sum = 0.f;
+  for (int j = d; j < nk; j += blockDim.x) {
+    const float e = expf(sc[j] - M);
+    sc[j] = e;
+    sum += e;
+  }
+  const float L = block_sum(sum, red + 32);
+  __syncthreads();
+  float o = 0.f;
+  for (int j = 0; j < nk; ++j) o = fmaf(sc[j], __bfloat162float(v[(size_t)j * HEAD_DIM + d]), o);
+  out[(size_t)t * Q_HEADS * HEAD_DIM + h * HEAD_DIM + d] = __float2bfloat16(o / L);
+}
+
+void prefix_lm_attention_ref(const bf16 *q, const bf16 *k, const bf16 *v, bf16 *out, int T, int P, float scale,
+                             cudaStream_t st) {
+  const size_t smem = (HEAD_DIM + (size_t)T + 64) * sizeof(float);
+  OXY_REQUIRE(smem <= 200 * 1024, "recompute sequence of %d positions too long", T);
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    OXY_CUDA(cudaFuncSetAttribute(prefix_lm_attention_ref_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+    attr = smem;
+  }
+  prefix_lm_attention_ref_kernel<<<dim3(T, Q_HEADS), HEAD_DIM, smem, st>>>(q, k, v, out, T, P, scale);
+  OXY_LAUNCH_CHECK();
+}
+
 // ============================================================ argmax
 
 constexpr int AM_CHUNKS = 64;

@@ -115,6 +115,10 @@ void decode_attention_v3(const CUtensorMap &kmap, const CUtensorMap &vmap, const
 
 // Greedy token + continuous-batching state update over logits [rows, V].
 // part: rows * 64 (val, idx) scratch.
+// no-cache recompute route: dense fp32 attention with the prefix-LM mask (q [T, 8*256],
+// k / v [T, 256] bf16 rows; keys [0, P) for t < P, else [0, t])
+void prefix_lm_attention_ref(const bf16 *q, const bf16 *k, const bf16 *v, bf16 *out, int T, int P, float scale,
+                             cudaStream_t st);
 void argmax_update(const float *logits, int rows, int V, int step, int k, int eos, int *active,
                    int *tok, int *pos, int *count, const int *budget, int *out_tokens,
                    float *part_val, int *part_idx, cudaStream_t st);

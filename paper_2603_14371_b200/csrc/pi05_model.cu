@@ -972,6 +972,58 @@ struct Model {
     else OXY_CUDA(cudaEventRecord(ev_out, mst));
   }
 
+  // ------------------------------------------------------------ no-cache recompute
+  // recompute_logits (kvweaver/backend.py:301-304): logits of the last of T tokens
+  // from one dense forward over the whole sequence — prefix [0, P) bidirectional,
+  // positions >= P causal — through the prefill GEMM plans and a plain fp32
+  // attention kernel; no pool, no block tables, no decode kernels.  The oracle
+  // route suite_reference compares cached decode against.
+  void recompute(cudaStream_t caller, const int *tok_h, int T, int P, float *logits_h) {
+    OXY_REQUIRE(T >= 1 && P >= 0 && P <= T, "recompute needs T >= 1 and 0 <= P <= T");
+    for (int i = 0; i < T; ++i)
+      OXY_REQUIRE(tok_h[i] >= 0 && tok_h[i] < c.vocab, "token %d outside vocab of %d", tok_h[i], c.vocab);
+    PhaseScope phase_scope(*this, gemm::PH_PREFILL);
+    const int W = c.width;
+    arena_used = 0;
+    x.as<float>((size_t)T * W);
+    y.as<bf16>((size_t)T * W);
+    q.as<bf16>((size_t)T * QDIM);
+    o.as<bf16>((size_t)T * QDIM);
+    kd.as<bf16>((size_t)T * HEAD_DIM);
+    vd.as<bf16>((size_t)T * HEAD_DIM);
+    hmid.as<bf16>((size_t)T * c.mlp);
+    logits.as<float>((size_t)c.vocab);
+    plan_gemm(QKV, W, T);
+    plan_gemm(W, QDIM, T);
+    plan_gemm(2 * c.mlp, W, T);
+    plan_gemm(W, c.mlp, T);
+    plan_gemm(c.vocab, W, 1);
+    reserve_common();
+    float *X = x.as<float>(0), *LG = logits.as<float>(0);
+    bf16 *Y = y.as<bf16>(0), *Qb = q.as<bf16>(0), *Ob = o.as<bf16>(0), *Kd = kd.as<bf16>(0), *Vd = vd.as<bf16>(0),
+         *Hm = hmid.as<bf16>(0);
+    std::vector<int> pos(T);
+    for (int i = 0; i < T; ++i) pos[i] = i;
+    int *d_tok = arena_put(tok_h, T), *d_pos = arena_put(pos.data(), T);
+    enter(caller);
+    arena_upload();
+    embed_rows(X, W, embed, d_tok, nullptr, T, W, std::sqrt((float)W), mst);
+    rmsnorm(X, W, Y, W, L[0].ln1, nullptr, nullptr, T, W, 1e-6f, mst);
+    for (int l = 0; l < c.depth; ++l) {
+      const LayerW &w = L[l];
+      const float *next_norm = l + 1 < c.depth ? L[l + 1].ln1 : final_norm;
+      gemm_qkv(w.wqkv, Y, W, T, d_pos, nullptr, Qb, Kd, Vd);
+      prefix_lm_attention_ref(Qb, Kd, Vd, Ob, T, P, 1.f / 16.f, mst);
+      gemm_res_norm(w.wo, Ob, W, QDIM, T, nullptr, X, Y, w.ln2, nullptr, nullptr);
+      gemm(w.wgu, Y, 2 * c.mlp, W, T, gemm::EPI_GEGLU_BF16, Hm, c.mlp);
+      gemm_res_norm(w.wd, Hm, W, c.mlp, T, nullptr, X, Y, next_norm, nullptr, nullptr);
+    }
+    gemm(lm_head, Y + (size_t)(T - 1) * W, c.vocab, W, 1, gemm::EPI_F32, LG, c.vocab);
+    OXY_CUDA(cudaMemcpyAsync(logits_h, LG, (size_t)c.vocab * sizeof(float), cudaMemcpyDeviceToHost, mst));
+    OXY_CUDA(cudaStreamSynchronize(mst));
+    leave(caller);
+  }
+
   // ------------------------------------------------------------ decode
   // A/B: OXY_DECODE_EARLY=0 turns off early PDL for the decode lane's skinny
   // GEMMs (their waiting CTAs then do not hold SMs the concurrent denoise needs)
@@ -1205,6 +1257,14 @@ int oxy_pi05_decode(oxy_pi05 *p, int32_t rows, int32_t k, const int32_t *block_t
   OXY_REQUIRE(k >= 1, "decode step count must be >= 1, got %d", k);
   p->m.decode(oxy::as_stream(stream), rows, k, block_tables_h, max_blocks, seq_lens_h, last_tokens_h, budgets_h,
               cow_h, out_tokens_h, out_count_h, logits_h);
+  OXY_API_END
+}
+
+int oxy_pi05_recompute_logits(oxy_pi05 *p, const int32_t *tokens_h, int32_t n, int32_t prefix_len, float *logits_h,
+                              void *stream) {
+  OXY_API_BEGIN
+  OXY_REQUIRE(tokens_h && logits_h && n >= 1, "recompute needs at least one token");
+  p->m.recompute(oxy::as_stream(stream), tokens_h, n, prefix_len, logits_h);
   OXY_API_END
 }
 

@@ -59,6 +59,8 @@ class BlockAllocator:
         _lib.call("oxy_alloc_incref", self._h, _lib.ptr_i32(b), C.c_int32(len(b)))
 
     def decref(self, blocks) -> None:
+        if self._h is None or not self._h.value:  # allocator already torn down (GC order)
+            return
         b = _lib.as_i32(blocks)
         _lib.call("oxy_alloc_decref", self._h, _lib.ptr_i32(b), C.c_int32(len(b)))
 

@@ -30,7 +30,7 @@ from .kv_manager import BatchedState, GenerationState, KvLayer
 from .paged import BlockAllocator, PagedKvCache
 from .timing import StageMeter
 
-__all__ = ["Pi05Config", "Pi05Observation", "Pi05Backend", "TINY", "smoke"]
+__all__ = ["Pi05Config", "Pi05Observation", "Pi05Backend", "TINY", "synthetic_images"]
 
 KV_BLOCK = 64
 HEAD_DIM = 256
@@ -317,6 +317,29 @@ class Pi05Backend(PricedBackend):
             return chunks
         return states, join
 
+    def recompute_logits(self, token_ids) -> np.ndarray:
+        """No-cache logits of the last position (``kvweaver/backend.py:301-304``), the
+        route ``suite_reference`` grades cached decode against: one dense forward over
+        the whole sequence with a plain fp32 attention kernel — no pool, no block
+        tables, no decode kernels.  The prefix (bidirectional, prefix-LM) is everything
+        before the LAST EOS: the first decode input is EOS at position P
+        (``kvweaver/backend.py:359-362``) and decoded tokens never contain EOS (a
+        request stops on it), so the last EOS is that marker.  Without an EOS the
+        whole sequence is prefix."""
+        toks = _lib.as_i32([int(t) for t in token_ids])
+        if len(toks) == 0:
+            raise ValueError("recompute needs at least one token")
+        v = self.config.vocab
+        for t in toks:
+            if not 0 <= t < v:
+                raise ValueError(f"token {int(t)} outside vocab of {v}")
+        eos = np.flatnonzero(toks == self.config.eos_token)
+        p = int(eos[-1]) if len(eos) else len(toks)
+        out = np.empty(v, np.float32)
+        _lib.call("oxy_pi05_recompute_logits", self._h, _lib.ptr_i32(toks), C.c_int32(len(toks)),
+                  C.c_int32(p), out.ctypes.data_as(C.c_void_p), _lib.stream_ptr())
+        return out.astype(np.float64)
+
     def batched_language_decode(self, batched: BatchedState, k: int,
                                 return_logits: bool = False):
         self._check_batch(batched, k)
@@ -369,25 +392,3 @@ def synthetic_images(n: int, seed: int) -> np.ndarray:
     from .rng import counter_u64
     raw = counter_u64(seed, 0, n * 224 * 224 * 3 // 8 + 1).view(np.uint8)
     return raw[: n * 224 * 224 * 3].reshape(n, 224, 224, 3).copy()
-
-
-def smoke() -> None:
-    """Tiny pi0.5 frame on cuda:0 checked against the CPU oracle."""
-    import sys
-    import os
-    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-    from oracle.pi05_ref import Pi05Ref
-
-    be = Pi05Backend(TINY, num_blocks=64)
-    ref = Pi05Ref.from_backend(be)
-    obs = Pi05Observation((5, 17, 99, 3), 0, synthetic_images(1, 11))
-    kv = be.prefill(obs)
-    chunk = be.action_denoise(kv, TINY.S)
-    out = be.batched_language_decode(BatchedState((kv,), ((),), (False,), (0,), (4,), (0,)), 4)
-    r_kv = ref.prefill(obs)
-    r_act = ref.denoise(r_kv, TINY.S)
-    r_toks = ref.decode(r_kv, (), 4)[0]
-    err = float(np.max(np.abs(chunk.actions - r_act)) / (np.max(np.abs(r_act)) + 1e-6))
-    assert err < 3e-2, f"pi05 action mismatch {err}"
-    print(f"smoke F2 ok: action rel err {err:.2e}, tokens {out.token_buffers[0]} "
-          f"(oracle {tuple(r_toks)})")

@@ -19,7 +19,8 @@ from .metrics import speedup, summarize
 from .sim_engine import SimConfig, run_simulation
 from .workload import generate_arrivals
 
-__all__ = ["CSV_COLUMNS", "CSV_VERSION_COMMENT", "CSV_NOTE_COMMENT", "csv_row", "measured_row", "write_csv"]
+__all__ = ["CSV_COLUMNS", "CSV_VERSION_COMMENT", "CSV_NOTE_COMMENT", "csv_row", "measured_row",
+           "speedup_vs_isolated", "write_csv"]
 
 CSV_COLUMNS = [
     "run_id", "variant", "backend", "N", "k", "H", "S", "lambda", "pattern",
@@ -52,6 +53,19 @@ def csv_row(run_id: str, config: SimConfig, result, report, spd: float, H=None, 
             str(wl.seed), str(len(result.traces)), _fmt(report.per_request_action_freq),
             _fmt(report.action_freq_hz), _fmt(report.token_throughput), _fmt(report.avg_batch_size),
             _fmt(report.deadline_miss_rate), str(report.warmup_frames), _fmt(spd)]
+
+
+def speedup_vs_isolated(config: SimConfig, report) -> float:
+    """Speedup column: f of this run over its IsolatedSequential twin (kvweaver/cli.py:73-77)."""
+    if config.variant == "IsolatedSequential":
+        return 1.0
+    twin = replace(config, variant="IsolatedSequential")
+    return speedup(report, summarize(run_simulation(twin), twin))
+
+
+# the reference CLI's private names for the same two functions (kvweaver/cli.py:73-101)
+_speedup_vs_isolated = speedup_vs_isolated
+_csv_row = csv_row
 
 
 def measured_row(run_id: str, config: SimConfig, backend) -> list[str]:

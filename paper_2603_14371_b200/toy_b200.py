@@ -126,11 +126,18 @@ class ToyBackend(PricedBackend):
         return h
 
     def _own(self, kv) -> PagedKvCache:
+        """The pool-resident handle for ``kv``.  A cache of the same backend tag that
+        lives elsewhere (a host ``KvCache`` — e.g. one a caller rebuilt from
+        ``layers`` — or another instance's pool) is accepted as the reference accepts
+        any cache with a matching tag (``kvweaver/backend.py:179-183``): its layers
+        are copied into this pool (``adopt``)."""
         self._check_tag(kv)
-        if not isinstance(kv, PagedKvCache) or kv.owner is not self:
-            raise ValueError(f"cache from backend {kv.backend_tag!r} is not resident in this "
-                             f"backend's KV pool")
-        return kv
+        if isinstance(kv, PagedKvCache) and kv.owner is self:
+            return kv
+        if hasattr(kv, "layers") and hasattr(kv, "seq_len"):
+            return self.adopt(kv)
+        raise ValueError(f"cache from backend {kv.backend_tag!r} is not resident in this "
+                         f"backend's KV pool")
 
     # ------------------------------------------------------------ protocol
 

@@ -2,7 +2,8 @@
 
 Loaded with ``-p ref_alias`` (tests/ on PYTHONPATH) by
 tests/test_reference_unmodified.py.  It maps the module ``kvweaver`` and its
-hot-path submodules (``kvweaver/__init__.py:12-72``) onto
+hot-path submodules (``kvweaver/__init__.py:12-72``; ``kvweaver.cli``'s CSV
+row helpers -> ``report``) onto
 ``paper_2603_14371_b200`` before the reference test files import them, so
 ``from kvweaver import ToyBackend, KvManager, run_simulation, ...`` binds the
 B200 package: ``ToyBackend`` / ``make_backend("Toy")`` are the CUDA toy
@@ -22,6 +23,8 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 _SUBMODULES = ("backend", "kv_manager", "metrics", "rng", "scheduler", "sim_engine", "verify", "workload")
+# the CSV row helpers the acceptance tests import from the (out-of-scope) CLI
+_RENAMED = {"cli": "report"}
 
 
 def _install() -> None:
@@ -31,6 +34,8 @@ def _install() -> None:
         mod = importlib.import_module(f"paper_2603_14371_b200.{sub}")
         sys.modules[f"kvweaver.{sub}"] = mod
         setattr(pkg, sub, mod)
+    for ref_name, ours in _RENAMED.items():
+        sys.modules[f"kvweaver.{ref_name}"] = importlib.import_module(f"paper_2603_14371_b200.{ours}")
 
 
 _install()

@@ -254,7 +254,29 @@ def test_extra_language_tasks_share_the_arrival():
     states = [mgr.retrieve(r) for r in mgr.active_ids()]  # the 2-token task finished this frame
     assert sorted(s.max_len for s in states) == [4, 6] and all(len(s.tokens) == 2 for s in states)
     assert len(res.finished) == 1 and len(res.finished[0][1]) == 2
-    assert len(res.actions) == 1  # one action chunk per observation
+    # one action chunk per observation, recorded under every task's request id
+    assert len(res.actions) == 3 and all(c is res.actions[0][1] for _, c in res.actions)
     import pytest
     with pytest.raises(ValueError):
         Arrival(0, Observation((1,), 0), 4, extra_tasks=(0,))
+
+
+def test_extra_tasks_get_action_entries_and_complete():
+    """Arrival.extra_tasks (several language tasks on one observation): every task's
+    request id gets the observation's action chunk, so a frame loop can transcribe
+    it when it completes (no orphaned request ids)."""
+    from paper_2603_14371_b200 import Arrival, KvManager, Observation
+    from paper_2603_14371_b200.backend import BackendConfig, CostModelParams, make_backend
+    from paper_2603_14371_b200.scheduler import run_frame_unified
+    be = make_backend("CostModel", BackendConfig(), CostModelParams())
+    mgr = KvManager()
+    res = run_frame_unified(0, [Arrival(0, Observation((1, 2, 3), 0), 2, extra_tasks=(5, 3))], mgr, be, 2, 30.0)
+    rids = [rid for rid, _ in res.actions]
+    assert sorted(rids) == [0, 1, 2]
+    assert all(chunk == res.actions[0][1] for _, chunk in res.actions)
+    pending = {rid for rid, _ in res.actions}
+    pending -= {rid for rid, _ in res.finished}
+    for t in range(1, 4):
+        res = run_frame_unified(t, [], mgr, be, 2, 30.0)
+        pending -= {rid for rid, _ in res.finished}
+    assert not pending and not mgr.active_ids()

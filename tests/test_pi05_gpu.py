@@ -10,7 +10,8 @@ import numpy as np
 import pytest
 
 from paper_2603_14371_b200 import BatchedState, BackendConfig, Observation
-from paper_2603_14371_b200.verify import (suite_batching, suite_resumption, suite_sharing)
+from paper_2603_14371_b200.verify import (suite_batching, suite_reference, suite_resumption,
+                                          suite_sharing)
 
 pytestmark = pytest.mark.gpu
 
@@ -171,7 +172,8 @@ def _pi05_factory(cfg: BackendConfig):
     return Pi05Backend(cfg, num_blocks=128)
 
 
-@pytest.mark.parametrize("suite, n", [(suite_batching, 6), (suite_resumption, 8), (suite_sharing, 5)])
+@pytest.mark.parametrize("suite, n", [(suite_batching, 6), (suite_resumption, 8), (suite_sharing, 5),
+                                      (suite_reference, 10)])
 def test_reference_suites_on_pi05_backend(suite, n):
     rep = suite(n, backend_factory=_pi05_factory)
     assert rep.ok, rep.failures[:3]
@@ -340,3 +342,28 @@ def test_failed_decode_reservation_leaves_the_pool_unchanged():
     after = be.allocator.snapshot()
     for x, y in zip(snap, after):
         assert np.array_equal(x, y)
+
+
+def test_recompute_logits_matches_cached_decode(tiny):
+    """The no-cache route (dense forward, prefix-LM mask, plain fp32 attention) and
+    the cached paged decode agree on every step's logits of a 4-step decode."""
+    be, _ = tiny
+    obs = _obs(1, (31, 32, 33))
+    kv = be.prefill(obs)
+    out, logits = be.batched_language_decode(
+        BatchedState((kv,), ((),), (False,), (0,), (4,), (0,)), 4, return_logits=True)
+    toks = out.token_buffers[0]
+    # image positions are not token ids: recompute covers token-only prefixes, so use
+    # a token-only observation for the route comparison
+    kv2 = be.prefill(_obs(0, (31, 32, 33, 34, 35)))
+    out2, logits2 = be.batched_language_decode(
+        BatchedState((kv2,), ((),), (False,), (0,), (4,), (0,)), 4, return_logits=True)
+    seq = [31, 32, 33, 34, 35, be.config.eos_token]
+    for s, t in enumerate(out2.token_buffers[0]):
+        want = be.recompute_logits(seq)
+        got = logits2[s, 0].astype(np.float64)
+        cos = got @ want / (np.linalg.norm(got) * np.linalg.norm(want))
+        assert cos > 0.9999, (s, cos)
+        assert int(np.argmax(want)) == t or np.sort(want)[-1] - np.sort(want)[-2] < 2 * np.abs(got - want).max()
+        seq.append(t)
+    assert len(toks) >= 1

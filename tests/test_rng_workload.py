@@ -45,6 +45,17 @@ def test_counter_form_is_the_stream(golden):
     assert r.next_u64() == int(g["seed7_u64"][40])
 
 
+def test_oracle_counter_form_is_the_stream(golden):
+    """The oracle's own restatement (oracle/rng_ref.py) is pinned to the same
+    reference vectors, independently of the product's rng module."""
+    from oracle import rng_ref
+    g = golden("rng.json")
+    assert rng_ref.counter_u64(7, 0, 64).tolist() == [int(x) for x in g["seed7_u64"]]
+    assert rng_ref.counter_uniform(7, 0, 64).tolist() == g["seed7_uniform"]
+    assert rng_ref.counter_u64(0, 0, 5).tolist() == [int(x) for x in g["seed0_u64"]]
+    assert rng_ref.counter_u64(0xDEADBEEF, 0, 3).tolist() == [int(x) for x in g["deadbeef_u64"]]
+
+
 def test_below_and_poisson_guards():
     with pytest.raises(ValueError, match="positive bound"):
         SplitMix64(1).below(0)
