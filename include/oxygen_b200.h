@@ -124,6 +124,10 @@ int oxy_gemm_bf16(const void *w_d, const void *x_d, int32_t n_out, int32_t k, in
                   int64_t ws_floats, void *stream);
 /* plan the launch: out6 = {bn, n_tiles, m_tiles, splits, stages, k_blocks} */
 int oxy_gemm_plan(int32_t n_out, int32_t k, int32_t t, int32_t splits, int32_t *out6);
+/* the batch-invariant split-K count the model uses for an (n_out, k) projection in
+ * a phase (0 = prefill, 1 = skinny decode / denoise chains); a function of
+ * (phase, n_out, k) only — never of the token count (gemm_sm100.cuh) */
+int oxy_gemm_policy_splits(int32_t phase, int32_t n_out, int32_t k, int32_t *splits);
 /* launches enqueued per plan class since the last reset (eager runs and CUDA
  * graph captures; replays are not re-counted): out[0..n) = {skinny, skinny
  * split-K, prefill deep-K band, prefill mid-K band, persistent 1-CTA, persistent

@@ -921,6 +921,16 @@ extern "C" int oxy_gemm_bf16(const void *w_d, const void *x_d, int32_t n_out, in
   OXY_API_END
 }
 
+extern "C" int oxy_gemm_policy_splits(int32_t phase, int32_t n_out, int32_t k, int32_t *splits) {
+  OXY_API_BEGIN
+  OXY_REQUIRE(splits && n_out > 0 && k > 0 && (phase == 0 || phase == 1), "bad policy query");
+  int dev = 0, sms = 148;
+  OXY_CUDA(cudaGetDevice(&dev));
+  OXY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  *splits = oxy::gemm::policy_splits(phase, n_out, k, sms);
+  OXY_API_END
+}
+
 extern "C" int oxy_plan_counts(int64_t *out, int32_t n, int32_t reset) {
   OXY_API_BEGIN
   OXY_REQUIRE(n >= 0 && (n == 0 || out), "bad plan-count buffer");
