@@ -394,17 +394,29 @@ void flash_attention(const AttnGroup *groups_d, int n_groups, int max_q_tiles, i
 
 constexpr int DA_PART = Q_HEADS * (HEAD_DIM + 2);
 
-// CTA = (row, chunk of `cb` pool blocks), 4 warps, 1 CTA/SM.  One thread
-// streams each block's K and V (2 x 32 KB) with 8 TMA tensor copies (64-column
-// sub-tiles, 128-byte swizzle) into a 3-stage mbarrier ring, so the SM keeps up
-// to 192 KB of KV in flight with a handful of instructions.  Warp w owns keys
-// 16w..16w+15 of every block (S = QK^T and O = PV on mma.sync bf16, online
-// softmax in registers); the 4 warps merge once per chunk; chunks of a row are
-// merged by decode_merge3_kernel in chunk order (deterministic).
-constexpr int D3_STAGES = 3;
-constexpr int D3_SUB = KV_BLOCK * 128;              // one 64-row x 64-col bf16 sub-tile: 8 KB
-constexpr int D3_STAGE_BYTES = 8 * D3_SUB;          // K (4 sub-tiles) + V (4 sub-tiles)
-constexpr size_t D3_SMEM = 1024 + 4 * 16 * 128 + D3_STAGES * D3_STAGE_BYTES + 64;
+// Persistent paged decode attention.  Work item = (row, chunk of cb pool
+// blocks; decode_row_chunk: a function of the row's own length).  Grid = up to
+// 2 CTAs per SM, each looping over items blockIdx.x, +gridDim.x, ... so the KV
+// stream never drains between items.  5 warps:
+//   warp 4     producer (one thread): per block, the K tile then the V tile
+//              (64 keys x 256 dims bf16 = 32 KB, four 64-column TMA boxes,
+//              128-byte swizzle) into a ring of D4_SLOTS 32 KB slots
+//              (full / empty mbarriers); 2 CTAs x 96 KB in flight per SM;
+//   warps 0-3  S = Q K^T split by keys (warp w: keys 16w..16w+15 of the block,
+//              mma.sync bf16, the 8 query heads as MMA rows), scores staged in
+//              smem; every warp then runs the same online softmax over all 64
+//              keys (4 lanes per head, shuffle reductions) and computes
+//              O += P V for ITS 64 of the 256 output dims — no cross-warp merge
+//              at the end of an item: a single-chunk row is written directly,
+//              a chunk's unnormalised O and (m, l) go to the workspace and
+//              decode_merge3_kernel combines the chunks in chunk order.
+// Pool slots past a sequence's length are masked (-inf scores).
+constexpr int D4_SLOTS = 3;
+constexpr int D4_SUB = KV_BLOCK * 128;           // one 64-key x 64-dim bf16 box: 8 KB
+constexpr int D4_TILE = 4 * D4_SUB;              // K or V tile of one pool block: 32 KB
+constexpr int D4_SLD = 72;                       // score row stride (floats)
+constexpr int D4_THREADS = 160;
+constexpr size_t D4_SMEM = 1024 + D4_SLOTS * D4_TILE + 2 * Q_HEADS * D4_SLD * 4 + 32 + 2 * D4_SLOTS * 8 + 64;
 
 // 16-byte chunk c (0..31) of row `row` in a tile of 4 swizzled 64-col sub-tiles
 __device__ __forceinline__ uint32_t tile16(uint32_t base, int rows_per_sub, int row, int c) {
@@ -416,6 +428,11 @@ __device__ __forceinline__ void d3_mbar_init(uint32_t bar, uint32_t count) {
 }
 __device__ __forceinline__ void d3_expect_tx(uint32_t bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+// consumer release of a ring slot (the callers first store a value that depends on
+// every MMA fed from the slot, see decode_attn_v4_kernel)
+__device__ __forceinline__ void d3_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 __device__ __forceinline__ void d3_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
@@ -433,204 +450,274 @@ __device__ __forceinline__ void d3_tma(const CUtensorMap *map, uint32_t bar, uin
       : "memory");
 }
 
-__global__ void __launch_bounds__(128, 1)
-    decode_attn_v3_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
-                          const bf16 *q, const int *bt, int bt_stride, const int *pos, const int *active, int cb,
-                          int max_chunks, float scale_log2, float *ws, bf16 *out) {
+// item -> (row, its chunking, the chunks [ca, cb) this item covers); false: nothing
+// to do.  row_mode: an item is a whole row (all its chunks, folded in registers);
+// else one chunk (partials folded by decode_fold_kernel).
+struct D4Item {
+  int r, n_keys, nb, cb, n_chunks, ca, ce;
+};
+__device__ __forceinline__ bool d4_item(int item, int row_mode, int max_chunks, int cb_min, const int *pos,
+                                        const int *active, D4Item &it) {
+  it.r = row_mode ? item : item / max_chunks;
+  if (active && !active[it.r]) return false;
+  it.n_keys = pos[it.r] + 1;
+  it.nb = (it.n_keys + KV_BLOCK - 1) / KV_BLOCK;
+  it.cb = decode_row_chunk(it.nb, cb_min);
+  it.n_chunks = (it.nb + it.cb - 1) / it.cb;
+  if (row_mode) {
+    it.ca = 0;
+    it.ce = it.n_chunks;
+    return true;
+  }
+  it.ca = item % max_chunks;
+  it.ce = it.ca + 1;
+  return it.ca < it.n_chunks;
+}
+
+// fold of chunk partials (m_c, l_c, O_c) in chunk order; out = O * (1 / L)
+__device__ __forceinline__ void d4_fold(float &M, float &L, float mc, float lc, float &fa, float &fb) {
+  const float mn = fmaxf(M, mc);
+  fa = M == -INFINITY ? 0.f : exp2f(M - mn);
+  fb = exp2f(mc - mn);
+  L = __fmaf_rn(lc, fb, __fmul_rn(L, fa));
+  M = mn;
+}
+
+__global__ void __launch_bounds__(D4_THREADS, 2)
+    decode_attn_v4_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
+                          const bf16 *q, const int *bt, int bt_stride, const int *pos, const int *active, int cb_min,
+                          int max_chunks, int n_items, int row_mode, float scale_log2, float *ws, bf16 *out) {
   pdl_trigger();
   extern __shared__ unsigned char d3_raw[];
-  unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(d3_raw) + 1023) &
-                                                          ~static_cast<uintptr_t>(1023));
-  const uint32_t sQ = smem_addr(smem);                    // 4 sub-tiles x 16 rows x 128 B
-  const uint32_t sKV = sQ + 4 * 16 * 128;                 // stages
-  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + 4 * 16 * 128 + D3_STAGES * D3_STAGE_BYTES);
-  const uint32_t full0 = smem_addr(bars);
+  // 1024-byte alignment in the SHARED address space (the 128-byte swizzle the TMA
+  // applies and the ldmatrix addressing below assume it)
+  const uint32_t raw_s = smem_addr(d3_raw);
+  unsigned char *smem = d3_raw + (((raw_s + 1023u) & ~1023u) - raw_s);
+  const uint32_t ring = smem_addr(smem);
+  float *sS = reinterpret_cast<float *>(smem + D4_SLOTS * D4_TILE);  // [2][8][D4_SLD]
+  float *sSink = sS + 2 * Q_HEADS * D4_SLD;                           // [4] slot-release dependencies
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + D4_SLOTS * D4_TILE + 2 * Q_HEADS * D4_SLD * 4 + 32);
+  const uint32_t full0 = smem_addr(bars), empty0 = full0 + 8 * D4_SLOTS;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < D3_STAGES; ++s) d3_mbar_init(full0 + 8 * s, 1);
+    for (int s = 0; s < D4_SLOTS; ++s) {
+      d3_mbar_init(full0 + 8 * s, 1);
+      d3_mbar_init(empty0 + 8 * s, 4);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&kmap)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&vmap)) : "memory");
   }
   __syncthreads();
-  // pos / active / block table come from earlier steps (argmax update, host
-  // plan), not from the kernel right before us (the QKV projection): read them
-  // and prefetch every pool block but the one holding this step's position
-  // before the PDL wait
-  const int r = blockIdx.x, chunk = blockIdx.y;
-  if (active && !active[r]) return;
-  const int n_keys = pos[r] + 1;
-  const int nb = (n_keys + KV_BLOCK - 1) / KV_BLOCK;
-  cb = decode_row_chunk(nb, cb);  // this row's own chunking: batch-invariant
-  const int n_chunks = (nb + cb - 1) / cb;
-  if (chunk >= n_chunks) return;
-  const int b0 = chunk * cb, nblk = min(nb, b0 + cb) - b0;
-  const int *btr = bt + (size_t)r * bt_stride + b0;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  auto issue = [&](int i) {  // block i of the chunk -> stage i % 3 (thread 0 only)
-    const int s = i % D3_STAGES, row0 = btr[i] * KV_BLOCK;
-    const uint32_t bar = full0 + 8 * s, kb = sKV + s * D3_STAGE_BYTES, vb = kb + 4 * D3_SUB;
-    d3_expect_tx(bar, D3_STAGE_BYTES);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      d3_tma(&kmap, bar, kb + j * D3_SUB, 64 * j, row0);
-      d3_tma(&vmap, bar, vb + j * D3_SUB, 64 * j, row0);
-    }
-  };
-  int pre = 0;  // blocks issued before the wait: all but the block holding pos[r]
-  if (threadIdx.x == 0)
-    for (; pre < min(nblk, D3_STAGES) && b0 + pre < nb - 1; ++pre) issue(pre);
+  // positions / activity come from the previous decode step and Q from the
+  // QKV projection right before us: wait for the whole chain
   pdl_wait();
-  if (threadIdx.x == 0)
-    for (int i = pre; i < min(nblk, D3_STAGES); ++i) issue(i);
-  // Q: the 8 heads as MMA rows 0..7 (rows 8..15 zero)
-  const bf16 *qr = q + (size_t)r * Q_HEADS * HEAD_DIM;
-  for (int i = threadIdx.x; i < 16 * 32; i += 128) {
-    const int row = i >> 5, c = i & 31;
-    const uint32_t dst = tile16(sQ, 16, row, c);
-    if (row < Q_HEADS) cp_async16(dst, qr + (size_t)row * HEAD_DIM + c * 8);
-    else asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(dst), "r"(0));
-  }
-  cp_commit();
-  cp_wait<0>();
-  __syncthreads();
-
-  float o[32][4];
+  D4Item it;
+  if (warp == 4) {
+    if (lane == 0) {
+      int t = 0;  // tiles issued (K and V alternate)
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        if (!d4_item(item, row_mode, max_chunks, cb_min, pos, active, it)) continue;
+        const int *btr = bt + (size_t)it.r * bt_stride;
+        const int b_end = min(it.nb, it.ce * it.cb);
+        for (int b = it.ca * it.cb; b < b_end; ++b) {
+          const int row0 = btr[b] * KV_BLOCK;
 #pragma unroll
-  for (int i = 0; i < 32; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
-  float m_run = -INFINITY, l_run = 0.f;
+          for (int kv = 0; kv < 2; ++kv, ++t) {
+            const int s = t % D4_SLOTS;
+            d3_wait(empty0 + 8 * s, ((t / D4_SLOTS) & 1) ^ 1);
+            d3_expect_tx(full0 + 8 * s, D4_TILE);
+            const uint32_t dst = ring + s * D4_TILE;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) d3_tma(kv ? &vmap : &kmap, full0 + 8 * s, dst + j * D4_SUB, 64 * j, row0);
+          }
+        }
+      }
+    }
+    return;
+  }
+  const int g = lane >> 2, c = lane & 3;  // MMA row (= query head) and column pair of this lane
   const int krow = warp * 16 + (lane & 7) + ((lane >> 4) << 3);
-  const int vrow = warp * 16 + (lane & 15);
-  for (int i = 0; i < nblk; ++i) {
-    const int s = i % D3_STAGES;
-    d3_wait(full0 + 8 * s, (i / D3_STAGES) & 1);
-    const uint32_t kb = sKV + s * D3_STAGE_BYTES, vb = kb + 4 * D3_SUB;
-    float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+  int t = 0, nbk = 0;  // tiles consumed, blocks processed (score buffer parity)
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    if (!d4_item(item, row_mode, max_chunks, cb_min, pos, active, it)) continue;
+    const int r = it.r, n_keys = it.n_keys;
+    // Q of this row as MMA A fragments: head g, dims 16ks + 2c (+1), +8 (rows 8-15 are zero).
+    // L2-coherent loads (ld.global.cg), not the non-coherent path: the QKV projection
+    // rewrites this buffer every layer, and under PDL an SM's L1 can still hold the
+    // previous layer's lines (measured: stale Q with __ldg once CTAs loop over items)
+    const uint32_t *qg = reinterpret_cast<const uint32_t *>(q + (size_t)r * Q_HEADS * HEAD_DIM + g * HEAD_DIM);
+    uint32_t qa0[16], qa2[16];
 #pragma unroll
-    for (int kk = 0; kk < HEAD_DIM / 16; ++kk) {
-      uint32_t a0, a1, a2, a3, k0, k1, k2, k3;
-      ldsm_x4(tile16(sQ, 16, lane & 15, kk * 2 + (lane >> 4)), a0, a1, a2, a3);
-      ldsm_x4(tile16(kb, 64, krow, kk * 2 + ((lane >> 3) & 1)), k0, k1, k2, k3);
-      mma16816(sc[0], a0, a1, a2, a3, k0, k1);
-      mma16816(sc[1], a0, a1, a2, a3, k2, k3);
+    for (int ks = 0; ks < 16; ++ks) {
+      qa0[ks] = __ldcg(qg + 8 * ks + c);
+      qa2[ks] = __ldcg(qg + 8 * ks + 4 + c);
     }
-    const int kbase = (b0 + i) * KV_BLOCK + warp * 16 + (lane & 3) * 2;
-    float mx = m_run;
+    // fold state of the row (row mode, or a single-chunk row): M, L per head g, O for
+    // this warp's 64 dims (MMA rows 0-7)
+    float FM = -INFINITY, FL = 0.f, fo[8][2];
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt)
+    for (int nt = 0; nt < 8; ++nt) fo[nt][0] = fo[nt][1] = 0.f;
+    const bool fold = row_mode || it.n_chunks == 1;
+    for (int chunk = it.ca; chunk < it.ce; ++chunk) {
+      const int b0 = chunk * it.cb, nblk = min(it.nb, b0 + it.cb) - b0;
+      float o[8][4];
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        float v = sc[nt][e] * scale_log2;
-        if (kbase + nt * 8 + e >= n_keys) v = -INFINITY;
-        sc[nt][e] = v;
-        mx = fmaxf(mx, v);
+      for (int i = 0; i < 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+      float m_run = -INFINITY, l_run = 0.f;
+      for (int i = 0; i < nblk; ++i, ++nbk) {
+        // ---- S = Q K^T for this warp's 16 keys
+        int s = t % D4_SLOTS;
+        d3_wait(full0 + 8 * s, (t / D4_SLOTS) & 1);
+        const uint32_t kb = ring + s * D4_TILE;
+        float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+  #pragma unroll
+        for (int ks = 0; ks < 16; ++ks) {
+          uint32_t k0, k1, k2, k3;
+          ldsm_x4(tile16(kb, 64, krow, ks * 2 + ((lane >> 3) & 1)), k0, k1, k2, k3);
+          mma16816(sc[0], qa0[ks], 0u, qa2[ks], 0u, k0, k1);
+          mma16816(sc[1], qa0[ks], 0u, qa2[ks], 0u, k2, k3);
+        }
+        float *Sb = sS + (nbk & 1) * Q_HEADS * D4_SLD;
+        const int kbase = (b0 + i) * KV_BLOCK;
+  #pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          const int kl = warp * 16 + nt * 8 + 2 * c;
+          float2 v;
+          v.x = kbase + kl < n_keys ? sc[nt][0] * scale_log2 : -INFINITY;
+          v.y = kbase + kl + 1 < n_keys ? sc[nt][1] * scale_log2 : -INFINITY;
+          *reinterpret_cast<float2 *>(Sb + g * D4_SLD + kl) = v;
+        }
+        // release the K slot only after a store that depends on every S MMA (and so
+        // on every ldmatrix of the slot): an mbarrier arrive right after the last
+        // ldmatrix does not wait for its read, and the next TMA into the slot raced it
+        __syncwarp();
+        if (lane == 0) d3_arrive(empty0 + 8 * s);
+        ++t;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        // ---- online softmax over the block's 64 keys (identical in every warp)
+        float p[4][4], mx = m_run;
+  #pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const float2 a = *reinterpret_cast<const float2 *>(Sb + g * D4_SLD + kk * 16 + 2 * c);
+          const float2 b = *reinterpret_cast<const float2 *>(Sb + g * D4_SLD + kk * 16 + 8 + 2 * c);
+          p[kk][0] = a.x;
+          p[kk][1] = a.y;
+          p[kk][2] = b.x;
+          p[kk][3] = b.y;
+          mx = fmaxf(mx, fmaxf(fmaxf(a.x, a.y), fmaxf(b.x, b.y)));
+        }
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        const float corr = mx == -INFINITY ? 1.f : exp2f(m_run - mx);
+        const float mxs = mx == -INFINITY ? 0.f : mx;
+        float ls = 0.f;
+  #pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+  #pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            p[kk][e] = exp2_approx(p[kk][e] - mxs);
+            ls += p[kk][e];
+          }
+        ls += __shfl_xor_sync(0xffffffffu, ls, 1);
+        ls += __shfl_xor_sync(0xffffffffu, ls, 2);
+        l_run = l_run * corr + ls;
+        m_run = mx;
+  #pragma unroll
+        for (int nt = 0; nt < 8; ++nt) {
+          o[nt][0] *= corr;
+          o[nt][1] *= corr;
+        }
+        // ---- O[:, 64 warp .. 64 warp + 63] += P V
+        s = t % D4_SLOTS;
+        d3_wait(full0 + 8 * s, (t / D4_SLOTS) & 1);
+        const uint32_t vb = ring + s * D4_TILE;
+  #pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const uint32_t pa0 = pack_bf16(p[kk][0], p[kk][1]), pa2 = pack_bf16(p[kk][2], p[kk][3]);
+  #pragma unroll
+          for (int np = 0; np < 4; ++np) {
+            uint32_t v0, v1, v2, v3;
+            ldsm_x4_t(tile16(vb, 64, kk * 16 + (lane & 15), warp * 8 + np * 2 + (lane >> 4)), v0, v1, v2, v3);
+            mma16816(o[2 * np], pa0, 0u, pa2, 0u, v0, v1);
+            mma16816(o[2 * np + 1], pa0, 0u, pa2, 0u, v2, v3);
+          }
+        }
+        // same for the V slot: a store depending on every PV MMA's result first
+        if (lane == 0) {
+          float dep = 0.f;
+  #pragma unroll
+          for (int nt = 0; nt < 8; ++nt) dep += o[nt][0];
+          sSink[warp] = dep;
+        }
+        __syncwarp();
+        if (lane == 0) d3_arrive(empty0 + 8 * s);
+        ++t;
       }
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-    const float corr = (mx == -INFINITY) ? 1.f : exp2f(m_run - mx);
-    float ls = 0.f;
-    const float mxs = mx == -INFINITY ? 0.f : mx;  // all keys masked: every score is -inf
+      // ---- this warp's 64 dims of the item's result (MMA rows 0-7 = heads)
+      if (fold) {
+        float fa, fb;
+        d4_fold(FM, FL, m_run, l_run, fa, fb);
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt)
+        for (int nt = 0; nt < 8; ++nt) {
+          fo[nt][0] = __fmaf_rn(o[nt][0], fb, __fmul_rn(fo[nt][0], fa));
+          fo[nt][1] = __fmaf_rn(o[nt][1], fb, __fmul_rn(fo[nt][1], fa));
+        }
+      } else {  // one chunk of a multi-chunk row: unnormalised O and (m, l) to the workspace
+        float *part = ws + ((size_t)r * max_chunks + chunk) * DA_PART + g * (HEAD_DIM + 2);
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const float p = exp2_approx(sc[nt][e] - mxs);
-        sc[nt][e] = p;
-        ls += p;
+        for (int nt = 0; nt < 8; ++nt)
+          *reinterpret_cast<float2 *>(part + warp * 64 + nt * 8 + 2 * c) = make_float2(o[nt][0], o[nt][1]);
+        if (warp == 0 && c == 0) {
+          part[HEAD_DIM] = m_run;
+          part[HEAD_DIM + 1] = l_run;
+        }
       }
-    ls += __shfl_xor_sync(0xffffffffu, ls, 1);
-    ls += __shfl_xor_sync(0xffffffffu, ls, 2);
-    l_run = l_run * corr + ls;
-    m_run = mx;
-#pragma unroll
-    for (int nt = 0; nt < 32; ++nt) {
-      o[nt][0] *= corr;
-      o[nt][1] *= corr;
     }
-    // P rows 8..15 (padding) are zero
-    const uint32_t pa0 = pack_bf16(sc[0][0], sc[0][1]), pa2 = pack_bf16(sc[1][0], sc[1][1]);
+    if (fold) {
+      const float inv = 1.f / FL;
+      bf16 *orow = out + (size_t)r * Q_HEADS * HEAD_DIM + g * HEAD_DIM + warp * 64 + 2 * c;
 #pragma unroll
-    for (int np = 0; np < 16; ++np) {
-      uint32_t v0, v1, v2, v3;
-      ldsm_x4_t(tile16(vb, 64, vrow, np * 2 + (lane >> 4)), v0, v1, v2, v3);
-      mma16816(o[2 * np], pa0, 0u, pa2, 0u, v0, v1);
-      mma16816(o[2 * np + 1], pa0, 0u, pa2, 0u, v2, v3);
-    }
-    __syncthreads();  // stage s fully consumed
-    if (threadIdx.x == 0 && i + D3_STAGES < nblk) issue(i + D3_STAGES);
-  }
-  // ---- merge the 4 warps (stage memory reused) -> chunk result
-  float *sO = reinterpret_cast<float *>(smem + 4 * 16 * 128);   // [4][8][256]
-  float *sM = sO + 4 * 8 * HEAD_DIM;                             // [4][8] m, [4][8] l
-  const int g = lane >> 2;
-#pragma unroll
-  for (int nt = 0; nt < 32; ++nt)
-    *reinterpret_cast<float2 *>(sO + (warp * 8 + g) * HEAD_DIM + nt * 8 + (lane & 3) * 2) =
-        make_float2(o[nt][0], o[nt][1]);
-  if ((lane & 3) == 0) {
-    sM[warp * 8 + g] = m_run;
-    sM[32 + warp * 8 + g] = l_run;
-  }
-  __syncthreads();
-  bf16 *orow = out + (size_t)r * Q_HEADS * HEAD_DIM;
-  float *part = ws + ((size_t)r * max_chunks + chunk) * DA_PART;
-  for (int i = threadIdx.x; i < Q_HEADS * HEAD_DIM; i += 128) {
-    const int h = i >> 8, d = i & 255;
-    float M = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) M = fmaxf(M, sM[w * 8 + h]);
-    float acc = 0.f, L = 0.f;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      const float mw = sM[w * 8 + h];
-      if (mw == -INFINITY) continue;
-      const float e = exp2f(mw - M);
-      acc += sO[(w * 8 + h) * HEAD_DIM + d] * e;
-      L += sM[32 + w * 8 + h] * e;
-    }
-    if (n_chunks == 1) {
-      orow[i] = __float2bfloat16(acc / L);
-    } else {
-      part[h * (HEAD_DIM + 2) + d] = acc;
-      if (d == 0) {
-        part[h * (HEAD_DIM + 2) + HEAD_DIM] = M;
-        part[h * (HEAD_DIM + 2) + HEAD_DIM + 1] = L;
-      }
+      for (int nt = 0; nt < 8; ++nt)
+        *reinterpret_cast<__nv_bfloat162 *>(orow + nt * 8) =
+            __floats2bfloat162_rn(__fmul_rn(fo[nt][0], inv), __fmul_rn(fo[nt][1], inv));
     }
   }
 }
 
-// chunk merge: CTA = (row, head), thread = output dim; chunk order fixed
-__global__ void decode_merge3_kernel(const float *ws, bf16 *out, const int *pos, const int *active, int cb,
-                                     int max_chunks) {
+// Fold of a multi-chunk row's partials (chunk mode): CTA = (row, head), thread =
+// output dim; the same fold, in chunk order, as the in-register one of row mode, so
+// a row's result does not depend on which mode its batch ran in.
+__global__ void decode_fold_kernel(const float *ws, bf16 *out, const int *pos, const int *active, int cb_min,
+                                   int max_chunks) {
   pdl_trigger();
   pdl_wait();
   const int r = blockIdx.x, h = blockIdx.y, d = threadIdx.x;
   if (active && !active[r]) return;
   const int nb = (pos[r] + KV_BLOCK) / KV_BLOCK;
-  cb = decode_row_chunk(nb, cb);
+  const int cb = decode_row_chunk(nb, cb_min);
   const int n_chunks = (nb + cb - 1) / cb;
-  if (n_chunks == 1) return;  // written directly by the attention kernel
-  const float *base = ws + (size_t)r * max_chunks * DA_PART + h * (HEAD_DIM + 2);
-  __shared__ float wsh[64];
-  __shared__ float s_inv;
-  if (threadIdx.x < 32) {  // warp 0: chunk weights once (chunks <= 64)
-    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
-    const int c0 = threadIdx.x, c1 = threadIdx.x + 32;
-    if (c0 < n_chunks) { m0 = base[(size_t)c0 * DA_PART + HEAD_DIM]; l0 = base[(size_t)c0 * DA_PART + HEAD_DIM + 1]; }
-    if (c1 < n_chunks) { m1 = base[(size_t)c1 * DA_PART + HEAD_DIM]; l1 = base[(size_t)c1 * DA_PART + HEAD_DIM + 1]; }
-    const float M = warp_max(fmaxf(m0, m1));
-    const float w0 = c0 < n_chunks ? exp2f(m0 - M) : 0.f, w1 = c1 < n_chunks ? exp2f(m1 - M) : 0.f;
-    const float L = warp_sum(l0 * w0 + l1 * w1);
-    wsh[c0] = w0;
-    wsh[c1] = w1;
-    if (threadIdx.x == 0) s_inv = 1.f / L;
+  if (n_chunks == 1) return;  // written by the attention kernel
+  const float *pr = ws + (size_t)r * max_chunks * DA_PART + h * (HEAD_DIM + 2);
+  float M = -INFINITY, L = 0.f, acc = 0.f;
+  for (int c0 = 0; c0 < n_chunks; c0 += 8) {
+    float mc[8], lc[8], v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float *pc = pr + (size_t)min(c0 + j, n_chunks - 1) * DA_PART;
+      mc[j] = __ldcg(pc + HEAD_DIM);
+      lc[j] = __ldcg(pc + HEAD_DIM + 1);
+      v[j] = __ldcg(pc + d);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (c0 + j >= n_chunks) break;
+      float fa, fb;
+      d4_fold(M, L, mc[j], lc[j], fa, fb);
+      acc = __fmaf_rn(v[j], fb, __fmul_rn(acc, fa));
+    }
   }
-  __syncthreads();
-  float acc = 0.f;
-#pragma unroll 8
-  for (int c = 0; c < n_chunks; ++c) acc += base[(size_t)c * DA_PART + d] * wsh[c];  // chunk order
-  out[(size_t)r * Q_HEADS * HEAD_DIM + h * HEAD_DIM + d] = __float2bfloat16(acc * s_inv);
+  out[(size_t)r * Q_HEADS * HEAD_DIM + h * HEAD_DIM + d] = __float2bfloat16(__fmul_rn(acc, 1.f / L));
 }
 
 void decode_attention_v3(const CUtensorMap &kmap, const CUtensorMap &vmap, const bf16 *q, bf16 *out, const int *bt,
@@ -639,18 +726,32 @@ void decode_attention_v3(const CUtensorMap &kmap, const CUtensorMap &vmap, const
   if (rows <= 0) return;
   static bool attr = false;
   if (!attr) {
-    OXY_CUDA(cudaFuncSetAttribute(decode_attn_v3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)D3_SMEM));
+    OXY_CUDA(cudaFuncSetAttribute(decode_attn_v4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)D4_SMEM));
     attr = true;
   }
-  (void)sms;
+  static const int knob_grid = [] {  // A/B knob: CTAs of the persistent grid (0: 2 per SM)
+    const char *e = getenv("OXY_DA_GRID");
+    return e ? atoi(e) : 0;
+  }();
+  static const int knob_rows = [] {  // A/B knob: row mode from this many rows (0: default)
+    const char *e = getenv("OXY_DA_ROW_MODE_ROWS");
+    return e ? atoi(e) : 0;
+  }();
   const int cb = DECODE_CHUNK_BLOCKS;
   const int max_chunks = std::min(64, (max_blocks + cb - 1) / cb);
-  launch_pdl(decode_attn_v3_kernel, dim3(rows, max_chunks), dim3(128), D3_SMEM, st, kmap, vmap, q, bt, bt_stride,
-             pos, active, cb, max_chunks, scale * 1.4426950408889634f, ws, out);
-  if (max_chunks > 1)
-    launch_pdl(decode_merge3_kernel, dim3(rows, Q_HEADS), dim3(HEAD_DIM), 0, st, ws, out, pos, active, cb,
-               max_chunks);
+  // From a quarter of the SMs' worth of rows: whole rows per item, chunks folded in
+  // registers (no partials, no fold launch; 256 x 1024: 0.66 of HBM vs 0.50); fewer
+  // rows: chunk items for parallelism (6 rows: 16.6 vs 22 us), folded by
+  // decode_fold_kernel.  Both fold the same chunk partials in the same order, so the
+  // mode (a function of the batch) never changes a row's result.
+  const int row_mode = rows >= (knob_rows > 0 ? knob_rows : std::max(1, sms / 4)) ? 1 : 0;
+  const int n_items = row_mode ? rows : rows * max_chunks;
+  const int grid = std::min(n_items, knob_grid > 0 ? knob_grid : 2 * sms);
+  launch_pdl(decode_attn_v4_kernel, dim3(grid), dim3(D4_THREADS), D4_SMEM, st, kmap, vmap, q, bt, bt_stride, pos,
+             active, cb, max_chunks, n_items, row_mode, scale * 1.4426950408889634f, ws, out);
+  if (!row_mode && max_chunks > 1)
+    launch_pdl(decode_fold_kernel, dim3(rows, Q_HEADS), dim3(HEAD_DIM), 0, st, ws, out, pos, active, cb, max_chunks);
 }
 
 // ============================================================ no-cache recompute attention
@@ -772,7 +873,8 @@ extern "C" int oxy_paged_decode_attention(const void *q_d, void *out_d, const vo
                                           int32_t bt_stride, const int32_t *pos_d, int32_t rows,
                                           int32_t max_blocks, float *ws_d, void *stream) {
   OXY_API_BEGIN
-  OXY_REQUIRE(rows >= 1 && max_blocks >= 1 && bt_stride >= max_blocks && num_blocks >= 1,
+  OXY_REQUIRE(rows >= 1 && rows <= oxy::pi05::MAX_DECODE_ROWS_ABI && max_blocks >= 1 && bt_stride >= max_blocks &&
+                  num_blocks >= 1,
               "bad decode-attention shape");
   using oxy::pi05::bf16;
   int dev = 0, sms = 148;

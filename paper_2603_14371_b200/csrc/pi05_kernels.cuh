@@ -105,10 +105,13 @@ constexpr int DECODE_CHUNK_BLOCKS = 2;
 __host__ __device__ inline int decode_row_chunk(int nb, int cb_min) {
   return nb > 64 * cb_min ? (nb + 63) / 64 : cb_min;
 }
-// Paged decode attention: rows x 8 q-heads vs 1 KV head, keys [0, pos[r]].  TMA-fed
-// 3-stage ring over chunks of pool blocks + ordered chunk merge.
+// Paged decode attention: rows x 8 q-heads vs 1 KV head, keys [0, pos[r]].  A
+// persistent grid (<= 2 CTAs per SM) streams work items — whole rows, or (row,
+// chunk) pairs when there are too few rows to fill the SMs — through a TMA-fed ring;
+// chunk partials are folded in chunk order (in registers, or by a fold kernel).
 // kmap/vmap: 2-D tensor maps over one layer's K / V pool viewed as [num_blocks*64, 256]
 // (box 64 x 64, 128-byte swizzle; gemm::make_map).  ws: rows*max_blocks*8*(256+2) floats.
+constexpr int MAX_DECODE_ROWS_ABI = 8192;
 void decode_attention_v3(const CUtensorMap &kmap, const CUtensorMap &vmap, const bf16 *q, bf16 *out, const int *bt,
                          int bt_stride, const int *pos, const int *active, int rows, int max_blocks, float scale,
                          float *ws, int sms, cudaStream_t st);

@@ -373,6 +373,7 @@ struct Model {
     cudaFree(gemm_counters);
   }
   void init_exec() {
+
     // The action-expert lane gets the highest stream priority: its denoise is a
     // latency-bound chain of small kernels, the concurrent language decode is
     // bandwidth-bound and fills whatever SMs the chain leaves (OXY_LANE_PRIO=0: equal)

@@ -121,3 +121,23 @@ def test_bf16_epilogues_ragged(n, k, t, pad):
         gelu = 0.5 * g * (1 + torch.tanh(0.7978845608028654 * (g + 0.044715 * g ** 3)))
         torch.testing.assert_close(out[:, :n // 2].float(), gelu * u, rtol=2e-2, atol=2e-2)
         assert (out[:, n // 2:] == 0).all()
+
+
+@pytest.mark.parametrize("n,k,splits,mode", [(2560, 2048, 7, 1), (32768, 2048, 1, 3), (2048, 16384, 9, 0),
+                                             (2048, 2048, 2, 2), (1024, 4096, 16, 0)])
+def test_rows_independent_of_token_count(n, k, splits, mode):
+    """Batch invariance of the GEMM: with the K partition fixed (the model's
+    policy), a token row's output is bit-identical whether it is projected alone
+    or inside 12, 64, 96, 400 or 2400 rows (different token tiles, 1- and 2-CTA
+    kernels)."""
+    import torch
+    w = rand((n, k), 3, 0.02)
+    xs = rand((2400, k), 4)
+    base = None
+    for t in (1, 12, 64, 96, 400, 2400):
+        out, plan = run(w, xs[:t].contiguous(), mode, splits=splits)
+        row = out[:1].clone()
+        if base is None:
+            base = row
+        else:
+            assert torch.equal(row, base), (t, plan.tolist(), (row.float() - base.float()).abs().max().item())
