@@ -431,6 +431,10 @@ __global__ void __launch_bounds__(192, 1)
           }
         }
       }
+      // the (m, l) staging below reuses the P tile's bytes: every P row is dead once
+      // the last PV MMA retired (b_od), but order the softmax threads explicitly so the
+      // reuse does not rest on the tensor-core commit alone (compute-sanitizer racecheck)
+      asm volatile("bar.sync 3, 128;" ::: "memory");
       if (a.cmerge) {  // (m, l) next to the partial; peers read both after the cluster barrier
         reinterpret_cast<float2 *>(sm + OFF_P)[row] = make_float2(m_ref, l);
       } else {

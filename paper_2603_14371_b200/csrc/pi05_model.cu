@@ -307,7 +307,10 @@ struct Model {
     unsigned long long kernels = 0;  // kernel nodes, counted per replay
   };
   std::map<std::string, Graph> graphs;
-  bool use_graphs = true;
+  bool use_graphs = [] {  // OXY_GRAPHS=0: every call eager (sanitizer runs, debugging)
+    const char *e = getenv("OXY_GRAPHS");
+    return !e || atoi(e) != 0;
+  }();
 
   int *gemm_counters = nullptr;
   // profiling only: OXY_DBG_SKIP bitmask drops kernels from the denoise chain
