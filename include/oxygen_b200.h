@@ -54,6 +54,12 @@ int oxy_alloc_reserve(oxy_alloc *a, const int32_t *blocks_h, int32_t seq_len, in
                       int32_t *new_blocks_h, int32_t *cow_h);
 /* after the decode: keep ceil((seq_len+n_actual)/B) blocks, free the rest,
  * lower the tail watermark to what was written */
+/* blocks oxy_alloc_reserve(blocks_h, seq_len, n_new) would take from the free
+ * list right now (new tail blocks + a copy-on-write copy); allocates nothing.
+ * Admission control (paged.BlockAllocator) uses it to keep decode from ever
+ * running out of blocks for admitted requests. */
+int oxy_alloc_reserve_need(const oxy_alloc *a, const int32_t *blocks_h, int32_t seq_len, int32_t n_new,
+                           int32_t *need);
 int oxy_alloc_settle(oxy_alloc *a, const int32_t *blocks_h, int32_t seq_len,
                      int32_t n_reserved, int32_t n_actual, int32_t *n_blocks_out);
 int oxy_alloc_num_free(const oxy_alloc *a, int32_t *out);

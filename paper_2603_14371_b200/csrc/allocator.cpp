@@ -175,6 +175,19 @@ int oxy_alloc_reserve(oxy_alloc *a, const int32_t *blocks_h, int32_t seq_len, in
   OXY_API_END
 }
 
+int oxy_alloc_reserve_need(const oxy_alloc *a, const int32_t *blocks_h, int32_t seq_len, int32_t n_new,
+                           int32_t *need) {
+  OXY_API_BEGIN
+  OXY_REQUIRE(a != nullptr && need != nullptr, "null allocator handle");
+  OXY_REQUIRE(seq_len >= 1 && n_new >= 0, "reserve needs seq_len >= 1 and n_new >= 0");
+  const int32_t nb_old = a->blocks_for(seq_len), off = seq_len % a->bs;
+  const int32_t tail = blocks_h[nb_old - 1];
+  a->check_id(tail);
+  const bool cow = off != 0 && n_new > 0 && a->fill[tail] != off;
+  *need = a->blocks_for((int64_t)seq_len + n_new) - nb_old + (cow ? 1 : 0);
+  OXY_API_END
+}
+
 int oxy_alloc_settle(oxy_alloc *a, const int32_t *blocks_h, int32_t seq_len, int32_t n_reserved,
                      int32_t n_actual, int32_t *n_blocks_out) {
   OXY_API_BEGIN

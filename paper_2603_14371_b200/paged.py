@@ -28,11 +28,21 @@ __all__ = ["BlockAllocator", "PagedKvCache"]
 
 
 class BlockAllocator:
-    """Thin owner of an ``oxy_alloc``; all policy lives in C++."""
+    """Owner of an ``oxy_alloc`` (block policy in C++) plus admission control.
+
+    The reference checks capacity only when a request is stored and lets decode
+    grow caches freely (``kvweaver/kv_manager.py:195-238``).  A physical pool
+    must keep that promise: ``promise_budget`` sets aside, when a request is
+    admitted, every block its decode can still take (ceil((P + max_len) / B)
+    minus the prefix blocks, plus one copy-on-write copy of a shared tail), so
+    a decode of admitted requests never runs out of blocks; allocations that
+    are not covered by a promise (prefills, forks of a state) only use blocks
+    nobody was promised, and fail loudly (``MemoryError``) up front instead."""
 
     def __init__(self, num_blocks: int, block_size: int):
         self.num_blocks = int(num_blocks)
         self.block_size = int(block_size)
+        self.promised = 0
         h = C.c_void_p()
         _lib.call("oxy_alloc_create", C.c_int32(num_blocks), C.c_int32(block_size), C.byref(h))
         self._h = h
@@ -49,7 +59,24 @@ class BlockAllocator:
     def blocks_for(self, n: int) -> int:
         return -(-n // self.block_size)
 
+    def unpromised_free(self) -> int:
+        return self.num_free - self.promised
+
+    def promise_budget(self, kv, max_len: int) -> None:
+        """Admission: set aside the blocks ``kv``'s request can take while decoding
+        up to ``max_len`` tokens; the promise travels with the handle through decodes."""
+        n = self.blocks_for(kv.seq_len + max_len) - self.blocks_for(kv.seq_len) + 1
+        if n > self.unpromised_free():
+            raise MemoryError(f"KV pool capacity exceeded: admitting a request needs {n} blocks, "
+                              f"{self.unpromised_free()} free and not promised to live requests")
+        self.promised += n
+        kv.promise += n
+
     def alloc_seq(self, n_tokens: int) -> tuple[int, ...]:
+        if self.blocks_for(n_tokens) > self.unpromised_free():
+            raise MemoryError(f"KV pool out of blocks: a {n_tokens}-position prefix needs "
+                              f"{self.blocks_for(n_tokens)}, {self.unpromised_free()} free and not "
+                              f"promised to live requests")
         out = np.empty(self.blocks_for(n_tokens), np.int32)
         _lib.call("oxy_alloc_seq", self._h, C.c_int32(n_tokens), _lib.ptr_i32(out))
         return tuple(out.tolist())
@@ -93,21 +120,55 @@ class BlockAllocator:
                   _lib.ptr_i32(free), C.byref(n))
         return ref, fill, free[:n.value].copy()
 
+    def reserve_need(self, kv, n_new: int) -> int:
+        b = _lib.as_i32(kv.blocks)
+        need = C.c_int32()
+        _lib.call("oxy_alloc_reserve_need", self._h, _lib.ptr_i32(b), C.c_int32(kv.seq_len),
+                  C.c_int32(n_new), C.byref(need))
+        return need.value
+
     def reserve_rows(self, caches, n_new):
-        """``reserve`` for every row of a decode batch.  If any row fails (pool
-        out of blocks), the rows already reserved are rolled back — blocks,
-        copy-on-write copies and raised tail watermarks — before re-raising,
-        so a failed call leaves the allocator exactly as it found it."""
-        tables, cows = [], []
+        """``reserve`` for every row of a decode batch.  A row draws first on its
+        handle's promise (the first row of a handle; forks of one state draw on
+        the unpromised free blocks only); a row needing more than that plus the
+        unpromised free blocks fails up front (``MemoryError``).  On any failure
+        the rows already reserved are rolled back — blocks, copy-on-write copies
+        and raised tail watermarks — so a failed call leaves the allocator as it
+        found it.  Returns the tables, copy-on-write triples and the promised
+        blocks each row drew on (``carry_promises`` settles them after the call)."""
+        tables, cows, drawn = [], [], []
+        seen, pending = set(), 0  # handles whose promise is taken; promised blocks drawn so far
         try:
             for kv, n in zip(caches, n_new):
+                need = self.reserve_need(kv, n)
+                own = kv.promise if id(kv) not in seen else 0
+                seen.add(id(kv))
+                use = min(own, need)
+                spare = self.num_free - (self.promised - pending)
+                if need - use > spare:
+                    raise MemoryError(f"KV pool out of blocks: a decode row needs {need} blocks, "
+                                      f"{use} of them admitted, {spare} free and not promised")
                 t, c = self.reserve(kv.blocks, kv.seq_len, n)
+                pending += use
                 tables.append(t)
                 cows.append(c)
+                drawn.append(use)
         except BaseException:
             self.unreserve(tables, [kv.seq_len for kv in caches], n_new)
             raise
-        return tables, cows
+        return tables, cows, drawn
+
+    def carry_promises(self, olds, news, drawn) -> None:
+        """After a decode: the blocks a row kept (new tail blocks, a copy-on-write
+        copy) come out of its promise; the rest of the promise moves to the row's
+        new handle."""
+        for old, new, d in zip(olds, news, drawn):
+            n_old = len(old.blocks)
+            kept = len(new.blocks) - n_old + (1 if new.blocks[n_old - 1] != old.blocks[-1] else 0)
+            use = min(d, max(0, kept))
+            self.promised -= use
+            new.promise += old.promise - use
+            old.promise = 0
 
     def unreserve(self, tables, seq_lens, n_new) -> None:
         """Undo ``reserve`` for rows that wrote nothing: settle at zero new
@@ -130,18 +191,26 @@ class PagedKvCache:
     lazily from HBM as read-only float64 ``KvLayer``s) and value equality.
     Dropping the last reference returns the blocks to the pool."""
 
-    __slots__ = ("owner", "blocks", "seq_len", "backend_tag", "__weakref__")
+    __slots__ = ("owner", "blocks", "seq_len", "backend_tag", "promise", "__weakref__")
 
     def __init__(self, owner, blocks: tuple, seq_len: int):
         self.owner = owner
         self.blocks = tuple(blocks)
         self.seq_len = int(seq_len)
         self.backend_tag = owner.backend_tag
+        self.promise = 0  # blocks set aside for this handle's request (BlockAllocator.promise_budget)
+
+    def share(self) -> "PagedKvCache":
+        """A second handle on the same blocks (refcounted): one per request when
+        several language tasks start from one observation's prefix."""
+        self.owner.allocator.incref(self.blocks)
+        return PagedKvCache(self.owner, self.blocks, self.seq_len)
 
     def __del__(self):
         owner = getattr(self, "owner", None)
         if owner is not None and self.blocks:
             try:
+                owner.allocator.promised -= self.promise  # the request is gone
                 owner.allocator.decref(self.blocks)
             except Exception:
                 pass

@@ -352,7 +352,7 @@ class Pi05Backend(PricedBackend):
             budgets.append(left if left > 0 else _BIG_BUDGET)
             reserved.append(min(k, left) if left > 0 else k)
             lasts.append(toks[-1] if toks else c.eos_token)
-        tables, cows = self.allocator.reserve_rows(caches, reserved)
+        tables, cows, drawn = self.allocator.reserve_rows(caches, reserved)
         maxb = max(len(t) for t in tables)
         bt = np.zeros((m, maxb), np.int32)
         for i, tb in enumerate(tables):
@@ -382,6 +382,7 @@ class Pi05Backend(PricedBackend):
             bufs.append(toks)
             flags.append(bool(adv and (toks[-1] == c.eos_token
                                        or len(toks) == batched.max_lens[i])))
+        self.allocator.carry_promises(caches, new_caches, drawn)
         res = BatchedState(tuple(new_caches), tuple(bufs), tuple(flags), batched.request_ids,
                            batched.max_lens, batched.created_frames)
         return (res, logits) if return_logits else res

@@ -181,7 +181,7 @@ class ToyBackend(PricedBackend):
             budgets.append(left if left > 0 else _BIG_BUDGET)
             reserved.append(min(k, left) if left > 0 else k)
             lasts.append(toks[-1] if toks else c.eos_token)
-        tables, cows = self.allocator.reserve_rows(caches, reserved)
+        tables, cows, drawn = self.allocator.reserve_rows(caches, reserved)
         maxb = max(len(t) for t in tables)
         bt = np.zeros((m, maxb), np.int32)
         for i, t in enumerate(tables):
@@ -207,5 +207,6 @@ class ToyBackend(PricedBackend):
             toks = batched.token_buffers[i] + tuple(int(t) for t in out[i, :adv])
             bufs.append(toks)
             flags.append(bool(adv and (toks[-1] == c.eos_token or len(toks) == batched.max_lens[i])))
+        self.allocator.carry_promises(caches, new_caches, drawn)
         return BatchedState(tuple(new_caches), tuple(bufs), tuple(flags), batched.request_ids,
                             batched.max_lens, batched.created_frames)

@@ -129,3 +129,54 @@ def test_random_walks_bit_exact(seed):
         r.decref(blocks)
     _same_state(a, r)
     assert a.num_free == nb
+
+
+class _Owner:
+    """Minimal backend stand-in for PagedKvCache on the CPU (allocator only)."""
+    backend_tag = "alloc-test"
+    num_layers = 1
+
+    def __init__(self, num_blocks, block_size):
+        from paper_2603_14371_b200.paged import BlockAllocator
+        self.allocator = BlockAllocator(num_blocks, block_size)
+
+
+def _decode(owner, handles, n_new, n_written):
+    """What a backend's batched decode does around its kernel: reserve -> settle -> carry."""
+    from paper_2603_14371_b200.paged import PagedKvCache
+    a = owner.allocator
+    tables, cows, drawn = a.reserve_rows(handles, n_new)
+    news = [PagedKvCache(owner, a.settle(t, h.seq_len, n, w), h.seq_len + w)
+            for t, h, n, w in zip(tables, handles, n_new, n_written)]
+    a.carry_promises(handles, news, drawn)
+    return news
+
+
+def test_admission_budget_keeps_decode_from_running_out():
+    """The reference checks capacity only at store (kvweaver/kv_manager.py:195-238)
+    and decode growth never fails.  Admission sets aside every block a request's
+    decode can take; allocations without a promise only use unpromised blocks and
+    fail up front, leaving the allocator untouched."""
+    from paper_2603_14371_b200.paged import PagedKvCache
+    owner = _Owner(10, 4)
+    a = owner.allocator
+    h = PagedKvCache(owner, a.alloc_seq(6), 6)            # 2 blocks, tail holds 2 of 4 slots
+    a.promise_budget(h, 10)                                # ceil(16/4) - 2 + 1 copy-on-write = 3
+    assert a.promised == 3 and a.unpromised_free() == 5
+    with pytest.raises(MemoryError, match="not promised"):
+        a.alloc_seq(24)                                    # 6 blocks > 5 unpromised
+    [h2] = _decode(owner, [h], [4], [4])                   # 1 new block, drawn from the promise
+    assert h2.seq_len == 10 and len(h2.blocks) == 3 and h2.promise == 2 and a.promised == 2
+    filler = PagedKvCache(owner, a.alloc_seq(20), 20)     # every unpromised block taken
+    assert a.unpromised_free() == 0 and a.num_free == 2
+    snap = a.snapshot()
+    with pytest.raises(MemoryError, match="decode row"):
+        _decode(owner, [h], [4], [4])                      # a fork of the old state: no promise left
+    for x, y in zip(snap, a.snapshot()):
+        assert np.array_equal(x, y)
+    [h3] = _decode(owner, [h2], [6], [6])                  # the admitted request still grows
+    assert h3.seq_len == 16 and a.num_free == 1 and a.promised == h3.promise == 1
+    del h, h2, h3, filler
+    import gc
+    gc.collect()
+    assert a.promised == 0 and a.num_free == 10

@@ -367,3 +367,27 @@ def test_recompute_logits_matches_cached_decode(tiny):
         assert int(np.argmax(want)) == t or np.sort(want)[-1] - np.sort(want)[-2] < 2 * np.abs(got - want).max()
         seq.append(t)
     assert len(toks) >= 1
+
+
+def test_pool_exhaustion_fails_at_admission_not_in_decode():
+    """With a pool too small for every arrival's full decode, the frame that cannot
+    be covered fails while admitting (its prefix or its decode budget does not fit
+    in the blocks not promised to live requests); the decodes of requests already
+    admitted never run out of blocks."""
+    from paper_2603_14371_b200 import Arrival, KvManager
+    from paper_2603_14371_b200.pi05 import TINY, Pi05Backend
+    from paper_2603_14371_b200.scheduler import run_frame_unified
+    be = Pi05Backend(TINY, num_blocks=12)
+    mgr = KvManager()
+    admitted_frames = 0
+    with pytest.raises(MemoryError, match="not promised"):
+        for t in range(40):
+            run_frame_unified(t, [Arrival(t, _obs(0, tuple(range(3, 63)), seed=t), 200)], mgr, be, 8, 30.0)
+            admitted_frames += 1
+    assert admitted_frames >= 2
+    # the live requests keep decoding to their budgets without touching the limit
+    for t in range(40, 80):
+        if not mgr.active_ids():
+            break
+        run_frame_unified(t, [], mgr, be, 8, 30.0)
+    assert be.allocator.promised >= 0
