@@ -330,8 +330,55 @@ __device__ __forceinline__ void stage_store_bf16(float *stg, const float (&y)[16
 // compiler cannot prove the outputs do not alias the operands, so a
 // load-after-store per token serialised the epilogue on L2 latency, and one
 // divergent region per token cost ~1 us per 16-token chunk (tools/gemm_prof.py).
-template <int MODE, typename P>
-__device__ __forceinline__ void epi_loop(const P &p, uint32_t trow, int c_begin, int c_end, int n0, int f, int split,
+// Accumulator sources of epi_loop: src(c, nv, v) fills v[0..16) with the fp32
+// accumulators (as bits) of tile columns c..c+15 of this thread's feature
+// (entries >= nv are don't-care).  TmemSrc is warp-collective.
+struct TmemSrc {
+  uint32_t trow;
+  __device__ __forceinline__ void operator()(int c, int, uint32_t (&v)[16]) const { tmem_ld16(trow + (uint32_t)c, v); }
+};
+
+// Cluster split-K: the sum of the S split partials ws[s, t, f] in split order
+// 0..S-1 (the order every other reduction path uses).  The loads of one round
+// are all issued before any add; the round shape follows the chunk width so a
+// slice of T/S tokens costs one L2 round trip whatever S is.
+struct SplitSumSrc {
+  const float *ws;
+  int splits, t, n_out, n0, f;
+  bool fok;
+  template <int J, int U>
+  __device__ __forceinline__ void rounds(int t0, int nv, float (&a)[16]) const {
+    for (int s0 = 0; s0 < splits; s0 += U) {
+      float v[U][J];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int j = 0; j < J; ++j)
+          v[u][j] = (fok && j < nv && s0 + u < splits)
+                        ? __ldcg(ws + ((size_t)(s0 + u) * t + t0 + j) * n_out + f)
+                        : 0.f;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int j = 0; j < J; ++j)
+          if (s0 + u < splits) a[j] = __fadd_rn(a[j], v[u][j]);
+    }
+  }
+  __device__ __forceinline__ void operator()(int c, int nv, uint32_t (&v)[16]) const {
+    float a[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) a[j] = 0.f;
+    const int t0 = n0 + c;
+    if (nv <= 4) rounds<4, 8>(t0, nv, a);
+    else if (nv <= 8) rounds<8, 4>(t0, nv, a);
+    else rounds<16, 2>(t0, nv, a);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(a[j]);
+  }
+};
+
+template <int MODE, typename P, typename SRC>
+__device__ __forceinline__ void epi_loop(const P &p, const SRC &src, int c_begin, int c_end, int n0, int f, int split,
                                          float *stg = nullptr) {
   const bool fok = f < p.n_out;
   const EpiParams &e = p.epi;
@@ -341,9 +388,10 @@ __device__ __forceinline__ void epi_loop(const P &p, uint32_t trow, int c_begin,
     const bool kv = (f >> 8) >= 8;  // k / v head rows: routed through the slot table
     for (int c = c_begin; c < c_end; c += 16) {
       uint32_t v[16];
-      tmem_ld16(trow + (uint32_t)c, v);
       const int t0 = n0 + c;
-      const int nv = fok ? max(0, min(16, p.t - t0)) : 0;
+      const int nvt = max(0, min(min(16, c_end - c), p.t - t0));  // valid tokens of the chunk
+      const int nv = fok ? nvt : 0;
+      src(c, nv, v);
       int pos[16], sl[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
@@ -372,7 +420,6 @@ __device__ __forceinline__ void epi_loop(const P &p, uint32_t trow, int c_begin,
           const float pair = __shfl_xor_sync(0xffffffffu, acc, 1);
           y[j] = rope_rot(second, acc, pair, csn[j].x, csn[j].y);
         }
-        const int nvt = max(0, min(16, p.t - t0));
         const int i0 = ((f - (threadIdx.x & 31)) & 255) >> 1;
         stage_store_bf16<2>(stg, y, nvt, r.q_out + (size_t)t0 * 2048 + hd * 256 + i0, 2048, 0);
         continue;
@@ -390,9 +437,10 @@ __device__ __forceinline__ void epi_loop(const P &p, uint32_t trow, int c_begin,
     const float gate = (MODE == EPI_ADD_GATED_F32 && fok) ? __ldg(e.gate + f) : 0.f;
     for (int c = c_begin; c < c_end; c += 16) {
       uint32_t v[16];
-      tmem_ld16(trow + (uint32_t)c, v);
       const int t0 = n0 + c;
-      const int nv = fok ? max(0, min(16, p.t - t0)) : 0;
+      const int nvt = max(0, min(min(16, c_end - c), p.t - t0));  // valid tokens of the chunk
+      const int nv = fok ? nvt : 0;
+      src(c, nv, v);
       if constexpr (MODE < 0) {
         float *dst = p.ws + ((size_t)split * p.t + t0) * p.n_out + f;
         const size_t ld = p.n_out;
@@ -443,7 +491,6 @@ __device__ __forceinline__ void epi_loop(const P &p, uint32_t trow, int c_begin,
             y[j] = acc;
           }
         }
-        const int nvt = max(0, min(16, p.t - t0));
         __nv_bfloat16 *o = static_cast<__nv_bfloat16 *>(e.out) + (size_t)t0 * e.ldo;
         if constexpr (MODE == EPI_GEGLU_BF16)
           stage_store_bf16<1>(stg, y, nvt, o + (f0 >> 1), e.ldo, (p.n_out - f0) >> 1);
@@ -485,22 +532,27 @@ __device__ __forceinline__ void epi_loop(const P &p, uint32_t trow, int c_begin,
 }
 
 // the mode switch sits outside the column loop: one tight loop per epilogue.
-// Columns [c_begin, c_end) of the tile (multiples of 16).
+// Columns [c_begin, c_end) of the tile (chunks of 16 from c_begin).
+template <typename P, typename SRC>
+__device__ __forceinline__ void epi_tile_src(const P &p, const SRC &src, int c_begin, int c_end, int n0, int f,
+                                             int split, bool split_out, float *stg = nullptr) {
+  switch (split_out ? -1 : p.epi.mode) {
+    case -1: epi_loop<-1>(p, src, c_begin, c_end, n0, f, split); break;
+    case EPI_F32: epi_loop<EPI_F32>(p, src, c_begin, c_end, n0, f, split, stg); break;
+    case EPI_BF16: epi_loop<EPI_BF16>(p, src, c_begin, c_end, n0, f, split, stg); break;
+    case EPI_ADD_F32: epi_loop<EPI_ADD_F32>(p, src, c_begin, c_end, n0, f, split, stg); break;
+    case EPI_GEGLU_BF16: epi_loop<EPI_GEGLU_BF16>(p, src, c_begin, c_end, n0, f, split, stg); break;
+    case EPI_GELU_BF16: epi_loop<EPI_GELU_BF16>(p, src, c_begin, c_end, n0, f, split, stg); break;
+    case EPI_ADD_BF16: epi_loop<EPI_ADD_BF16>(p, src, c_begin, c_end, n0, f, split, stg); break;
+    case EPI_ADD_GATED_F32: epi_loop<EPI_ADD_GATED_F32>(p, src, c_begin, c_end, n0, f, split, stg); break;
+    case EPI_SWISH_BF16: epi_loop<EPI_SWISH_BF16>(p, src, c_begin, c_end, n0, f, split, stg); break;
+    case EPI_QKV_ROPE: epi_loop<EPI_QKV_ROPE>(p, src, c_begin, c_end, n0, f, split, stg); break;
+  }
+}
 template <typename P>
 __device__ __forceinline__ void epi_tile(const P &p, uint32_t trow, int c_begin, int c_end, int n0, int f, int split,
                                          bool split_out, float *stg = nullptr) {
-  switch (split_out ? -1 : p.epi.mode) {
-    case -1: epi_loop<-1>(p, trow, c_begin, c_end, n0, f, split); break;
-    case EPI_F32: epi_loop<EPI_F32>(p, trow, c_begin, c_end, n0, f, split, stg); break;
-    case EPI_BF16: epi_loop<EPI_BF16>(p, trow, c_begin, c_end, n0, f, split, stg); break;
-    case EPI_ADD_F32: epi_loop<EPI_ADD_F32>(p, trow, c_begin, c_end, n0, f, split, stg); break;
-    case EPI_GEGLU_BF16: epi_loop<EPI_GEGLU_BF16>(p, trow, c_begin, c_end, n0, f, split, stg); break;
-    case EPI_GELU_BF16: epi_loop<EPI_GELU_BF16>(p, trow, c_begin, c_end, n0, f, split, stg); break;
-    case EPI_ADD_BF16: epi_loop<EPI_ADD_BF16>(p, trow, c_begin, c_end, n0, f, split, stg); break;
-    case EPI_ADD_GATED_F32: epi_loop<EPI_ADD_GATED_F32>(p, trow, c_begin, c_end, n0, f, split, stg); break;
-    case EPI_SWISH_BF16: epi_loop<EPI_SWISH_BF16>(p, trow, c_begin, c_end, n0, f, split, stg); break;
-    case EPI_QKV_ROPE: epi_loop<EPI_QKV_ROPE>(p, trow, c_begin, c_end, n0, f, split, stg); break;
-  }
+  epi_tile_src(p, TmemSrc{trow}, c_begin, c_end, n0, f, split, split_out, stg);
 }
 
 // Deterministic split-K fix-up, run by the epilogue warps (named barrier 1 over

@@ -25,7 +25,73 @@ struct KParams {
   int fixup;      // 1: last-arriving split CTA reduces; 0: separate reduce kernel
   int prefetch;   // 1: issue the first ring of weight tiles before griddepcontrol.wait
   int trigger;    // 1: launch_dependents once all operand loads are issued
+  int csk;        // 1: cluster split-K — the split CTAs of a tile are one cluster (along z)
 };
+
+// One residual row's RMSNorm / adaRMSNorm by one warp (NormFuse): lane l owns
+// float4 columns l, l + 32, ...; the sum of squares runs in that fixed order and
+// then a fixed butterfly, so the fused tail and rownorm_kernel agree bit for bit.
+constexpr int NORM_MAX_V4 = 16;  // rows of up to 2048 features
+constexpr int NORM_V4_PASS = 8;  // float4 per lane held at once (register budget of gemm_kernel)
+__device__ __forceinline__ void warp_rownorm(const float *xrow, int n, const NormFuse &nf, __nv_bfloat16 *yrow) {
+  const int lane = threadIdx.x & 31, nv4 = n >> 7;
+  const float4 *xr = reinterpret_cast<const float4 *>(xrow);
+  float ss = 0.f;
+  for (int i0 = 0; i0 < nv4; i0 += NORM_V4_PASS) {
+    float4 xv[NORM_V4_PASS];
+#pragma unroll
+    for (int i = 0; i < NORM_V4_PASS; ++i)
+      if (i0 + i < nv4) xv[i] = __ldcg(xr + (i0 + i) * 32 + lane);
+#pragma unroll
+    for (int i = 0; i < NORM_V4_PASS; ++i)
+      if (i0 + i < nv4) {
+        ss = __fmaf_rn(xv[i].x, xv[i].x, ss);
+        ss = __fmaf_rn(xv[i].y, xv[i].y, ss);
+        ss = __fmaf_rn(xv[i].z, xv[i].z, ss);
+        ss = __fmaf_rn(xv[i].w, xv[i].w, ss);
+      }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss = __fadd_rn(ss, __shfl_xor_sync(0xffffffffu, ss, o));
+  const float inv = rsqrtf(__fadd_rn(__fdiv_rn(ss, (float)n), nf.eps));
+#pragma unroll 4
+  for (int i = 0; i < nv4; ++i) {
+    const int c = (i * 32 + lane) * 4;
+    const float4 x4 = __ldcg(xr + i * 32 + lane);
+    float o[4] = {x4.x, x4.y, x4.z, x4.w};
+    if (nf.w) {
+      const float4 w = __ldg(reinterpret_cast<const float4 *>(nf.w + c));
+      const float wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) o[k] = __fmul_rn(__fmul_rn(o[k], inv), __fadd_rn(1.f, wv[k]));
+    } else {
+      const float4 a = __ldg(reinterpret_cast<const float4 *>(nf.ms + c));
+      const float4 b = __ldg(reinterpret_cast<const float4 *>(nf.mb + c));
+      const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) o[k] = __fadd_rn(__fmul_rn(__fmul_rn(o[k], inv), __fadd_rn(1.f, av[k])), bv[k]);
+    }
+    __nv_bfloat162 h0 = __floats2bfloat162_rn(o[0], o[1]), h1 = __floats2bfloat162_rn(o[2], o[3]);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t *>(&h0);
+    u.y = *reinterpret_cast<uint32_t *>(&h1);
+    *reinterpret_cast<uint2 *>(yrow + c) = u;
+  }
+}
+
+__global__ void __launch_bounds__(256) rownorm_kernel(const float *x, int ldx, int t, int n, NormFuse nf) {
+  pdl_trigger();
+  pdl_wait();
+  const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (r < t) warp_rownorm(x + (size_t)r * ldx, n, nf, nf.y + (size_t)r * nf.ldy);
+}
+
+void rownorm(const float *x, int ldx, int t, int n, const NormFuse &nf, cudaStream_t st) {
+  if (t <= 0) return;
+  if (n % 128 != 0 || n > 128 * NORM_MAX_V4 || ldx % 4 != 0 || nf.ldy % 4 != 0)
+    fail(OXY_EINVAL, "row norm: rows of 128..2048 features (multiple of 128), strides multiple of 4");
+  launch_pdl(rownorm_kernel, dim3((t + 7) / 8), dim3(256), 0, st, x, ldx, t, n, nf);
+}
 
 // Launch-time knobs (env, read once): OXY_SPLITK=fixup|kernel, OXY_PDL=0|1,
 // OXY_GEMM_SMEM_KB=<per-CTA smem budget>.  Used for A/B measurements.
@@ -153,7 +219,11 @@ __device__ int g_gemm_prof_sel[2];
   } while (0)
 #endif
 
-__global__ void __launch_bounds__(192, 2)
+// 128 registers: two CTAs per SM still leave register room for the next
+// kernel's early (PDL) CTAs and the other lane's kernels (168 registers, the
+// compiler's free choice with the cluster split-K tail, filled the register file
+// and serialised the chain)
+__global__ void __maxnreg__(128)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 KParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -249,9 +319,12 @@ __global__ void __launch_bounds__(192, 2)
       GPROF(6);
     }
     __syncwarp();
-  } else {
-    const int q = warp & 3;
-    const int f = m0 + q * 32 + lane;
+  }
+  const int q = warp & 3;
+  const int f = m0 + q * 32 + lane;
+  // the operand ring is idle once `done` fired: 4 x 2.3 KB transpose tiles for the bf16 epilogues
+  float *stg = reinterpret_cast<float *>(sA) + q * (16 * STG_LD);
+  if (warp >= 2) {
     const bool split_out = p.splits > 1;
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
     pdl_wait();  // the epilogue reads bias/residual/gates and writes outputs
@@ -259,8 +332,6 @@ __global__ void __launch_bounds__(192, 2)
     mbar_wait(done, 0);
     tc_fence_after();
     if (threadIdx.x == 64) GPROF(8);
-    // the operand ring is idle once `done` fired: 4 x 2.3 KB transpose tiles for the bf16 epilogues
-    float *stg = reinterpret_cast<float *>(sA) + q * (16 * STG_LD);
 #ifdef OXY_GEMM_PROF
     if (bn > 32) {
       epi_tile(p, trow, 0, 16, n0, f, split, split_out, stg);
@@ -273,6 +344,49 @@ __global__ void __launch_bounds__(192, 2)
     epi_tile(p, trow, 0, bn, n0, f, split, split_out, stg);
     if (threadIdx.x == 64) GPROF(9);
     if (split_out && p.fixup) splitk_fixup(p, blockIdx.y * gridDim.x + blockIdx.x, n0, 0, bn, f, s_last, 128, 64);
+  }
+  if (p.csk) {
+    // Cluster split-K: every split CTA of this tile is in the cluster.  Once all
+    // partials are stored, CTA r reduces token slice r of the tile (split order
+    // 0..S-1) and runs the real epilogue on it — no reduce launch.
+    __syncwarp();
+    cluster_sync_all();
+    if (threadIdx.x == 64) GPROF(13);
+    const int valid = min(bn, p.t - n0);
+    const int per = (valid + p.splits - 1) / p.splits;
+    const int cb = min(valid, split * per), ce = min(valid, cb + per);
+    if (warp >= 2 && cb < ce)
+      epi_tile_src(p, SplitSumSrc{p.ws, p.splits, p.t, p.n_out, n0, f, f < p.n_out}, cb, ce, n0, f, split, false,
+                   stg);
+    if (threadIdx.x == 64) GPROF(14);
+    if (p.epi.norm.y) {
+      // Residual RMSNorm: the last cluster to finish (a grid-wide arrival count,
+      // kept by cluster rank 0) normalises every row.  Each thread's fence plus
+      // the cluster barrier order its residual stores before rank 0's release.
+      __shared__ int s_norm_last;
+      __threadfence();
+      __syncwarp();
+      cluster_sync_all();
+      if (split == 0 && threadIdx.x == 64) {
+        int old;
+        int *ctr = p.counters + (MAX_TILES - 1);
+        asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(ctr) : "memory");
+        const int last = old == (int)(gridDim.x * gridDim.y) - 1;
+        if (last) *ctr = 0;  // self-resetting for the next launch on this lane
+        s_norm_last = last;
+      }
+      cluster_sync_all();
+      int last;
+      asm volatile("ld.shared::cluster.b32 %0, [%1];" : "=r"(last) : "r"(map_to_rank(smem_u32(&s_norm_last), 0)));
+      if (last) {
+        const int nw = blockDim.x >> 5;
+        for (int r = split * nw + warp; r < p.t; r += p.splits * nw)
+          warp_rownorm(static_cast<const float *>(p.epi.out) + (size_t)r * p.epi.ldo, p.n_out, p.epi.norm,
+                       p.epi.norm.y + (size_t)r * p.epi.norm.ldy);
+      }
+      if (threadIdx.x == 64) GPROF(15);
+      cluster_sync_all();  // rank 0's flag is read by the peers before it exits
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -793,7 +907,24 @@ void launch(const void *w, const void *x, int n_out, int k, int t, const EpiPara
   kp.fixup = knobs().fixup;
   kp.prefetch = kp.trigger = t <= 64 ? (g_early_override >= 0 ? g_early_override : knobs().early_skinny)
                                      : knobs().early_wide;
+  kp.csk = plan.csk && plan.splits > 1;
+  if (epi.norm.y && !(kp.csk && t <= NORM_FUSE_MAX_T && (epi.mode == EPI_ADD_F32 || epi.mode == EPI_ADD_GATED_F32)))
+    fail(OXY_EINVAL, "fused row norm needs a cluster split-K residual GEMM of <= %d rows", NORM_FUSE_MAX_T);
+  if (epi.norm.y && (n_out % 128 != 0 || n_out > 128 * NORM_MAX_V4 || epi.ldo % 4 != 0 || epi.norm.ldy % 4 != 0))
+    fail(OXY_EINVAL, "fused row norm: rows of 128..2048 features (multiple of 128), strides multiple of 4");
   dim3 grid(plan.n_tiles, plan.m_tiles, plan.splits);
+  if (kp.csk) {
+    if (plan.splits > CSK_MAX) fail(OXY_EINVAL, "cluster split-K: at most %d splits", CSK_MAX);
+    static bool np_set = false;
+    if (!np_set) {
+      OXY_CUDA(cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      np_set = true;
+    }
+    ++g_plan_counts[PC_CSK];
+    if (epi.norm.y) ++g_plan_counts[PC_CSK_NORM];
+    launch_pdl_cluster(gemm_kernel, grid, dim3(192), smem_bytes(plan), st, dim3(1, 1, plan.splits), ma, mb, kp);
+    return;
+  }
   if (knobs().pdl) {
     launch_pdl(gemm_kernel, grid, dim3(192), smem_bytes(plan), st, ma, mb, kp);
   } else {

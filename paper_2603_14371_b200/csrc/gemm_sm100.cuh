@@ -52,6 +52,18 @@ struct QkvRope {
   __nv_bfloat16 *k_dst, *v_dst;  // pool layer base (slot rows) or dense [T, 256]
 };
 
+// RMSNorm / adaRMSNorm of the finished residual rows, fused into a cluster
+// split-K GEMM with an EPI_ADD_F32 / EPI_ADD_GATED_F32 epilogue (y != null):
+//   y[t, :] = bf16( x * rsqrt(mean(x^2) + eps) * (1 + w) )            (w != null)
+//           = bf16( x * rsqrt(mean(x^2) + eps) * (1 + ms) + mb )      (adaRMS)
+// over the whole row x[t, 0..N) (x = the epilogue's out, N = n_out).
+struct NormFuse {
+  __nv_bfloat16 *y = nullptr;
+  int ldy = 0;
+  const float *w = nullptr, *ms = nullptr, *mb = nullptr;
+  float eps = 1e-6f;
+};
+
 struct EpiParams {
   int mode;
   void *out;
@@ -61,7 +73,14 @@ struct EpiParams {
   int ldr;
   const float *gate;    // EPI_ADD_GATED_F32 per-feature gate [N]
   QkvRope rope;         // EPI_QKV_ROPE
+  NormFuse norm{};      // cluster split-K residual modes only
 };
+
+// The row norm of NormFuse as a stand-alone kernel (one warp per row), bit-identical
+// to the fused one: used when the rows are too many for the fused tail.
+void rownorm(const float *x, int ldx, int t, int n, const NormFuse &nf, cudaStream_t st);
+constexpr int NORM_FUSE_MAX_T = 64;  // rows the last cluster normalises in-kernel
+constexpr int CSK_MAX = 16;          // cluster split-K: splits per cluster (non-portable above 8)
 
 // Row permutation that puts rotary pair (i, i + 128) of every q/k head at rows
 // (2i, 2i + 1): new row -> canonical row.  V rows (f >= 2304) are unchanged.
@@ -84,6 +103,7 @@ struct Plan {
   int cg;  // 0: one-tile-per-CTA kernel (skinny); 1 / 2: persistent wide kernel, 1-CTA / CTA-pair tiles
   int cl;  // wide kernel: CTA pairs per cluster sharing (multicasting) the weight tile (1 or 2)
   int band;  // prefill token-tile band applied: 0 none, 1 deep-K, 2 mid-K
+  int csk;   // 1: the split CTAs of a tile form one cluster and reduce in-kernel (no reduce launch)
 };
 
 // Plan classes counted at enqueue time (eager runs and graph captures; replays are
@@ -99,6 +119,8 @@ enum PlanClass {
   PC_ATTN_CMERGE,     // tcgen05 attention, key splits merged over a cluster
   PC_ATTN_WSMERGE,    // tcgen05 attention, key splits merged through the workspace
   PC_ATTN_ONE,        // tcgen05 attention, one split
+  PC_CSK,             // gemm_kernel, cluster split-K (in-kernel reduction)
+  PC_CSK_NORM,        // ... with the residual RMSNorm fused into the last cluster
   PC_COUNT
 };
 extern long long g_plan_counts[PC_COUNT];

@@ -503,8 +503,21 @@ struct Model {
     PhaseScope(Model &mm, int ph) : m(mm), prev(mm.phase) { m.phase = ph; }
     ~PhaseScope() { m.phase = prev; }
   };
+  // Cluster split-K (gemm_sm100.cu) for the decode / denoise chains: the split
+  // reduction (and a residual projection's RMSNorm) run inside the GEMM instead of
+  // a reduce launch.  Bit-identical to the reduce kernels, so the choice may vary.
+  // Off by default: measured slower in the chain (denoise 10.1 -> 17.1 ms per
+  // frame; the in-kernel slice reduce + epilogue costs ~4.5 us of dependent L2
+  // round trips after the cluster barrier, against ~2-3 us for the PDL-overlapped
+  // reduce launch; profiles/r02_csk.md).  OXY_CSK=1 turns it on (A/B).
+  bool use_csk = [] {
+    const char *e = getenv("OXY_CSK");
+    return e && atoi(e) != 0;
+  }();
   gemm::Plan plan_for(int n_out, int k, int t) const {
-    return gemm::make_plan(n_out, k, t, psms(), gemm::policy_splits(phase, n_out, k, sms));
+    gemm::Plan p = gemm::make_plan(n_out, k, t, psms(), gemm::policy_splits(phase, n_out, k, sms));
+    p.csk = use_csk && phase == gemm::PH_CHAIN && p.cg == 0 && p.splits >= 2 && p.splits <= gemm::CSK_MAX;
+    return p;
   }
   // split-K workspace is reserved by plan_gemm(); gemm() only fetches it
   size_t ws_need = 0;
@@ -527,6 +540,25 @@ struct Model {
                      const float *norm_w, const float *mod_scale, const float *mod_shift) {
     if (t <= 0) return;
     gemm::Plan plan = plan_for(n_out, k, t);
+    if (plan.csk && n_out % 128 == 0 && n_out <= 2048) {
+      // chain phase: residual add in the cluster split-K epilogue, then the row norm —
+      // fused into the GEMM's last cluster for up to NORM_FUSE_MAX_T rows, else one
+      // bit-identical row-norm launch (so a row's result never depends on the batch)
+      float *wsp = ws.as<float>((size_t)plan.splits * t * n_out);
+      gemm::NormFuse nf;
+      nf.y = Y;
+      nf.ldy = n_out;
+      nf.w = norm_w;
+      nf.ms = mod_scale;
+      nf.mb = mod_shift;
+      nf.eps = 1e-6f;
+      const bool fuse = t <= gemm::NORM_FUSE_MAX_T;
+      EpiParams e{gate ? gemm::EPI_ADD_GATED_F32 : gemm::EPI_ADD_F32, X, n_out, nullptr, nullptr, 0, gate, {}};
+      if (fuse) e.norm = nf;
+      gemm::launch(w, xin, n_out, k, t, e, plan, wsp, gemm_counters, mst);
+      if (!fuse && !(dbg_skip & 128)) gemm::rownorm(X, n_out, t, n_out, nf, mst);
+      return;
+    }
     if (plan.splits > 1 && n_out <= 2048) {
       float *wsp = ws.as<float>((size_t)plan.splits * t * n_out);
       EpiParams e{gemm::EPI_PARTIALS, nullptr, 0, nullptr, nullptr, 0, nullptr, {}};

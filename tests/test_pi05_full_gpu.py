@@ -33,7 +33,7 @@ from paper_2603_14371_b200 import BatchedState
 pytestmark = pytest.mark.gpu
 
 PLAN_NAMES = ("skinny", "skinny_split", "band_deepk", "band_midk", "wide_1cta", "wide_2cta",
-              "split_res_norm", "attn_cmerge", "attn_wsmerge", "attn_one")
+              "split_res_norm", "attn_cmerge", "attn_wsmerge", "attn_one", "csk", "csk_norm")
 
 
 def plan_counts(reset=False):

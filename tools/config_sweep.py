@@ -59,7 +59,7 @@ def run(backend, frames, warm, k, variant="Unified"):
 
 
 def point(name, backend, cfg, streams, budget, k, steps, warm, variant="Unified", extra_tasks=0):
-    frames = bench.build_frames(cfg, streams, warm + steps, budget, device=True)
+    frames = bench.build_frames(cfg, list(range(streams)), warm + steps, budget, device=True)
     if extra_tasks:  # memory + narration style: more language tasks on each observation's prefix
         import dataclasses
         frames = [[dataclasses.replace(a, extra_tasks=(budget,) * extra_tasks) for a in f] for f in frames]

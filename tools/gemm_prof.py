@@ -16,7 +16,7 @@ from paper_2603_14371_b200 import _lib  # noqa: E402
 from paper_2603_14371_b200.pi05 import Pi05Backend, Pi05Config, Pi05Observation, synthetic_images  # noqa: E402
 
 EV = ["entry", "setup", "pre_issued", "prod_wait", "loads_issued", "mma_first", "mma_done", "epi_wait",
-      "acc_ready", "epi_stored", "exit", "chunk0", "chunk1"]
+      "acc_ready", "epi_stored", "exit", "chunk0", "chunk1", "csk_sync", "csk_epi", "csk_norm"]
 n_out, k = int(sys.argv[1]), int(sys.argv[2])
 be = Pi05Backend(Pi05Config(), num_blocks=64)
 assert _lib.lib().oxy_debug_gemm_prof_select(n_out, k) == 0

@@ -24,7 +24,7 @@ def main():
     warm = int(os.environ.get("WARM", "8"))
     cfg = Pi05Config()
     be = Pi05Backend(cfg, num_blocks=256 + streams * 64)
-    frames = bench.build_frames(cfg, streams, warm + 1, 30, device=True)
+    frames = bench.build_frames(cfg, list(range(streams)), warm + 1, 30, device=True)
     mgr = KvManager()
     for t in range(warm):
         run_frame_unified(t, frames[t], mgr, be, 5, 30.0)
