@@ -168,6 +168,14 @@ int oxy_prefix_attention(const void *q_d, void *out_d, const void *kpool_d, cons
                          const void *vd_d, int32_t nkb, int32_t nq, int32_t splits, float *ws_o,
                          float *ws_ml, void *stream);
 
+/* tcgen05 SigLIP self-attention (the vision tower of the pi0.5 prefix, SURVEY.md
+ * §8f rank 1; the reference stands patches in as token ids, kvweaver/backend.py:56-66):
+ * qkv_d bf16 [n_images * 256, 3 * 72 * heads] (q | k | v, head-major 72-dim
+ * slices, the fused projection's rows), out_d bf16 [n_images * 256, 72 * heads];
+ * each image's 256 tokens attend to each other, scale 1/sqrt(72).
+ * Device pointers, 16-byte aligned. */
+int oxy_vit_attention(const void *qkv_d, void *out_d, int32_t n_images, int32_t heads, void *stream);
+
 /* kernels launched by this library so far (process-wide counter) */
 int64_t oxy_launch_count(void);
 

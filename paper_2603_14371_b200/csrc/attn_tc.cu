@@ -541,6 +541,202 @@ __global__ void __launch_bounds__(192, 1)
   }
 }
 
+// ------------------------------------------------------------------ SigLIP attention
+//
+// SigLIP So400m/14 self-attention on tcgen05: 16 heads of dim 72 over the 256
+// patch tokens of one image (no mask).  CTA = (image, head, 128-query tile);
+// all 256 keys fit at once, so no online softmax:
+//   warp 0     TMA: Q (128 x [64 | 64] dims), K and V (256 x [64 | 64] dims) of the
+//              head straight out of the fused qkv rows [T, 3 * 1152]; the second
+//              64-dim box of a head also covers the next head's first dims;
+//   warps 2-5  zero Q's dims 72..127 in smem (so S only sums the head's 72 dims:
+//              the MMAs run K = 80), then softmax with thread = query row: max and
+//              exp2 over the row's 256 TMEM scores, P bf16 into the (now free) K
+//              smem in the 128B-swizzled K-major layout, O / l to bf16;
+//   warp 1     S = Q K^T (M 128, N 256, K 80) into TMEM; O = P V (M 128, N 80,
+//              K 256; V read MN-major from its TMA layout; O dims >= 72 dropped).
+namespace vt {
+constexpr int TQ = 128, NK = 256, HD = 72;
+constexpr int Q_ATOM = TQ * 128;    // 16 KB: 128 rows x 64 dims
+constexpr int KV_ATOM = NK * 128;   // 32 KB: 256 keys x 64 dims
+constexpr int OFF_K = 2 * Q_ATOM;   // P (4 atoms of 128 rows x 64 keys) reuses K's 64 KB
+constexpr int OFF_V = OFF_K + 2 * KV_ATOM;
+constexpr int OFF_BAR = OFF_V + 2 * KV_ATOM;  // 160 KB
+// barriers: q_full, k_full, v_full, q_ready (4 warps), s_full, p_full (4 warps), o_full
+constexpr int N_BARS = 7;
+constexpr size_t SMEM = 1024 + OFF_BAR + N_BARS * 8 + 16;
+constexpr uint32_t TMEM_COLS = 512;  // S: 0..255, O: 256..335
+}  // namespace vt
+
+__global__ void __launch_bounds__(192, 1)
+    vit_attn_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kvmap, bf16 *out,
+                       int heads, float scale_log2) {
+  using namespace vt;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                            ~static_cast<uintptr_t>(1023));
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sm + OFF_BAR);
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + N_BARS);
+  const uint32_t b_q = smem_u32(bars), b_k = b_q + 8, b_v = b_q + 16, b_qr = b_q + 24, b_s = b_q + 32,
+                 b_p = b_q + 40, b_o = b_q + 48;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int img = blockIdx.x / heads, h = blockIdx.x % heads, q0 = blockIdx.y * TQ;
+  const int D = heads * HD;  // 1152
+  const int row_img = img * NK;
+  if (threadIdx.x == 0) {
+    mbar_init(b_q, 1);
+    mbar_init(b_k, 1);
+    mbar_init(b_v, 1);
+    mbar_init(b_qr, 4);
+    mbar_init(b_s, 1);
+    mbar_init(b_p, 4);
+    mbar_init(b_o, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&qmap)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&kvmap)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) pdl_trigger();  // the o-projection may start streaming its weights
+  pdl_wait();                           // q/k/v rows come from the qkv projection
+  if (warp == 0) {
+    if (lane == 0) {
+      const int cq = h * HD, ck = D + h * HD, cv = 2 * D + h * HD;
+      mbar_expect_tx(b_q, 2 * Q_ATOM);
+      mbar_expect_tx(b_k, 2 * KV_ATOM);
+      mbar_expect_tx(b_v, 2 * KV_ATOM);
+      for (int b = 0; b < 2; ++b) tma_load_2d(&qmap, b_q, smem_u32(sm + b * Q_ATOM), cq + 64 * b, row_img + q0);
+      for (int b = 0; b < 2; ++b) tma_load_2d(&kvmap, b_k, smem_u32(sm + OFF_K + b * KV_ATOM), ck + 64 * b, row_img);
+      for (int b = 0; b < 2; ++b) tma_load_2d(&kvmap, b_v, smem_u32(sm + OFF_V + b * KV_ATOM), cv + 64 * b, row_img);
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc_s = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(NK >> 3) << 17) |
+                               ((uint32_t)(TQ >> 4) << 24);
+      const uint32_t idesc_o = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(80 >> 3) << 17) |
+                               ((uint32_t)(TQ >> 4) << 24);
+      const uint32_t q_s = smem_u32(sm), k_s = smem_u32(sm + OFF_K), v_s = smem_u32(sm + OFF_V);
+      mbar_wait(b_k, 0);
+      mbar_wait(b_qr, 0);
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < 5; ++kk)  // K = 80: dims 0..63 (atom 0), 64..79 (atom 1; Q zero past 71)
+        mma_bf16(tmem, make_sdesc(q_s + (kk >> 2) * Q_ATOM + (kk & 3) * 32),
+                 make_sdesc(k_s + (kk >> 2) * KV_ATOM + (kk & 3) * 32), idesc_s, kk != 0 ? 1u : 0u);
+      mma_commit(b_s);
+      mbar_wait(b_v, 0);
+      mbar_wait(b_p, 0);
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < NK / 16; ++kk)  // P atoms of 64 keys at OFF_K + 16 KB each
+        mma_bf16(tmem + 256, make_sdesc(k_s + (kk >> 2) * Q_ATOM + (kk & 3) * 32),
+                 make_sdesc_mn(v_s + kk * 2048, KV_ATOM), idesc_o, kk != 0 ? 1u : 0u);
+      mma_commit(b_o);
+    }
+    __syncwarp();
+  } else {
+    const int quad = warp & 3, row = quad * 32 + lane;
+    const uint32_t lanes = (uint32_t)(quad * 32) << 16;
+    // Q dims 72..127 (atom 1, logical 16-byte chunks 1..7 of the row) -> 0
+    mbar_wait(b_q, 0);
+    uint8_t *qrow = sm + Q_ATOM + row * 128;
+#pragma unroll
+    for (int ch = 1; ch < 8; ++ch) *reinterpret_cast<uint4 *>(qrow + ((ch ^ (row & 7)) << 4)) = make_uint4(0, 0, 0, 0);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) mbar_arrive_local(b_qr);
+    // softmax over the row's 256 scores
+    mbar_wait(b_s, 0);
+    tc_fence_after();
+    float mx = -INFINITY;
+#pragma unroll 1
+    for (int c = 0; c < NK / 16; ++c) {
+      uint32_t v[16];
+      tmem_ld16_nowait(tmem + lanes + c * 16, v);
+      tmem_ld_wait();
+#pragma unroll
+      for (int e = 0; e < 16; ++e) mx = fmaxf(mx, __uint_as_float(v[e]));
+    }
+    const float mref = mx * scale_log2;
+    float l = 0.f;
+#pragma unroll 1
+    for (int c = 0; c < NK / 16; ++c) {
+      uint32_t v[16];
+      tmem_ld16_nowait(tmem + lanes + c * 16, v);
+      tmem_ld_wait();
+      uint32_t pk[8];
+#pragma unroll
+      for (int e = 0; e < 16; e += 2) {
+        const float p0 = exp2_approx(__uint_as_float(v[e]) * scale_log2 - mref);
+        const float p1 = exp2_approx(__uint_as_float(v[e + 1]) * scale_log2 - mref);
+        l += p0 + p1;
+        __nv_bfloat162 hh = __floats2bfloat162_rn(p0, p1);
+        pk[e / 2] = *reinterpret_cast<uint32_t *>(&hh);
+      }
+      // P atom c / 4 (keys 64 (c/4) ..), 16-byte chunks 2 (c % 4), +1 of the row, 128B swizzle
+      uint8_t *prow = sm + OFF_K + (c >> 2) * Q_ATOM + row * 128;
+      const int ch = 2 * (c & 3);
+      *reinterpret_cast<uint4 *>(prow + ((ch ^ (row & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      *reinterpret_cast<uint4 *>(prow + (((ch + 1) ^ (row & 7)) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive_local(b_p);
+    mbar_wait(b_o, 0);
+    tc_fence_after();
+    const float inv = 1.f / l;
+    uint32_t o[40];
+#pragma unroll
+    for (int c = 0; c < 5; ++c) {
+      uint32_t v[16];
+      tmem_ld16_nowait(tmem + lanes + 256 + c * 16, v);
+      tmem_ld_wait();
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        __nv_bfloat162 hh =
+            __floats2bfloat162_rn(__uint_as_float(v[2 * e]) * inv, __uint_as_float(v[2 * e + 1]) * inv);
+        o[c * 8 + e] = *reinterpret_cast<uint32_t *>(&hh);
+      }
+    }
+    uint4 *orow = reinterpret_cast<uint4 *>(out + (size_t)(row_img + q0 + row) * D + h * HD);  // 144 B, 16-aligned
+#pragma unroll
+    for (int i = 0; i < HD / 8; ++i) orow[i] = make_uint4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
+  }
+}
+
+void vit_attention_tc(const bf16 *qkv, bf16 *out, int n_images, int heads, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    OXY_CUDA(cudaFuncSetAttribute(vit_attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vt::SMEM));
+    attr = true;
+  }
+  if (n_images <= 0) return;
+  if (heads < 1 || (reinterpret_cast<uintptr_t>(qkv) & 15) || (reinterpret_cast<uintptr_t>(out) & 15))
+    fail(OXY_EINVAL, "SigLIP attention: heads >= 1 and 16-byte aligned q/k/v and output rows");
+  const int D = heads * vt::HD;
+  // boxes of 64 dims over the fused [n_images * 256, 3 D] qkv rows: 128 query rows, 256 key rows
+  const CUtensorMap qm = gemm::make_map(qkv, n_images * vt::NK, 3 * D, vt::TQ);
+  const CUtensorMap kvm = gemm::make_map(qkv, n_images * vt::NK, 3 * D, vt::NK);
+  ++gemm::g_plan_counts[gemm::PC_VIT_TC];
+  launch_pdl(vit_attn_tc_kernel, dim3(n_images * heads, vt::NK / vt::TQ), dim3(192), vt::SMEM, st, qm, kvm, out,
+             heads, 1.4426950408889634f / std::sqrt((float)vt::HD));
+}
+
 int attn_cluster_merge_max() {
   static const int v = [] {
     const char *e = getenv("OXY_ATTN_CMERGE");
@@ -625,6 +821,14 @@ extern "C" int oxy_prefix_attention(const void *q_d, void *out_d, const void *kp
   if (splits > 1 && !cm)
     oxy::pi05::flash_merge(gd, 1, ws_rows, splits, tps, reinterpret_cast<const bf16 *>(ws_o), ws_ml, ws_rows, st);
   OXY_CUDA(cudaFreeAsync(gd, st));
+  OXY_API_END
+}
+
+extern "C" int oxy_vit_attention(const void *qkv_d, void *out_d, int32_t n_images, int32_t heads, void *stream) {
+  OXY_API_BEGIN
+  OXY_REQUIRE(n_images >= 1 && heads >= 1 && heads <= 64, "bad SigLIP attention shape");
+  oxy::pi05::vit_attention_tc(static_cast<const oxy::pi05::bf16 *>(qkv_d), static_cast<oxy::pi05::bf16 *>(out_d),
+                              n_images, heads, oxy::as_stream(stream));
   OXY_API_END
 }
 

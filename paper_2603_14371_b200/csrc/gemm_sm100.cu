@@ -219,6 +219,61 @@ __device__ int g_gemm_prof_sel[2];
   } while (0)
 #endif
 
+// Greedy-decode epilogue of the LM head (EPI_ARGMAX): per 16-token chunk each
+// warp folds its 32 vocabulary rows per token (butterfly: every lane ends with
+// the warp's (max, lowest id)), the 4 warps meet in smem, and one (max, id) per
+// (token, weight tile) is stored.  The order-free rule — larger value wins,
+// equal values go to the lower id, NaN never wins — is the reference's
+// lowest-id tie-break (kvweaver/backend.py:387-388), so the fold order does not
+// matter and the result equals an argmax over the materialised logits.
+__device__ __forceinline__ void amax_better(float &bv, int &bi, float v, int i) {
+  if (v > bv || (v == bv && i < bi)) {
+    bv = v;
+    bi = i;
+  }
+}
+__device__ __forceinline__ void argmax_epilogue(const KParams &p, uint32_t trow, int bn, int n0, int f, int tile,
+                                                float (*s_v)[16], int (*s_i)[16]) {
+  const int lane = threadIdx.x & 31, q = (threadIdx.x >> 5) & 3;
+  for (int c = 0; c < bn; c += 16) {
+    uint32_t v[16];
+    tmem_ld16(trow + (uint32_t)c, v);
+    const int t0 = n0 + c;
+    float bv[16];
+    int bi[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      bv[j] = (f < p.n_out && t0 + j < p.t) ? __uint_as_float(v[j]) : -INFINITY;
+      bi[j] = f;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv[j], o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi[j], o);
+        amax_better(bv[j], bi[j], ov, oi);
+      }
+    if (lane == 0) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        s_v[q][j] = bv[j];
+        s_i[q][j] = bi[j];
+      }
+    }
+    asm volatile("bar.sync 2, 128;" ::: "memory");
+    if (q == 0 && lane < 16 && t0 + lane < p.t) {
+      float b = s_v[0][lane];
+      int i = s_i[0][lane];
+      for (int w = 1; w < 4; ++w) amax_better(b, i, s_v[w][lane], s_i[w][lane]);
+      const size_t o = (size_t)(t0 + lane) * p.epi.ldo + tile;
+      static_cast<float *>(p.epi.out)[o] = b;
+      p.epi.amax_idx[o] = i;
+    }
+    asm volatile("bar.sync 2, 128;" ::: "memory");
+  }
+}
+
 // 128 registers: two CTAs per SM still leave register room for the next
 // kernel's early (PDL) CTAs and the other lane's kernels (168 registers, the
 // compiler's free choice with the cluster split-K tail, filled the register file
@@ -332,6 +387,11 @@ __global__ void __maxnreg__(128)
     mbar_wait(done, 0);
     tc_fence_after();
     if (threadIdx.x == 64) GPROF(8);
+    if (p.epi.mode == EPI_ARGMAX) {
+      __shared__ float s_amv[4][16];
+      __shared__ int s_ami[4][16];
+      argmax_epilogue(p, trow, bn, n0, f, blockIdx.y, s_amv, s_ami);
+    } else
 #ifdef OXY_GEMM_PROF
     if (bn > 32) {
       epi_tile(p, trow, 0, 16, n0, f, split, split_out, stg);
@@ -882,10 +942,12 @@ void launch(const void *w, const void *x, int n_out, int k, int t, const EpiPara
   if (plan.splits > 1 && (!ws || !counters)) fail(OXY_EINVAL, "split-K GEMM needs a workspace");
   if (plan.splits > 1 && plan.m_tiles * plan.n_tiles * 2 > MAX_TILES) fail(OXY_EINVAL, "too many split-K tiles");
   if (plan.cg > 0) {
+    if (epi.mode == EPI_ARGMAX) fail(OXY_EINVAL, "argmax LM head: one-tile-per-CTA plans only");
     ++g_plan_counts[plan.cg == 2 ? PC_WIDE_2CTA : PC_WIDE_1CTA];
     launch_wide(w, x, n_out, k, t, epi, plan, ws, counters, st);
     return;
   }
+  if (epi.mode == EPI_ARGMAX) ++g_plan_counts[PC_ARGMAX_HEAD];
   ++g_plan_counts[plan.band == 1 ? PC_BAND_DEEPK
                   : plan.band == 2 ? PC_BAND_MIDK
                   : plan.splits > 1 ? PC_SKINNY_SPLIT
@@ -908,6 +970,8 @@ void launch(const void *w, const void *x, int n_out, int k, int t, const EpiPara
   kp.prefetch = kp.trigger = t <= 64 ? (g_early_override >= 0 ? g_early_override : knobs().early_skinny)
                                      : knobs().early_wide;
   kp.csk = plan.csk && plan.splits > 1;
+  if (epi.mode == EPI_ARGMAX && (plan.splits != 1 || !epi.amax_idx))
+    fail(OXY_EINVAL, "argmax LM head: unsplit plan and an index buffer required");
   if (epi.norm.y && !(kp.csk && t <= NORM_FUSE_MAX_T && (epi.mode == EPI_ADD_F32 || epi.mode == EPI_ADD_GATED_F32)))
     fail(OXY_EINVAL, "fused row norm needs a cluster split-K residual GEMM of <= %d rows", NORM_FUSE_MAX_T);
   if (epi.norm.y && (n_out % 128 != 0 || n_out > 128 * NORM_MAX_V4 || epi.ldo % 4 != 0 || epi.norm.ldy % 4 != 0))

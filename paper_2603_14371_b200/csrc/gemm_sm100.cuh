@@ -31,6 +31,9 @@ enum Epi : int {
   EPI_QKV_ROPE = 8,       // fused QKV projection: RoPE on q/k (rotary pairs interleaved in the
                           // weight rows), q -> bf16 [T, 2048], k/v -> pool slot rows or dense rows
   EPI_PARTIALS = 9,       // split-K partials only; the caller launches its own fused reduction
+  EPI_ARGMAX = 10,        // greedy LM head: no logits; per (token, 128-row weight tile) the max
+                          // accumulator and its lowest row id -> out_f32[t, tile] / amax_idx[t, tile]
+                          // (ldo = tiles per token row); unsplit one-tile-per-CTA plans only
 };
 
 // Fused split-K reduction + residual + RMSNorm (one CTA per token row):
@@ -74,6 +77,7 @@ struct EpiParams {
   const float *gate;    // EPI_ADD_GATED_F32 per-feature gate [N]
   QkvRope rope;         // EPI_QKV_ROPE
   NormFuse norm{};      // cluster split-K residual modes only
+  int *amax_idx = nullptr;  // EPI_ARGMAX row ids
 };
 
 // The row norm of NormFuse as a stand-alone kernel (one warp per row), bit-identical
@@ -121,6 +125,8 @@ enum PlanClass {
   PC_ATTN_ONE,        // tcgen05 attention, one split
   PC_CSK,             // gemm_kernel, cluster split-K (in-kernel reduction)
   PC_CSK_NORM,        // ... with the residual RMSNorm fused into the last cluster
+  PC_ARGMAX_HEAD,     // LM head with the greedy argmax epilogue (no logits in HBM)
+  PC_VIT_TC,          // SigLIP attention on tcgen05 (vit_attn_tc_kernel)
   PC_COUNT
 };
 extern long long g_plan_counts[PC_COUNT];

@@ -858,6 +858,49 @@ __global__ void argmax_final_kernel(int rows, const float *pv, const int *pi, in
   if (bi == eos || c == budget[r]) active[r] = 0;
 }
 
+// Greedy step from the LM head's EPI_ARGMAX partials: one (max, lowest id) per
+// (row, 128-row weight tile), folded per row by one CTA with the same order-free
+// rule, then the same per-row state update as argmax_final_kernel.
+__global__ void __launch_bounds__(256) argmax_tiles_final_kernel(int tiles, const float *pv, const int *pi, int step,
+                                                                 int k, int eos, int *active, int *tok, int *pos,
+                                                                 int *count, const int *budget, int *out_tokens) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ float sv[8];
+  __shared__ int si[8];
+  const int r = blockIdx.x;
+  if (active && !active[r]) return;
+  float bv = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int c = threadIdx.x; c < tiles; c += blockDim.x)
+    better(bv, bi, __ldcg(pv + (size_t)r * tiles + c), __ldcg(pi + (size_t)r * tiles + c));
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    better(bv, bi, ov, oi);
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) {
+    sv[w] = bv;
+    si[w] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  for (int i = 1; i < (int)(blockDim.x >> 5); ++i) better(bv, bi, sv[i], si[i]);
+  if (bi == 0x7fffffff) bi = 0;
+  out_tokens[(size_t)r * k + step] = bi;
+  tok[r] = bi;
+  pos[r] += 1;
+  const int c = ++count[r];
+  if (bi == eos || c == budget[r]) active[r] = 0;
+}
+
+void argmax_tiles_update(int rows, int tiles, const float *pv, const int *pi, int step, int k, int eos, int *active,
+                         int *tok, int *pos, int *count, const int *budget, int *out_tokens, cudaStream_t st) {
+  launch_pdl(argmax_tiles_final_kernel, dim3(rows), dim3(256), 0, st, tiles, pv, pi, step, k, eos, active, tok, pos,
+             count, budget, out_tokens);
+}
+
 void argmax_update(const float *logits, int rows, int V, int step, int k, int eos, int *active, int *tok,
                    int *pos, int *count, const int *budget, int *out_tokens, float *pv, int *pi,
                    cudaStream_t st) {

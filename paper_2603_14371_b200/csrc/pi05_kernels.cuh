@@ -95,6 +95,10 @@ void flash_attention_tc(const AttnGroup *groups_d, int n_groups, int q_tiles, in
 // the cap (default 16; 0 or 1 = always the workspace merge)
 int attn_cluster_merge_max();
 // split-order merge of the tcgen05 kernel's bf16 head-dim-256 partials (ws rows as in flash_attention)
+// SigLIP self-attention on tcgen05: 256 tokens per image, `heads` heads of dim 72,
+// q/k/v read from the fused qkv rows [n_images * 256, 3 * 72 heads], output
+// [n_images * 256, 72 heads] bf16.  One CTA per (image, head, 128 queries).
+void vit_attention_tc(const bf16 *qkv, bf16 *out, int n_images, int heads, cudaStream_t st);
 void flash_merge(const AttnGroup *groups_d, int n_groups, int max_rows, int splits, int tps, const bf16 *ws_o,
                  const float *ws_ml, int ws_rows, cudaStream_t st);
 
@@ -122,6 +126,9 @@ void decode_attention_v3(const CUtensorMap &kmap, const CUtensorMap &vmap, const
 // k / v [T, 256] bf16 rows; keys [0, P) for t < P, else [0, t])
 void prefix_lm_attention_ref(const bf16 *q, const bf16 *k, const bf16 *v, bf16 *out, int T, int P, float scale,
                              cudaStream_t st);
+// fold of the LM head's EPI_ARGMAX partials ([rows][tiles] max / id) + the same state update
+void argmax_tiles_update(int rows, int tiles, const float *pv, const int *pi, int step, int k, int eos, int *active,
+                         int *tok, int *pos, int *count, const int *budget, int *out_tokens, cudaStream_t st);
 void argmax_update(const float *logits, int rows, int V, int step, int k, int eos, int *active,
                    int *tok, int *pos, int *count, const int *budget, int *out_tokens,
                    float *part_val, int *part_idx, cudaStream_t st);

@@ -629,6 +629,11 @@ struct Model {
     const char *e = getenv("OXY_ATTN_TC");
     return !e || atoi(e) != 0;
   }();
+  // SigLIP attention on tcgen05 (vit_attn_tc_kernel); OXY_VIT_TC=0: the mma.sync kernel (A/B)
+  bool use_vit_tc = [] {
+    const char *e = getenv("OXY_VIT_TC");
+    return !e || atoi(e) != 0;
+  }();
   // tps: key tiles (of 64) per split, per phase (batch invariance: a group's split
   // count is attn_group_splits(its key tiles, tps) whatever else shares the call)
   AttnPlan shape_attention_tc(std::vector<AttnGroup> &groups, int tps) {
@@ -833,7 +838,8 @@ struct Model {
           const VitW &w = V[l];
           layernorm(hv, Dv, yv, Dv, w.ln1w, w.ln1b, Tv, Dv, 1e-6f, mst);
           gemm(w.wqkv, yv, 3 * Dv, Dv, Tv, gemm::EPI_BF16, qkvv, 3 * Dv, w.bqkv);
-          attend(a_vit, nullptr, nullptr);
+          if (use_vit_tc) vit_attention_tc(qkvv, ov, n_images, nh, mst);
+          else attend(a_vit, nullptr, nullptr);
           gemm(w.wo, ov, Dv, Dv, Tv, gemm::EPI_ADD_F32, hv, Dv, w.bo);
           layernorm(hv, Dv, yv, Dv, w.ln2w, w.ln2b, Tv, Dv, 1e-6f, mst);
           gemm(w.w1, yv, c.vit_mlp, Dv, Tv, gemm::EPI_GELU_BF16, mv, c.vit_mlp, w.b1);
@@ -1067,6 +1073,11 @@ struct Model {
     const char *e = getenv("OXY_PREFILL_DEEPK");
     return !e || atoi(e) != 0;
   }();
+  // OXY_FUSED_ARGMAX=0: materialise the logits and argmax them in two kernels (A/B)
+  bool fused_argmax = [] {
+    const char *e = getenv("OXY_FUSED_ARGMAX");
+    return !e || atoi(e) != 0;
+  }();
   int decode_early = [] {
     const char *e = getenv("OXY_DECODE_EARLY");
     return e ? atoi(e) : -1;
@@ -1100,8 +1111,9 @@ struct Model {
     o.as<bf16>((size_t)rows * QDIM);
     hmid.as<bf16>((size_t)rows * c.mlp);
     logits.as<float>((size_t)rows * c.vocab);
-    amv.as<float>((size_t)rows * 64);
-    ami.as<int>((size_t)rows * 64);
+    const int head_tiles = (c.vocab + gemm::BM - 1) / gemm::BM;
+    amv.as<float>((size_t)rows * std::max(64, head_tiles));
+    ami.as<int>((size_t)rows * std::max(64, head_tiles));
     dec_ws.as<float>((size_t)rows * maxb * Q_HEADS * (HEAD_DIM + 2));
     plan_gemm(QKV, W, rows);
     plan_gemm(W, QDIM, rows);
@@ -1125,6 +1137,10 @@ struct Model {
     int *d_slot = arena_put(zeros.data(), rows);
     int *d_out = arena_put(zeros.data(), (size_t)rows * k);
     const float scale = 1.f / 16.f;  // 1/sqrt(256)
+    // the argmax epilogue needs the unsplit one-tile-per-CTA LM-head plan (always the
+    // case for decode rows <= 64); logits requested -> the materialising path
+    const gemm::Plan head_plan = plan_for(c.vocab, W, rows);
+    const bool fused_head = fused_argmax && !logits_h && head_plan.cg == 0 && head_plan.splits == 1;
     enter(caller);
     arena_upload();
     auto body = [&]() {
@@ -1143,6 +1159,17 @@ struct Model {
           if (!(dbg_skip & 2048)) gemm_res_norm(w.wo, Ob, W, QDIM, rows, nullptr, X, Y, w.ln2, nullptr, nullptr);
           if (!(dbg_skip & 4096)) gemm(w.wgu, Y, 2 * c.mlp, W, rows, gemm::EPI_GEGLU_BF16, Hm, c.mlp);
           if (!(dbg_skip & 8192)) gemm_res_norm(w.wd, Hm, W, c.mlp, rows, nullptr, X, Y, next_norm, nullptr, nullptr);
+        }
+        if (fused_head) {
+          // greedy LM head: per-(row, weight tile) (max, id) straight from the
+          // accumulators, no logits in HBM
+          const gemm::Plan hp = plan_for(c.vocab, W, rows);
+          EpiParams e{gemm::EPI_ARGMAX, pv, head_tiles, nullptr, nullptr, 0, nullptr, {}};
+          e.amax_idx = pi;
+          if (!(dbg_skip & 16384)) gemm::launch(lm_head, Y, c.vocab, W, rows, e, hp, nullptr, gemm_counters, mst);
+          argmax_tiles_update(rows, head_tiles, pv, pi, s, k, c.eos_token, d_active, d_tok, d_pos, d_cnt, d_bud,
+                              d_out, mst);
+          continue;
         }
         if (!(dbg_skip & 16384)) gemm(lm_head, Y, c.vocab, W, rows, gemm::EPI_F32, LG, c.vocab);
         if (logits_h)

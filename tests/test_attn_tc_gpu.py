@@ -74,3 +74,30 @@ def test_prefix_attention_workspace_merge():
            "-k", "test_prefix_attention_matches_torch"]
     res = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=300)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-2000:]
+
+
+@pytest.mark.parametrize("n_images,heads", [(1, 16), (3, 16), (2, 2), (5, 3)])
+def test_vit_attention_matches_torch(n_images, heads):
+    """oxy_vit_attention (tcgen05 SigLIP attention: head dim 72 run as K = 80 with Q
+    zero-padded, all 256 keys per CTA) against torch fp32 softmax attention on the
+    same bf16 fused qkv rows.  Tolerance: P and the output are bf16 -> 2e-2 of max|V|.
+    The next head's dims ride along in the second 64-dim TMA box of every head, so
+    a leak of them into S or O would show."""
+    import ctypes as C
+    import torch
+    from paper_2603_14371_b200 import _lib
+    D = 72 * heads
+    g = torch.Generator(device="cpu").manual_seed(n_images * 100 + heads)
+    qkv = torch.randn(n_images * 256, 3 * D, generator=g) * 1.5
+    out = torch.zeros(n_images * 256, D, dtype=torch.bfloat16, device="cuda")
+    qkv_b = qkv.to(torch.bfloat16)
+    dev = qkv_b.cuda()
+    _lib.call("oxy_vit_attention", C.c_void_p(dev.data_ptr()), C.c_void_p(out.data_ptr()), C.c_int32(n_images),
+              C.c_int32(heads), _lib.stream_ptr())
+    torch.cuda.synchronize()
+    x = qkv_b.float().reshape(n_images, 256, 3, heads, 72)
+    q, k, v = (x[:, :, i].permute(0, 2, 1, 3) for i in range(3))  # [img, head, tok, 72]
+    ref = torch.softmax(q @ k.transpose(-1, -2) / 72 ** 0.5, dim=-1) @ v
+    ref = ref.permute(0, 2, 1, 3).reshape(n_images * 256, D)
+    err = (out.float().cpu() - ref).abs().max().item()
+    assert err < 2e-2 * v.abs().max().item(), err

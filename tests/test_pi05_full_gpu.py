@@ -33,7 +33,7 @@ from paper_2603_14371_b200 import BatchedState
 pytestmark = pytest.mark.gpu
 
 PLAN_NAMES = ("skinny", "skinny_split", "band_deepk", "band_midk", "wide_1cta", "wide_2cta",
-              "split_res_norm", "attn_cmerge", "attn_wsmerge", "attn_one", "csk", "csk_norm")
+              "split_res_norm", "attn_cmerge", "attn_wsmerge", "attn_one", "csk", "csk_norm", "argmax_head", "vit_tc")
 
 
 def plan_counts(reset=False):
@@ -80,7 +80,7 @@ def test_full_prefill_kv_and_plans(full):
     kv = be.prefill(o)
     used = plan_counts(reset=True)
     assert kv.seq_len == 800
-    for name in ("band_deepk", "band_midk", "wide_2cta", "split_res_norm", "attn_cmerge"):
+    for name in ("band_deepk", "band_midk", "wide_2cta", "split_res_norm", "attn_cmerge", "vit_tc"):
         assert used[name] > 0, (name, used)
     want = ref.prefill(o)
     errs = []
@@ -141,6 +141,27 @@ def test_full_decode_logits_six_rows(full):
                 compared += 1
     assert worst_cos >= 0.9999 and worst_abs <= 0.1, (worst_cos, worst_abs)
     assert compared >= 18, compared
+
+
+def test_full_fused_argmax_head_equals_logits_argmax(full):
+    """The greedy LM head (EPI_ARGMAX: per weight-tile (max, lowest id) folded per row,
+    no logits in HBM) emits exactly the tokens of an argmax over the materialised
+    logits of the same call — 12 rows x 5 steps, ties broken to the lowest id
+    (kvweaver/backend.py:387-388)."""
+    be, _ = full
+    rows = [be.prefill(obs(3 if i % 3 else 1, 32 - i, 30 + i)) for i in range(12)]
+    st = BatchedState(tuple(rows), ((),) * 12, (False,) * 12, tuple(range(12)), (40,) * 12, (0,) * 12)
+    plan_counts(reset=True)
+    fused = be.batched_language_decode(st, 5)
+    used = plan_counts(reset=True)
+    assert used["argmax_head"] == 5, used
+    ref, logits = be.batched_language_decode(st, 5, return_logits=True)
+    assert plan_counts(reset=True)["argmax_head"] == 0
+    assert fused.token_buffers == ref.token_buffers
+    for r in range(12):
+        for s, tok in enumerate(ref.token_buffers[r]):
+            row = logits[s, r]
+            assert tok == int(np.flatnonzero(row == row.max())[0]), (r, s)
 
 
 def test_full_batched_prefill_is_bit_exact(full):
