@@ -26,6 +26,9 @@ struct KParams {
   int prefetch;   // 1: issue the first ring of weight tiles before griddepcontrol.wait
   int trigger;    // 1: launch_dependents once all operand loads are issued
   int csk;        // 1: cluster split-K — the split CTAs of a tile are one cluster (along z)
+  int tma_ws;     // 1: split partials leave through a TMA tensor store (tmW) instead of st.global
+  int b_box;      // token rows per B TMA box: bn, or T when one token tile covers T (rows past
+                  // it stay stale in smem; their accumulator columns are never stored)
 };
 
 // One residual row's RMSNorm / adaRMSNorm by one warp (NormFuse): lane l owns
@@ -97,6 +100,8 @@ void rownorm(const float *x, int ldx, int t, int n, const NormFuse &nf, cudaStre
 // OXY_GEMM_SMEM_KB=<per-CTA smem budget>.  Used for A/B measurements.
 struct Knobs {
   int fixup = 0, pdl = 1, smem_kb = 100;  // 2 CTAs per SM (measured best)
+  int tma_ws = 0;  // split partials via TMA tensor store (OXY_GEMM_TMA_WS=1; neutral in the frame)
+  int bbox_exact = 1;  // B boxes of T rows when T < bn (OXY_GEMM_BBOX_EXACT=0: padded boxes)
   // early PDL (weight prefetch + trigger) for skinny / wide GEMMs: -1 = default policy
   // (T > 64 on the one-tile-per-CTA kernel: neutral at 1 stream, 0 to -1.3 ms per
   // 8-stream frame and 0 to -1 ms at 16 across same-session A/Bs)
@@ -124,6 +129,8 @@ struct Knobs {
     if (const char *s = getenv("OXY_SPLITK")) fixup = std::string(s) == "fixup";
     if (const char *s = getenv("OXY_PDL")) pdl = atoi(s);
     if (const char *s = getenv("OXY_GEMM_SMEM_KB")) smem_kb = std::max(64, std::min(200, atoi(s)));
+    if (const char *s = getenv("OXY_GEMM_TMA_WS")) tma_ws = atoi(s);
+    if (const char *s = getenv("OXY_GEMM_BBOX_EXACT")) bbox_exact = atoi(s);
   }
 };
 // per-enqueue override of the skinny early-PDL policy (-1: knob); set by the
@@ -202,18 +209,25 @@ __global__ void splitk_reduce_kernel(const float *ws, int splits, int t_rows, in
 // timing builds: %globaltimer at pipeline events of weight tile 0 / token tile 0
 // of the launches matching (n_out, k) set by oxy_debug_gemm_prof_select, one row
 // per split (the last matching launch wins)
-__device__ unsigned long long g_gemm_prof[32][16];
+__device__ unsigned long long g_gemm_prof[32][24];
 __device__ int g_gemm_prof_sel[2];
+// (the selection is read once per CTA into gprof_on: a global load per event put an
+// L2 round trip into every probed step and skewed the timelines)
+#define GPROF_INIT()                                                                                 \
+  const bool gprof_on = blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z < 32 &&                     \
+                        p.n_out == g_gemm_prof_sel[0] && p.k == g_gemm_prof_sel[1]
 #define GPROF(ev)                                                                             \
   do {                                                                                        \
-    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z < 32 && p.n_out == g_gemm_prof_sel[0] && \
-        p.k == g_gemm_prof_sel[1]) {                                                          \
+    if (gprof_on) {                                                                           \
       unsigned long long t_;                                                                  \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                  \
       g_gemm_prof[blockIdx.z][ev] = t_;                                                       \
     }                                                                                         \
   } while (0)
 #else
+#define GPROF_INIT() \
+  do {               \
+  } while (0)
 #define GPROF(ev) \
   do {            \
   } while (0)
@@ -232,12 +246,12 @@ __device__ __forceinline__ void amax_better(float &bv, int &bi, float v, int i) 
     bi = i;
   }
 }
-__device__ __forceinline__ void argmax_epilogue(const KParams &p, uint32_t trow, int bn, int n0, int f, int tile,
-                                                float (*s_v)[16], int (*s_i)[16]) {
+__device__ __forceinline__ void argmax_epilogue(const KParams &p, const TmemSrc &src, int bn, int n0, int f,
+                                                int tile, float (*s_v)[16], int (*s_i)[16]) {
   const int lane = threadIdx.x & 31, q = (threadIdx.x >> 5) & 3;
   for (int c = 0; c < bn; c += 16) {
     uint32_t v[16];
-    tmem_ld16(trow + (uint32_t)c, v);
+    src(c, 16, v);
     const int t0 = n0 + c;
     float bv[16];
     int bi[16];
@@ -280,12 +294,13 @@ __device__ __forceinline__ void argmax_epilogue(const KParams &p, uint32_t trow,
 // and serialised the chain)
 __global__ void __maxnreg__(128)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                KParams p) {
+                const __grid_constant__ CUtensorMap tmW, KParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~static_cast<uintptr_t>(1023));
   const int bn = p.bn, stages = p.stages;
   const int b_bytes = bn * BK * 2;
+  const uint32_t stage_tx = A_STAGE_BYTES + p.b_box * BK * 2;  // bytes one stage's two TMA boxes deliver
   uint8_t *sA = smem;
   uint8_t *sB = smem + stages * A_STAGE_BYTES;
   uint64_t *bars = reinterpret_cast<uint64_t *>(sB + stages * b_bytes);
@@ -301,6 +316,7 @@ __global__ void __maxnreg__(128)
                  done = smem_u32(bars + 2 * MAX_STAGES);
   uint32_t ncols = 32;
   while (ncols < (uint32_t)bn) ncols <<= 1;
+  GPROF_INIT();
   if (threadIdx.x == 0) GPROF(0);
 
   if (threadIdx.x == 0) {
@@ -331,19 +347,24 @@ __global__ void __maxnreg__(128)
       // weight tiles before waiting on it, activations after.
       const int pre = p.prefetch ? min(nkb, stages) : 0;
       for (int i = 0; i < pre; ++i) {
-        mbar_expect_tx(full0 + 8 * i, A_STAGE_BYTES + b_bytes);
+        mbar_expect_tx(full0 + 8 * i, stage_tx);
         tma_load_2d(&tmA, full0 + 8 * i, smem_u32(sA + i * A_STAGE_BYTES), (kb0 + i) * BK, m0);
+#ifdef OXY_GEMM_PROF_PREB  // timing experiment only (races the previous kernel): B before the wait too
+        tma_load_2d(&tmB, full0 + 8 * i, smem_u32(sB + i * b_bytes), (kb0 + i) * BK, n0);
+#endif
       }
       GPROF(2);
       pdl_wait();
       GPROF(3);
+#ifndef OXY_GEMM_PROF_PREB
       for (int i = 0; i < pre; ++i)
         tma_load_2d(&tmB, full0 + 8 * i, smem_u32(sB + i * b_bytes), (kb0 + i) * BK, n0);
+#endif
       for (int i = pre; i < nkb; ++i) {
         const int s = i % stages;
         const uint32_t ph = (i / stages) & 1;
         mbar_wait(empty0 + 8 * s, ph ^ 1);
-        mbar_expect_tx(full0 + 8 * s, A_STAGE_BYTES + b_bytes);
+        mbar_expect_tx(full0 + 8 * s, stage_tx);
         const int kc = (kb0 + i) * BK;
         tma_load_2d(&tmA, full0 + 8 * s, smem_u32(sA + s * A_STAGE_BYTES), kc, m0);
         tma_load_2d(&tmB, full0 + 8 * s, smem_u32(sB + s * b_bytes), kc, n0);
@@ -363,11 +384,11 @@ __global__ void __maxnreg__(128)
         mbar_wait(full0 + 8 * s, ph);
         tc_fence_after();
         if (i == 0) GPROF(5);
+        if (i > 0 && i < 4) GPROF(15 + i);
         const uint32_t a = smem_u32(sA + s * A_STAGE_BYTES), b = smem_u32(sB + s * b_bytes);
 #pragma unroll
         for (int kk = 0; kk < BK / 16; ++kk)
-          mma_bf16(tmem, make_sdesc(a + kk * 32), make_sdesc(b + kk * 32), idesc,
-                   (i | kk) != 0 ? 1u : 0u);
+          mma_bf16(tmem, make_sdesc(a + kk * 32), make_sdesc(b + kk * 32), idesc, (i | kk) != 0 ? 1u : 0u);
         mma_commit(empty0 + 8 * s);
       }
       mma_commit(done);
@@ -390,7 +411,32 @@ __global__ void __maxnreg__(128)
     if (p.epi.mode == EPI_ARGMAX) {
       __shared__ float s_amv[4][16];
       __shared__ int s_ami[4][16];
-      argmax_epilogue(p, trow, bn, n0, f, blockIdx.y, s_amv, s_ami);
+      argmax_epilogue(p, TmemSrc{trow}, bn, n0, f, blockIdx.y, s_amv, s_ami);
+    } else if (split_out && p.tma_ws) {
+      // split-K partials through one TMA tensor store: the 128 x bn fp32 tile is
+      // staged token-major in the idle operand ring (thread = feature column, so
+      // a warp's 32 stores per token row are conflict-free) and written by a
+      // single bulk copy instead of 16 x bn/16 per-thread store instructions;
+      // token rows past T and features past N_out are clipped by the 3-D map
+      float *stage = reinterpret_cast<float *>(sA);
+      const int col = q * 32 + lane;
+      const TmemSrc src{trow};
+      for (int c = 0; c < bn; c += 16) {
+        uint32_t v[16];
+        src(c, 16, v);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) stage[(c + j) * BM + col] = __uint_as_float(v[j]);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("bar.sync 2, 128;" ::: "memory");
+      if (threadIdx.x == 64) {
+        asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                         reinterpret_cast<uint64_t>(&tmW)),
+                     "r"(m0), "r"(n0), "r"(split), "r"(smem_u32(stage))
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem released once read
+      }
     } else
 #ifdef OXY_GEMM_PROF
     if (bn > 32) {
@@ -769,6 +815,22 @@ static bool wide_plan(Plan &p, int n_out, int k, int t, int sms, int req_splits)
   return true;
 }
 
+// split-K workspace [splits][t][n_out] fp32 as a 3-D map, box 128 features x bn tokens x 1
+// split, no swizzle (the staged tile is dense token-major)
+static CUtensorMap make_map_ws(const float *ws, int splits, int t, int n_out, int bn) {
+  if (reinterpret_cast<uintptr_t>(ws) % 16 != 0) fail(OXY_EINVAL, "split-K workspace not 16-byte aligned");
+  CUtensorMap map;
+  cuuint64_t dims[3] = {(cuuint64_t)n_out, (cuuint64_t)t, (cuuint64_t)splits};
+  cuuint64_t strides[2] = {(cuuint64_t)n_out * 4, (cuuint64_t)t * n_out * 4};
+  cuuint32_t box[3] = {(cuuint32_t)BM, (cuuint32_t)bn, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(ws), dims, strides, box,
+                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(OXY_ECUDA, "cuTensorMapEncodeTiled (split-K workspace) failed (%d)", (int)r);
+  return map;
+}
+
 // rows x cols fp32 row-major, box (box_cols x box_rows), 128-byte swizzle (box_cols * 4 == 128)
 CUtensorMap make_map_f32(const void *ptr, int rows, int cols, int box_cols, int box_rows) {
   if ((cols * 4) % 16 != 0 || reinterpret_cast<uintptr_t>(ptr) % 16 != 0) fail(OXY_EINVAL, "fp32 map alignment");
@@ -953,7 +1015,10 @@ void launch(const void *w, const void *x, int n_out, int k, int t, const EpiPara
                   : plan.splits > 1 ? PC_SKINNY_SPLIT
                                     : PC_SKINNY];
   CUtensorMap ma = make_map(w, n_out, k, BM);
-  CUtensorMap mb = make_map(x, t, k, plan.bn);
+  // one token tile covering T < bn: a T-row box (no out-of-bounds zero fill; fewer bytes,
+  // neutral in the frame — profiles/r02_skinny_gemm.md)
+  const int b_box = plan.n_tiles == 1 && t < plan.bn && knobs().bbox_exact ? t : plan.bn;
+  CUtensorMap mb = make_map(x, t, k, b_box);
   KParams kp;
   kp.n_out = n_out;
   kp.k = k;
@@ -969,6 +1034,7 @@ void launch(const void *w, const void *x, int n_out, int k, int t, const EpiPara
   kp.fixup = knobs().fixup;
   kp.prefetch = kp.trigger = t <= 64 ? (g_early_override >= 0 ? g_early_override : knobs().early_skinny)
                                      : knobs().early_wide;
+  kp.b_box = b_box;
   kp.csk = plan.csk && plan.splits > 1;
   if (epi.mode == EPI_ARGMAX && (plan.splits != 1 || !epi.amax_idx))
     fail(OXY_EINVAL, "argmax LM head: unsplit plan and an index buffer required");
@@ -976,6 +1042,12 @@ void launch(const void *w, const void *x, int n_out, int k, int t, const EpiPara
     fail(OXY_EINVAL, "fused row norm needs a cluster split-K residual GEMM of <= %d rows", NORM_FUSE_MAX_T);
   if (epi.norm.y && (n_out % 128 != 0 || n_out > 128 * NORM_MAX_V4 || epi.ldo % 4 != 0 || epi.norm.ldy % 4 != 0))
     fail(OXY_EINVAL, "fused row norm: rows of 128..2048 features (multiple of 128), strides multiple of 4");
+  // TMA-stored partials: [splits][t][n_out] fp32, box 128 features x bn tokens x 1 split
+  // (staged in the operand ring, which must hold the 128 x bn fp32 tile)
+  kp.tma_ws = plan.splits > 1 && !kp.fixup && !kp.csk && knobs().tma_ws &&
+              (size_t)BM * plan.bn * 4 <= (size_t)plan.stages * (A_STAGE_BYTES + plan.bn * BK * 2) &&
+              (n_out * 4) % 16 == 0;
+  const CUtensorMap mw = kp.tma_ws ? make_map_ws(ws, plan.splits, t, n_out, plan.bn) : ma;
   dim3 grid(plan.n_tiles, plan.m_tiles, plan.splits);
   if (kp.csk) {
     if (plan.splits > CSK_MAX) fail(OXY_EINVAL, "cluster split-K: at most %d splits", CSK_MAX);
@@ -986,13 +1058,13 @@ void launch(const void *w, const void *x, int n_out, int k, int t, const EpiPara
     }
     ++g_plan_counts[PC_CSK];
     if (epi.norm.y) ++g_plan_counts[PC_CSK_NORM];
-    launch_pdl_cluster(gemm_kernel, grid, dim3(192), smem_bytes(plan), st, dim3(1, 1, plan.splits), ma, mb, kp);
+    launch_pdl_cluster(gemm_kernel, grid, dim3(192), smem_bytes(plan), st, dim3(1, 1, plan.splits), ma, mb, mw, kp);
     return;
   }
   if (knobs().pdl) {
-    launch_pdl(gemm_kernel, grid, dim3(192), smem_bytes(plan), st, ma, mb, kp);
+    launch_pdl(gemm_kernel, grid, dim3(192), smem_bytes(plan), st, ma, mb, mw, kp);
   } else {
-    gemm_kernel<<<grid, 192, smem_bytes(plan), st>>>(ma, mb, kp);
+    gemm_kernel<<<grid, 192, smem_bytes(plan), st>>>(ma, mb, mw, kp);
     OXY_LAUNCH_CHECK();
   }
   if (plan.splits > 1 && !kp.fixup && epi.mode != EPI_PARTIALS) {

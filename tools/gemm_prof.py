@@ -16,7 +16,8 @@ from paper_2603_14371_b200 import _lib  # noqa: E402
 from paper_2603_14371_b200.pi05 import Pi05Backend, Pi05Config, Pi05Observation, synthetic_images  # noqa: E402
 
 EV = ["entry", "setup", "pre_issued", "prod_wait", "loads_issued", "mma_first", "mma_done", "epi_wait",
-      "acc_ready", "epi_stored", "exit", "chunk0", "chunk1", "csk_sync", "csk_epi", "csk_norm"]
+      "acc_ready", "epi_stored", "exit", "chunk0", "chunk1", "csk_sync", "csk_epi", "csk_norm",
+      "full1", "full2", "full3", "-", "-", "-", "-", "-"]
 n_out, k = int(sys.argv[1]), int(sys.argv[2])
 be = Pi05Backend(Pi05Config(), num_blocks=64)
 assert _lib.lib().oxy_debug_gemm_prof_select(n_out, k) == 0
@@ -24,9 +25,9 @@ kv = be.prefill(Pi05Observation(tuple(range(100, 132)), 0, synthetic_images(3, 5
 for _ in range(4):
     be.denoise_many([kv], 10)
 torch.cuda.synchronize()
-buf = (C.c_ulonglong * (32 * 16))()
+buf = (C.c_ulonglong * (32 * 24))()
 assert _lib.lib().oxy_debug_gemm_prof(buf) == 0
-a = np.array(buf, dtype=np.int64).reshape(32, 16)
+a = np.array(buf, dtype=np.int64).reshape(32, 24)
 rows = [i for i in range(32) if a[i, 0] > 0]
 t0 = min(a[i, 0] for i in rows)
 print(f"n_out {n_out} k {k}\nsplit " + " ".join(f"{e:>12s}" for e in EV))

@@ -12,9 +12,12 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CAPTURES = {  # profile_all.sh report name -> (profiles name, description)
     "ncu_lm_head": ("lm_head", "gemm_sm100 (tcgen05) @ LM head 257152x2048, T=6"),
+    "ncu_dn_down": ("dn_down", "gemm_sm100 (tcgen05, split-K 16) @ expert down 1024x4096, T=50"),
+    "ncu_dec_down": ("dec_down", "gemm_sm100 (tcgen05, split-K 9) @ decode down 2048x16384, T=6"),
     "ncu_prefill_gu": ("prefill_gu", "gemm_wide_kernel<2> (tcgen05 cta_group::2) @ prefill gate/up 32768x2048, T=800"),
-    "ncu_decode_attn": ("decode_attn", "decode_attn_v3 @ 64 rows x 1024 ctx"),
+    "ncu_decode_attn": ("decode_attn", "decode attention (TMA ring) @ 256 rows x 1024 ctx"),
     "ncu_flash_tc": ("flash_tc", "flash_tc (tcgen05 attention) @ prefill P=800, 8 heads, 2 key splits"),
+    "ncu_vit_attn": ("vit_attn", "vit_attn_tc (tcgen05 SigLIP attention) @ 3 images x 16 heads x 256 tokens"),
 }
 
 
