@@ -367,6 +367,7 @@ def skinny_gemm_class(cfg, m_decode, r, k, timer, hbm, kind):
     shapes += [(f"denoise.{nm}", n, kk, cfg.H * r, md, cfg.S * cfg.depth)
                for nm, (n, kk), md in zip(names, exp, modes)]
     entries, tot_b, tot_s = {}, 0.0, 0.0
+    traffic = ncu_traffic().get("skinny_shapes", {})
     for name, n, kk, t, mode, per_frame in shapes:
         sp = policy_splits(1, n, kk)
         fn, keep = gemm_launcher(n, kk, t, mode, sp)
@@ -374,7 +375,8 @@ def skinny_gemm_class(cfg, m_decode, r, k, timer, hbm, kind):
         byts = n * kk * 2 + t * kk * 2 + t * (n // 2 if mode == 3 else n) * (4 if mode in (0, 2) else 2)
         entries[name] = {"achieved": byts / sec / 1e9, "frac": byts / sec / 1e9 / hbm, "us": sec * 1e6,
                          "algorithmic_bytes": byts, "shape": f"{n}x{kk} T={t} splits={sp}",
-                         "launches_per_frame": per_frame}
+                         "launches_per_frame": per_frame,
+                         "traffic": traffic.get(name, {}).get("traffic_bytes")}
         tot_b += byts * per_frame
         tot_s += sec * per_frame
         del keep

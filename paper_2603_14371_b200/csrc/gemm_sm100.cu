@@ -102,6 +102,7 @@ struct Knobs {
   int fixup = 0, pdl = 1, smem_kb = 100;  // 2 CTAs per SM (measured best)
   int tma_ws = 0;  // split partials via TMA tensor store (OXY_GEMM_TMA_WS=1; neutral in the frame)
   int bbox_exact = 1;  // B boxes of T rows when T < bn (OXY_GEMM_BBOX_EXACT=0: padded boxes)
+  int band_cap = 0;    // prefill band tile width as a cap on the generic tiling (OXY_GEMM_BAND_CAP=1)
   // early PDL (weight prefetch + trigger) for skinny / wide GEMMs: -1 = default policy
   // (T > 64 on the one-tile-per-CTA kernel: neutral at 1 stream, 0 to -1.3 ms per
   // 8-stream frame and 0 to -1 ms at 16 across same-session A/Bs)
@@ -131,6 +132,7 @@ struct Knobs {
     if (const char *s = getenv("OXY_GEMM_SMEM_KB")) smem_kb = std::max(64, std::min(200, atoi(s)));
     if (const char *s = getenv("OXY_GEMM_TMA_WS")) tma_ws = atoi(s);
     if (const char *s = getenv("OXY_GEMM_BBOX_EXACT")) bbox_exact = atoi(s);
+    if (const char *s = getenv("OXY_GEMM_BAND_CAP")) band_cap = atoi(s);
   }
 };
 // per-enqueue override of the skinny early-PDL policy (-1: knob); set by the
@@ -899,7 +901,9 @@ Plan make_plan(int n_out, int k, int t, int sms, int force_splits) {
   if (knobs().bigk_min <= 0 && dk[0] > 0 && k < dk[0] && dk[3] > 0) dk += 3;  // second band
   if (dk[0] > 0 && k >= dk[0] && t >= 256) {
     p.band = dk == g_deepk + 3 ? 2 : 1;
-    if (dk[1] > 0) p.bn = std::min(MAX_BN, dk[1]);
+    // the band's tile width is a cap when the generic tiling already needed narrower
+    // tiles to fill the SMs (ViT o-proj / fc2: 72 / 108 CTAs at the band width)
+    if (dk[1] > 0) p.bn = knobs().band_cap ? std::min(p.bn, std::min(MAX_BN, dk[1])) : std::min(MAX_BN, dk[1]);
     if (dk[2] > 0 && force_splits <= 0) force_splits = dk[2];
   }
   p.n_tiles = (t + p.bn - 1) / p.bn;
