@@ -142,6 +142,59 @@ __device__ unsigned long long g_attn_prof[32][24];
   } while (0)
 #endif
 
+// Cluster-merge output rows [rb, rb + nr) of a query tile: the gs bf16 partials of
+// each (row, 8 columns) item read over DSMEM from the cluster's staged tiles (4 boxes
+// of 128 rows x 64 bf16, 128B-swizzled), weighted in split order.  GS >= gs; 16 / GS
+// items per thread are loaded before any is combined.
+template <int GS>
+__device__ __forceinline__ void merge_rows(const AttnGroup &g, int q0, int rb, int nr, int gs, uint32_t st_s,
+                                           const float *wgt) {
+  constexpr int IT = 16 / GS, HD = tc::HD, TQ = tc::TQ;
+  const int total = nr * (HD / 8);
+  for (int base = threadIdx.x; base < total; base += blockDim.x * IT) {
+    uint4 v[IT][GS];
+#pragma unroll
+    for (int u = 0; u < IT; ++u) {
+      const int idx = base + u * blockDim.x;
+      const int i = idx / (HD / 8), c8 = idx % (HD / 8), row = rb + i;
+      // 8 bf16 c8 of the row: box c8/8 (64 columns), 16-byte chunk (c8%8) ^ (row%8)
+      const uint32_t off = (c8 >> 3) * (TQ * 128) + row * 128 + (((c8 & 7) ^ (row & 7)) << 4);
+#pragma unroll
+      for (int j = 0; j < GS; ++j)
+        if (idx < total && j < gs)
+          asm volatile("ld.shared::cluster.v4.u32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(v[u][j].x), "=r"(v[u][j].y), "=r"(v[u][j].z), "=r"(v[u][j].w)
+                       : "r"(map_to_rank(st_s + off, j)));
+    }
+#pragma unroll
+    for (int u = 0; u < IT; ++u) {
+      const int idx = base + u * blockDim.x;
+      if (idx >= total) continue;
+      const int i = idx / (HD / 8), c8 = idx % (HD / 8), row = rb + i;
+      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int j = 0; j < GS; ++j)
+        if (j < gs) {  // split order
+          const float w = wgt[i * 16 + j];
+          const uint32_t uu[4] = {v[u][j].x, v[u][j].y, v[u][j].z, v[u][j].w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&uu[e]));
+            acc[2 * e] += w * f.x;
+            acc[2 * e + 1] += w * f.y;
+          }
+        }
+      uint32_t o[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        __nv_bfloat162 h = __floats2bfloat162_rn(acc[2 * e], acc[2 * e + 1]);
+        o[e] = *reinterpret_cast<uint32_t *>(&h);
+      }
+      *reinterpret_cast<uint4 *>(g.o + (size_t)(q0 + row) * g.ldo + c8 * 8) = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+  }
+}
+
 struct TcAttnArgs {
   const AttnGroup *groups;
   int q_tiles, splits, ws_rows;  // splits = grid y = the largest group's split count
@@ -314,6 +367,8 @@ __global__ void __launch_bounds__(192, 1)
         m_ref = mx;
       }
       // PV(i-1) must be complete before O is rescaled and before P is overwritten
+      // (a second P buffer, letting this tile's exp overlap PV(i-1), measured no
+      // faster: the tile pace is K/V ingest, profiles/r02_attn.md)
       if (i > 0) {
         MBW(b_od, (i - 1) & 1, 7);
         tc_fence_after();
@@ -363,6 +418,7 @@ __global__ void __launch_bounds__(192, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive_local(b_pf);
       if (threadIdx.x == 64) APROF(6);
+      if (threadIdx.x == 64 && i >= 2 && i < 6) APROF(18 + i);  // P of tile i written (tiles 2..5)
     }
     // epilogue
     if (n > 0) {
@@ -502,39 +558,13 @@ __global__ void __launch_bounds__(192, 1)
         if (j < gs) wgt[i * 16 + j] = m[j] * inv;
     }
     __syncthreads();
-    for (int idx = threadIdx.x; idx < nr * (HD / 8); idx += blockDim.x) {
-      const int i = idx / (HD / 8), c8 = idx % (HD / 8), row = rb + i;
-      // 8 bf16 c8 of the row: box c8/8 (64 columns), 16-byte chunk (c8%8) ^ (row%8)
-      const uint32_t off = (c8 >> 3) * (TQ * 128) + row * 128 + (((c8 & 7) ^ (row & 7)) << 4);
-      uint4 v[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j)
-        if (j < gs)
-          asm volatile("ld.shared::cluster.v4.u32 {%0, %1, %2, %3}, [%4];"
-                       : "=r"(v[j].x), "=r"(v[j].y), "=r"(v[j].z), "=r"(v[j].w)
-                       : "r"(map_to_rank(st_s + off, j))
-                       : "memory");
-      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int j = 0; j < 16; ++j)
-        if (j < gs) {  // split order
-          const float w = wgt[i * 16 + j];
-          const uint32_t u[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&u[e]));
-            acc[2 * e] += w * f.x;
-            acc[2 * e + 1] += w * f.y;
-          }
-        }
-      uint32_t o[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        __nv_bfloat162 h = __floats2bfloat162_rn(acc[2 * e], acc[2 * e + 1]);
-        o[e] = *reinterpret_cast<uint32_t *>(&h);
-      }
-      *reinterpret_cast<uint4 *>(g.o + (size_t)(q0 + row) * g.ldo + c8 * 8) = make_uint4(o[0], o[1], o[2], o[3]);
-    }
+    // the DSMEM loads of several (row, 8-column) items are in flight before any is
+    // used (a plain loop waited one DSMEM round trip per item: 8 us for the 2-split
+    // prefill tile, profiles/r02_attn.md)
+    if (gs <= 2) merge_rows<2>(g, q0, rb, nr, gs, st_s, wgt);
+    else if (gs <= 4) merge_rows<4>(g, q0, rb, nr, gs, st_s, wgt);
+    else if (gs <= 8) merge_rows<8>(g, q0, rb, nr, gs, st_s, wgt);
+    else merge_rows<16>(g, q0, rb, nr, gs, st_s, wgt);
     if (threadIdx.x == 0) APROF(12);
     cluster_sync_all();  // peers may still be reading this CTA's smem
     if (threadIdx.x == 0) APROF(13);
