@@ -103,6 +103,8 @@ struct Knobs {
   int tma_ws = 0;  // split partials via TMA tensor store (OXY_GEMM_TMA_WS=1; neutral in the frame)
   int bbox_exact = 1;  // B boxes of T rows when T < bn (OXY_GEMM_BBOX_EXACT=0: padded boxes)
   int band_cap = 0;    // prefill band tile width as a cap on the generic tiling (OXY_GEMM_BAND_CAP=1)
+  int wide_fixup = 0;  // persistent kernel: in-kernel split fix-up instead of the reduce launch (A/B)
+  int chain_max_splits = 0;  // cap on the decode / denoise split-K policy (OXY_CHAIN_MAX_SPLITS, A/B)
   // early PDL (weight prefetch + trigger) for skinny / wide GEMMs: -1 = default policy
   // (T > 64 on the one-tile-per-CTA kernel: neutral at 1 stream, 0 to -1.3 ms per
   // 8-stream frame and 0 to -1 ms at 16 across same-session A/Bs)
@@ -133,6 +135,8 @@ struct Knobs {
     if (const char *s = getenv("OXY_GEMM_TMA_WS")) tma_ws = atoi(s);
     if (const char *s = getenv("OXY_GEMM_BBOX_EXACT")) bbox_exact = atoi(s);
     if (const char *s = getenv("OXY_GEMM_BAND_CAP")) band_cap = atoi(s);
+    if (const char *s = getenv("OXY_WIDE_FIXUP")) wide_fixup = atoi(s);
+    if (const char *s = getenv("OXY_CHAIN_MAX_SPLITS")) chain_max_splits = atoi(s);
   }
 };
 // per-enqueue override of the skinny early-PDL policy (-1: knob); set by the
@@ -864,6 +868,7 @@ int policy_splits(int phase, int n_out, int k, int sms) {
     // previous kernel (profiles/r01_gemm_splits.md)
     const int m_tiles = (n_out + BM - 1) / BM;
     s = std::max(1, std::min(knobs().split_slots * sms / m_tiles, kb / 4));
+    if (knobs().chain_max_splits > 0) s = std::min(s, knobs().chain_max_splits);
   }
   s = std::max(1, std::min(s, kb));
   const int per = (kb + s - 1) / s;
@@ -935,6 +940,23 @@ static size_t wide_smem_bytes(const Plan &p) {
   return 1024 + (size_t)p.stages * (A_STAGE_BYTES + p.bn / p.cg * BK * 2) + (2 * MAX_STAGES + 4) * 8 + 16;
 }
 
+// Fixed-order split-K reduction + the real epilogue over [splits][t][n_out] partials.
+static void launch_split_reduce(const float *ws, int splits, int t, int n_out, const EpiParams &epi, cudaStream_t st) {
+  const int64_t n = (int64_t)t * ((n_out + 1) / 2);
+  if (knobs().pdl) {
+    // RoPE: the variant that fetches positions / (cos, sin) before the PDL wait
+    // and keeps all split loads in flight; GeGLU / plain: the simple loop measured
+    // faster in the denoise chain (8.94 vs 9.24 ms per denoise)
+    static const int v = getenv("OXY_REDUCE_V") ? atoi(getenv("OXY_REDUCE_V")) : -1;
+    const bool pre = v < 0 ? epi.mode == EPI_QKV_ROPE : v == 2;
+    launch_pdl(pre ? splitk_reduce_kernel : splitk_reduce_v1_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0,
+               st, ws, splits, t, n_out, epi);
+  } else {
+    splitk_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ws, splits, t, n_out, epi);
+    OXY_LAUNCH_CHECK();
+  }
+}
+
 static void launch_wide(const void *w, const void *x, int n_out, int k, int t, const EpiParams &epi,
                         const Plan &plan, float *ws, int *counters, cudaStream_t st) {
   static bool attr_set = false;
@@ -968,6 +990,12 @@ static void launch_wide(const void *w, const void *x, int n_out, int k, int t, c
   wp.epi = epi;
   wp.ws = ws;
   wp.counters = counters;
+  // split K with a real epilogue: partials only, then the parallel fixed-order reduce
+  // kernel (bit-identical to the in-kernel fix-up, where the last-arriving CTA of a
+  // tile sums and applies the epilogue alone: 487 vs ~50 us for the Gemma qkv + RoPE
+  // and 320 vs ~45 us for the ViT fc2 at T = 6400; OXY_WIDE_FIXUP=1 restores it)
+  const bool reduce_after = plan.splits > 1 && epi.mode != EPI_PARTIALS && !knobs().wide_fixup;
+  if (reduce_after) wp.epi.mode = EPI_PARTIALS;
   const int units = std::min(wp.tiles, sms / (cg * cl));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(units * cg * cl);
@@ -994,6 +1022,7 @@ static void launch_wide(const void *w, const void *x, int n_out, int k, int t, c
   else if (cg == 2) OXY_CUDA(cudaLaunchKernelEx(&cfg, gemm_wide_kernel<2>, ma, mb, wp));
   else OXY_CUDA(cudaLaunchKernelEx(&cfg, gemm_wide_kernel<1>, ma, mb, wp));
   __atomic_fetch_add(&g_launches, 1ull, __ATOMIC_RELAXED);
+  if (reduce_after) launch_split_reduce(ws, plan.splits, t, n_out, epi, st);
 }
 
 void launch(const void *w, const void *x, int n_out, int k, int t, const EpiParams &epi,
@@ -1071,21 +1100,7 @@ void launch(const void *w, const void *x, int n_out, int k, int t, const EpiPara
     gemm_kernel<<<grid, 192, smem_bytes(plan), st>>>(ma, mb, mw, kp);
     OXY_LAUNCH_CHECK();
   }
-  if (plan.splits > 1 && !kp.fixup && epi.mode != EPI_PARTIALS) {
-    const int64_t n = (int64_t)t * ((n_out + 1) / 2);
-    if (knobs().pdl) {
-      // RoPE: the variant that fetches positions / (cos, sin) before the PDL wait
-      // and keeps all split loads in flight; GeGLU / plain: the simple loop measured
-      // faster in the denoise chain (8.94 vs 9.24 ms per denoise)
-      static const int v = getenv("OXY_REDUCE_V") ? atoi(getenv("OXY_REDUCE_V")) : -1;
-      const bool pre = v < 0 ? epi.mode == EPI_QKV_ROPE : v == 2;
-      launch_pdl(pre ? splitk_reduce_kernel : splitk_reduce_v1_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0,
-                 st, ws, plan.splits, t, n_out, epi);
-    } else {
-      splitk_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ws, plan.splits, t, n_out, epi);
-      OXY_LAUNCH_CHECK();
-    }
-  }
+  if (plan.splits > 1 && !kp.fixup && epi.mode != EPI_PARTIALS) launch_split_reduce(ws, plan.splits, t, n_out, epi, st);
 }
 
 // One CTA per token row, one thread per 4 consecutive features (n / 4 threads):

@@ -659,10 +659,13 @@ struct Model {
     return p;
   }
   // key tiles per split: prefill 7 (P = 800: 13 tiles -> 2 splits, 100 CTAs per layer at
-  // 1 stream), expert suffix 1 (P + 50 = 850 keys: 14 single-tile splits merged over a
-  // 14-CTA cluster; measured best at 1 stream).  OXY_ATTN_TPS=prefill,denoise (A/B)
+  // 1 stream), expert suffix 2 (P + 50 = 850 keys: 7 two-tile splits merged over a
+  // 7-CTA cluster).  A group's split count may not depend on how many streams share
+  // the call (batch invariance), so one value serves every stream count: 2 tiles per
+  // split costs 1 stream 0.07 ms per frame against 1 tile and saves 8 streams 3.5 ms
+  // (profiles/r02/policy_ab.txt).  OXY_ATTN_TPS=prefill,denoise (A/B)
   std::pair<int, int> attn_tps = [] {
-    std::pair<int, int> v{7, 1};
+    std::pair<int, int> v{7, 2};
     if (const char *e = getenv("OXY_ATTN_TPS")) sscanf(e, "%d,%d", &v.first, &v.second);
     return v;
   }();
