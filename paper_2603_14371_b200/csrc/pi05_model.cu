@@ -391,8 +391,10 @@ struct Model {
     }
     OXY_CUDA(cudaEventCreate(&alt.t0));
     OXY_CUDA(cudaEventCreate(&alt.t1));
+    init_green();
   }
   void destroy_exec() {
+    destroy_green();
     destroy_lane();
     {
       LaneSwap g(*this);
@@ -403,8 +405,115 @@ struct Model {
     for (DevBuf *b : {&alt.y, &alt.q, &alt.o, &alt.hmid, &alt.ws, &alt.kd, &alt.vd, &alt.attn_ws, &alt.attn_ml})
       b->release();
   }
+  // ---- SM partition of the overlapped section (OXY_GREEN=<expert SMs>, 0 = off).
+  // While a frame's denoise overlaps its decode, the two chains otherwise fight
+  // for SM slots: the decode's long weight-streaming CTAs hold the slots the
+  // expert chain's next kernel needs, and the 209 KB tcgen05 attention needs a
+  // whole SM.  Two green contexts split the SMs; an overlapped denoise of up to
+  // OXY_GREEN_MAX_STREAMS streams runs on one partition and the decode it overlaps
+  // on the other.  Stand-alone calls (prefill, a denoise or decode with nothing
+  // overlapping, multi-stream denoise) keep every SM.  Plans do not change
+  // (split-K partitions depend on (phase, N, K) only), so results are bit-identical
+  // either way.  Measured (profiles/r02/green_ab*.txt): 1 stream 16.6 -> 15.8 ms per
+  // frame with 80 expert SMs (64: 16.2, 72: 15.9, 88: 16.8); 2-8 streams slower with
+  // any split (the expert chain needs the whole GPU), hence the stream cap.
+  struct Green {
+    int dn_sms = 0, dec_sms = 0;
+    cudaStream_t dn = nullptr, dec = nullptr;
+    void *g_dn = nullptr, *g_dec = nullptr;  // CUgreenCtx
+  } green;
+  bool denoise_pending = false;  // an overlapped denoise on the partition was enqueued, not joined yet
+  int green_max_streams = [] {
+    const char *e = getenv("OXY_GREEN_MAX_STREAMS");
+    return e ? atoi(e) : 1;
+  }();
+  void init_green() {
+    const char *e = getenv("OXY_GREEN");
+    const int want = e ? atoi(e) : 80;
+    if (want <= 0 || want >= sms) return;
+    try {
+      make_green(want);
+    } catch (const std::exception &) {  // no green contexts on this driver: one shared SM pool
+      green = Green{};
+    }
+  }
+  void make_green(int want) {
+    typedef CUresult (*GetRes)(CUdevice, CUdevResource *, CUdevResourceType);
+    typedef CUresult (*Split)(CUdevResource *, unsigned *, const CUdevResource *, CUdevResource *, unsigned, unsigned);
+    typedef CUresult (*GenDesc)(CUdevResourceDesc *, CUdevResource *, unsigned);
+    typedef CUresult (*Create)(CUgreenCtx *, CUdevResourceDesc, CUdevice, unsigned);
+    typedef CUresult (*StreamCreate)(CUstream *, CUgreenCtx, unsigned, int);
+    auto sym = [](const char *name) {
+      void *fn = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      OXY_CUDA(cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q));
+      if (!fn || q != cudaDriverEntryPointSuccess) fail(OXY_ECUDA, "%s unavailable", name);
+      return fn;
+    };
+    int dev = 0;
+    OXY_CUDA(cudaGetDevice(&dev));
+    CUdevResource all{}, part[2]{}, rest{};
+    unsigned n = 1;
+    auto chk = [](CUresult r, const char *what) {
+      if (r != CUDA_SUCCESS) fail(OXY_ECUDA, "%s failed (%d)", what, (int)r);
+    };
+    chk(reinterpret_cast<GetRes>(sym("cuDeviceGetDevResource"))((CUdevice)dev, &all, CU_DEV_RESOURCE_TYPE_SM),
+        "cuDeviceGetDevResource");
+    chk(reinterpret_cast<Split>(sym("cuDevSmResourceSplitByCount"))(part, &n, &all, &rest, 0, (unsigned)want),
+        "cuDevSmResourceSplitByCount");
+    CUdevResourceDesc d_dn, d_dec;
+    auto gen = reinterpret_cast<GenDesc>(sym("cuDevResourceGenerateDesc"));
+    chk(gen(&d_dn, &part[0], 1), "cuDevResourceGenerateDesc");
+    chk(gen(&d_dec, &rest, 1), "cuDevResourceGenerateDesc");
+    auto create = reinterpret_cast<Create>(sym("cuGreenCtxCreate"));
+    CUgreenCtx g_dn, g_dec;
+    chk(create(&g_dn, d_dn, (CUdevice)dev, CU_GREEN_CTX_DEFAULT_STREAM), "cuGreenCtxCreate");
+    chk(create(&g_dec, d_dec, (CUdevice)dev, CU_GREEN_CTX_DEFAULT_STREAM), "cuGreenCtxCreate");
+    int lo = 0, hi = 0;
+    OXY_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    auto screate = reinterpret_cast<StreamCreate>(sym("cuGreenCtxStreamCreate"));
+    CUstream s_dn, s_dec;
+    chk(screate(&s_dn, g_dn, CU_STREAM_NON_BLOCKING, hi), "cuGreenCtxStreamCreate");
+    chk(screate(&s_dec, g_dec, CU_STREAM_NON_BLOCKING, lo), "cuGreenCtxStreamCreate");
+    green.dn = reinterpret_cast<cudaStream_t>(s_dn);
+    green.dec = reinterpret_cast<cudaStream_t>(s_dec);
+    green.g_dn = g_dn;
+    green.g_dec = g_dec;
+    green.dn_sms = (int)part[0].sm.smCount;
+    green.dec_sms = (int)rest.sm.smCount;
+  }
+  void destroy_green() {
+    if (!green.g_dn) return;
+    typedef CUresult (*Destroy)(CUgreenCtx);
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuGreenCtxDestroy", &fn, cudaEnableDefault, &q) == cudaSuccess && fn) {
+      cudaStreamDestroy(green.dn);
+      cudaStreamDestroy(green.dec);
+      reinterpret_cast<Destroy>(fn)(static_cast<CUgreenCtx>(green.g_dn));
+      reinterpret_cast<Destroy>(fn)(static_cast<CUgreenCtx>(green.g_dec));
+    }
+    green = Green{};
+  }
+  // run one call of the active lane on a partition stream (graph keys get a suffix:
+  // a graph captured on a partition stream keeps running on that partition)
+  struct StreamScope {
+    Model &m;
+    cudaStream_t prev;
+    bool on;
+    StreamScope(Model &mm, cudaStream_t s) : m(mm), prev(mm.mst), on(s != nullptr) {
+      if (on) m.mst = s;
+    }
+    ~StreamScope() {
+      if (on) m.mst = prev;
+    }
+  };
+
   // the action-expert lane's last denoise: make `caller` wait for it
-  void join_alt(cudaStream_t caller) { OXY_CUDA(cudaStreamWaitEvent(caller, alt.ev_out, 0)); }
+  void join_alt(cudaStream_t caller) {
+    OXY_CUDA(cudaStreamWaitEvent(caller, alt.ev_out, 0));
+    denoise_pending = false;
+  }
   float alt_elapsed_ms() {
     OXY_CUDA(cudaEventSynchronize(alt.t1));
     float ms = 0.f;
@@ -912,10 +1021,12 @@ struct Model {
                bool join = true) {
     OXY_REQUIRE(S >= 1, "denoise step count must be >= 1, got %d", S);
     LaneSwap lane(*this);
+    const bool part = !join && green.dn && n <= green_max_streams;  // overlapped: expert partition
     PlanSms plan_scope(*this, lane_sms.first);
     const int We = c.expert_width, H = c.H, A = c.action_dim, T = n * H, AP = apad();
     ensure_mod(S);
-    std::string key = "denoise/" + std::to_string(S);
+    StreamScope stream_scope(*this, part ? green.dn : nullptr);
+    std::string key = std::string(part ? "denoise-g/" : "denoise/") + std::to_string(S);
     int nb = 0;
     for (int i = 0; i < n; ++i) {
       OXY_REQUIRE(P[i] >= 1, "denoise needs a non-empty prefix");
@@ -1015,6 +1126,7 @@ struct Model {
     OXY_CUDA(cudaEventRecord(alt.t1, mst));
     if (join) leave(caller);
     else OXY_CUDA(cudaEventRecord(ev_out, mst));
+    denoise_pending = part;
   }
 
   // ------------------------------------------------------------ no-cache recompute
@@ -1091,7 +1203,9 @@ struct Model {
       explicit EarlyScope(int v) { gemm::g_early_override = v; }
       ~EarlyScope() { gemm::g_early_override = -1; }
     } early_scope(decode_early);
-    PlanSms plan_scope(*this, lane_sms.second);
+    const bool part = green.dec && denoise_pending;  // overlapping the expert: decode partition
+    PlanSms plan_scope(*this, part ? green.dec_sms : lane_sms.second);
+    StreamScope stream_scope(*this, part ? green.dec : nullptr);
     const int W = c.width;
     // a row appends at most min(k, budget) positions (argmax_update stops it at its
     // budget), so its table only has to cover seq + min(k, budget)
@@ -1182,7 +1296,8 @@ struct Model {
                       mst);
       }
     };
-    const std::string key = "decode/" + std::to_string(rows) + "," + std::to_string(k) + "," + std::to_string(maxb);
+    const std::string key = std::string(part ? "decode-g/" : "decode/") + std::to_string(rows) + "," +
+                            std::to_string(k) + "," + std::to_string(maxb);
     run_body(key, logits_h == nullptr, body);
     OXY_CUDA(cudaMemcpyAsync(out_tok_h, d_out, (size_t)rows * k * sizeof(int), cudaMemcpyDeviceToHost, mst));
     OXY_CUDA(cudaMemcpyAsync(out_cnt_h, d_cnt, rows * sizeof(int), cudaMemcpyDeviceToHost, mst));
