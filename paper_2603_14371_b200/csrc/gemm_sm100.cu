@@ -102,7 +102,9 @@ struct Knobs {
   int fixup = 0, pdl = 1, smem_kb = 100;  // 2 CTAs per SM (measured best)
   int tma_ws = 0;  // split partials via TMA tensor store (OXY_GEMM_TMA_WS=1; neutral in the frame)
   int bbox_exact = 1;  // B boxes of T rows when T < bn (OXY_GEMM_BBOX_EXACT=0: padded boxes)
-  int band_cap = 0;    // prefill band tile width as a cap on the generic tiling (OXY_GEMM_BAND_CAP=1)
+  // prefill band tile width as a cap on the generic tiling: ViT o-proj / fc2 go from 72 /
+  // 108 to 144 CTAs (prefill 6.14 -> 5.97 ms, profiles/r02/prefill_ab2.txt; =0: off)
+  int band_cap = 1;
   int wide_fixup = 0;  // persistent kernel: in-kernel split fix-up instead of the reduce launch (A/B)
   int chain_max_splits = 0;  // cap on the decode / denoise split-K policy (OXY_CHAIN_MAX_SPLITS, A/B)
   // early PDL (weight prefetch + trigger) for skinny / wide GEMMs: -1 = default policy
