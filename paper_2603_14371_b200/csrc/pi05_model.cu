@@ -423,6 +423,7 @@ struct Model {
     void *g_dn = nullptr, *g_dec = nullptr;  // CUgreenCtx
   } green;
   bool denoise_pending = false;  // an overlapped denoise on the partition was enqueued, not joined yet
+  bool on_partition = false;     // the call being enqueued runs on a green-context partition
   int green_max_streams = [] {
     const char *e = getenv("OXY_GREEN_MAX_STREAMS");
     return e ? atoi(e) : 1;
@@ -502,10 +503,16 @@ struct Model {
     cudaStream_t prev;
     bool on;
     StreamScope(Model &mm, cudaStream_t s) : m(mm), prev(mm.mst), on(s != nullptr) {
-      if (on) m.mst = s;
+      if (on) {
+        m.mst = s;
+        m.on_partition = true;
+      }
     }
     ~StreamScope() {
-      if (on) m.mst = prev;
+      if (on) {
+        m.mst = prev;
+        m.on_partition = false;
+      }
     }
   };
 
@@ -786,7 +793,10 @@ struct Model {
       wo = attn_ws.as<float>((size_t)p.splits * p.rows * 256);
       wml = attn_ml.as<float>((size_t)p.splits * p.rows * 2);
     }
-    const bool cm = p.splits > 1 && p.splits <= attn_cluster_merge_max();
+    // inside an SM partition (green context) only portable clusters (<= 8 CTAs) are sure
+    // to be schedulable; larger split counts merge through the workspace (same arithmetic)
+    const int cmax = on_partition ? std::min(8, attn_cluster_merge_max()) : attn_cluster_merge_max();
+    const bool cm = p.splits > 1 && p.splits <= cmax;
     flash_attention_tc(p.groups, p.n, p.q_tiles, p.splits, p.tps, q_base, q_rows, kv_maps[2 * layer],
                        kv_maps[2 * layer + 1], kd, vd, kd_rows, 1.f / 16.f, wo, wml, p.rows, kv_ready, cm, mst);
     if (p.splits > 1 && !cm && !(dbg_skip & 4))

@@ -238,3 +238,28 @@ def test_full_cross_variant_uniform_r2(full):
         for rid, entry in base.items():
             assert runs[v][rid].tokens == entry.tokens, (v, rid)
             assert runs[v][rid].action == entry.action, (v, rid)
+
+
+@pytest.mark.parametrize("obs_len", [150, 1100])
+def test_full_cross_variant_one_stream_on_sm_partition(full, obs_len):
+    """Acceptance criterion 3 at full shape with one stream per frame: Unified runs each
+    frame's denoise on the expert SM partition (green context) overlapping the decode on
+    the other partition; IsolatedSequential runs every stage alone on all SMs.  Same
+    requests, tokens and action chunks, exactly — the partition changes no plan.  At
+    obs_len 1100 the expert attention has 9 key splits: merged over a 9-CTA cluster on
+    all SMs but through the workspace inside the partition (portable clusters only) —
+    the two merges must agree bit for bit."""
+    from paper_2603_14371_b200 import BackendConfig
+    from paper_2603_14371_b200.sim_engine import SimConfig, run_simulation
+    from paper_2603_14371_b200.workload import WorkloadSpec
+    be, _ = full
+    wl = WorkloadSpec(pattern="OnePerFrame", default_N=7, obs_len=obs_len, num_frames=4, seed=78)
+    bc = BackendConfig(vocab=be.config.vocab)
+    runs = {v: run_simulation(SimConfig(variant=v, backend_kind="Pi05", backend_config=bc, workload=wl, k=3),
+                              backend=be).transcript
+            for v in ("Unified", "IsolatedSequential")}
+    base = runs["Unified"]
+    assert len(base) == 4 and sorted(runs["IsolatedSequential"]) == sorted(base)
+    for rid, entry in base.items():
+        assert runs["IsolatedSequential"][rid].tokens == entry.tokens, rid
+        assert runs["IsolatedSequential"][rid].action == entry.action, rid

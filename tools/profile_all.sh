@@ -4,7 +4,7 @@
 set -x
 mkdir -p gpurun_out
 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
-ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
+OXY_GREEN=0 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/frame_launches.csv python tools/profile_frame.py > gpurun_out/pf.log 2>&1
 python tools/summarize_launches.py gpurun_out/frame_launches.csv > gpurun_out/frame_summary.txt
 full="ncu --set full --clock-control none --import-source on"

@@ -1,9 +1,13 @@
 """Run warm-up frames, then ONE steady frame inside cudaProfilerStart/Stop so
 `ncu --profile-from-start off` sees exactly one frame's kernels.
 
-    ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none \
+    OXY_GREEN=0 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none \
         --csv --log-file gpurun_out/frame_launches.csv python tools/profile_frame.py
     python tools/summarize_launches.py gpurun_out/frame_launches.csv
+
+OXY_GREEN=0: cudaProfilerStart scopes the primary context, and the overlapped
+denoise / decode otherwise run in their green-context SM partitions (the launch
+list is serialised under ncu either way).
 """
 
 import os
