@@ -394,12 +394,12 @@ struct Model {
     init_green();
   }
   void destroy_exec() {
-    destroy_green();
     destroy_lane();
     {
       LaneSwap g(*this);
       destroy_lane();
     }
+    destroy_green();  // after the graphs captured on its streams
     if (alt.t0) cudaEventDestroy(alt.t0);
     if (alt.t1) cudaEventDestroy(alt.t1);
     for (DevBuf *b : {&alt.y, &alt.q, &alt.o, &alt.hmid, &alt.ws, &alt.kd, &alt.vd, &alt.attn_ws, &alt.attn_ml})
