@@ -107,6 +107,8 @@ struct Knobs {
   int band_cap = 1;
   int wide_fixup = 0;  // persistent kernel: in-kernel split fix-up instead of the reduce launch (A/B)
   int chain_max_splits = 0;  // cap on the decode / denoise split-K policy (OXY_CHAIN_MAX_SPLITS, A/B)
+  int kdual = 1;  // split-2 plans on the persistent kernel accumulate both K halves in-CTA (OXY_KDUAL=0: off)
+  int kdual_bn = 0;  // cap on the token tile of kdual plans (128 keeps two accumulators; A/B)
   // early PDL (weight prefetch + trigger) for skinny / wide GEMMs: -1 = default policy
   // (T > 64 on the one-tile-per-CTA kernel: neutral at 1 stream, 0 to -1.3 ms per
   // 8-stream frame and 0 to -1 ms at 16 across same-session A/Bs)
@@ -139,6 +141,8 @@ struct Knobs {
     if (const char *s = getenv("OXY_GEMM_BAND_CAP")) band_cap = atoi(s);
     if (const char *s = getenv("OXY_WIDE_FIXUP")) wide_fixup = atoi(s);
     if (const char *s = getenv("OXY_CHAIN_MAX_SPLITS")) chain_max_splits = atoi(s);
+    if (const char *s = getenv("OXY_KDUAL")) kdual = atoi(s);
+    if (const char *s = getenv("OXY_KDUAL_BN")) kdual_bn = atoi(s);
   }
 };
 // per-enqueue override of the skinny early-PDL policy (-1: knob); set by the
@@ -536,9 +540,22 @@ __device__ __forceinline__ void mma_commit_mask(uint32_t bar, uint16_t mask) {
 // pair computes a 256-feature x BN-token tile with tcgen05.mma.cta_group::2:
 // each CTA stages its 128 weight rows and BN/2 token rows per stage, so the
 // smem/L2 bytes per MAC halve against the 1-CTA tile.
+// The two K-half accumulators of a kdual tile, summed p0 + p1 (the split reduce's order).
+struct DualTmemSrc {
+  uint32_t t0, t1;
+  __device__ __forceinline__ void operator()(int c, int, uint32_t (&v)[16]) const {
+    uint32_t w[16];
+    tmem_ld16(t0 + (uint32_t)c, v);
+    tmem_ld16(t1 + (uint32_t)c, w);
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = __float_as_uint(__fadd_rn(__uint_as_float(v[e]), __uint_as_float(w[e])));
+  }
+};
+
 struct WParams {
   int n_out, k, t, bn, stages, kb_total;
   int m_tiles, n_tiles, splits, kb_per_split, tiles;
+  int kdual;  // splits == 2 done in-CTA: tiles are (m, n) only, K half h -> accumulator region h
   EpiParams epi;
   float *ws;
   int *counters;  // one per (tile, CTA of the pair); self-resetting
@@ -574,8 +591,12 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
   const int ngr = (p.n_tiles + CL - 1) / CL;  // token-tile groups (one tile per pair)
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + MAX_STAGES),
                  tfull0 = smem_u32(bars + 2 * MAX_STAGES), tempty0 = smem_u32(bars + 2 * MAX_STAGES + 2);
-  const uint32_t ncols = bn <= 128 ? (bn <= 64 ? 128u : 256u) : 512u;  // two accumulators
-  const uint32_t acc_stride = ncols / 2;
+  // two accumulators (tile i's epilogue overlaps tile i+1's mainloop); kdual: two regions
+  // (K halves) each — for bn > 128 only one accumulator then (no epilogue overlap)
+  const int nbuf = p.kdual && bn > 128 ? 1 : 2;
+  const uint32_t ncols = p.kdual ? (bn <= 64 ? 256u : 512u) : bn <= 128 ? (bn <= 64 ? 128u : 256u) : 512u;
+  const uint32_t acc_stride = ncols / nbuf, half_stride = acc_stride / 2;
+  const int per_m_split = p.kdual ? 1 : p.splits;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
@@ -608,7 +629,7 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int per_m = p.splits * ngr;
+  const int per_m = per_m_split * ngr;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -621,8 +642,8 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
       for (int tile = unit; tile < p.tiles; tile += units) {
         if (tile + units >= p.tiles) pdl_trigger();  // last tile: let the next kernel get scheduled
         const int mt = tile / per_m, rem = tile % per_m, split = rem / ngr, nt = (rem % ngr) * CL + (int)pp;
-        const int kb0 = split * p.kb_per_split;
-        const int nkb = min(p.kb_total, kb0 + p.kb_per_split) - kb0;
+        const int kb0 = p.kdual ? 0 : split * p.kb_per_split;
+        const int nkb = p.kdual ? p.kb_total : min(p.kb_total, kb0 + p.kb_per_split) - kb0;
         const int arow = mt * BM * CG + (int)rank * BM + (CL == 2 ? (int)pp * (BM / 2) : 0),
                   brow = nt * bn + (int)rank * b_rows;
         for (int i = 0; i < nkb; ++i, ++it) {
@@ -658,24 +679,29 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
       int it = 0, lt = 0;
       for (int tile = unit; tile < p.tiles; tile += units, ++lt) {
         const int rem = tile % per_m, split = rem / ngr;
-        const int kb0 = split * p.kb_per_split;
-        const int nkb = min(p.kb_total, kb0 + p.kb_per_split) - kb0;
-        const int acc = lt & 1;
-        mbar_wait(tempty0 + 8 * acc, ((lt >> 1) & 1) ^ 1);
+        const int kb0 = p.kdual ? 0 : split * p.kb_per_split;
+        const int nkb = p.kdual ? p.kb_total : min(p.kb_total, kb0 + p.kb_per_split) - kb0;
+        const int acc = lt % nbuf;
+        mbar_wait(tempty0 + 8 * acc, ((lt / nbuf) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t d = tmem + (uint32_t)acc * acc_stride;
+        const uint32_t d0 = tmem + (uint32_t)acc * acc_stride;
         for (int i = 0; i < nkb; ++i, ++it) {
           const int s = it % stages;
           const uint32_t ph = (it / stages) & 1;
           mbar_wait(full0 + 8 * s, ph);
           tc_fence_after();
           const uint32_t a = smem_u32(sA + s * A_STAGE_BYTES), b = smem_u32(sB + s * b_bytes);
+          // kdual: k-blocks of the second K half accumulate into the second region, each
+          // half from zero — the split-2 partials, kept in TMEM
+          const bool hi = p.kdual && i >= p.kb_per_split;
+          const uint32_t d = d0 + (hi ? half_stride : 0u);
+          const int i0 = hi ? i - p.kb_per_split : i;
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
             if (CG == 2)
-              mma_bf16_pair(d, make_sdesc(a + kk * 32), make_sdesc(b + kk * 32), idesc, (i | kk) != 0 ? 1u : 0u);
+              mma_bf16_pair(d, make_sdesc(a + kk * 32), make_sdesc(b + kk * 32), idesc, (i0 | kk) != 0 ? 1u : 0u);
             else
-              mma_bf16(d, make_sdesc(a + kk * 32), make_sdesc(b + kk * 32), idesc, (i | kk) != 0 ? 1u : 0u);
+              mma_bf16(d, make_sdesc(a + kk * 32), make_sdesc(b + kk * 32), idesc, (i0 | kk) != 0 ? 1u : 0u);
           }
           if (CG == 2) mma_commit_mask(empty0 + 8 * s, all_mask);  // both pairs may refill the stage
           else mma_commit(empty0 + 8 * s);
@@ -691,25 +717,27 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
     const int q = warp & 3, half = (warp - 2) >> 2;
     const int chunks = bn / 16, c_mid = ((chunks + 1) / 2) * 16;
     const int cb = half ? c_mid : 0, ce = half ? bn : c_mid;
-    const bool split_out = p.splits > 1;
+    // kdual: the summed halves take the real epilogue, or leave as ONE partial slab
+    const bool split_out = p.kdual ? p.epi.mode == EPI_PARTIALS : p.splits > 1;
     const uint32_t tempty_l = CG == 2 ? map_to_rank(tempty0, 2 * pp) : tempty0;
     int lt = 0;
     for (int tile = unit; tile < p.tiles; tile += units, ++lt) {
       const int mt = tile / per_m, rem = tile % per_m, split = rem / ngr, nt = (rem % ngr) * CL + (int)pp;
-      const int acc = lt & 1;
-      mbar_wait(tfull0 + 8 * acc, (lt >> 1) & 1);
+      const int acc = lt % nbuf;
+      mbar_wait(tfull0 + 8 * acc, (lt / nbuf) & 1);
       tc_fence_after();
       const int f = mt * BM * CG + (int)rank * BM + q * 32 + lane;
       const int n0 = nt * bn;
       const uint32_t trow = tmem + (uint32_t)acc * acc_stride + ((uint32_t)(q * 32) << 16);
-      epi_tile(p, trow, cb, ce, n0, f, split, split_out);
+      if (p.kdual) epi_tile_src(p, DualTmemSrc{trow, trow + half_stride}, cb, ce, n0, f, 0, split_out);
+      else epi_tile(p, trow, cb, ce, n0, f, split, split_out);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
         if (CG == 2) mbar_arrive_cluster(tempty_l + 8 * acc);
         else mbar_arrive_local(tempty0 + 8 * acc);
       }
-      if (split_out && p.epi.mode != EPI_PARTIALS && nt < p.n_tiles)  // (the odd pair of a ragged group idles)
+      if (!p.kdual && split_out && p.epi.mode != EPI_PARTIALS && nt < p.n_tiles)  // (the odd pair of a ragged group idles)
         splitk_fixup(p, (mt * p.n_tiles + nt) * CG + (int)rank, n0, cb, ce, f, s_last, WIDE_THREADS - 64, 64);
     }
   }
@@ -819,6 +847,13 @@ static bool wide_plan(Plan &p, int n_out, int k, int t, int sms, int req_splits)
   p.n_tiles = (t + p.bn - 1) / p.bn;
   const int per_split = (p.kb_total + p.splits - 1) / p.splits;
   p.splits = (p.kb_total + per_split - 1) / per_split;
+  // a fixed split-2 partition (prefill deep-K policy) on the persistent kernel: both K
+  // halves in one CTA (pair), two TMEM regions per accumulator -> token tiles <= 128
+  p.kdual = kn.kdual && req_splits == 2 && p.splits == 2 && p.cl == 1;
+  if (p.kdual && kn.kdual_bn > 0 && p.bn > kn.kdual_bn) {
+    p.bn = kn.kdual_bn;
+    p.n_tiles = (t + p.bn - 1) / p.bn;
+  }
   p.stages = wide_stages(p.bn, p.cg);
   return true;
 }
@@ -988,7 +1023,8 @@ static void launch_wide(const void *w, const void *x, int n_out, int k, int t, c
   wp.n_tiles = plan.n_tiles;
   wp.splits = plan.splits;
   wp.kb_per_split = (plan.kb_total + plan.splits - 1) / plan.splits;
-  wp.tiles = plan.m_tiles * ((plan.n_tiles + cl - 1) / cl) * plan.splits;
+  wp.kdual = plan.kdual;
+  wp.tiles = plan.m_tiles * ((plan.n_tiles + cl - 1) / cl) * (plan.kdual ? 1 : plan.splits);
   wp.epi = epi;
   wp.ws = ws;
   wp.counters = counters;
@@ -996,7 +1032,7 @@ static void launch_wide(const void *w, const void *x, int n_out, int k, int t, c
   // kernel (bit-identical to the in-kernel fix-up, where the last-arriving CTA of a
   // tile sums and applies the epilogue alone: 487 vs ~50 us for the Gemma qkv + RoPE
   // and 320 vs ~45 us for the ViT fc2 at T = 6400; OXY_WIDE_FIXUP=1 restores it)
-  const bool reduce_after = plan.splits > 1 && epi.mode != EPI_PARTIALS && !knobs().wide_fixup;
+  const bool reduce_after = plan.splits > 1 && !plan.kdual && epi.mode != EPI_PARTIALS && !knobs().wide_fixup;
   if (reduce_after) wp.epi.mode = EPI_PARTIALS;
   const int units = std::min(wp.tiles, sms / (cg * cl));
   cudaLaunchConfig_t cfg{};

@@ -108,6 +108,10 @@ struct Plan {
   int cl;  // wide kernel: CTA pairs per cluster sharing (multicasting) the weight tile (1 or 2)
   int band;  // prefill token-tile band applied: 0 none, 1 deep-K, 2 mid-K
   int csk;   // 1: the split CTAs of a tile form one cluster and reduce in-kernel (no reduce launch)
+  int kdual; // persistent kernel, 2 K splits: one CTA (pair) accumulates both K halves of a tile
+             // into two TMEM accumulators and sums them (p0 + p1) in its epilogue — the
+             // split-2 result bit for bit, without the fp32 partial round trip
+  int partials() const { return kdual ? 1 : splits; }  // partial slabs an EPI_PARTIALS launch writes
 };
 
 // Plan classes counted at enqueue time (eager runs and graph captures; replays are

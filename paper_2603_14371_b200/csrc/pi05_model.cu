@@ -680,7 +680,7 @@ struct Model {
       EpiParams e{gemm::EPI_PARTIALS, nullptr, 0, nullptr, nullptr, 0, nullptr, {}};
       gemm::launch(w, xin, n_out, k, t, e, plan, wsp, gemm_counters, mst);
       if (!(dbg_skip & 128))
-        gemm::splitk_residual_norm(wsp, plan.splits, t, n_out, gate, X, n_out, Y, n_out, norm_w, mod_scale,
+        gemm::splitk_residual_norm(wsp, plan.partials(), t, n_out, gate, X, n_out, Y, n_out, norm_w, mod_scale,
                                    mod_shift, 1e-6f, mst);
       return;
     }

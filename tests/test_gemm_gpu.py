@@ -46,7 +46,7 @@ def rand(shape, seed, scale=1.0):
 @pytest.mark.parametrize("n,k,t,splits", [
     (256, 128, 16, 1), (128, 64, 1, 1), (2560, 2048, 1, 0), (2048, 2048, 50, 0),
     (2048, 2048, 800, 0), (200, 136, 37, 1), (384, 512, 300, 3), (1152, 4304, 256, 0),
-    (257152 // 64, 2048, 5, 0),
+    (257152 // 64, 2048, 5, 0), (2048, 2048, 2400, 2), (1152, 4304, 2304, 2),
 ])
 def test_gemm_matches_torch_fp32(n, k, t, splits):
     w = rand((n, k), 1, 0.05)
@@ -124,12 +124,14 @@ def test_bf16_epilogues_ragged(n, k, t, pad):
 
 
 @pytest.mark.parametrize("n,k,splits,mode", [(2560, 2048, 7, 1), (32768, 2048, 1, 3), (2048, 16384, 9, 0),
-                                             (2048, 2048, 2, 2), (1024, 4096, 16, 0)])
+                                             (2048, 2048, 2, 2), (1024, 4096, 16, 0), (2560, 2048, 2, 1),
+                                             (1152, 4304, 2, 2), (2048, 16384, 2, 0)])
 def test_rows_independent_of_token_count(n, k, splits, mode):
     """Batch invariance of the GEMM: with the K partition fixed (the model's
     policy), a token row's output is bit-identical whether it is projected alone
     or inside 12, 64, 96, 400 or 2400 rows (different token tiles, 1- and 2-CTA
-    kernels)."""
+    kernels; at 2400 rows a split-2 partition runs both K halves in one CTA pair,
+    summed in its epilogue instead of through fp32 partials and a reduce launch)."""
     import torch
     w = rand((n, k), 3, 0.02)
     xs = rand((2400, k), 4)
