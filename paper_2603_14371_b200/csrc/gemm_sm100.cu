@@ -107,6 +107,7 @@ struct Knobs {
   int band_cap = 1;
   int wide_fixup = 0;  // persistent kernel: in-kernel split fix-up instead of the reduce launch (A/B)
   int chain_max_splits = 0;  // cap on the decode / denoise split-K policy (OXY_CHAIN_MAX_SPLITS, A/B)
+  int chain_bigk_splits = 0;  // decode down projection (K >= 8192) split count (OXY_CHAIN_BIGK_SPLITS, A/B)
   int kdual = 1;  // split-2 plans on the persistent kernel accumulate both K halves in-CTA (OXY_KDUAL=0: off)
   int kdual_bn = 0;  // cap on the token tile of kdual plans (128 keeps two accumulators; A/B)
   // early PDL (weight prefetch + trigger) for skinny / wide GEMMs: -1 = default policy
@@ -141,6 +142,7 @@ struct Knobs {
     if (const char *s = getenv("OXY_GEMM_BAND_CAP")) band_cap = atoi(s);
     if (const char *s = getenv("OXY_WIDE_FIXUP")) wide_fixup = atoi(s);
     if (const char *s = getenv("OXY_CHAIN_MAX_SPLITS")) chain_max_splits = atoi(s);
+    if (const char *s = getenv("OXY_CHAIN_BIGK_SPLITS")) chain_bigk_splits = atoi(s);
     if (const char *s = getenv("OXY_KDUAL")) kdual = atoi(s);
     if (const char *s = getenv("OXY_KDUAL_BN")) kdual_bn = atoi(s);
   }
@@ -906,6 +908,7 @@ int policy_splits(int phase, int n_out, int k, int sms) {
     const int m_tiles = (n_out + BM - 1) / BM;
     s = std::max(1, std::min(knobs().split_slots * sms / m_tiles, kb / 4));
     if (knobs().chain_max_splits > 0) s = std::min(s, knobs().chain_max_splits);
+    if (knobs().chain_bigk_splits > 0 && k >= 8192) s = knobs().chain_bigk_splits;
   }
   s = std::max(1, std::min(s, kb));
   const int per = (kb + s - 1) / s;

@@ -1031,7 +1031,8 @@ struct Model {
                bool join = true) {
     OXY_REQUIRE(S >= 1, "denoise step count must be >= 1, got %d", S);
     LaneSwap lane(*this);
-    const bool part = !join && green.dn && n <= green_max_streams;  // overlapped: expert partition
+    static const bool force_part = getenv("OXY_GREEN_FORCE") && atoi(getenv("OXY_GREEN_FORCE")) != 0;  // measurement
+    const bool part = (!join || force_part) && green.dn && n <= green_max_streams;  // overlapped: expert partition
     PlanSms plan_scope(*this, lane_sms.first);
     const int We = c.expert_width, H = c.H, A = c.action_dim, T = n * H, AP = apad();
     ensure_mod(S);
@@ -1213,7 +1214,8 @@ struct Model {
       explicit EarlyScope(int v) { gemm::g_early_override = v; }
       ~EarlyScope() { gemm::g_early_override = -1; }
     } early_scope(decode_early);
-    const bool part = green.dec && denoise_pending;  // overlapping the expert: decode partition
+    static const bool force_part = getenv("OXY_GREEN_FORCE") && atoi(getenv("OXY_GREEN_FORCE")) != 0;  // measurement
+    const bool part = green.dec && (denoise_pending || force_part);  // overlapping the expert: decode partition
     PlanSms plan_scope(*this, part ? green.dec_sms : lane_sms.second);
     StreamScope stream_scope(*this, part ? green.dec : nullptr);
     const int W = c.width;
