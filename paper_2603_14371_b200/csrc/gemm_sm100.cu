@@ -27,6 +27,7 @@ struct KParams {
   int trigger;    // 1: launch_dependents once all operand loads are issued
   int csk;        // 1: cluster split-K — the split CTAs of a tile are one cluster (along z)
   int tma_ws;     // 1: split partials leave through a TMA tensor store (tmW) instead of st.global
+  int kmulti;     // > 1: all K partitions of the tile in this CTA, region r = k-block / kb_per_split
   int b_box;      // token rows per B TMA box: bn, or T when one token tile covers T (rows past
                   // it stay stale in smem; their accumulator columns are never stored)
 };
@@ -110,6 +111,7 @@ struct Knobs {
   int chain_bigk_splits = 0;  // decode down projection (K >= 8192) split count (OXY_CHAIN_BIGK_SPLITS, A/B)
   int kdual = 1;  // split-2 plans on the persistent kernel accumulate both K halves in-CTA (OXY_KDUAL=0: off)
   int kdual_bn = 0;  // cap on the token tile of kdual plans (128 keeps two accumulators; A/B)
+  int kmulti = 1;    // chain plans at >= KMULTI_MIN_T tokens: 2-4 splits in-CTA (OXY_KMULTI=0: off)
   // early PDL (weight prefetch + trigger) for skinny / wide GEMMs: -1 = default policy
   // (T > 64 on the one-tile-per-CTA kernel: neutral at 1 stream, 0 to -1.3 ms per
   // 8-stream frame and 0 to -1 ms at 16 across same-session A/Bs)
@@ -145,6 +147,7 @@ struct Knobs {
     if (const char *s = getenv("OXY_CHAIN_BIGK_SPLITS")) chain_bigk_splits = atoi(s);
     if (const char *s = getenv("OXY_KDUAL")) kdual = atoi(s);
     if (const char *s = getenv("OXY_KDUAL_BN")) kdual_bn = atoi(s);
+    if (const char *s = getenv("OXY_KMULTI")) kmulti = atoi(s);
   }
 };
 // per-enqueue override of the skinny early-PDL policy (-1: knob); set by the
@@ -247,6 +250,22 @@ __device__ int g_gemm_prof_sel[2];
   } while (0)
 #endif
 
+// The `n` K-partition accumulators of a kmulti tile, `stride` columns apart, summed in
+// partition order r0 + r1 + ... (the split reduce's order).
+struct MultiTmemSrc {
+  uint32_t t0;
+  int n, stride;
+  __device__ __forceinline__ void operator()(int c, int, uint32_t (&v)[16]) const {
+    tmem_ld16(t0 + (uint32_t)c, v);
+    for (int r = 1; r < n; ++r) {
+      uint32_t w[16];
+      tmem_ld16(t0 + (uint32_t)(c + r * stride), w);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) v[e] = __float_as_uint(__fadd_rn(__uint_as_float(v[e]), __uint_as_float(w[e])));
+    }
+  }
+};
+
 // Greedy-decode epilogue of the LM head (EPI_ARGMAX): per 16-token chunk each
 // warp folds its 32 vocabulary rows per token (butterfly: every lane ends with
 // the warp's (max, lowest id)), the 4 warps meet in smem, and one (max, id) per
@@ -324,12 +343,12 @@ __global__ void __maxnreg__(128)
   // token tiles fastest: the CTAs sharing one weight tile run in the same wave
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * bn, split = blockIdx.z;
   __shared__ int s_last;
-  const int kb0 = split * p.kb_per_split;
-  const int nkb = min(p.kb_total, kb0 + p.kb_per_split) - kb0;
+  const int kb0 = p.kmulti > 1 ? 0 : split * p.kb_per_split;
+  const int nkb = p.kmulti > 1 ? p.kb_total : min(p.kb_total, kb0 + p.kb_per_split) - kb0;
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + MAX_STAGES),
                  done = smem_u32(bars + 2 * MAX_STAGES);
   uint32_t ncols = 32;
-  while (ncols < (uint32_t)bn) ncols <<= 1;
+  while (ncols < (uint32_t)(bn * (p.kmulti > 1 ? p.kmulti : 1))) ncols <<= 1;
   GPROF_INIT();
   if (threadIdx.x == 0) GPROF(0);
 
@@ -400,9 +419,12 @@ __global__ void __maxnreg__(128)
         if (i == 0) GPROF(5);
         if (i > 0 && i < 4) GPROF(15 + i);
         const uint32_t a = smem_u32(sA + s * A_STAGE_BYTES), b = smem_u32(sB + s * b_bytes);
+        // kmulti: k-block i accumulates into region i / kb_per_split, each region from zero
+        const int reg = p.kmulti > 1 ? i / p.kb_per_split : 0, i0 = i - reg * p.kb_per_split;
+        const uint32_t d = tmem + (uint32_t)(reg * bn);
 #pragma unroll
         for (int kk = 0; kk < BK / 16; ++kk)
-          mma_bf16(tmem, make_sdesc(a + kk * 32), make_sdesc(b + kk * 32), idesc, (i | kk) != 0 ? 1u : 0u);
+          mma_bf16(d, make_sdesc(a + kk * 32), make_sdesc(b + kk * 32), idesc, (i0 | kk) != 0 ? 1u : 0u);
         mma_commit(empty0 + 8 * s);
       }
       mma_commit(done);
@@ -415,7 +437,8 @@ __global__ void __maxnreg__(128)
   // the operand ring is idle once `done` fired: 4 x 2.3 KB transpose tiles for the bf16 epilogues
   float *stg = reinterpret_cast<float *>(sA) + q * (16 * STG_LD);
   if (warp >= 2) {
-    const bool split_out = p.splits > 1;
+    // kmulti: the summed partitions take the real epilogue, or leave as ONE partial slab
+    const bool split_out = p.kmulti > 1 ? p.epi.mode == EPI_PARTIALS : p.splits > 1;
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
     pdl_wait();  // the epilogue reads bias/residual/gates and writes outputs
     if (threadIdx.x == 64) GPROF(7);
@@ -461,7 +484,8 @@ __global__ void __maxnreg__(128)
       epi_tile(p, trow, 32, bn, n0, f, split, split_out, stg);
     } else
 #endif
-    epi_tile(p, trow, 0, bn, n0, f, split, split_out, stg);
+    if (p.kmulti > 1) epi_tile_src(p, MultiTmemSrc{trow, p.kmulti, bn}, 0, bn, n0, f, 0, split_out, stg);
+    else epi_tile(p, trow, 0, bn, n0, f, split, split_out, stg);
     if (threadIdx.x == 64) GPROF(9);
     if (split_out && p.fixup) splitk_fixup(p, blockIdx.y * gridDim.x + blockIdx.x, n0, 0, bn, f, s_last, 128, 64);
   }
@@ -972,6 +996,20 @@ Plan make_plan(int n_out, int k, int t, int sms, int force_splits) {
   return p;
 }
 
+Plan make_chain_plan(int n_out, int k, int t, int sms, int splits) {
+  Plan p = make_plan(n_out, k, t, sms, splits);
+  if (knobs().kmulti && p.cg == 0 && t >= KMULTI_MIN_T && p.splits >= 2 && p.splits <= 4) {
+    const int max_bn = 256 / p.splits / 16 * 16;
+    if (p.bn > max_bn) {
+      p.bn = max_bn;
+      p.n_tiles = (t + p.bn - 1) / p.bn;
+    }
+    p.kmulti = p.splits;
+    p.stages = std::max(2, std::min(MAX_STAGES, knobs().smem_kb * 1024 / (A_STAGE_BYTES + p.bn * BK * 2)));
+  }
+  return p;
+}
+
 static size_t smem_bytes(const Plan &p) {
   return 1024 + (size_t)p.stages * (A_STAGE_BYTES + p.bn * BK * 2) + (2 * MAX_STAGES + 1) * 8 + 16;
 }
@@ -1109,7 +1147,10 @@ void launch(const void *w, const void *x, int n_out, int k, int t, const EpiPara
   kp.prefetch = kp.trigger = t <= 64 ? (g_early_override >= 0 ? g_early_override : knobs().early_skinny)
                                      : knobs().early_wide;
   kp.b_box = b_box;
-  kp.csk = plan.csk && plan.splits > 1;
+  kp.kmulti = plan.kmulti > 1 && plan.cg == 0 ? plan.kmulti : 0;
+  if (kp.kmulti && (plan.bn * kp.kmulti > 256 || kp.kmulti != plan.splits))
+    fail(OXY_EINVAL, "in-CTA split-K: %d partitions x %d token columns", kp.kmulti, plan.bn);
+  kp.csk = plan.csk && plan.splits > 1 && !plan.kmulti;
   if (epi.mode == EPI_ARGMAX && (plan.splits != 1 || !epi.amax_idx))
     fail(OXY_EINVAL, "argmax LM head: unsplit plan and an index buffer required");
   if (epi.norm.y && !(kp.csk && t <= NORM_FUSE_MAX_T && (epi.mode == EPI_ADD_F32 || epi.mode == EPI_ADD_GATED_F32)))
@@ -1118,11 +1159,11 @@ void launch(const void *w, const void *x, int n_out, int k, int t, const EpiPara
     fail(OXY_EINVAL, "fused row norm: rows of 128..2048 features (multiple of 128), strides multiple of 4");
   // TMA-stored partials: [splits][t][n_out] fp32, box 128 features x bn tokens x 1 split
   // (staged in the operand ring, which must hold the 128 x bn fp32 tile)
-  kp.tma_ws = plan.splits > 1 && !kp.fixup && !kp.csk && knobs().tma_ws &&
+  kp.tma_ws = plan.splits > 1 && !kp.kmulti && !kp.fixup && !kp.csk && knobs().tma_ws &&
               (size_t)BM * plan.bn * 4 <= (size_t)plan.stages * (A_STAGE_BYTES + plan.bn * BK * 2) &&
               (n_out * 4) % 16 == 0;
   const CUtensorMap mw = kp.tma_ws ? make_map_ws(ws, plan.splits, t, n_out, plan.bn) : ma;
-  dim3 grid(plan.n_tiles, plan.m_tiles, plan.splits);
+  dim3 grid(plan.n_tiles, plan.m_tiles, kp.kmulti ? 1 : plan.splits);
   if (kp.csk) {
     if (plan.splits > CSK_MAX) fail(OXY_EINVAL, "cluster split-K: at most %d splits", CSK_MAX);
     static bool np_set = false;
@@ -1141,7 +1182,8 @@ void launch(const void *w, const void *x, int n_out, int k, int t, const EpiPara
     gemm_kernel<<<grid, 192, smem_bytes(plan), st>>>(ma, mb, mw, kp);
     OXY_LAUNCH_CHECK();
   }
-  if (plan.splits > 1 && !kp.fixup && epi.mode != EPI_PARTIALS) launch_split_reduce(ws, plan.splits, t, n_out, epi, st);
+  if (plan.splits > 1 && !kp.kmulti && !kp.fixup && epi.mode != EPI_PARTIALS)
+    launch_split_reduce(ws, plan.splits, t, n_out, epi, st);
 }
 
 // One CTA per token row, one thread per 4 consecutive features (n / 4 threads):

@@ -111,7 +111,10 @@ struct Plan {
   int kdual; // persistent kernel, 2 K splits: one CTA (pair) accumulates both K halves of a tile
              // into two TMEM accumulators and sums them (p0 + p1) in its epilogue — the
              // split-2 result bit for bit, without the fp32 partial round trip
-  int partials() const { return kdual ? 1 : splits; }  // partial slabs an EPI_PARTIALS launch writes
+  int kmulti;  // one-tile kernel: the `splits` K partitions of a tile accumulated by ONE CTA into
+              // `splits` TMEM regions and summed in split order in its epilogue (no partials,
+              // no reduce launch; bit-identical to split CTAs + reduce).  0 = split CTAs.
+  int partials() const { return kdual || kmulti ? 1 : splits; }  // partial slabs an EPI_PARTIALS launch writes
 };
 
 // Plan classes counted at enqueue time (eager runs and graph captures; replays are
@@ -152,6 +155,10 @@ int policy_splits(int phase, int n_out, int k, int sms);
 // Host: build a plan for (N_out, K, T) on `sms` SMs.  force_splits > 0 fixes the K
 // partition (every kernel variant honours it); 0 = pick for speed (C ABI tests).
 Plan make_plan(int n_out, int k, int t, int sms, int force_splits = 0);
+// chain-phase variant: for token counts >= KMULTI_MIN_T (>= 11 streams) and 2..4 splits,
+// accumulate the splits in-CTA (Plan::kmulti) with token tiles of <= 256 / splits
+Plan make_chain_plan(int n_out, int k, int t, int sms, int splits);
+constexpr int KMULTI_MIN_T = 512;
 
 // Host: launch.  ws must hold splits * T * N_out floats when splits > 1.
 void launch(const void *w, const void *x, int n_out, int k, int t, const EpiParams &epi,

@@ -631,8 +631,11 @@ struct Model {
     return e && atoi(e) != 0;
   }();
   gemm::Plan plan_for(int n_out, int k, int t) const {
-    gemm::Plan p = gemm::make_plan(n_out, k, t, psms(), gemm::policy_splits(phase, n_out, k, sms));
-    p.csk = use_csk && phase == gemm::PH_CHAIN && p.cg == 0 && p.splits >= 2 && p.splits <= gemm::CSK_MAX;
+    const int sp = gemm::policy_splits(phase, n_out, k, sms);
+    gemm::Plan p = phase == gemm::PH_CHAIN ? gemm::make_chain_plan(n_out, k, t, psms(), sp)
+                                           : gemm::make_plan(n_out, k, t, psms(), sp);
+    p.csk = use_csk && !p.kmulti && phase == gemm::PH_CHAIN && p.cg == 0 && p.splits >= 2 &&
+            p.splits <= gemm::CSK_MAX;
     return p;
   }
   // split-K workspace is reserved by plan_gemm(); gemm() only fetches it
