@@ -6,6 +6,8 @@
 // {A 128x64, B BNx64} bf16 tiles with full/empty mbarriers; tcgen05.commit
 // releases a stage when the MMAs that read it retire.
 #include <algorithm>
+#include <array>
+#include <vector>
 #include <cstdio>
 #include <cstdlib>
 #include <string>
@@ -112,6 +114,7 @@ struct Knobs {
   int kdual = 1;  // split-2 plans on the persistent kernel accumulate both K halves in-CTA (OXY_KDUAL=0: off)
   int kdual_bn = 0;  // cap on the token tile of kdual plans (128 keeps two accumulators; A/B)
   int kmulti = 1;    // chain plans at >= KMULTI_MIN_T tokens: 2-4 splits in-CTA (OXY_KMULTI=0: off)
+  std::vector<std::array<int, 3>> split_overrides;  // OXY_SPLITS="n,k,s;...": chain split count per shape (A/B)
   // early PDL (weight prefetch + trigger) for skinny / wide GEMMs: -1 = default policy
   // (T > 64 on the one-tile-per-CTA kernel: neutral at 1 stream, 0 to -1.3 ms per
   // 8-stream frame and 0 to -1 ms at 16 across same-session A/Bs)
@@ -148,6 +151,17 @@ struct Knobs {
     if (const char *s = getenv("OXY_KDUAL")) kdual = atoi(s);
     if (const char *s = getenv("OXY_KDUAL_BN")) kdual_bn = atoi(s);
     if (const char *s = getenv("OXY_KMULTI")) kmulti = atoi(s);
+    if (const char *s = getenv("OXY_SPLITS")) {
+      std::string v(s);
+      size_t pos = 0;
+      while (pos < v.size()) {
+        size_t e = v.find(';', pos);
+        if (e == std::string::npos) e = v.size();
+        std::array<int, 3> o{};
+        if (sscanf(v.substr(pos, e - pos).c_str(), "%d,%d,%d", &o[0], &o[1], &o[2]) == 3) split_overrides.push_back(o);
+        pos = e + 1;
+      }
+    }
   }
 };
 // per-enqueue override of the skinny early-PDL policy (-1: knob); set by the
@@ -933,6 +947,14 @@ int policy_splits(int phase, int n_out, int k, int sms) {
     s = std::max(1, std::min(knobs().split_slots * sms / m_tiles, kb / 4));
     if (knobs().chain_max_splits > 0) s = std::min(s, knobs().chain_max_splits);
     if (knobs().chain_bigk_splits > 0 && k >= 8192) s = knobs().chain_bigk_splits;
+    // measured per-shape choices for the action expert's K = 1024 projections (the
+    // partitioned 1-stream denoise and the 8-stream frame, profiles/r02/split_ab*.txt):
+    // gate/up 8192 x 1024 unsplit (the GeGLU epilogue in the GEMM, no reduce launch),
+    // qkv 2560 x 1024 in 8 (more CTAs streaming its 5 MB)
+    if (k == 1024 && n_out == 8192) s = 1;
+    if (k == 1024 && n_out == 2560) s = 8;
+    for (const auto &o : knobs().split_overrides)  // OXY_SPLITS="n,k,s;..." (A/B)
+      if (o[0] == n_out && o[1] == k) s = o[2];
   }
   s = std::max(1, std::min(s, kb));
   const int per = (kb + s - 1) / s;
