@@ -114,7 +114,8 @@ struct Knobs {
   int kdual = 1;  // split-2 plans on the persistent kernel accumulate both K halves in-CTA (OXY_KDUAL=0: off)
   int kdual_bn = 0;  // cap on the token tile of kdual plans (128 keeps two accumulators; A/B)
   int kmulti = 1;    // chain plans at >= KMULTI_MIN_T tokens: 2-4 splits in-CTA (OXY_KMULTI=0: off)
-  std::vector<std::array<int, 3>> split_overrides;  // OXY_SPLITS="n,k,s;...": chain split count per shape (A/B)
+  std::vector<std::array<int, 3>> split_overrides;  // OXY_SPLITS="n,k,s;...": chain split count per shape,
+                                                    // n < 0: prefill entry for |n| (A/B)
   // early PDL (weight prefetch + trigger) for skinny / wide GEMMs: -1 = default policy
   // (T > 64 on the one-tile-per-CTA kernel: neutral at 1 stream, 0 to -1.3 ms per
   // 8-stream frame and 0 to -1 ms at 16 across same-session A/Bs)
@@ -938,6 +939,8 @@ int policy_splits(int phase, int n_out, int k, int sms) {
     // down residual + RMSNorm fuse into the split reduce; the gate/up projections
     // (n_out >= 16384) run on the persistent 2-CTA kernel unsplit
     s = (k >= 2048 && n_out < 16384) ? 2 : 1;
+    for (const auto &o : knobs().split_overrides)  // OXY_SPLITS="-n,k,s": prefill entries (A/B)
+      if (o[0] == -n_out && o[1] == k) s = o[2];
   } else {
     // skinny chains: split K until the weight tiles of one token tile fill the SMs.
     // Inside the PDL chain every split CTA streams its weight ring before
