@@ -950,12 +950,12 @@ int policy_splits(int phase, int n_out, int k, int sms) {
     s = std::max(1, std::min(knobs().split_slots * sms / m_tiles, kb / 4));
     if (knobs().chain_max_splits > 0) s = std::min(s, knobs().chain_max_splits);
     if (knobs().chain_bigk_splits > 0 && k >= 8192) s = knobs().chain_bigk_splits;
-    // measured per-shape choices for the action expert's K = 1024 projections (the
+    // measured per-shape choice for the action expert's gate/up 8192 x 1024 (the
     // partitioned 1-stream denoise and the 8-stream frame, profiles/r02/split_ab*.txt):
-    // gate/up 8192 x 1024 unsplit (the GeGLU epilogue in the GEMM, no reduce launch),
-    // qkv 2560 x 1024 in 8 (more CTAs streaming its 5 MB)
+    // unsplit, the GeGLU epilogue in the GEMM and no reduce launch.  (qkv in 8 was
+    // 0.02 ms faster at 1 stream but takes it off the in-CTA split path at >= 16
+    // streams, where its 8 fp32 partial slabs cost 3-10 ms per frame.)
     if (k == 1024 && n_out == 8192) s = 1;
-    if (k == 1024 && n_out == 2560) s = 8;
     for (const auto &o : knobs().split_overrides)  // OXY_SPLITS="n,k,s;..." (A/B)
       if (o[0] == n_out && o[1] == k) s = o[2];
   }
