@@ -148,15 +148,16 @@ __device__ unsigned long long g_attn_prof[32][24];
 // items per thread are loaded before any is combined.
 template <int GS>
 __device__ __forceinline__ void merge_rows(const AttnGroup &g, int q0, int rb, int nr, int gs, uint32_t st_s,
-                                           const float *wgt) {
-  constexpr int IT = 16 / GS, HD = tc::HD, TQ = tc::TQ;
-  const int total = nr * (HD / 8);
+                                           const float *wgt, int ndb, int db0) {
+  constexpr int IT = 16 / GS, TQ = tc::TQ;
+  const int cpr = ndb * 8;  // 8-column chunks per row of this CTA's dim range
+  const int total = nr * cpr;
   for (int base = threadIdx.x; base < total; base += blockDim.x * IT) {
     uint4 v[IT][GS];
 #pragma unroll
     for (int u = 0; u < IT; ++u) {
       const int idx = base + u * blockDim.x;
-      const int i = idx / (HD / 8), c8 = idx % (HD / 8), row = rb + i;
+      const int i = idx / cpr, c8 = idx % cpr, row = rb + i;
       // 8 bf16 c8 of the row: box c8/8 (64 columns), 16-byte chunk (c8%8) ^ (row%8)
       const uint32_t off = (c8 >> 3) * (TQ * 128) + row * 128 + (((c8 & 7) ^ (row & 7)) << 4);
 #pragma unroll
@@ -170,7 +171,7 @@ __device__ __forceinline__ void merge_rows(const AttnGroup &g, int q0, int rb, i
     for (int u = 0; u < IT; ++u) {
       const int idx = base + u * blockDim.x;
       if (idx >= total) continue;
-      const int i = idx / (HD / 8), c8 = idx % (HD / 8), row = rb + i;
+      const int i = idx / cpr, c8 = idx % cpr, row = rb + i;
       float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int j = 0; j < GS; ++j)
@@ -190,7 +191,8 @@ __device__ __forceinline__ void merge_rows(const AttnGroup &g, int q0, int rb, i
         __nv_bfloat162 h = __floats2bfloat162_rn(acc[2 * e], acc[2 * e + 1]);
         o[e] = *reinterpret_cast<uint32_t *>(&h);
       }
-      *reinterpret_cast<uint4 *>(g.o + (size_t)(q0 + row) * g.ldo + c8 * 8) = make_uint4(o[0], o[1], o[2], o[3]);
+      *reinterpret_cast<uint4 *>(g.o + (size_t)(q0 + row) * g.ldo + db0 * 64 + c8 * 8) =
+          make_uint4(o[0], o[1], o[2], o[3]);
     }
   }
 }
@@ -202,6 +204,7 @@ struct TcAttnArgs {
   const bf16 *q_base, *kd_base;  // row offsets of the groups' q / dense k,v pointers
   int kv_ready;  // 1: the paged K/V were not written by the previous kernel (prefetch before the PDL wait)
   int cmerge;    // 1: launched as clusters of `splits` CTAs along y, merge over DSMEM
+  int dsplit;    // 1 or 2: grid z = head-dim halves of V / O (each CTA: full S, PV over its half)
   float scale_log2;
   float *ws_o, *ws_ml;
 };
@@ -226,6 +229,10 @@ __global__ void __launch_bounds__(192, 1)
   const int qt = blockIdx.x % a.q_tiles, q0 = qt * TQ;
   if (q0 >= g.nq) return;  // uniform per CTA, before any barrier or TMEM use
   const int split = blockIdx.y;
+  // dim split: this CTA computes S and the softmax over all 256 dims but P.V (and the
+  // merge / output) only for V-dim boxes [db0, db0 + ndb): half the V ingest and half the
+  // merge volume per CTA, twice the CTAs; every output element's arithmetic is unchanged
+  const int ndb = 4 / a.dsplit, db0 = blockIdx.z * ndb, dw = ndb * 64;
   const int ta = (g.nka + TK - 1) / TK, tb = (g.nkb + TK - 1) / TK, tiles = ta + tb;
   // this group's own key partition (a function of its key count only: batch-invariant);
   // CTAs past it (split >= gs) idle, or only help with the cluster merge
@@ -271,13 +278,14 @@ __global__ void __launch_bounds__(192, 1)
       auto issue = [&](int i) {
         const int j = t0 + i, s = i & 1;
         MBW(b_kve + 8 * s, ((i >> 1) & 1) ^ 1, 1);
-        mbar_expect_tx(b_kvf + 8 * s, 2 * KV_BYTES);
+        mbar_expect_tx(b_kvf + 8 * s, KV_BYTES + ndb * KV_BOX);
         const bool paged = j < ta;
         const int row = paged ? g.bt[j] * TK : drow0 + (j - ta) * TK;
         const CUtensorMap *km = paged ? &kpmap : &kdmap, *vm = paged ? &vpmap : &vdmap;
         for (int b = 0; b < 4; ++b) {
           tma_load_2d(km, b_kvf + 8 * s, smem_u32(sm + OFF_K + s * KV_BYTES + b * KV_BOX), b * 64, row);
-          tma_load_2d(vm, b_kvf + 8 * s, smem_u32(sm + OFF_V + s * KV_BYTES + b * KV_BOX), b * 64, row);
+          if (b < ndb)
+            tma_load_2d(vm, b_kvf + 8 * s, smem_u32(sm + OFF_V + s * KV_BYTES + b * KV_BOX), (db0 + b) * 64, row);
         }
       };
       int i = 0;
@@ -297,7 +305,7 @@ __global__ void __launch_bounds__(192, 1)
       // kind::f16, bf16 in, f32 accumulate; S: K-major A and B, N = 64; O: B (V) MN-major, N = 256
       const uint32_t idesc_s = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TK >> 3) << 17) |
                                ((uint32_t)(TQ >> 4) << 24);
-      const uint32_t idesc_o = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(HD >> 3) << 17) |
+      const uint32_t idesc_o = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(dw >> 3) << 17) |
                                ((uint32_t)(TQ >> 4) << 24);
       const uint32_t q_s = smem_u32(sm), p_s = smem_u32(sm + OFF_P);
       MBW(b_q, 0, 2);
@@ -376,7 +384,7 @@ __global__ void __launch_bounds__(192, 1)
         // whenever any of them needs it (rows that do not multiply by 1)
         if (__any_sync(0xffffffffu, corr != 1.f)) {
 #pragma unroll 1
-          for (int c = 0; c < HD; c += 16) {
+          for (int c = 0; c < dw; c += 16) {
             uint32_t v[16];
             tmem_ld16_nowait(tmem + lanes + c, v);
             tmem_ld_wait();
@@ -429,9 +437,9 @@ __global__ void __launch_bounds__(192, 1)
     const bool ok = r < g.nq && split == 0;
     if (gs == 1) {
       const float inv = l > 0.f ? 1.f / l : 0.f;
-      bf16 *orow = g.o + (size_t)r * g.ldo;
+      bf16 *orow = g.o + (size_t)r * g.ldo + db0 * 64;
 #pragma unroll 1
-      for (int c = 0; c < HD; c += 16) {
+      for (int c = 0; c < dw; c += 16) {
         uint32_t v[16];
         if (n > 0) {
           tmem_ld16_nowait(tmem + lanes + c, v);
@@ -460,7 +468,7 @@ __global__ void __launch_bounds__(192, 1)
       // multiples of 128, so rows past nq land in that group's padding.
       uint8_t *stage = sm;  // Q slot: free once the last PV retired
 #pragma unroll 1
-      for (int b = 0; b < HD / 64; ++b) {  // partials in bf16 (unnormalised O; m, l stay fp32)
+      for (int b = 0; b < ndb; ++b) {  // partials in bf16 (unnormalised O; m, l stay fp32)
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
           uint32_t v[32];
@@ -494,7 +502,7 @@ __global__ void __launch_bounds__(192, 1)
       if (a.cmerge) {  // (m, l) next to the partial; peers read both after the cluster barrier
         reinterpret_cast<float2 *>(sm + OFF_P)[row] = make_float2(m_ref, l);
       } else {
-        if (r < g.nq) {
+        if (r < g.nq && blockIdx.z == 0) {  // (m, l) are the same in every dim half
           const size_t wr = (size_t)split * a.ws_rows + g.wrow0 + r;
           a.ws_ml[wr * 2] = m_ref;
           a.ws_ml[wr * 2 + 1] = l;
@@ -505,10 +513,10 @@ __global__ void __launch_bounds__(192, 1)
       if (threadIdx.x == 64) APROF(8);
       if (threadIdx.x == 64 && !a.cmerge) {
         const int row0 = split * a.ws_rows + g.wrow0 + q0;
-        for (int b = 0; b < HD / 64; ++b)
+        for (int b = 0; b < ndb; ++b)
           asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
                            reinterpret_cast<uint64_t>(&wsmap)),
-                       "r"(b * 64), "r"(row0), "r"(smem_u32(stage + b * (TQ * 128)))
+                       "r"((db0 + b) * 64), "r"(row0), "r"(smem_u32(stage + b * (TQ * 128)))
                        : "memory");
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         // smem may be released once the copies have READ it; the global writes
@@ -561,10 +569,10 @@ __global__ void __launch_bounds__(192, 1)
     // the DSMEM loads of several (row, 8-column) items are in flight before any is
     // used (a plain loop waited one DSMEM round trip per item: 8 us for the 2-split
     // prefill tile, profiles/r02_attn.md)
-    if (gs <= 2) merge_rows<2>(g, q0, rb, nr, gs, st_s, wgt);
-    else if (gs <= 4) merge_rows<4>(g, q0, rb, nr, gs, st_s, wgt);
-    else if (gs <= 8) merge_rows<8>(g, q0, rb, nr, gs, st_s, wgt);
-    else merge_rows<16>(g, q0, rb, nr, gs, st_s, wgt);
+    if (gs <= 2) merge_rows<2>(g, q0, rb, nr, gs, st_s, wgt, ndb, db0);
+    else if (gs <= 4) merge_rows<4>(g, q0, rb, nr, gs, st_s, wgt, ndb, db0);
+    else if (gs <= 8) merge_rows<8>(g, q0, rb, nr, gs, st_s, wgt, ndb, db0);
+    else merge_rows<16>(g, q0, rb, nr, gs, st_s, wgt, ndb, db0);
     if (threadIdx.x == 0) APROF(12);
     cluster_sync_all();  // peers may still be reading this CTA's smem
     if (threadIdx.x == 0) APROF(13);
@@ -800,9 +808,24 @@ void flash_attention_tc(const AttnGroup *groups_d, int n_groups, int q_tiles, in
       splits > 1 && !cmerge ? gemm::make_map(reinterpret_cast<const bf16 *>(ws_o), splits * ws_rows, tc::HD, tc::TQ)
                             : qm;
   ++gemm::g_plan_counts[splits == 1 ? gemm::PC_ATTN_ONE : cmerge ? gemm::PC_ATTN_CMERGE : gemm::PC_ATTN_WSMERGE];
+  // head-dim halves when twice the (query tile, key split) CTAs still fit one wave (the
+  // expert suffix: 28 -> 56 CTAs; not the 1-stream prefill, 100 CTAs, where 200 made two
+  // waves): half the V ingest and merge volume per CTA, same arithmetic per element
+  static const int sms = [] {
+    int dev = 0, n = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  static const int knob = [] {
+    const char *e = getenv("OXY_ATTN_DSPLIT");  // 0: off, 1: auto (default), 2: always
+    return e ? atoi(e) : 1;
+  }();
+  const int ctas = n_groups * q_tiles * splits;
+  const int dsplit = knob == 2 || (knob == 1 && 2 * ctas <= sms) ? 2 : 1;
   TcAttnArgs a{groups_d, q_tiles, splits, ws_rows, tps, q_base, kd_base, kv_ready ? 1 : 0, cmerge ? 1 : 0,
-               scale * 1.4426950408889634f, ws_o, ws_ml};
-  launch_pdl_cluster(flash_tc_kernel, dim3(n_groups * q_tiles, splits), dim3(192), tc::SMEM, st,
+               dsplit, scale * 1.4426950408889634f, ws_o, ws_ml};
+  launch_pdl_cluster(flash_tc_kernel, dim3(n_groups * q_tiles, splits, dsplit), dim3(192), tc::SMEM, st,
                      dim3(1, cmerge ? splits : 1, 1), qm, kpool_map, vpool_map, kdm, vdm, wsm, a);
 }
 
