@@ -204,7 +204,7 @@ struct TcAttnArgs {
   const bf16 *q_base, *kd_base;  // row offsets of the groups' q / dense k,v pointers
   int kv_ready;  // 1: the paged K/V were not written by the previous kernel (prefetch before the PDL wait)
   int cmerge;    // 1: launched as clusters of `splits` CTAs along y, merge over DSMEM
-  int dsplit;    // 1 or 2: grid z = head-dim halves of V / O (each CTA: full S, PV over its half)
+  int dsplit;    // 1, 2 or 4: grid z = head-dim parts of V / O (each CTA: full S, PV over its part)
   float scale_log2;
   float *ws_o, *ws_ml;
 };
@@ -786,7 +786,7 @@ int attn_cluster_merge_max() {
 void flash_attention_tc(const AttnGroup *groups_d, int n_groups, int q_tiles, int splits, int tps, const bf16 *q_base,
                         int q_rows, const CUtensorMap &kpool_map, const CUtensorMap &vpool_map, const bf16 *kd_base,
                         const bf16 *vd_base, int kd_rows, float scale, float *ws_o, float *ws_ml, int ws_rows,
-                        bool kv_ready, bool cmerge, cudaStream_t st) {
+                        bool kv_ready, bool cmerge, cudaStream_t st, int lane_sms) {
   static bool attr = false;
   if (!attr) {
     OXY_CUDA(cudaFuncSetAttribute(flash_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::SMEM));
@@ -818,11 +818,23 @@ void flash_attention_tc(const AttnGroup *groups_d, int n_groups, int q_tiles, in
     return n;
   }();
   static const int knob = [] {
-    const char *e = getenv("OXY_ATTN_DSPLIT");  // 0: off, 1: auto (default), 2: always
+    const char *e = getenv("OXY_ATTN_DSPLIT");  // 0: off, 1: auto (default), 2 / 4: always that many
     return e ? atoi(e) : 1;
   }();
+  static const int auto_max = [] {
+    const char *e = getenv("OXY_ATTN_DSPLIT_MAX");  // largest automatic split (A/B)
+    return e ? atoi(e) : 2;
+  }();
   const int ctas = n_groups * q_tiles * splits;
-  const int dsplit = knob == 2 || (knob == 1 && 2 * ctas <= sms) ? 2 : 1;
+  const int avail = lane_sms > 0 ? std::min(lane_sms, sms) : sms;  // the caller's SM partition
+  int dsplit = knob >= 2 ? knob : 1;
+  if (knob == 1)
+    for (int d = auto_max; d >= 2; d /= 2)
+      if (d * ctas <= avail) {
+        dsplit = d;
+        break;
+      }
+  if (dsplit != 1 && dsplit != 2 && dsplit != 4) fail(OXY_EINVAL, "attention head-dim split must be 1, 2 or 4");
   TcAttnArgs a{groups_d, q_tiles, splits, ws_rows, tps, q_base, kd_base, kv_ready ? 1 : 0, cmerge ? 1 : 0,
                dsplit, scale * 1.4426950408889634f, ws_o, ws_ml};
   launch_pdl_cluster(flash_tc_kernel, dim3(n_groups * q_tiles, splits, dsplit), dim3(192), tc::SMEM, st,

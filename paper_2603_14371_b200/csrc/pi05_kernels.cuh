@@ -89,7 +89,7 @@ __host__ __device__ inline int attn_group_splits(int tiles, int tps, int &per) {
 void flash_attention_tc(const AttnGroup *groups_d, int n_groups, int q_tiles, int splits, int tps, const bf16 *q_base,
                         int q_rows, const CUtensorMap &kpool_map, const CUtensorMap &vpool_map, const bf16 *kd_base,
                         const bf16 *vd_base, int kd_rows, float scale, float *ws_o, float *ws_ml, int ws_rows,
-                        bool kv_ready, bool cmerge, cudaStream_t st);
+                        bool kv_ready, bool cmerge, cudaStream_t st, int lane_sms = 0);
 // largest split count merged inside the attention kernel over DSMEM (clusters of
 // `splits` CTAs); larger counts use the workspace + flash_merge.  OXY_ATTN_CMERGE:
 // the cap (default 16; 0 or 1 = always the workspace merge)

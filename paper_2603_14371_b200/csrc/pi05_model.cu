@@ -801,7 +801,8 @@ struct Model {
     const int cmax = on_partition ? std::min(8, attn_cluster_merge_max()) : attn_cluster_merge_max();
     const bool cm = p.splits > 1 && p.splits <= cmax;
     flash_attention_tc(p.groups, p.n, p.q_tiles, p.splits, p.tps, q_base, q_rows, kv_maps[2 * layer],
-                       kv_maps[2 * layer + 1], kd, vd, kd_rows, 1.f / 16.f, wo, wml, p.rows, kv_ready, cm, mst);
+                       kv_maps[2 * layer + 1], kd, vd, kd_rows, 1.f / 16.f, wo, wml, p.rows, kv_ready, cm, mst,
+                       psms());
     if (p.splits > 1 && !cm && !(dbg_skip & 4))
       flash_merge(p.groups, p.n, p.q_tiles * 128, p.splits, p.tps, reinterpret_cast<const bf16 *>(wo), wml, p.rows,
                   mst);
@@ -1036,7 +1037,7 @@ struct Model {
     LaneSwap lane(*this);
     static const bool force_part = getenv("OXY_GREEN_FORCE") && atoi(getenv("OXY_GREEN_FORCE")) != 0;  // measurement
     const bool part = (!join || force_part) && green.dn && n <= green_max_streams;  // overlapped: expert partition
-    PlanSms plan_scope(*this, lane_sms.first);
+    PlanSms plan_scope(*this, part ? green.dn_sms : lane_sms.first);
     const int We = c.expert_width, H = c.H, A = c.action_dim, T = n * H, AP = apad();
     ensure_mod(S);
     StreamScope stream_scope(*this, part ? green.dn : nullptr);
