@@ -301,7 +301,7 @@ __global__ void __launch_bounds__(192, 1)
       for (; i < n; ++i) issue(i);
     }
   } else if (warp == 1) {
-    if (lane == 0 && n > 0) {
+    if (n > 0) {  // the whole warp walks the loop (uniform registers); the elected lane issues
       // kind::f16, bf16 in, f32 accumulate; S: K-major A and B, N = 64; O: B (V) MN-major, N = 256
       const uint32_t idesc_s = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TK >> 3) << 17) |
                                ((uint32_t)(TQ >> 4) << 24);
@@ -309,17 +309,20 @@ __global__ void __launch_bounds__(192, 1)
                                ((uint32_t)(TQ >> 4) << 24);
       const uint32_t q_s = smem_u32(sm), p_s = smem_u32(sm + OFF_P);
       MBW(b_q, 0, 2);
-      APROF(3);
+      if (lane == 0) APROF(3);
       auto issue_pv = [&](int i) {
         MBW(b_pf, i & 1, 3);
         tc_fence_after();
         const uint32_t v_s = smem_u32(sm + OFF_V + (i & 1) * KV_BYTES);
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < TK / 16; ++kk)
-          mma_bf16(tmem, make_sdesc(p_s + kk * 32), make_sdesc_mn(v_s + kk * 2048, KV_BOX), idesc_o,
-                   (i | kk) != 0 ? 1u : 0u);
-        mma_commit(b_kve + 8 * (i & 1));
-        mma_commit(b_od);
+          for (int kk = 0; kk < TK / 16; ++kk)
+            mma_bf16(tmem, make_sdesc(p_s + kk * 32), make_sdesc_mn(v_s + kk * 2048, KV_BOX), idesc_o,
+                     (i | kk) != 0 ? 1u : 0u);
+          mma_commit(b_kve + 8 * (i & 1));
+          mma_commit(b_od);
+        }
+        __syncwarp();
       };
       for (int i = 0; i < n; ++i) {
         const int s = i & 1;
@@ -328,11 +331,14 @@ __global__ void __launch_bounds__(192, 1)
         tc_fence_after();
         const uint32_t k_s = smem_u32(sm + OFF_K + s * KV_BYTES);
         const uint32_t d_s = tmem + 256 + s * TK;
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk)
-          mma_bf16(d_s, make_sdesc(q_s + (kk >> 2) * Q_BOX + (kk & 3) * 32),
-                   make_sdesc(k_s + (kk >> 2) * KV_BOX + (kk & 3) * 32), idesc_s, kk != 0 ? 1u : 0u);
-        mma_commit(b_sf + 8 * s);
+          for (int kk = 0; kk < HD / 16; ++kk)
+            mma_bf16(d_s, make_sdesc(q_s + (kk >> 2) * Q_BOX + (kk & 3) * 32),
+                     make_sdesc(k_s + (kk >> 2) * KV_BOX + (kk & 3) * 32), idesc_s, kk != 0 ? 1u : 0u);
+          mma_commit(b_sf + 8 * s);
+        }
+        __syncwarp();
         if (i > 0) issue_pv(i - 1);
       }
       issue_pv(n - 1);
@@ -656,7 +662,7 @@ __global__ void __launch_bounds__(192, 1)
       for (int b = 0; b < 2; ++b) tma_load_2d(&kvmap, b_v, smem_u32(sm + OFF_V + b * KV_ATOM), cv + 64 * b, row_img);
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // the whole warp waits; the elected lane issues
       const uint32_t idesc_s = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(NK >> 3) << 17) |
                                ((uint32_t)(TQ >> 4) << 24);
       const uint32_t idesc_o = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(80 >> 3) << 17) |
@@ -665,19 +671,24 @@ __global__ void __launch_bounds__(192, 1)
       mbar_wait(b_k, 0);
       mbar_wait(b_qr, 0);
       tc_fence_after();
+      if (elect_one()) {
 #pragma unroll
-      for (int kk = 0; kk < 5; ++kk)  // K = 80: dims 0..63 (atom 0), 64..79 (atom 1; Q zero past 71)
-        mma_bf16(tmem, make_sdesc(q_s + (kk >> 2) * Q_ATOM + (kk & 3) * 32),
-                 make_sdesc(k_s + (kk >> 2) * KV_ATOM + (kk & 3) * 32), idesc_s, kk != 0 ? 1u : 0u);
-      mma_commit(b_s);
+        for (int kk = 0; kk < 5; ++kk)  // K = 80: dims 0..63 (atom 0), 64..79 (atom 1; Q zero past 71)
+          mma_bf16(tmem, make_sdesc(q_s + (kk >> 2) * Q_ATOM + (kk & 3) * 32),
+                   make_sdesc(k_s + (kk >> 2) * KV_ATOM + (kk & 3) * 32), idesc_s, kk != 0 ? 1u : 0u);
+        mma_commit(b_s);
+      }
+      __syncwarp();
       mbar_wait(b_v, 0);
       mbar_wait(b_p, 0);
       tc_fence_after();
+      if (elect_one()) {
 #pragma unroll
-      for (int kk = 0; kk < NK / 16; ++kk)  // P atoms of 64 keys at OFF_K + 16 KB each
-        mma_bf16(tmem + 256, make_sdesc(k_s + (kk >> 2) * Q_ATOM + (kk & 3) * 32),
-                 make_sdesc_mn(v_s + kk * 2048, KV_ATOM), idesc_o, kk != 0 ? 1u : 0u);
-      mma_commit(b_o);
+        for (int kk = 0; kk < NK / 16; ++kk)  // P atoms of 64 keys at OFF_K + 16 KB each
+          mma_bf16(tmem + 256, make_sdesc(k_s + (kk >> 2) * Q_ATOM + (kk & 3) * 32),
+                   make_sdesc_mn(v_s + kk * 2048, KV_ATOM), idesc_o, kk != 0 ? 1u : 0u);
+        mma_commit(b_o);
+      }
     }
     __syncwarp();
   } else {

@@ -45,6 +45,39 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       : "memory");
 }
 
+// One lane of a converged warp (elect.sync).  The MMA-issuing loops run on the whole
+// warp and issue from the elected lane: with the loop warp-uniform the compiler keeps
+// descriptors and addresses in uniform registers; a loop under `if (lane == 0)` had
+// every tcgen05.mma wrapped in an R2UR.BROADCAST / elect re-convergence loop.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "elect.sync _|P, 0xffffffff;\n\t"
+      "selp.b32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
+__device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+// A long wait (an epilogue warp waiting for the next accumulator): poll with a sleep
+// between probes so the waiting warps do not compete with the tensor pipe's shared-
+// memory traffic.
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity, int ns) {
+  while (!mbar_try(bar, parity)) __nanosleep(ns);
+}
+
 __device__ __forceinline__ void tma_load_2d(const CUtensorMap *map, uint32_t bar, uint32_t dst,
                                             int c0, int c1) {
   asm volatile(

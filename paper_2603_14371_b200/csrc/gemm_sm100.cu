@@ -124,6 +124,11 @@ struct Knobs {
   int wide = -1, wide_bn = 0, wide_splits = 0;  // -1 auto (see make_plan), 0 off, 1 / 2 force
   int wide_cl = 0;  // 0 auto, 1 / 2 force the pairs per cluster
   int wide_min_k = 0;  // > 0: also take the wide kernel for K >= this at T >= 256 (A/B knob)
+  int wide_stages = 0;  // > 0: cap the persistent kernel's smem stages (A/B knob)
+  int wide_diag = 0;    // timing diagnosis only (wrong results): 1 skip the MMAs, 2 skip the operand loads
+  int wide_units = 0;   // > 0: cap the persistent grid at this many CTA pairs (diagnosis)
+  int wide_nofence = 0; // 1: no tcgen05.fence::after_thread_sync per k-block in the MMA loop (A/B)
+  int wide_sleep = 0;   // > 0: epilogue warps poll the accumulator barrier with this ns sleep (A/B)
   int split_slots = 1;  // skinny split-K fills split_slots CTAs per SM (A/B knob)
   int bigk_min = 0, bigk_bn = 0, bigk_splits = 0;  // OXY_GEMM_BIGK=kmin,bn,splits (A/B knob)
   // split K (fixed-order reduction) for token counts up to this when the tiles do not fill
@@ -136,6 +141,11 @@ struct Knobs {
     if (const char *s = getenv("OXY_GEMM_WIDE_SPLITS")) wide_splits = atoi(s);
     if (const char *s = getenv("OXY_GEMM_WIDE_CL")) wide_cl = atoi(s);
     if (const char *s = getenv("OXY_GEMM_WIDE_MIN_K")) wide_min_k = atoi(s);
+    if (const char *s = getenv("OXY_GEMM_WIDE_STAGES")) wide_stages = atoi(s);
+    if (const char *s = getenv("OXY_GEMM_WIDE_DIAG")) wide_diag = atoi(s);
+    if (const char *s = getenv("OXY_GEMM_WIDE_UNITS")) wide_units = atoi(s);
+    if (const char *s = getenv("OXY_GEMM_WIDE_NOFENCE")) wide_nofence = atoi(s);
+    if (const char *s = getenv("OXY_GEMM_WIDE_SLEEP")) wide_sleep = atoi(s);
     if (const char *s = getenv("OXY_GEMM_SPLIT_SLOTS")) split_slots = std::max(1, atoi(s));
     if (const char *s = getenv("OXY_GEMM_BIGK")) sscanf(s, "%d,%d,%d", &bigk_min, &bigk_bn, &bigk_splits);
     if (const char *s = getenv("OXY_PDL_EARLY_SKINNY")) early_skinny = atoi(s);
@@ -256,7 +266,27 @@ __device__ int g_gemm_prof_sel[2];
       g_gemm_prof[blockIdx.z][ev] = t_;                                                       \
     }                                                                                         \
   } while (0)
+// persistent wide kernel: per CTA 0..3 and local tile 0..15: [0] MMA warp starts the
+// tile (accumulator free), [1] last k-block issued, [2] epilogue warp 2 sees the
+// accumulator, [3] epilogue warp 2 done; row 16: [0] entry [1] setup done [2] exit
+__device__ unsigned long long g_wide_prof[4][17][6];
+#define WPROF(cta, lt, ev)                                                                     \
+  do {                                                                                         \
+    if (gprof_on && (cta) < 4 && (lt) < 17) {                                                  \
+      unsigned long long t_;                                                                   \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                   \
+      g_wide_prof[cta][lt][ev] = t_;                                                           \
+      if ((ev) < 2) g_wide_prof[cta][lt][4 + (ev)] = clock64();                                \
+    }                                                                                          \
+  } while (0)
+#define WPROF_INIT() const bool gprof_on = p.n_out == g_gemm_prof_sel[0] && p.k == g_gemm_prof_sel[1]
 #else
+#define WPROF(cta, lt, ev) \
+  do {                     \
+  } while (0)
+#define WPROF_INIT() \
+  do {               \
+  } while (0)
 #define GPROF_INIT() \
   do {               \
   } while (0)
@@ -423,29 +453,33 @@ __global__ void __maxnreg__(128)
       if (p.trigger) pdl_trigger();
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(bn >> 3) << 17) |
-                             ((uint32_t)(BM >> 4) << 24);
-      for (int i = 0; i < nkb; ++i) {
-        const int s = i % stages;
-        const uint32_t ph = (i / stages) & 1;
-        mbar_wait(full0 + 8 * s, ph);
-        tc_fence_after();
+    // the whole warp walks the k-loop (uniform registers); the elected lane issues
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(bn >> 3) << 17) |
+                           ((uint32_t)(BM >> 4) << 24);
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % stages;
+      const uint32_t ph = (i / stages) & 1;
+      mbar_wait(full0 + 8 * s, ph);
+      tc_fence_after();
+      if (lane == 0) {
         if (i == 0) GPROF(5);
         if (i > 0 && i < 4) GPROF(15 + i);
-        const uint32_t a = smem_u32(sA + s * A_STAGE_BYTES), b = smem_u32(sB + s * b_bytes);
-        // kmulti: k-block i accumulates into region i / kb_per_split, each region from zero
-        const int reg = p.kmulti > 1 ? i / p.kb_per_split : 0, i0 = i - reg * p.kb_per_split;
-        const uint32_t d = tmem + (uint32_t)(reg * bn);
+      }
+      const uint32_t a = smem_u32(sA + s * A_STAGE_BYTES), b = smem_u32(sB + s * b_bytes);
+      // kmulti: k-block i accumulates into region i / kb_per_split, each region from zero
+      const int reg = p.kmulti > 1 ? i / p.kb_per_split : 0, i0 = i - reg * p.kb_per_split;
+      const uint32_t d = tmem + (uint32_t)(reg * bn);
+      if (elect_one()) {
 #pragma unroll
         for (int kk = 0; kk < BK / 16; ++kk)
           mma_bf16(d, make_sdesc(a + kk * 32), make_sdesc(b + kk * 32), idesc, (i0 | kk) != 0 ? 1u : 0u);
         mma_commit(empty0 + 8 * s);
       }
-      mma_commit(done);
-      GPROF(6);
+      __syncwarp();
     }
+    if (elect_one()) mma_commit(done);
     __syncwarp();
+    if (lane == 0) GPROF(6);
   }
   const int q = warp & 3;
   const int f = m0 + q * 32 + lane;
@@ -597,6 +631,8 @@ struct WParams {
   int n_out, k, t, bn, stages, kb_total;
   int m_tiles, n_tiles, splits, kb_per_split, tiles;
   int kdual;  // splits == 2 done in-CTA: tiles are (m, n) only, K half h -> accumulator region h
+  int diag;   // OXY_GEMM_WIDE_DIAG (timing diagnosis): 1 no MMAs, 2 no operand loads
+  int sleep_ns;  // > 0: the epilogue's accumulator wait sleeps between probes
   EpiParams epi;
   float *ws;
   int *counters;  // one per (tile, CTA of the pair); self-resetting
@@ -626,6 +662,8 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
   __shared__ int s_last;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  WPROF_INIT();
+  if (threadIdx.x == 0) WPROF(blockIdx.x, 16, 0);
   const uint32_t crank = CG == 2 ? cluster_rank() : 0;
   const uint32_t rank = crank & 1, pp = crank >> 1;  // CTA within its pair, pair within the cluster
   const int unit = blockIdx.x / (CG * CL), units = gridDim.x / (CG * CL);
@@ -671,6 +709,7 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int per_m = per_m_split * ngr;
+  if (threadIdx.x == 0) WPROF(blockIdx.x, 16, 1);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -691,6 +730,11 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
           const int s = it % stages;
           const uint32_t ph = (it / stages) & 1;
           mbar_wait(empty0 + 8 * s, ph ^ 1);
+          if ((p.diag & 3) == 2) {  // diagnosis: the pipeline without operand traffic
+            if (rank == 0) mbar_arrive_local(full0 + 8 * s);
+            if (!waited) { pdl_wait(); waited = true; }
+            continue;
+          }
           if (rank == 0) mbar_expect_tx(full0 + 8 * s, CG * (A_STAGE_BYTES + b_bytes));
           const int kc = (kb0 + i) * BK;
           if (CL == 2) {  // half of this CTA's weight rows, to both pairs
@@ -712,7 +756,7 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
       if (!waited) pdl_wait();
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {
+    if (rank == 0) {  // the whole warp walks the loop; the elected lane issues
       // kind::f16, bf16 x bf16 -> f32, K-major A/B, N = bn, M = 128 * CG
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(bn >> 3) << 17) |
                              ((uint32_t)((BM * CG) >> 4) << 24);
@@ -725,30 +769,39 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
         const int acc = lt % nbuf;
         mbar_wait(tempty0 + 8 * acc, ((lt / nbuf) & 1) ^ 1);
         tc_fence_after();
+        WPROF(blockIdx.x, lt, 0);
         const uint32_t d0 = tmem + (uint32_t)acc * acc_stride;
         for (int i = 0; i < nkb; ++i, ++it) {
           const int s = it % stages;
           const uint32_t ph = (it / stages) & 1;
           mbar_wait(full0 + 8 * s, ph);
-          tc_fence_after();
+          if (!(p.diag & 4)) tc_fence_after();
           const uint32_t a = smem_u32(sA + s * A_STAGE_BYTES), b = smem_u32(sB + s * b_bytes);
           // kdual: k-blocks of the second K half accumulate into the second region, each
           // half from zero — the split-2 partials, kept in TMEM
           const bool hi = p.kdual && i >= p.kb_per_split;
           const uint32_t d = d0 + (hi ? half_stride : 0u);
           const int i0 = hi ? i - p.kb_per_split : i;
+          if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            if (CG == 2)
-              mma_bf16_pair(d, make_sdesc(a + kk * 32), make_sdesc(b + kk * 32), idesc, (i0 | kk) != 0 ? 1u : 0u);
-            else
-              mma_bf16(d, make_sdesc(a + kk * 32), make_sdesc(b + kk * 32), idesc, (i0 | kk) != 0 ? 1u : 0u);
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              if ((p.diag & 3) == 1) break;  // diagnosis: the pipeline without MMAs
+              if (CG == 2)
+                mma_bf16_pair(d, make_sdesc(a + kk * 32), make_sdesc(b + kk * 32), idesc, (i0 | kk) != 0 ? 1u : 0u);
+              else
+                mma_bf16(d, make_sdesc(a + kk * 32), make_sdesc(b + kk * 32), idesc, (i0 | kk) != 0 ? 1u : 0u);
+            }
+            if (CG == 2) mma_commit_mask(empty0 + 8 * s, all_mask);  // both pairs may refill the stage
+            else mma_commit(empty0 + 8 * s);
           }
-          if (CG == 2) mma_commit_mask(empty0 + 8 * s, all_mask);  // both pairs may refill the stage
-          else mma_commit(empty0 + 8 * s);
+          __syncwarp();
         }
-        if (CG == 2) mma_commit_mask(tfull0 + 8 * acc, pair_mask);
-        else mma_commit(tfull0 + 8 * acc);
+        if (elect_one()) {
+          if (CG == 2) mma_commit_mask(tfull0 + 8 * acc, pair_mask);
+          else mma_commit(tfull0 + 8 * acc);
+        }
+        __syncwarp();
+        WPROF(blockIdx.x, lt, 1);
       }
     }
     __syncwarp();
@@ -765,8 +818,10 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
     for (int tile = unit; tile < p.tiles; tile += units, ++lt) {
       const int mt = tile / per_m, rem = tile % per_m, split = rem / ngr, nt = (rem % ngr) * CL + (int)pp;
       const int acc = lt % nbuf;
-      mbar_wait(tfull0 + 8 * acc, (lt / nbuf) & 1);
+      if (p.sleep_ns > 0) mbar_wait_sleep(tfull0 + 8 * acc, (lt / nbuf) & 1, p.sleep_ns);
+      else mbar_wait(tfull0 + 8 * acc, (lt / nbuf) & 1);
       tc_fence_after();
+      if (threadIdx.x == 64) WPROF(blockIdx.x, lt, 2);
       const int f = mt * BM * CG + (int)rank * BM + q * 32 + lane;
       const int n0 = nt * bn;
       const uint32_t trow = tmem + (uint32_t)acc * acc_stride + ((uint32_t)(q * 32) << 16);
@@ -778,6 +833,7 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
         if (CG == 2) mbar_arrive_cluster(tempty_l + 8 * acc);
         else mbar_arrive_local(tempty0 + 8 * acc);
       }
+      if (threadIdx.x == 64) WPROF(blockIdx.x, lt, 3);
       if (!p.kdual && split_out && p.epi.mode != EPI_PARTIALS && nt < p.n_tiles)  // (the odd pair of a ragged group idles)
         splitk_fixup(p, (mt * p.n_tiles + nt) * CG + (int)rank, n0, cb, ce, f, s_last, WIDE_THREADS - 64, 64);
     }
@@ -785,6 +841,7 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
   tc_fence_before();
   if (CG == 2) cluster_sync_all();
   else __syncthreads();
+  if (threadIdx.x == 0) WPROF(blockIdx.x, 16, 2);
   if (warp == 1) {
     tc_fence_after();
     if (CG == 2)
@@ -833,7 +890,8 @@ CUtensorMap make_map(const void *ptr, int rows, int k, int box_rows) {
 constexpr int WIDE_SMEM = 220 * 1024;
 
 static int wide_stages(int bn, int cg) {
-  return std::min(MAX_STAGES, (WIDE_SMEM - 2048) / (A_STAGE_BYTES + bn / cg * BK * 2));
+  const int s = std::min(MAX_STAGES, (WIDE_SMEM - 2048) / (A_STAGE_BYTES + bn / cg * BK * 2));
+  return knobs().wide_stages > 0 ? std::min(s, knobs().wide_stages) : s;
 }
 
 // Cost model (SM cycles) of the persistent wide kernel.  Per k-block a CTA
@@ -841,9 +899,9 @@ static int wide_stages(int bn, int cg) {
 // ingest = (16 KB of weights + bn/CG token rows of 128 B) at ~33 B/cycle/SM
 // (measured: the 2-CTA GEMM at T=800 streams 32-35 B/cycle/SM whether 80 or
 // 148 SMs are active).  Split-K pays a partial-sum round trip and a fix-up.
-static double wide_cost(int n_out, int kb_total, int t, int sms, int cg, int bn, int splits, int cl = 1) {
+static double wide_cost(int n_out, int kb_total, int t, int units, int cg, int bn, int splits, int cl = 1) {
   const int m_tiles = (n_out + BM * cg - 1) / (BM * cg), n_tiles = (t + bn - 1) / bn;
-  const int tiles = m_tiles * ((n_tiles + cl - 1) / cl) * splits, units = sms / (cg * cl);
+  const int tiles = m_tiles * ((n_tiles + cl - 1) / cl) * splits;
   const int waves = (tiles + units - 1) / units;
   const int kbs = (kb_total + splits - 1) / splits;
   // weight bytes per CTA and k-block are read from L2 once per cluster (multicast)
@@ -855,15 +913,64 @@ static double wide_cost(int n_out, int kb_total, int t, int sms, int cg, int bn,
   return c;
 }
 
+static void wide_attrs() {
+  static bool done = false;
+  if (done) return;
+  OXY_CUDA(cudaFuncSetAttribute(gemm_wide_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
+  OXY_CUDA(cudaFuncSetAttribute(gemm_wide_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
+  OXY_CUDA(cudaFuncSetAttribute(gemm_wide_kernel<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
+  done = true;
+}
+
+static int device_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    OXY_CUDA(cudaGetDevice(&dev));
+    OXY_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return n;
+}
+
+// Work units (CTA pairs, or clusters of two pairs) the persistent wide kernel keeps
+// co-resident on `sms` SMs.  A 4-CTA cluster needs two TPCs of one GPC, so fewer than
+// sms / 4 fit at once: a grid of sms / 4 clusters ran its last clusters as a second
+// wave (the round-1 CL = 2 measurement, 1139 vs 651 us).  The cluster count comes from
+// the occupancy query; CL = 2 only on the whole device (not inside an SM partition,
+// where clusters above 8 CTAs and the GPC split are not ours to know).
+static int wide_units(int cg, int cl, int sms) {
+  if (cl == 1) return sms / cg;
+  static int cap = -1;
+  if (cap < 0) {
+    wide_attrs();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(device_sms());
+    cfg.blockDim = dim3(WIDE_THREADS);
+    cfg.dynamicSmemBytes = WIDE_SMEM;
+    cudaLaunchAttribute a;
+    a.id = cudaLaunchAttributeClusterDimension;
+    a.val.clusterDim.x = 4;
+    a.val.clusterDim.y = 1;
+    a.val.clusterDim.z = 1;
+    cfg.attrs = &a;
+    cfg.numAttrs = 1;
+    int n = 0;
+    OXY_CUDA(cudaOccupancyMaxActiveClusters(&n, gemm_wide_kernel<2, 2>, &cfg));
+    cap = n;
+  }
+  return sms == device_sms() ? std::min(cap, sms / 4) : 0;
+}
+
 static bool wide_plan(Plan &p, int n_out, int k, int t, int sms, int req_splits) {
   const Knobs &kn = knobs();
   double best = 1e30;
   for (int cg = 1; cg <= 2; ++cg) {
     if (kn.wide > 0 && cg != kn.wide) continue;
     for (int cl = 1; cl <= (cg == 2 ? 2 : 1); ++cl) {
-      // two pairs per cluster multicasting the weight tile is correct but measured
-      // slower (gate/up at T = 6400: 1139 vs 651 us), so only when forced
+      // two pairs per cluster multicasting the weight tile: only when forced (A/B)
       if (kn.wide_cl ? cl != kn.wide_cl : cl != 1) continue;
+      const int units = wide_units(cg, cl, sms);
+      if (units <= 0) continue;
       for (int bn = 32; bn <= MAX_BN; bn += 16) {
         if (kn.wide_bn && bn != kn.wide_bn) continue;
         if (cl == 2 && (t + bn - 1) / bn < 2) continue;
@@ -871,7 +978,7 @@ static bool wide_plan(Plan &p, int n_out, int k, int t, int sms, int req_splits)
           if (req_splits > 0 ? splits != req_splits
                              : ((kn.wide_splits && splits != kn.wide_splits) || (splits > 1 && p.kb_total / splits < 4)))
             continue;
-          const double c = wide_cost(n_out, p.kb_total, t, sms, cg, bn, splits, cl);
+          const double c = wide_cost(n_out, p.kb_total, t, units, cg, bn, splits, cl);
           if (c < best * 0.999) {
             best = c;
             p.cg = cg;
@@ -966,6 +1073,7 @@ int policy_splits(int phase, int n_out, int k, int sms) {
 
 Plan make_plan(int n_out, int k, int t, int sms, int force_splits) {
   Plan p{};
+  p.sms = sms;
   p.kb_total = (k + BK - 1) / BK;
   // persistent 2-CTA kernel: in-frame it wins for the gate/up projections from
   // T = 256 and for every projection once T >= 2048 (multi-stream prefill);
@@ -1062,19 +1170,7 @@ static void launch_split_reduce(const float *ws, int splits, int t, int n_out, c
 
 static void launch_wide(const void *w, const void *x, int n_out, int k, int t, const EpiParams &epi,
                         const Plan &plan, float *ws, int *counters, cudaStream_t st) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    OXY_CUDA(cudaFuncSetAttribute(gemm_wide_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
-    OXY_CUDA(cudaFuncSetAttribute(gemm_wide_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
-    OXY_CUDA(cudaFuncSetAttribute(gemm_wide_kernel<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
-    attr_set = true;
-  }
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    OXY_CUDA(cudaGetDevice(&dev));
-    OXY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  }
+  wide_attrs();
   const int cg = plan.cg, cl = plan.cl > 0 ? plan.cl : 1;
   CUtensorMap ma = make_map(w, n_out, k, cl == 2 ? BM / 2 : BM);  // CL = 2: each CTA loads half its rows
   CUtensorMap mb = make_map(x, t, k, plan.bn / cg);
@@ -1090,6 +1186,8 @@ static void launch_wide(const void *w, const void *x, int n_out, int k, int t, c
   wp.splits = plan.splits;
   wp.kb_per_split = (plan.kb_total + plan.splits - 1) / plan.splits;
   wp.kdual = plan.kdual;
+  wp.diag = knobs().wide_diag | (knobs().wide_nofence ? 4 : 0);
+  wp.sleep_ns = knobs().wide_sleep;
   wp.tiles = plan.m_tiles * ((plan.n_tiles + cl - 1) / cl) * (plan.kdual ? 1 : plan.splits);
   wp.epi = epi;
   wp.ws = ws;
@@ -1100,7 +1198,8 @@ static void launch_wide(const void *w, const void *x, int n_out, int k, int t, c
   // and 320 vs ~45 us for the ViT fc2 at T = 6400; OXY_WIDE_FIXUP=1 restores it)
   const bool reduce_after = plan.splits > 1 && !plan.kdual && epi.mode != EPI_PARTIALS && !knobs().wide_fixup;
   if (reduce_after) wp.epi.mode = EPI_PARTIALS;
-  const int units = std::min(wp.tiles, sms / (cg * cl));
+  int units = std::min(wp.tiles, std::max(1, wide_units(cg, cl, cl == 2 ? device_sms() : plan.sms)));
+  if (knobs().wide_units > 0) units = std::min(units, knobs().wide_units);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(units * cg * cl);
   cfg.blockDim = dim3(WIDE_THREADS);
@@ -1336,7 +1435,7 @@ extern "C" int oxy_plan_counts(int64_t *out, int32_t n, int32_t reset) {
 
 extern "C" int oxy_gemm_plan(int32_t n_out, int32_t k, int32_t t, int32_t splits, int32_t *out6) {
   OXY_API_BEGIN
-  oxy::gemm::Plan p = oxy::gemm::make_plan(n_out, k, t, 148, splits);
+  oxy::gemm::Plan p = oxy::gemm::make_plan(n_out, k, t, oxy::gemm::device_sms(), splits);
   out6[0] = p.bn;
   out6[1] = p.n_tiles;
   out6[2] = p.m_tiles;
@@ -1350,6 +1449,9 @@ extern "C" int oxy_gemm_plan(int32_t n_out, int32_t k, int32_t t, int32_t splits
 extern "C" int oxy_debug_gemm_prof_select(int n_out, int k) {
   const int v[2] = {n_out, k};
   return cudaMemcpyToSymbol(oxy::gemm::g_gemm_prof_sel, v, sizeof(v)) == cudaSuccess ? 0 : -1;
+}
+extern "C" int oxy_debug_wide_prof(unsigned long long *out) {
+  return cudaMemcpyFromSymbol(out, oxy::gemm::g_wide_prof, sizeof(oxy::gemm::g_wide_prof)) == cudaSuccess ? 0 : -1;
 }
 extern "C" int oxy_debug_gemm_prof(unsigned long long *out) {
   return cudaMemcpyFromSymbol(out, oxy::gemm::g_gemm_prof, sizeof(oxy::gemm::g_gemm_prof)) == cudaSuccess ? 0 : -1;

@@ -114,6 +114,7 @@ struct Plan {
   int kmulti;  // one-tile kernel: the `splits` K partitions of a tile accumulated by ONE CTA into
               // `splits` TMEM regions and summed in split order in its epilogue (no partials,
               // no reduce launch; bit-identical to split CTAs + reduce).  0 = split CTAs.
+  int sms;     // SMs the plan was made for (the persistent kernel's grid; an SM partition's size)
   int partials() const { return kdual || kmulti ? 1 : splits; }  // partial slabs an EPI_PARTIALS launch writes
 };
 
