@@ -273,20 +273,23 @@ __global__ void __launch_bounds__(192, 1)
   }
 
   if (warp == 0) {
-    if (lane == 0 && n > 0) {
+    if (n > 0) {  // the whole warp walks the loads (uniform registers); the elected lane issues
       const int drow0 = g.kb ? (int)((g.kb - a.kd_base) / HD) : 0;
       auto issue = [&](int i) {
         const int j = t0 + i, s = i & 1;
         MBW(b_kve + 8 * s, ((i >> 1) & 1) ^ 1, 1);
-        mbar_expect_tx(b_kvf + 8 * s, KV_BYTES + ndb * KV_BOX);
         const bool paged = j < ta;
         const int row = paged ? g.bt[j] * TK : drow0 + (j - ta) * TK;
         const CUtensorMap *km = paged ? &kpmap : &kdmap, *vm = paged ? &vpmap : &vdmap;
-        for (int b = 0; b < 4; ++b) {
-          tma_load_2d(km, b_kvf + 8 * s, smem_u32(sm + OFF_K + s * KV_BYTES + b * KV_BOX), b * 64, row);
-          if (b < ndb)
-            tma_load_2d(vm, b_kvf + 8 * s, smem_u32(sm + OFF_V + s * KV_BYTES + b * KV_BOX), (db0 + b) * 64, row);
+        if (elect_one()) {
+          mbar_expect_tx(b_kvf + 8 * s, KV_BYTES + ndb * KV_BOX);
+          for (int b = 0; b < 4; ++b) {
+            tma_load_2d(km, b_kvf + 8 * s, smem_u32(sm + OFF_K + s * KV_BYTES + b * KV_BOX), b * 64, row);
+            if (b < ndb)
+              tma_load_2d(vm, b_kvf + 8 * s, smem_u32(sm + OFF_V + s * KV_BYTES + b * KV_BOX), (db0 + b) * 64, row);
+          }
         }
+        __syncwarp();
       };
       int i = 0;
       // paged prefix K/V written long before this kernel (the expert suffix case):
@@ -294,10 +297,13 @@ __global__ void __launch_bounds__(192, 1)
       if (a.kv_ready)
         for (; i < n && i < 2 && t0 + i < ta; ++i) issue(i);
       pdl_wait();  // Q (and dense K/V) come from the previous kernel
-      APROF(2);
+      if (lane == 0) APROF(2);
       const int qrow = (int)((g.q - a.q_base) / HD) + q0;
-      mbar_expect_tx(b_q, Q_BYTES);
-      for (int b = 0; b < 4; ++b) tma_load_2d(&qmap, b_q, smem_u32(sm + b * Q_BOX), b * 64, qrow);
+      if (elect_one()) {
+        mbar_expect_tx(b_q, Q_BYTES);
+        for (int b = 0; b < 4; ++b) tma_load_2d(&qmap, b_q, smem_u32(sm + b * Q_BOX), b * 64, qrow);
+      }
+      __syncwarp();
       for (; i < n; ++i) issue(i);
     }
   } else if (warp == 1) {

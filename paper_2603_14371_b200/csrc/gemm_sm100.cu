@@ -420,10 +420,11 @@ __global__ void __maxnreg__(128)
   const uint32_t tmem = *tmem_slot;
   if (threadIdx.x == 0) GPROF(1);
   if (warp == 0) {
-    if (lane == 0) {
-      // Weights never depend on the previous kernel: stream the first ring of
-      // weight tiles before waiting on it, activations after.
-      const int pre = p.prefetch ? min(nkb, stages) : 0;
+    // the whole warp walks the loads (uniform registers); the elected lane issues them
+    // Weights never depend on the previous kernel: stream the first ring of
+    // weight tiles before waiting on it, activations after.
+    const int pre = p.prefetch ? min(nkb, stages) : 0;
+    if (elect_one()) {
       for (int i = 0; i < pre; ++i) {
         mbar_expect_tx(full0 + 8 * i, stage_tx);
         tma_load_2d(&tmA, full0 + 8 * i, smem_u32(sA + i * A_STAGE_BYTES), (kb0 + i) * BK, m0);
@@ -431,27 +432,33 @@ __global__ void __maxnreg__(128)
         tma_load_2d(&tmB, full0 + 8 * i, smem_u32(sB + i * b_bytes), (kb0 + i) * BK, n0);
 #endif
       }
-      GPROF(2);
-      pdl_wait();
-      GPROF(3);
+    }
+    __syncwarp();
+    if (lane == 0) GPROF(2);
+    pdl_wait();
+    if (lane == 0) GPROF(3);
 #ifndef OXY_GEMM_PROF_PREB
+    if (elect_one())
       for (int i = 0; i < pre; ++i)
         tma_load_2d(&tmB, full0 + 8 * i, smem_u32(sB + i * b_bytes), (kb0 + i) * BK, n0);
+    __syncwarp();
 #endif
-      for (int i = pre; i < nkb; ++i) {
-        const int s = i % stages;
-        const uint32_t ph = (i / stages) & 1;
-        mbar_wait(empty0 + 8 * s, ph ^ 1);
+    for (int i = pre; i < nkb; ++i) {
+      const int s = i % stages;
+      const uint32_t ph = (i / stages) & 1;
+      mbar_wait(empty0 + 8 * s, ph ^ 1);
+      const int kc = (kb0 + i) * BK;
+      if (elect_one()) {
         mbar_expect_tx(full0 + 8 * s, stage_tx);
-        const int kc = (kb0 + i) * BK;
         tma_load_2d(&tmA, full0 + 8 * s, smem_u32(sA + s * A_STAGE_BYTES), kc, m0);
         tma_load_2d(&tmB, full0 + 8 * s, smem_u32(sB + s * b_bytes), kc, n0);
       }
-      // all operand loads are in flight: let the next kernel start its
-      // prologue and weight prefetch while this CTA drains
-      GPROF(4);
-      if (p.trigger) pdl_trigger();
+      __syncwarp();
     }
+    // all operand loads are in flight: let the next kernel start its
+    // prologue and weight prefetch while this CTA drains
+    if (lane == 0) GPROF(4);
+    if (p.trigger && lane == 0) pdl_trigger();
   } else if (warp == 1) {
     // the whole warp walks the k-loop (uniform registers); the elected lane issues
     const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(bn >> 3) << 17) |
@@ -712,49 +719,52 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
   if (threadIdx.x == 0) WPROF(blockIdx.x, 16, 1);
 
   if (warp == 0) {
-    if (lane == 0) {
-      // completion is counted on the pair leader's barrier: the cvta address of
-      // a cluster CTA carries its rank in bits 24+, so clearing bit 24 names it
-      const uint32_t full_l = full0 & ~(1u << 24);
-      const uint16_t a_mask = (uint16_t)((1u << rank) | (1u << (2 + rank)));  // same rank in both pairs
-      int it = 0;
-      bool waited = false;
-      for (int tile = unit; tile < p.tiles; tile += units) {
-        if (tile + units >= p.tiles) pdl_trigger();  // last tile: let the next kernel get scheduled
-        const int mt = tile / per_m, rem = tile % per_m, split = rem / ngr, nt = (rem % ngr) * CL + (int)pp;
-        const int kb0 = p.kdual ? 0 : split * p.kb_per_split;
-        const int nkb = p.kdual ? p.kb_total : min(p.kb_total, kb0 + p.kb_per_split) - kb0;
-        const int arow = mt * BM * CG + (int)rank * BM + (CL == 2 ? (int)pp * (BM / 2) : 0),
-                  brow = nt * bn + (int)rank * b_rows;
-        for (int i = 0; i < nkb; ++i, ++it) {
-          const int s = it % stages;
-          const uint32_t ph = (it / stages) & 1;
-          mbar_wait(empty0 + 8 * s, ph ^ 1);
-          if ((p.diag & 3) == 2) {  // diagnosis: the pipeline without operand traffic
-            if (rank == 0) mbar_arrive_local(full0 + 8 * s);
-            if (!waited) { pdl_wait(); waited = true; }
-            continue;
-          }
+    // the whole warp walks the loads (uniform registers); the elected lane issues them
+    // completion is counted on the pair leader's barrier: the cvta address of
+    // a cluster CTA carries its rank in bits 24+, so clearing bit 24 names it
+    const uint32_t full_l = full0 & ~(1u << 24);
+    const uint16_t a_mask = (uint16_t)((1u << rank) | (1u << (2 + rank)));  // same rank in both pairs
+    int it = 0;
+    bool waited = false;
+    for (int tile = unit; tile < p.tiles; tile += units) {
+      if (tile + units >= p.tiles && lane == 0) pdl_trigger();  // last tile: let the next kernel get scheduled
+      const int mt = tile / per_m, rem = tile % per_m, split = rem / ngr, nt = (rem % ngr) * CL + (int)pp;
+      const int kb0 = p.kdual ? 0 : split * p.kb_per_split;
+      const int nkb = p.kdual ? p.kb_total : min(p.kb_total, kb0 + p.kb_per_split) - kb0;
+      const int arow = mt * BM * CG + (int)rank * BM + (CL == 2 ? (int)pp * (BM / 2) : 0),
+                brow = nt * bn + (int)rank * b_rows;
+      for (int i = 0; i < nkb; ++i, ++it) {
+        const int s = it % stages;
+        const uint32_t ph = (it / stages) & 1;
+        mbar_wait(empty0 + 8 * s, ph ^ 1);
+        if ((p.diag & 3) == 2) {  // diagnosis: the pipeline without operand traffic
+          if (rank == 0 && elect_one()) mbar_arrive_local(full0 + 8 * s);
+          __syncwarp();
+          if (!waited) { pdl_wait(); waited = true; }
+          continue;
+        }
+        const int kc = (kb0 + i) * BK;
+        if (elect_one()) {
           if (rank == 0) mbar_expect_tx(full0 + 8 * s, CG * (A_STAGE_BYTES + b_bytes));
-          const int kc = (kb0 + i) * BK;
           if (CL == 2) {  // half of this CTA's weight rows, to both pairs
             tma_load_2d_pair_mc(&tmA, full_l + 8 * s, smem_u32(sA + s * A_STAGE_BYTES + (int)pp * (A_STAGE_BYTES / 2)),
                                 kc, arow, a_mask);
-            if (!waited) { pdl_wait(); waited = true; }
-            tma_load_2d_pair(&tmB, full_l + 8 * s, smem_u32(sB + s * b_bytes), kc, brow);
           } else if (CG == 2) {
             tma_load_2d_pair(&tmA, full_l + 8 * s, smem_u32(sA + s * A_STAGE_BYTES), kc, arow);
-            if (!waited) { pdl_wait(); waited = true; }  // activations come from the previous kernel
-            tma_load_2d_pair(&tmB, full_l + 8 * s, smem_u32(sB + s * b_bytes), kc, brow);
           } else {
             tma_load_2d(&tmA, full0 + 8 * s, smem_u32(sA + s * A_STAGE_BYTES), kc, arow);
-            if (!waited) { pdl_wait(); waited = true; }
-            tma_load_2d(&tmB, full0 + 8 * s, smem_u32(sB + s * b_bytes), kc, brow);
           }
         }
+        __syncwarp();
+        if (!waited) { pdl_wait(); waited = true; }  // activations come from the previous kernel
+        if (elect_one()) {
+          if (CG == 2) tma_load_2d_pair(&tmB, full_l + 8 * s, smem_u32(sB + s * b_bytes), kc, brow);
+          else tma_load_2d(&tmB, full0 + 8 * s, smem_u32(sB + s * b_bytes), kc, brow);
+        }
+        __syncwarp();
       }
-      if (!waited) pdl_wait();
     }
+    if (!waited) pdl_wait();
   } else if (warp == 1) {
     if (rank == 0) {  // the whole warp walks the loop; the elected lane issues
       // kind::f16, bf16 x bf16 -> f32, K-major A/B, N = bn, M = 128 * CG

@@ -456,6 +456,14 @@ __device__ __forceinline__ void d3_tma(const CUtensorMap *map, uint32_t bar, uin
 struct D4Item {
   int r, n_keys, nb, cb, n_chunks, ca, ce;
 };
+// one lane of the converged producer warp (elect.sync): the warp walks the items with
+// its values in uniform registers, the elected lane issues the TMA loads
+__device__ __forceinline__ bool d4_elect() {
+  uint32_t pred = 0;
+  asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}" : "=r"(pred));
+  return pred != 0;
+}
+
 __device__ __forceinline__ bool d4_item(int item, int row_mode, int max_chunks, int cb_min, const int *pos,
                                         const int *active, D4Item &it) {
   it.r = row_mode ? item : item / max_chunks;
@@ -514,23 +522,25 @@ __global__ void __launch_bounds__(D4_THREADS, 2)
   pdl_wait();
   D4Item it;
   if (warp == 4) {
-    if (lane == 0) {
-      int t = 0;  // tiles issued (K and V alternate)
-      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-        if (!d4_item(item, row_mode, max_chunks, cb_min, pos, active, it)) continue;
-        const int *btr = bt + (size_t)it.r * bt_stride;
-        const int b_end = min(it.nb, it.ce * it.cb);
-        for (int b = it.ca * it.cb; b < b_end; ++b) {
-          const int row0 = btr[b] * KV_BLOCK;
+    // the whole warp walks the items (uniform registers); the elected lane issues the loads
+    int t = 0;  // tiles issued (K and V alternate)
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      if (!d4_item(item, row_mode, max_chunks, cb_min, pos, active, it)) continue;
+      const int *btr = bt + (size_t)it.r * bt_stride;
+      const int b_end = min(it.nb, it.ce * it.cb);
+      for (int b = it.ca * it.cb; b < b_end; ++b) {
+        const int row0 = btr[b] * KV_BLOCK;
 #pragma unroll
-          for (int kv = 0; kv < 2; ++kv, ++t) {
-            const int s = t % D4_SLOTS;
-            d3_wait(empty0 + 8 * s, ((t / D4_SLOTS) & 1) ^ 1);
+        for (int kv = 0; kv < 2; ++kv, ++t) {
+          const int s = t % D4_SLOTS;
+          d3_wait(empty0 + 8 * s, ((t / D4_SLOTS) & 1) ^ 1);
+          const uint32_t dst = ring + s * D4_TILE;
+          if (d4_elect()) {
             d3_expect_tx(full0 + 8 * s, D4_TILE);
-            const uint32_t dst = ring + s * D4_TILE;
 #pragma unroll
             for (int j = 0; j < 4; ++j) d3_tma(kv ? &vmap : &kmap, full0 + 8 * s, dst + j * D4_SUB, 64 * j, row0);
           }
+          __syncwarp();
         }
       }
     }
