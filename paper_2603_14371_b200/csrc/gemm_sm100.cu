@@ -129,6 +129,8 @@ struct Knobs {
   int wide_units = 0;   // > 0: cap the persistent grid at this many CTA pairs (diagnosis)
   int wide_nofence = 0; // 1: no tcgen05.fence::after_thread_sync per k-block in the MMA loop (A/B)
   int wide_sleep = 0;   // > 0: epilogue warps poll the accumulator barrier with this ns sleep (A/B)
+  int prefill_kmulti = 0;  // 1: prefill split plans accumulate their splits in-CTA (A/B; 5.66 -> 7.71 ms prefill)
+  int wide_min_n = 16384;  // the persistent kernel from T = 256 for n_out >= this (A/B knob)
   int split_slots = 1;  // skinny split-K fills split_slots CTAs per SM (A/B knob)
   int bigk_min = 0, bigk_bn = 0, bigk_splits = 0;  // OXY_GEMM_BIGK=kmin,bn,splits (A/B knob)
   // split K (fixed-order reduction) for token counts up to this when the tiles do not fill
@@ -146,6 +148,8 @@ struct Knobs {
     if (const char *s = getenv("OXY_GEMM_WIDE_UNITS")) wide_units = atoi(s);
     if (const char *s = getenv("OXY_GEMM_WIDE_NOFENCE")) wide_nofence = atoi(s);
     if (const char *s = getenv("OXY_GEMM_WIDE_SLEEP")) wide_sleep = atoi(s);
+    if (const char *s = getenv("OXY_PREFILL_KMULTI")) prefill_kmulti = atoi(s);
+    if (const char *s = getenv("OXY_GEMM_WIDE_MIN_N")) wide_min_n = atoi(s);
     if (const char *s = getenv("OXY_GEMM_SPLIT_SLOTS")) split_slots = std::max(1, atoi(s));
     if (const char *s = getenv("OXY_GEMM_BIGK")) sscanf(s, "%d,%d,%d", &bigk_min, &bigk_bn, &bigk_splits);
     if (const char *s = getenv("OXY_PDL_EARLY_SKINNY")) early_skinny = atoi(s);
@@ -1092,7 +1096,7 @@ Plan make_plan(int n_out, int k, int t, int sms, int force_splits) {
   // (K >= 8192 projections at T = 800 — the prefill down projection, 73.7 vs 98 us
   // stand-alone with split-K 2 — measured slower in the frame: 9.37 vs 9.27 ms prefill)
   const bool wide_ok =
-      knobs().wide > 0 || (knobs().wide < 0 && ((n_out >= 16384 && t >= 256) || t >= 2048 ||
+      knobs().wide > 0 || (knobs().wide < 0 && ((n_out >= knobs().wide_min_n && t >= 256) || t >= 2048 ||
                                                 (knobs().wide_min_k > 0 && k >= knobs().wide_min_k && t >= 256)));
   if (t > 64 && wide_ok && wide_plan(p, n_out, k, t, sms, force_splits)) return p;
   p.cg = 0;
@@ -1139,9 +1143,10 @@ Plan make_plan(int n_out, int k, int t, int sms, int force_splits) {
   return p;
 }
 
-Plan make_chain_plan(int n_out, int k, int t, int sms, int splits) {
-  Plan p = make_plan(n_out, k, t, sms, splits);
-  if (knobs().kmulti && p.cg == 0 && t >= KMULTI_MIN_T && p.splits >= 2 && p.splits <= 4) {
+// the plan's split partition accumulated in-CTA (kmulti) where the one-tile kernel
+// can hold the splits' accumulators (2-4 regions of <= 256 / splits columns)
+static void to_kmulti(Plan &p, int t) {
+  if (p.cg == 0 && p.splits >= 2 && p.splits <= 4) {
     const int max_bn = 256 / p.splits / 16 * 16;
     if (p.bn > max_bn) {
       p.bn = max_bn;
@@ -1150,6 +1155,17 @@ Plan make_chain_plan(int n_out, int k, int t, int sms, int splits) {
     p.kmulti = p.splits;
     p.stages = std::max(2, std::min(MAX_STAGES, knobs().smem_kb * 1024 / (A_STAGE_BYTES + p.bn * BK * 2)));
   }
+}
+
+Plan make_chain_plan(int n_out, int k, int t, int sms, int splits) {
+  Plan p = make_plan(n_out, k, t, sms, splits);
+  if (knobs().kmulti && t >= KMULTI_MIN_T) to_kmulti(p, t);
+  return p;
+}
+
+Plan make_prefill_plan(int n_out, int k, int t, int sms, int splits) {
+  Plan p = make_plan(n_out, k, t, sms, splits);
+  if (knobs().prefill_kmulti) to_kmulti(p, t);
   return p;
 }
 

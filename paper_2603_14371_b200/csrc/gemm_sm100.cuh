@@ -159,6 +159,7 @@ Plan make_plan(int n_out, int k, int t, int sms, int force_splits = 0);
 // chain-phase variant: for token counts >= KMULTI_MIN_T (>= 11 streams) and 2..4 splits,
 // accumulate the splits in-CTA (Plan::kmulti) with token tiles of <= 256 / splits
 Plan make_chain_plan(int n_out, int k, int t, int sms, int splits);
+Plan make_prefill_plan(int n_out, int k, int t, int sms, int splits);
 constexpr int KMULTI_MIN_T = 512;
 
 // Host: launch.  ws must hold splits * T * N_out floats when splits > 1.

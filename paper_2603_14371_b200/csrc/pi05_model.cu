@@ -633,7 +633,7 @@ struct Model {
   gemm::Plan plan_for(int n_out, int k, int t) const {
     const int sp = gemm::policy_splits(phase, n_out, k, sms);
     gemm::Plan p = phase == gemm::PH_CHAIN ? gemm::make_chain_plan(n_out, k, t, psms(), sp)
-                                           : gemm::make_plan(n_out, k, t, psms(), sp);
+                                           : gemm::make_prefill_plan(n_out, k, t, psms(), sp);
     p.csk = use_csk && !p.kmulti && phase == gemm::PH_CHAIN && p.cg == 0 && p.splits >= 2 &&
             p.splits <= gemm::CSK_MAX;
     return p;
