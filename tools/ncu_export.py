@@ -54,8 +54,14 @@ def main(rnd):
                          "tensor_pipe_pct_active": num(
                              "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"),
                          "grid": g.get("launch__grid_size")}
-    with open(os.path.join(ROOT, "profiles", f"{rnd}_ncu_traffic.json"), "w") as f:
-        json.dump(traffic, f, indent=1)
+    path = os.path.join(ROOT, "profiles", f"{rnd}_ncu_traffic.json")
+    merged = {}
+    if os.path.exists(path):  # keep entries written by other tools (skinny_traffic.py's class)
+        with open(path) as f:
+            merged = json.load(f)
+    merged.update(traffic)
+    with open(path, "w") as f:
+        json.dump(merged, f, indent=1)
     print(json.dumps(traffic, indent=1))
 
 
