@@ -30,6 +30,7 @@ struct KParams {
   int csk;        // 1: cluster split-K — the split CTAs of a tile are one cluster (along z)
   int tma_ws;     // 1: split partials leave through a TMA tensor store (tmW) instead of st.global
   int kmulti;     // > 1: all K partitions of the tile in this CTA, region r = k-block / kb_per_split
+  int bm;         // weight rows per tile: 128, or 64 (Plan::bm; epilogue warps 4-5 idle)
   int b_box;      // token rows per B TMA box: bn, or T when one token tile covers T (rows past
                   // it stay stale in smem; their accumulator columns are never stored)
 };
@@ -132,6 +133,9 @@ struct Knobs {
   int prefill_kmulti = 0;  // 1: prefill split plans accumulate their splits in-CTA (A/B; 5.66 -> 7.71 ms prefill)
   int wide_min_n = 16384;  // the persistent kernel from T = 256 for n_out >= this (A/B knob)
   int split_slots = 1;  // skinny split-K fills split_slots CTAs per SM (A/B knob)
+  // 64-row weight tiles for skinny (T <= 64) plans whose 64-row grid still fits
+  // half_m CTAs per SM (OXY_GEMM_HALF; 0: off)
+  int half_m = 0;
   int bigk_min = 0, bigk_bn = 0, bigk_splits = 0;  // OXY_GEMM_BIGK=kmin,bn,splits (A/B knob)
   // split K (fixed-order reduction) for token counts up to this when the tiles do not fill
   // the SMs: the multi-stream denoise (T = 50 x streams); 8 streams 67.9 -> 61.1 ms/frame
@@ -151,6 +155,7 @@ struct Knobs {
     if (const char *s = getenv("OXY_PREFILL_KMULTI")) prefill_kmulti = atoi(s);
     if (const char *s = getenv("OXY_GEMM_WIDE_MIN_N")) wide_min_n = atoi(s);
     if (const char *s = getenv("OXY_GEMM_SPLIT_SLOTS")) split_slots = std::max(1, atoi(s));
+    if (const char *s = getenv("OXY_GEMM_HALF")) half_m = atoi(s);
     if (const char *s = getenv("OXY_GEMM_BIGK")) sscanf(s, "%d,%d,%d", &bigk_min, &bigk_bn, &bigk_splits);
     if (const char *s = getenv("OXY_PDL_EARLY_SKINNY")) early_skinny = atoi(s);
     if (const char *s = getenv("OXY_PDL_EARLY_WIDE")) early_wide = atoi(s);
@@ -382,7 +387,7 @@ __global__ void __maxnreg__(128)
                                               ~static_cast<uintptr_t>(1023));
   const int bn = p.bn, stages = p.stages;
   const int b_bytes = bn * BK * 2;
-  const uint32_t stage_tx = A_STAGE_BYTES + p.b_box * BK * 2;  // bytes one stage's two TMA boxes deliver
+  const uint32_t stage_tx = (p.bm * BK + p.b_box * BK) * 2;  // bytes one stage's two TMA boxes deliver
   uint8_t *sA = smem;
   uint8_t *sB = smem + stages * A_STAGE_BYTES;
   uint64_t *bars = reinterpret_cast<uint64_t *>(sB + stages * b_bytes);
@@ -390,7 +395,7 @@ __global__ void __maxnreg__(128)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // token tiles fastest: the CTAs sharing one weight tile run in the same wave
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * bn, split = blockIdx.z;
+  const int m0 = blockIdx.y * p.bm, n0 = blockIdx.x * bn, split = blockIdx.z;
   __shared__ int s_last;
   const int kb0 = p.kmulti > 1 ? 0 : split * p.kb_per_split;
   const int nkb = p.kmulti > 1 ? p.kb_total : min(p.kb_total, kb0 + p.kb_per_split) - kb0;
@@ -544,7 +549,9 @@ __global__ void __maxnreg__(128)
       epi_tile(p, trow, 32, bn, n0, f, split, split_out, stg);
     } else
 #endif
-    if (p.kmulti > 1) epi_tile_src(p, MultiTmemSrc{trow, p.kmulti, bn}, 0, bn, n0, f, 0, split_out, stg);
+    if (q * 32 >= p.bm) {
+      // 64-row tile: these accumulator lanes came from stale A rows — nothing to store
+    } else if (p.kmulti > 1) epi_tile_src(p, MultiTmemSrc{trow, p.kmulti, bn}, 0, bn, n0, f, 0, split_out, stg);
     else epi_tile(p, trow, 0, bn, n0, f, split, split_out, stg);
     if (threadIdx.x == 64) GPROF(9);
     if (split_out && p.fixup) splitk_fixup(p, blockIdx.y * gridDim.x + blockIdx.x, n0, 0, bn, f, s_last, 128, 64);
@@ -1140,6 +1147,12 @@ Plan make_plan(int n_out, int k, int t, int sms, int force_splits) {
   const int per_split = (p.kb_total + splits - 1) / splits;
   p.splits = (p.kb_total + per_split - 1) / per_split;
   p.stages = std::max(2, std::min(MAX_STAGES, knobs().smem_kb * 1024 / (A_STAGE_BYTES + p.bn * BK * 2)));
+  p.bm = BM;
+  if (knobs().half_m > 0 && t <= 64 && n_out % 64 == 0 &&
+      2 * p.m_tiles * p.n_tiles * p.splits <= knobs().half_m * sms) {
+    p.bm = 64;
+    p.m_tiles = n_out / 64;
+  }
   return p;
 }
 
@@ -1276,7 +1289,14 @@ void launch(const void *w, const void *x, int n_out, int k, int t, const EpiPara
                   : plan.band == 2 ? PC_BAND_MIDK
                   : plan.splits > 1 ? PC_SKINNY_SPLIT
                                     : PC_SKINNY];
-  CUtensorMap ma = make_map(w, n_out, k, BM);
+  // 64-row tiles only on the per-warp epilogue paths (argmax / TMA-stored partials /
+  // fix-up / cluster split-K use all four epilogue warps)
+  const int bm = plan.bm == 64 && epi.mode != EPI_ARGMAX && !knobs().tma_ws && !knobs().fixup && !plan.csk &&
+                         !(plan.kmulti > 1)
+                     ? 64
+                     : BM;
+  const int m_tiles = (n_out + bm - 1) / bm;
+  CUtensorMap ma = make_map(w, n_out, k, bm);
   // one token tile covering T < bn: a T-row box (no out-of-bounds zero fill; fewer bytes,
   // neutral in the frame — profiles/r02_skinny_gemm.md)
   const int b_box = plan.n_tiles == 1 && t < plan.bn && knobs().bbox_exact ? t : plan.bn;
@@ -1297,6 +1317,7 @@ void launch(const void *w, const void *x, int n_out, int k, int t, const EpiPara
   kp.prefetch = kp.trigger = t <= 64 ? (g_early_override >= 0 ? g_early_override : knobs().early_skinny)
                                      : knobs().early_wide;
   kp.b_box = b_box;
+  kp.bm = bm;
   kp.kmulti = plan.kmulti > 1 && plan.cg == 0 ? plan.kmulti : 0;
   if (kp.kmulti && (plan.bn * kp.kmulti > 256 || kp.kmulti != plan.splits))
     fail(OXY_EINVAL, "in-CTA split-K: %d partitions x %d token columns", kp.kmulti, plan.bn);
@@ -1313,7 +1334,7 @@ void launch(const void *w, const void *x, int n_out, int k, int t, const EpiPara
               (size_t)BM * plan.bn * 4 <= (size_t)plan.stages * (A_STAGE_BYTES + plan.bn * BK * 2) &&
               (n_out * 4) % 16 == 0;
   const CUtensorMap mw = kp.tma_ws ? make_map_ws(ws, plan.splits, t, n_out, plan.bn) : ma;
-  dim3 grid(plan.n_tiles, plan.m_tiles, kp.kmulti ? 1 : plan.splits);
+  dim3 grid(plan.n_tiles, m_tiles, kp.kmulti ? 1 : plan.splits);
   if (kp.csk) {
     if (plan.splits > CSK_MAX) fail(OXY_EINVAL, "cluster split-K: at most %d splits", CSK_MAX);
     static bool np_set = false;

@@ -114,6 +114,10 @@ struct Plan {
   int kmulti;  // one-tile kernel: the `splits` K partitions of a tile accumulated by ONE CTA into
               // `splits` TMEM regions and summed in split order in its epilogue (no partials,
               // no reduce launch; bit-identical to split CTAs + reduce).  0 = split CTAs.
+  int bm;      // one-tile kernel: weight rows per CTA tile — 128, or 64 for skinny chains whose
+              // 128-row grid leaves CTA slots idle (the MMA stays M = 128: rows 64..127 of the
+              // A stage are stale and their accumulator lanes are never stored, so every output
+              // element is computed bit for bit as with 128-row tiles); 0 = 128
   int sms;     // SMs the plan was made for (the persistent kernel's grid; an SM partition's size)
   int partials() const { return kdual || kmulti ? 1 : splits; }  // partial slabs an EPI_PARTIALS launch writes
 };
