@@ -129,6 +129,35 @@ def _as_pi05(cfg) -> Pi05Config:
                       mlp=512, expert_width=128, expert_mlp=256, vit_depth=0)
 
 
+class DeferredActionChunk(ActionChunk):
+    """An ActionChunk whose values are still being copied to the host behind a CUDA
+    event: the first read of ``actions`` waits for the event and converts and
+    validates exactly as ``ActionChunk`` does (same float64 values, same errors).
+    Returned by an overlapped frame's join when no stage meter is attached, so the
+    frame call returns without waiting for its denoise and the host enqueues the
+    next frame while the action expert is still running."""
+
+    __slots__ = ("_host", "_row", "_done", "_val")
+
+    def __init__(self, host, row: int, done):
+        object.__setattr__(self, "_host", host)  # pinned torch tensor [n, H, A] (kept alive)
+        object.__setattr__(self, "_row", row)
+        object.__setattr__(self, "_done", done)
+        object.__setattr__(self, "_val", None)
+
+    @property
+    def actions(self) -> np.ndarray:
+        v = self._val
+        if v is None:
+            self._done.synchronize()
+            v = ActionChunk(self._host[self._row].numpy().astype(np.float64)).actions
+            object.__setattr__(self, "_val", v)
+        return v
+
+    def __repr__(self) -> str:
+        return f"DeferredActionChunk(actions={self.actions!r})"
+
+
 class Pi05Backend(PricedBackend):
     def __init__(self, config=None, cost: CostModelParams | None = None, num_blocks: int = 2048,
                  measure: bool = False, overlap: bool = True):
@@ -308,6 +337,8 @@ class Pi05Backend(PricedBackend):
             done.record()
 
             def chunks():
+                if self.meter is None:
+                    return [DeferredActionChunk(host, i, done) for i in range(n)]
                 done.synchronize()
                 if self.meter is not None:
                     us = C.c_double()
