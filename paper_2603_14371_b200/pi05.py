@@ -173,6 +173,8 @@ class Pi05Backend(PricedBackend):
         self.block_size = KV_BLOCK
         self.allocator = BlockAllocator(num_blocks, KV_BLOCK)
         self.meter = StageMeter() if measure else None
+        self._stage = [(None, None), (None, None)]  # pinned image staging ring (host frames)
+        self._stage_next = 0
         if not overlap:   # stage-serial frames (the reference's order, scheduler.py:117-171)
             self.admit_overlapped = None
         h = C.c_void_p()
@@ -253,10 +255,28 @@ class Pi05Backend(PricedBackend):
         if all(isinstance(i, torch.Tensor) and i.is_cuda for i in imgs):
             dev = imgs[0] if len(imgs) == 1 else torch.cat(imgs)
         else:
-            host = np.concatenate([np.asarray(i.cpu() if isinstance(i, torch.Tensor) else i,
-                                              dtype=np.uint8) for i in imgs])
-            pinned = torch.from_numpy(host).pin_memory()
-            dev = pinned.to("cuda", non_blocking=True)
+            parts = [np.asarray(i.cpu() if isinstance(i, torch.Tensor) else i, dtype=np.uint8) for i in imgs]
+            nbytes = sum(p.nbytes for p in parts)
+            # one copy into a reused pinned staging buffer (a ring of two; the H2D copy
+            # that last read a slot is waited for before it is overwritten), then an
+            # asynchronous H2D on the caller's stream
+            slot = self._stage_next
+            self._stage_next ^= 1
+            buf, ev = self._stage[slot]
+            if buf is None or buf.numel() < nbytes:
+                buf = torch.empty(max(nbytes, 1), dtype=torch.uint8, pin_memory=True)
+            elif ev is not None:
+                ev.synchronize()
+            flat = buf.numpy()
+            off = 0
+            for p in parts:
+                flat[off:off + p.nbytes] = p.reshape(-1)
+                off += p.nbytes
+            shape = (sum(p.shape[0] for p in parts),) + parts[0].shape[1:]
+            dev = buf[:nbytes].to("cuda", non_blocking=True).view(shape)
+            ev = torch.cuda.Event()
+            ev.record()
+            self._stage[slot] = (buf, ev)
         return dev.contiguous(), C.c_void_p(dev.data_ptr())
 
     # ---------------------------------------------------------------- protocol
