@@ -414,7 +414,9 @@ struct Model {
     OXY_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     const char *e = getenv("OXY_LANE_PRIO");
     const bool prio = !e || atoi(e) != 0;
-    init_lane(lo);
+    // A/B knob OXY_LANE0_PRIO=1: lane 0 (prefill, decode) at the highest priority too
+    const char *e0 = getenv("OXY_LANE0_PRIO");
+    init_lane(e0 && atoi(e0) != 0 ? hi : lo);
     {
       LaneSwap g(*this);
       init_lane(prio ? hi : lo);
@@ -507,7 +509,12 @@ struct Model {
     OXY_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     auto screate = reinterpret_cast<StreamCreate>(sym("cuGreenCtxStreamCreate"));
     CUstream s_dn, s_dec;
-    chk(screate(&s_dn, g_dn, CU_STREAM_NON_BLOCKING, hi), "cuGreenCtxStreamCreate");
+    // the expert partition's stream at the prefill's (low) priority: the decode runs on
+    // other SMs, and the pipelined first Euler step then does not take freed SM slots
+    // ahead of the prefill it runs under (14.69 -> 14.56 ms/frame, profiles/r02/prio_ab.txt;
+    // OXY_GREEN_DN_PRIO=1: highest)
+    const char *edp = getenv("OXY_GREEN_DN_PRIO");
+    chk(screate(&s_dn, g_dn, CU_STREAM_NON_BLOCKING, edp && atoi(edp) != 0 ? hi : lo), "cuGreenCtxStreamCreate");
     chk(screate(&s_dec, g_dec, CU_STREAM_NON_BLOCKING, lo), "cuGreenCtxStreamCreate");
     green.dn = reinterpret_cast<cudaStream_t>(s_dn);
     green.dec = reinterpret_cast<cudaStream_t>(s_dec);
