@@ -462,10 +462,10 @@ struct Model {
   }();
   void init_green() {
     const char *e = getenv("OXY_GREEN");
-    // 72 expert SMs with the layer-pipelined first Euler step (it starts under the
-    // prefill, so the decode partition becomes the longer lane at 80: 15.08 vs 14.90 ms,
-    // profiles/r02/pipe_ab*.txt), else 80
-    const int want = e ? atoi(e) : pipe_prefill ? 72 : 80;
+    // with the layer-pipelined first Euler step: 96 expert SMs and an 80-SM decode
+    // partition sharing 28 of them (14.56 ms/frame with disjoint 72 / 76, 14.43 shared,
+    // profiles/r02/overlap_ab*.txt); else disjoint 80 / 68
+    const int want = e ? atoi(e) : pipe_prefill ? 96 : 80;
     if (want <= 0 || want >= sms) return;
     try {
       make_green(want);
@@ -497,6 +497,19 @@ struct Model {
         "cuDeviceGetDevResource");
     chk(reinterpret_cast<Split>(sym("cuDevSmResourceSplitByCount"))(part, &n, &all, &rest, 0, (unsigned)want),
         "cuDevSmResourceSplitByCount");
+    // OXY_GREEN_DEC=<SMs> (default 80 with the pipelined first step, else 0 = the
+    // complement): the decode partition from a second split of all SMs (the complement
+    // of its first sms - <SMs>), so it shares SMs with the expert's.  Green contexts may
+    // overlap; plans do not depend on the partition, so results are unchanged.
+    const char *edec = getenv("OXY_GREEN_DEC");
+    const int want_dec = edec ? atoi(edec) : pipe_prefill ? 80 : 0;
+    if (want_dec > 0 && want_dec < sms && want_dec + want > sms) {
+      CUdevResource part2[1]{};
+      unsigned n2 = 1;
+      chk(reinterpret_cast<Split>(sym("cuDevSmResourceSplitByCount"))(part2, &n2, &all, &rest, 0,
+                                                                       (unsigned)(sms - want_dec)),
+          "cuDevSmResourceSplitByCount (decode)");
+    }
     CUdevResourceDesc d_dn, d_dec;
     auto gen = reinterpret_cast<GenDesc>(sym("cuDevResourceGenerateDesc"));
     chk(gen(&d_dn, &part[0], 1), "cuDevResourceGenerateDesc");
