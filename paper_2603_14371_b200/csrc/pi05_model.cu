@@ -462,10 +462,10 @@ struct Model {
   }();
   void init_green() {
     const char *e = getenv("OXY_GREEN");
-    // with the layer-pipelined first Euler step: 96 expert SMs and an 80-SM decode
-    // partition sharing 28 of them (14.56 ms/frame with disjoint 72 / 76, 14.43 shared,
-    // profiles/r02/overlap_ab*.txt); else disjoint 80 / 68
-    const int want = e ? atoi(e) : pipe_prefill ? 96 : 80;
+    // with the layer-pipelined first Euler step: 136 expert SMs and an 88-SM decode
+    // partition sharing 76 of them (14.56 ms/frame with disjoint 72 / 76, 14.43 at 96 / 80,
+    // 14.23 at 136 / 88, profiles/r02/overlap_ab*.txt); else disjoint 80 / 68
+    const int want = e ? atoi(e) : pipe_prefill ? 136 : 80;
     if (want <= 0 || want >= sms) return;
     try {
       make_green(want);
@@ -497,12 +497,12 @@ struct Model {
         "cuDeviceGetDevResource");
     chk(reinterpret_cast<Split>(sym("cuDevSmResourceSplitByCount"))(part, &n, &all, &rest, 0, (unsigned)want),
         "cuDevSmResourceSplitByCount");
-    // OXY_GREEN_DEC=<SMs> (default 80 with the pipelined first step, else 0 = the
+    // OXY_GREEN_DEC=<SMs> (default 88 with the pipelined first step, else 0 = the
     // complement): the decode partition from a second split of all SMs (the complement
     // of its first sms - <SMs>), so it shares SMs with the expert's.  Green contexts may
     // overlap; plans do not depend on the partition, so results are unchanged.
     const char *edec = getenv("OXY_GREEN_DEC");
-    const int want_dec = edec ? atoi(edec) : pipe_prefill ? 80 : 0;
+    const int want_dec = edec ? atoi(edec) : pipe_prefill ? 88 : 0;
     if (want_dec > 0 && want_dec < sms && want_dec + want > sms) {
       CUdevResource part2[1]{};
       unsigned n2 = 1;
