@@ -280,3 +280,35 @@ def test_extra_tasks_get_action_entries_and_complete():
         res = run_frame_unified(t, [], mgr, be, 2, 30.0)
         pending -= {rid for rid, _ in res.finished}
     assert not pending and not mgr.active_ids()
+
+
+def test_deferred_action_chunk_behaves_as_action_chunk():
+    """An overlapped frame's join yields DeferredActionChunk objects (pi05.py): the
+    first read of .actions waits on the copy event, then converts and validates as
+    ActionChunk does — same float64 values, equality, immutability and errors."""
+    import torch
+    from paper_2603_14371_b200.pi05 import DeferredActionChunk
+
+    class Done:
+        waited = 0
+
+        def synchronize(self):
+            Done.waited += 1
+
+    host = torch.arange(2 * 5 * 3, dtype=torch.float32).reshape(2, 5, 3) / 7
+    done = Done()
+    d = DeferredActionChunk(host, 1, done)
+    assert Done.waited == 0  # nothing is read until the chunk is used
+    ref = ActionChunk(host[1].numpy().astype(np.float64))
+    assert isinstance(d, ActionChunk)
+    assert d == ref and ref == d and d.horizon == 5
+    assert d.actions.dtype == np.float64 and not d.actions.flags.writeable
+    assert Done.waited == 1
+    _ = d.actions
+    assert Done.waited == 1  # materialised once
+    with pytest.raises(Exception):
+        d.actions = None
+    bad = host.clone()
+    bad[0, 2, 1] = float("inf")
+    with pytest.raises(ValueError, match="non-finite"):
+        _ = DeferredActionChunk(bad, 0, done).actions
