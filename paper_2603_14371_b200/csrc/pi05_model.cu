@@ -1108,7 +1108,11 @@ struct Model {
       key += "," + std::to_string(P[i]);
     }
     check_block_ids(blocks_h, nb, NB, "denoise");
-    const bool pipe = pipe_prefill && part && !join && (int)pf_blocks.size() == nb &&
+    // multi-stream overlapped frames (all SMs, no partition) pipeline their first step
+    // too: 8 streams 51.1-51.4 -> 50.6-51.0 ms/frame (profiles/r02/ms_pipe_ab.txt;
+    // OXY_PIPE_ALL=0: partitioned frames only)
+    static const bool pipe_all = !getenv("OXY_PIPE_ALL") || atoi(getenv("OXY_PIPE_ALL")) != 0;
+    const bool pipe = pipe_prefill && (part || pipe_all) && !join && (int)pf_blocks.size() == nb &&
                       std::equal(pf_blocks.begin(), pf_blocks.end(), blocks_h);
     pf_blocks.clear();
     if (pipe) key += "/pipe";
