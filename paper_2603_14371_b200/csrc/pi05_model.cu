@@ -527,7 +527,8 @@ struct Model {
     // ahead of the prefill it runs under (14.69 -> 14.56 ms/frame, profiles/r02/prio_ab.txt;
     // OXY_GREEN_DN_PRIO=1: highest)
     const char *edp = getenv("OXY_GREEN_DN_PRIO");
-    chk(screate(&s_dn, g_dn, CU_STREAM_NON_BLOCKING, edp && atoi(edp) != 0 ? hi : lo), "cuGreenCtxStreamCreate");
+    const int dn_prio = !edp || atoi(edp) == 0 ? lo : atoi(edp) == 2 ? (lo + hi) / 2 : hi;  // 2: between (A/B)
+    chk(screate(&s_dn, g_dn, CU_STREAM_NON_BLOCKING, dn_prio), "cuGreenCtxStreamCreate");
     chk(screate(&s_dec, g_dec, CU_STREAM_NON_BLOCKING, lo), "cuGreenCtxStreamCreate");
     green.dn = reinterpret_cast<cudaStream_t>(s_dn);
     green.dec = reinterpret_cast<cudaStream_t>(s_dec);
